@@ -1,0 +1,324 @@
+"""Benchmark of the hierarchical Hough hot path (BASELINE.json metric: line-region tests/s and
+ms/image at 1/2/4/8 B200; % of HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl reference]
+
+One step = one full detection (all levels, both halves, records + leaves) of the configuration's
+synthetic edge points, resident in HBM. N > 1 runs under torch.distributed.run: points are sharded
+contiguously across ranks, per-level votes are summed with NCCL inside libhht, the timed region is
+bracketed by barrier + synchronize on every rank and the MAX over ranks is reported.
+`--impl reference` times the CPU oracle (oracle/, the only other place bench.py executes it) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "line-region tests/s"
+UNIT = "tests/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="hht", choices=["hht", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--oracle-tests", type=float, default=4e8, help="bounded oracle sample (code evaluations)")
+    return ap.parse_args()
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _workload(cfg):
+    return {"workload": f"config{cfg.cid}: {cfg.text}", "N": cfg.N, "depth": cfg.D, "threshold": cfg.T,
+            "images": cfg.images, "halves": "both" if cfg.halves == 3 else "alpha",
+            "points_per_image": None, "seed": 0,
+            "l2": "inputs and candidate lists larger than L2 (126 MB); no flush"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md recipe)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def _dist_init(n_gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def _cpu_baseline(pts, cfg, budget_tests):
+    """The oracle as it stands on one host core, over a bounded depth-first prefix of the same
+    detection (stops after `budget_tests` code evaluations)."""
+    import oracle
+    t0 = time.perf_counter()
+    r = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves, max_tests=int(budget_tests))
+    dt = time.perf_counter() - t0
+    return {"value": r.tests / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle DFS over config{cfg.cid} image 0 (ALPHA tree first), stopped after "
+                      f"{r.tests:.3g} code evaluations ({dt:.1f} s, single thread, plain C -O2)",
+            "seconds": dt, "tests": r.tests}
+
+
+def run_reference(a):
+    rank, world, _ = (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0)
+    if rank != 0:
+        return
+    from paper_1007_0547_b200 import synth
+    cfg = synth.CONFIGS[a.config]
+    pts, _ = synth.config_image(a.config, 0)
+    per_step = max(a.oracle_tests / max(a.steps, 1), 2e7)
+    for _ in range(a.warmup):
+        _cpu_baseline(pts, cfg, min(per_step, 2e7))
+    tot_tests, tot_s = 0, 0.0
+    for _ in range(a.steps):
+        r = _cpu_baseline(pts, cfg, per_step)
+        tot_tests += r["tests"]
+        tot_s += r["seconds"]
+    v = tot_tests / tot_s
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * tot_s / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": _workload(cfg),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{a.steps} steps, each the oracle DFS over config{cfg.cid} stopped after "
+                                       f"{per_step:.3g} code evaluations"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = _args()
+    if a.impl == "reference":
+        return run_reference(a)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1007_0547_b200 import hht, synth
+
+    rank, world, local = _dist_init(a.gpus)
+    dev = torch.device("cuda", local)
+    cfg = synth.CONFIGS[a.config]
+    if cfg.images > 1:
+        pts, offs = synth.config_batch(a.config)
+    else:
+        pts, _ = synth.config_image(a.config)
+        offs = np.array([0, pts.shape[0]], dtype=np.int64)
+    # shard: images across ranks for batches (independent trees), points within the image otherwise
+    if cfg.images > 1 and world > 1:
+        lo, hi = synth.shard(cfg.images, rank, world)
+        my = pts[offs[lo]:offs[hi]]
+        my_offs = offs[lo:hi + 1] - offs[lo]
+        comm_world = 1
+    else:
+        lo, hi = synth.shard(pts.shape[0], rank, world)
+        my = pts[lo:hi]
+        my_offs = np.array([0, my.shape[0]], dtype=np.int64)
+        comm_world = world
+    nccl_id = None
+    if comm_world > 1:
+        obj = [hht.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    h = hht.HHT(device=local, halves=cfg.halves, record_levels=True, profile=True,
+                rank=rank if comm_world > 1 else 0, world=comm_world, nccl_id=nccl_id)
+    d_pts = torch.from_numpy(np.ascontiguousarray(my)).to(dev)
+    B = my_offs.shape[0] - 1
+
+    def step():
+        if B > 1 or cfg.images > 1:
+            h.detect_batch(d_pts, my_offs, cfg.N, cfg.D, cfg.T)
+        else:
+            h.detect(d_pts, cfg.N, cfg.D, cfg.T)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(max(a.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    prof_tot = {}
+    tests_tot = 0
+    launches = 0
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        h.timer_begin()
+        step_ms = []
+        for _ in range(a.steps):
+            step()
+            st = h.stats()
+            step_ms.append(st["ms"])
+            tests_tot += st["tests"]
+            for k, v in h.profile().items():
+                p = prof_tot.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0})
+                p["launches"] += v["launches"]
+                p["ms"] += v["ms"]
+                p["bytes"] += v["bytes"]
+        ms = h.timer_end()
+        torch.cuda.synchronize()
+        barrier()
+    clocks = clk.summary()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        if cfg.images > 1:   # image-sharded: each rank's tests are its own; sum them
+            tt = torch.tensor([tests_tot], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt)
+            tests_tot = float(tt.item())
+    st = h.stats()
+    launches = sum(v["launches"] for k, v in prof_tot.items() if k != "allreduce")
+    value = tests_tot / (ms / 1e3)
+    ms_per_step = ms / a.steps
+    images = cfg.images
+
+    # roofline of the dominant kernel class (largest device time inside the timed region)
+    peak, peak_kind = _peaks()
+    dom = max((k for k in prof_tot if k not in ("allreduce",)), key=lambda k: prof_tot[k]["ms"])
+    d = prof_tot[dom]
+    avg_ms = d["ms"] / max(d["launches"], 1)
+    achieved = (d["bytes"] / max(d["launches"], 1)) / (avg_ms / 1e3) / 1e9 if d["launches"] else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"config{cfg.cid}", {}).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                "kernel_share_of_step": d["ms"] / max(sum(step_ms), 1e-9),
+                "launches": d["launches"], "avg_launch_ms": avg_ms,
+                "algorithmic_bytes_per_launch": d["bytes"] / max(d["launches"], 1)}
+
+    e2e = None
+    if not a.no_e2e:
+        host = torch.from_numpy(np.ascontiguousarray(my)).pin_memory()
+        h2 = hht.HHT(device=local, halves=cfg.halves, record_levels=True,
+                     rank=rank if comm_world > 1 else 0, world=comm_world, nccl_id=None) if comm_world == 1 else h
+        hnp = host.numpy()
+        h2.detect_batch(hnp, my_offs, cfg.N, cfg.D, cfg.T)   # warm
+        h2.leaves()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_steps = max(1, min(a.steps, 3))
+        d2h = 0
+        for _ in range(e_steps):
+            h2.detect_batch(hnp, my_offs, cfg.N, cfg.D, cfg.T)   # H2D inside the call
+            lv = h2.leaves()                                       # D2H of the detected lines
+            d2h = lv.shape[0] * 16
+        torch.cuda.synchronize()
+        et = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([et], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            et = float(t.item())
+        e2e = {"value": tests_tot / a.steps * e_steps / et, "unit": UNIT,
+               "h2d_bytes_per_step": int(hnp.nbytes), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * et / e_steps, "timing": "wall clock around detect(host points) + leaves()"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            cpu = _cpu_baseline(pts[offs[0]:offs[1]], cfg, a.oracle_tests)
+            cpu.pop("seconds", None)
+            cpu.pop("tests", None)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        wl = _workload(cfg)
+        wl["points_per_image"] = int(offs[1] - offs[0])
+        wl["parallelism"] = (f"points sharded x{world}, per-level NCCL allreduce" if comm_world > 1 else
+                             (f"images sharded x{world}" if world > 1 else "single GPU"))
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": ms_per_step, "ms_per_image": ms_per_step / images,
+                "higher_is_better": True, "scaling": "weak" if cfg.images > 1 else "strong",
+                "vs_baseline": None, "dtype": "int32" if st["int_bits"] == 32 else "int64",
+                "data": "synthetic (seeded generator, paper_1007_0547_b200/synth.py)", "config": wl,
+                "tests_per_step": tests_tot / a.steps, "votes_per_step": st["votes"],
+                "leaves_per_step": st["leaves"], "pairs_per_step": st["pairs"], "ranges": st["ranges"],
+                "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches,
+                "kernel_ms": {k: v["ms"] / a.steps for k, v in prof_tot.items()}}
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

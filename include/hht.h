@@ -1,0 +1,161 @@
+/*
+ * hht.h -- C ABI of libhht.so, a B200-native (sm_100a) implementation of the level-synchronous
+ * hot path of Singh & Bhatia's hierarchical slope-intercept Hough transform with the exact 4-bit
+ * corner-code membership test (arXiv 1007.0547; PAPER.md = the paper's text).
+ *
+ * What one detect call computes (§3 pseudocode, with getcode()
+ * PAPER.md:146-164; readings R1-R16 in DESIGN.md §2):
+ *   for every tree (image x half; ALPHA uses (x,y), BETA uses (y,x)) the quadtree over
+ *   parameter space m in [-1,1] x b in [-N,2N] down to level `depth`; a region's votes are the
+ *   number of edge points whose line b = y - x*m has a corner code other than 0000 and 1111 with
+ *   respect to it; a region with votes > threshold is split into its four
+ *   children NE, NW, SW, SE, which test only the lines that crossed it
+ *   (PAPER.md:100-103); a level-`depth` region with votes > threshold is a detected line
+ *   (solution() without point removal).
+ *
+ * Conventions shared by every call:
+ *   - Every call returns hht_status; none throws, exits or prints. On error, hht_last_error(ctx)
+ *     holds one line of text (CUDA / NCCL error strings included).
+ *   - A ctx is not thread-safe: use one ctx per (host thread, device).
+ *   - Point arrays are int32 (x, y) pairs, row-major [n][2], 8-byte aligned. They may be device
+ *     memory (the fast path) or host memory (pageable or pinned: the library stages them with one
+ *     host-to-device copy per call, counted in the result's h2d_bytes). They are borrowed for the
+ *     duration of the call only; every detect call is synchronous on return.
+ *   - Lattice: corners m_i = -1 + 2i/2^D, b_j = -N + 3N*j/2^D, i,j in [0, 2^D]; a level-l region
+ *     (a, c) spans lattice [a*s, (a+1)*s] x [c*s, (c+1)*s] with s = 2^(D-l). A leaf (i, j) at level D
+ *     covers m in [m_i, m_(i+1)], b in [b_j, b_(j+1)] -- exact dyadic rationals.
+ *   - Outputs are owned by the ctx until the next detect call or hht_destroy; getters copy out
+ *     to host OR device memory (cudaMemcpyDefault). A too-small `cap` returns HHT_EINVAL with
+ *     *count set to the required number of elements.
+ */
+#ifndef HHT_H
+#define HHT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HHT_OK = 0,
+    HHT_EINVAL = 1,     /* null pointer, n < 0, N < 1 or N > 65536, depth < 1 or > 30, threshold < 1,
+                           bad halves, unaligned points, bad image/half/level in a getter, small cap */
+    HHT_ERANGE = 2,     /* a point outside [0,N)^2, found before any traversal */
+    HHT_EOVERFLOW = 3,  /* 5*N*2^depth >= 2^62: exact int64 corner arithmetic impossible */
+    HHT_ENOMEM = 4,     /* device memory budget cannot hold one region's candidate list */
+    HHT_ECUDA = 5,      /* CUDA runtime error (text in hht_last_error) */
+    HHT_ENCCL = 6,      /* NCCL error (text in hht_last_error) */
+    HHT_EMISMATCH = 7,  /* ranks disagree on (N, depth, threshold, halves, images) */
+    HHT_ESTATE = 8      /* getter called before a successful detect */
+} hht_status;
+
+#define HHT_ALPHA 1u    /* |m| <= 1 set: point (x, y) */
+#define HHT_BETA 2u     /* |m| > 1 set: point taken as (y, x) */
+
+typedef struct hht_ctx hht_ctx;   /* opaque */
+
+typedef struct {
+    int32_t device;          /* CUDA ordinal */
+    int32_t rank;            /* this process's rank in [0, world) */
+    int32_t world;           /* ranks sharing one detection (points sharded); 1 = single GPU */
+    uint32_t halves;         /* HHT_ALPHA | HHT_BETA (default both) */
+    uint32_t record_levels;  /* 1 (default): keep every level's (a, c, votes) records */
+    uint32_t force_int64;    /* 1: use the int64 kernels even where int32 is exact (testing) */
+    uint32_t profile;        /* 1: time every kernel launch with CUDA events (hht_result_profile) */
+    uint32_t reserved;
+    size_t mem_budget;       /* device bytes for candidate lists; 0 = 80% of free memory at create.
+                                Levels whose lists do not fit are processed in depth-first ranges. */
+    const void* nccl_id;     /* world > 1: 128-byte ncclUniqueId from hht_nccl_unique_id on rank 0,
+                                identical on every rank; NULL when world == 1 */
+} hht_opts;
+
+/* One detected line: leaf (i, j) of tree (image, half) with votes > threshold. */
+typedef struct {
+    int32_t image;
+    uint32_t half;           /* HHT_ALPHA or HHT_BETA */
+    uint32_t i, j;           /* leaf lattice indices (see conventions) */
+    uint32_t votes;
+} hht_leaf;
+
+typedef struct {
+    uint64_t tests;          /* line-region code evaluations: per tree E + 4 * sum of votes of every
+                                split region (PAPER.md:296-298 unit; R9) */
+    uint64_t votes;          /* sum of votes over every visited region (Table 1 "Number of votes") */
+    uint64_t leaves;         /* detected lines */
+    uint64_t pairs;          /* (split region, local candidate line) pairs streamed from HBM */
+    uint64_t visited[64];    /* regions visited per level, all trees */
+    uint64_t split[64];      /* regions split per level, all trees */
+    uint64_t h2d_bytes, d2h_bytes;   /* host<->device bytes moved inside the call */
+    uint32_t levels;         /* depth + 1 */
+    uint32_t int_bits;       /* 32 or 64: corner arithmetic width used */
+    uint32_t ranges;         /* list ranges processed (1 per level when everything fits) */
+    uint32_t images;
+    double ms;               /* device time of the call (CUDA events on the ctx stream) */
+} hht_stats;
+
+/* Per-kernel-class timings of the last detect (opts.profile = 1), CUDA events per launch. */
+typedef struct {
+    uint64_t launches[8];    /* 0 stage, 1 count pass, 2 write pass (list compaction + count-ahead),
+                                3 count-only pass, 4 split (threshold + scan), 5 chunk map,
+                                6 other (memsets, range selection), 7 allreduce */
+    double ms[8];
+    uint64_t bytes[8];       /* algorithmic HBM bytes moved by that class */
+} hht_profile;
+
+/* Fill opts with defaults (device 0, rank 0 of 1, both halves, records on). */
+hht_status hht_default_opts(hht_opts* opts);
+
+/* Create a context on opts->device. For world > 1 this joins the NCCL communicator (collective:
+ * every rank must call it). */
+hht_status hht_create(hht_ctx** out, const hht_opts* opts);
+
+/* Write a fresh 128-byte ncclUniqueId into out (cap >= 128). Call on rank 0 and broadcast. */
+hht_status hht_nccl_unique_id(void* out, size_t cap);
+
+/* Detect lines in one image: points = int32 [n][2] (x, y) with 0 <= x, y < N; depth D >= 1 is the
+ * leaf level (PAPER.md:69 uses ceil(log2 N)); threshold T >= 1 (strict: votes > T splits / emits).
+ * world > 1: each rank passes its own shard (n = local count); results are global and identical
+ * on every rank. n = 0 is valid. */
+hht_status hht_detect(hht_ctx* ctx, const int32_t* points, int64_t n, int32_t N, int32_t depth,
+                      int64_t threshold);
+
+/* Detect lines in B independent images at once (one tree per image and half): image b owns
+ * points[offsets[b] .. offsets[b+1]) ; offsets is a HOST array of B+1 non-decreasing values with
+ * offsets[0] = 0. */
+hht_status hht_detect_batch(hht_ctx* ctx, const int32_t* points, const int64_t* offsets, int32_t B,
+                            int32_t N, int32_t depth, int64_t threshold);
+
+/* Detected lines of `image` (ALPHA tree first, each in the paper's depth-first NE,NW,SW,SE order);
+ * image = -1 returns every image's lines in image order. */
+hht_status hht_result_leaves(hht_ctx* ctx, int32_t image, hht_leaf* out, int64_t cap, int64_t* count);
+
+/* Visited regions of tree (image, half) at `level` in depth-first quad order, as uint32 triplets
+ * (a, c, votes): out holds cap triplets (3*cap uint32). Needs opts.record_levels = 1. */
+hht_status hht_result_level(hht_ctx* ctx, int32_t image, uint32_t half, int32_t level, uint32_t* out,
+                            int64_t cap, int64_t* count);
+
+hht_status hht_result_stats(hht_ctx* ctx, hht_stats* out);
+hht_status hht_result_profile(hht_ctx* ctx, hht_profile* out);
+
+/* Device-time bracket on the ctx stream (CUDA events): begin records, end records, synchronises
+ * and returns the milliseconds between the two. */
+hht_status hht_timer_begin(hht_ctx* ctx);
+hht_status hht_timer_end(hht_ctx* ctx, double* ms);
+
+/* One line describing the last error of ctx (never NULL; "" if none). */
+const char* hht_last_error(const hht_ctx* ctx);
+const char* hht_status_str(hht_status s);
+
+/* Release every resource; NULL-safe; synchronises the ctx stream first. */
+void hht_destroy(hht_ctx* ctx);
+
+/* Library build identification: "hht <version> sm_100a". */
+const char* hht_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HHT_H */

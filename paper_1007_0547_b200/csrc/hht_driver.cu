@@ -1,0 +1,892 @@
+// Level driver and C ABI of libhht.so (declared in include/hht.h).
+//
+// Control flow of one detection (paper: PAPER.md:73-138 run level-synchronously):
+//   K0 stage/validate -> roots (every line crosses the root, votes = E) -> count pass over the
+//   roots' lists (level-1 votes) -> [allreduce] -> split(level 1) -> descend(0):
+//     descend(l): for each depth-first range of the level-(l+1) frontier whose candidate lists fit
+//       the memory budget: write pass over the level-l lists (compacts the level-(l+1) lists and
+//       counts level-(l+2) votes) -> [allreduce] -> split(level l+2) -> descend(l+1).
+//     At level D-2 the pass is count-only (level-D votes) -> split(level D) emits the leaves.
+// One host synchronisation per split (the next frontier's size sizes the next launch).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hht.h"
+#include "hht_internal.h"
+
+using namespace hht;
+
+namespace {
+
+struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+struct Level {
+    Buf tree, a, c, parent, len, off, choff, chunk_region;   // frontier R_l
+    Buf nf;                                                   // children of R_(l-1) range -> R_l
+    Buf votes, votes_local;                                   // votes of R_l's children (range)
+    Buf cursor;                                               // append cursors of R_l lists (range)
+    Buf list_own;                                             // R_l candidate lists (range)
+    uint32_t F = 0;
+    uint64_t S = 0, C = 0;
+    const uint32_t* list = nullptr;
+    uint64_t list_base = 0;
+
+    Frontier frontier() {
+        return {(uint32_t*)tree.p, (uint32_t*)a.p, (uint32_t*)c.p, (uint32_t*)parent.p, (uint32_t*)len.p,
+                (uint64_t*)off.p, (uint64_t*)choff.p, (uint32_t*)chunk_region.p};
+    }
+};
+
+struct Grow {          // append-only device vector
+    Buf b;
+    uint64_t n = 0;
+};
+
+struct ProfEv {
+    cudaEvent_t a, b;
+    int cls;
+    uint64_t bytes;
+};
+
+}  // namespace
+
+struct hht_ctx {
+    hht_opts opts{};
+    int sms = 148;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, tb0 = nullptr, tb1 = nullptr;
+    ncclComm_t comm = nullptr;
+    std::string err;
+    size_t budget = 0;
+    size_t list_used = 0;
+    int grid[3][2] = {};
+
+    // last call
+    int N = 0, D = 0, B = 0, H = 0, ntrees = 0;
+    uint64_t T = 0;
+    bool int64 = false;
+    bool have = false;
+    std::vector<uint8_t> tree_half;         // HHT_ALPHA / HHT_BETA per tree
+    std::vector<int64_t> tree_E;            // global points per tree
+
+    Buf stage_in, packed, errflag, beta, stats, tiles, tilectr, totals, rng, bounds, vtmp;
+    Totals* totals_h = nullptr;
+    RangeInfo* range_h = nullptr;
+    uint64_t* misc_h = nullptr;
+    std::vector<Level> lv;
+    Grow rec[64];
+    Grow leaves;
+    std::vector<Record> rec_host[64];
+    bool rec_host_ok[64] = {};
+    std::vector<LeafRec> leaves_host;
+    bool leaves_host_ok = false;
+    hht_stats stat{};
+    hht_profile prof{};
+    std::vector<ProfEv> pev;
+    size_t pev_used = 0;
+};
+
+namespace {
+
+hht_status set_err(hht_ctx* x, hht_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (x) x->err = buf;
+    return s;
+}
+
+#define CK(expr)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return set_err(x, HHT_ECUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_),   \
+                           __FILE__, __LINE__, #expr);                                            \
+    } while (0)
+
+#define CKN(expr)                                                                                 \
+    do {                                                                                          \
+        ncclResult_t r_ = (expr);                                                                 \
+        if (r_ != ncclSuccess)                                                                    \
+            return set_err(x, HHT_ENCCL, "NCCL error %s at %s:%d (%s)", ncclGetErrorString(r_),   \
+                           __FILE__, __LINE__, #expr);                                            \
+    } while (0)
+
+#define TRY(expr)                                                                                 \
+    do {                                                                                          \
+        hht_status s_ = (expr);                                                                   \
+        if (s_ != HHT_OK) return s_;                                                              \
+    } while (0)
+
+// Ensure capacity (contents are NOT preserved). exact: allocate exactly `bytes` (list buffers,
+// which are accounted against the budget); otherwise grow geometrically.
+hht_status ensure(hht_ctx* x, Buf& b, size_t bytes, bool exact = false) {
+    if (bytes <= b.cap) return HHT_OK;
+    size_t want = exact ? bytes : std::max(bytes, b.cap + b.cap / 2);
+    want = (want + 255) & ~size_t(255);
+    if (b.p) CK(cudaFreeAsync(b.p, x->st));
+    b.p = nullptr;
+    b.cap = 0;
+    cudaError_t e = cudaMallocAsync(&b.p, want, x->st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(x, HHT_ENOMEM, "device allocation of %zu bytes failed (%s)", want, cudaGetErrorString(e));
+    }
+    b.cap = want;
+    return HHT_OK;
+}
+
+hht_status release(hht_ctx* x, Buf& b) {
+    if (b.p) CK(cudaFreeAsync(b.p, x->st));
+    b.p = nullptr;
+    b.cap = 0;
+    return HHT_OK;
+}
+
+// Ensure capacity, preserving the first `keep` bytes.
+hht_status grow(hht_ctx* x, Grow& g, size_t elem, uint64_t need) {
+    if (need * elem <= g.b.cap) return HHT_OK;
+    size_t want = std::max<size_t>(need * elem, g.b.cap * 2);
+    want = (want + 255) & ~size_t(255);
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, want, x->st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(x, HHT_ENOMEM, "device allocation of %zu bytes failed (%s)", want, cudaGetErrorString(e));
+    }
+    if (g.n) CK(cudaMemcpyAsync(p, g.b.p, g.n * elem, cudaMemcpyDeviceToDevice, x->st));
+    if (g.b.p) CK(cudaFreeAsync(g.b.p, x->st));
+    g.b.p = p;
+    g.b.cap = want;
+    return HHT_OK;
+}
+
+// Profiling: event pair around one launch.
+int prof_begin(hht_ctx* x, int cls, uint64_t bytes) {
+    if (!x->opts.profile) return -1;
+    if (x->pev_used == x->pev.size()) {
+        ProfEv e{};
+        if (cudaEventCreate(&e.a) != cudaSuccess || cudaEventCreate(&e.b) != cudaSuccess) return -1;
+        x->pev.push_back(e);
+    }
+    ProfEv& e = x->pev[x->pev_used];
+    e.cls = cls;
+    e.bytes = bytes;
+    cudaEventRecord(e.a, x->st);
+    return (int)x->pev_used++;
+}
+void prof_end(hht_ctx* x, int id) {
+    if (id >= 0) cudaEventRecord(x->pev[id].b, x->st);
+}
+
+hht_status allreduce_sum_u32(hht_ctx* x, uint32_t* buf, size_t count) {
+    if (x->opts.world <= 1 || count == 0) return HHT_OK;
+    const int id = prof_begin(x, 7, count * 4);
+    CKN(ncclAllReduce(buf, buf, count, ncclUint32, ncclSum, x->comm, x->st));
+    prof_end(x, id);
+    return HHT_OK;
+}
+
+hht_status sync(hht_ctx* x) {
+    CK(cudaStreamSynchronize(x->st));
+    return HHT_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// split: threshold the votes of the children of parents P[r0, r0+Fp) into level child_level.
+// ---------------------------------------------------------------------------------------------
+hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t Fp, const uint32_t* V,
+                    const uint32_t* VL) {
+    if (Fp == 0) return HHT_OK;
+    Level& C = x->lv[child_level];
+    const bool leaf = child_level == x->D;
+    const bool need_lists = child_level <= x->D - 2;
+    const uint64_t nch = 4ull * Fp;
+    if (!leaf) {
+        TRY(ensure(x, C.tree, nch * 4));
+        TRY(ensure(x, C.a, nch * 4));
+        TRY(ensure(x, C.c, nch * 4));
+        TRY(ensure(x, C.parent, nch * 4));
+        TRY(ensure(x, C.len, nch * 4));
+        TRY(ensure(x, C.off, (nch + 1) * 8));
+        TRY(ensure(x, C.choff, (nch + 1) * 8));
+        TRY(ensure(x, C.nf, nch * 4));
+    } else {
+        TRY(grow(x, x->leaves, sizeof(LeafRec), x->leaves.n + nch));
+    }
+    const bool record = x->opts.record_levels != 0;
+    if (record) TRY(grow(x, x->rec[child_level], sizeof(Record), x->rec[child_level].n + nch));
+    const uint32_t ntiles = (Fp + kSplitThreads - 1) / kSplitThreads;
+    TRY(ensure(x, x->tiles, (size_t)ntiles * sizeof(TileDesc)));
+    CK(cudaMemsetAsync(x->tiles.p, 0, (size_t)ntiles * sizeof(TileDesc), x->st));
+    CK(cudaMemsetAsync(x->tilectr.p, 0, 4, x->st));
+
+    SplitArgs a{};
+    a.V = V;
+    a.VL = VL;
+    a.Fp = Fp;
+    a.p_tree = (const uint32_t*)P.tree.p + r0;
+    a.p_a = (const uint32_t*)P.a.p + r0;
+    a.p_c = (const uint32_t*)P.c.p + r0;
+    a.parent_base = r0;
+    a.child_level = child_level;
+    a.leaf_level = leaf;
+    a.need_lists = need_lists;
+    a.record = record;
+    a.T = x->T;
+    a.nf = (uint32_t*)C.nf.p;
+    a.out = C.frontier();
+    a.rec = record ? (Record*)x->rec[child_level].b.p + x->rec[child_level].n : nullptr;
+    a.leaves = leaf ? (LeafRec*)x->leaves.b.p + x->leaves.n : nullptr;
+    a.tiles = (TileDesc*)x->tiles.p;
+    a.tile_counter = (uint32_t*)x->tilectr.p;
+    a.stats = (unsigned long long*)x->stats.p;
+    a.totals = (Totals*)x->totals.p;
+    a.ntiles = ntiles;
+    const uint64_t bytes = (uint64_t)Fp * (16 + (VL != V ? 16 : 0) + 12 + (leaf ? 0 : 16) + (record ? 64 : 0));
+    const int id = prof_begin(x, 4, bytes);
+    CK(launch_split(a, x->st));
+    prof_end(x, id);
+    CK(cudaMemcpyAsync(x->totals_h, x->totals.p, sizeof(Totals), cudaMemcpyDeviceToHost, x->st));
+    TRY(sync(x));
+    const Totals t = *x->totals_h;
+    if (record) x->rec[child_level].n += nch;
+    if (leaf) {
+        x->leaves.n += t.F;
+        return HHT_OK;
+    }
+    C.F = (uint32_t)t.F;
+    C.S = t.S;
+    C.C = t.C;
+    if (x->opts.profile) x->prof.bytes[4] += (uint64_t)C.F * 36;
+    if (need_lists && C.F) {
+        TRY(ensure(x, C.chunk_region, std::max<uint64_t>(C.C, 1) * 4));
+        const int id2 = prof_begin(x, 5, C.C * 4 + (uint64_t)C.F * 16);
+        CK(launch_chunk_map((const uint64_t*)C.choff.p, C.F, (uint32_t*)C.chunk_region.p, x->st));
+        prof_end(x, id2);
+    }
+    return HHT_OK;
+}
+
+PassArgs pass_args(hht_ctx* x, Level& P, int level) {
+    PassArgs a{};
+    a.list = P.list;
+    a.list_base = P.list_base;
+    a.p_tree = (const uint32_t*)P.tree.p;
+    a.p_a = (const uint32_t*)P.a.p;
+    a.p_c = (const uint32_t*)P.c.p;
+    a.p_len = (const uint32_t*)P.len.p;
+    a.p_off = (const uint64_t*)P.off.p;
+    a.p_choff = (const uint64_t*)P.choff.p;
+    a.chunk_region = (const uint32_t*)P.chunk_region.p;
+    a.chunk_bounds = (const uint64_t*)x->bounds.p;
+    a.tree_beta = (const uint8_t*)x->beta.p;
+    a.level = level;
+    a.D = x->D;
+    a.N = x->N;
+    return a;
+}
+
+hht_status run_pass(hht_ctx* x, int mode, const PassArgs& a, uint64_t pairs, uint64_t written) {
+    const int cls = mode == MODE_COUNT ? 1 : (mode == MODE_WRITE ? 2 : 3);
+    const int id = prof_begin(x, cls, pairs * 4 + written * 4);
+    CK(launch_pass(mode, x->int64, a, x->grid[mode][x->int64 ? 1 : 0], x->st));
+    prof_end(x, id);
+    x->stat.pairs += pairs;
+    return HHT_OK;
+}
+
+// Choose [q0, q1) over the level-lc frontier; W > 1 agrees on the smallest proposal.
+hht_status choose_range(hht_ctx* x, int lc, uint32_t q0, uint64_t cap_entries, bool all, RangeInfo* out) {
+    Level& C = x->lv[lc];
+    Level& P = x->lv[lc - 1];
+    const int id = prof_begin(x, 6, 0);
+    CK(launch_range((const uint64_t*)C.off.p, (const uint32_t*)C.parent.p, C.F, q0, cap_entries,
+                    all ? C.F : 0, (const uint64_t*)P.off.p, (const uint64_t*)P.choff.p,
+                    (const uint32_t*)P.len.p, lc == 1, (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->st));
+    prof_end(x, id);
+    if (x->opts.world > 1 && !all) {
+        // min over ranks of the proposed end, then recompute with the agreed end
+        CKN(ncclAllReduce((const char*)x->rng.p + offsetof(RangeInfo, q1), (char*)x->vtmp.p, 1, ncclUint64,
+                          ncclMin, x->comm, x->st));
+        CK(cudaMemcpyAsync(x->misc_h, x->vtmp.p, 8, cudaMemcpyDeviceToHost, x->st));
+        TRY(sync(x));
+        const uint64_t q1 = x->misc_h[0];
+        CK(launch_range((const uint64_t*)C.off.p, (const uint32_t*)C.parent.p, C.F, q0, cap_entries, q1,
+                        (const uint64_t*)P.off.p, (const uint64_t*)P.choff.p, (const uint32_t*)P.len.p,
+                        lc == 1, (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->st));
+    }
+    CK(cudaMemcpyAsync(x->range_h, x->rng.p, sizeof(RangeInfo), cudaMemcpyDeviceToHost, x->st));
+    TRY(sync(x));
+    *out = *x->range_h;
+    return HHT_OK;
+}
+
+// Preconditions: lv[l] holds the lists of R_l[r0, r1) and lv[l+1] holds R_(l+1) = the split
+// children of R_l[r0, r1) with NF_(l+1). Processes everything below.
+hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
+    const int lc = l + 1;
+    if (lc >= x->D) return HHT_OK;
+    Level& P = x->lv[l];
+    Level& C = x->lv[lc];
+    const uint32_t Fc = C.F;
+    if (Fc == 0) return HHT_OK;
+    (void)r1;
+
+    if (lc == x->D - 1) {
+        // count-only pass: level-D votes of the children of R_(D-1), then the leaves.
+        RangeInfo ri{};
+        TRY(choose_range(x, lc, 0, 0, true, &ri));
+        TRY(ensure(x, C.votes, 16ull * Fc));
+        CK(cudaMemsetAsync(C.votes.p, 0, 16ull * Fc, x->st));
+        PassArgs a = pass_args(x, P, l);
+        a.nf = (const uint32_t*)C.nf.p;
+        a.nf_rbase = r0;
+        a.q0 = 0;
+        a.q1 = Fc;
+        a.votes = (uint32_t*)C.votes.p;
+        TRY(run_pass(x, MODE_COUNT2, a, ri.pairs, 0));
+        TRY(allreduce_sum_u32(x, (uint32_t*)C.votes.p, 4ull * Fc));
+        return do_split(x, x->D, C, 0, Fc, (const uint32_t*)C.votes.p, (const uint32_t*)C.votes.p);
+    }
+
+    uint32_t q0 = 0;
+    while (q0 < Fc) {
+        // list budget left for this level: everything not held by the other levels' buffers
+        // (their capacities persist across ranges and calls, so steady state does no allocation)
+        const size_t others = x->list_used - C.list_own.cap;
+        const size_t avail = x->budget > others ? x->budget - others : 0;
+        const uint64_t cap = (lc == x->D - 2 ? avail : avail / 3) / 4;
+        RangeInfo ri{};
+        TRY(choose_range(x, lc, q0, cap, false, &ri));
+        const uint32_t q1 = (uint32_t)ri.q1;
+        const uint64_t entries = ri.s_hi - ri.s_lo;
+        if (entries * 4 > avail)
+            return set_err(x, HHT_ENOMEM, "level %d region list of %llu entries exceeds the list budget (%zu B free)",
+                           lc, (unsigned long long)entries, avail);
+        if (entries * 4 > C.list_own.cap) {
+            x->list_used -= C.list_own.cap;
+            TRY(release(x, C.list_own));
+            TRY(ensure(x, C.list_own, std::max<uint64_t>(entries, 1) * 4, true));
+            x->list_used += C.list_own.cap;
+        }
+        C.list = (const uint32_t*)C.list_own.p;
+        C.list_base = ri.s_lo;
+        const uint32_t nq = q1 - q0;
+        TRY(ensure(x, C.cursor, 4ull * nq));
+        TRY(ensure(x, C.votes, 16ull * nq));
+        CK(cudaMemsetAsync(C.cursor.p, 0, 4ull * nq, x->st));
+        CK(cudaMemsetAsync(C.votes.p, 0, 16ull * nq, x->st));
+        PassArgs a = pass_args(x, P, l);
+        a.nf = (const uint32_t*)C.nf.p;
+        a.nf_rbase = r0;
+        a.q0 = q0;
+        a.q1 = q1;
+        a.c_off = (const uint64_t*)C.off.p;
+        a.c_list_base = ri.s_lo;
+        a.c_cursor = (uint32_t*)C.cursor.p;
+        a.c_list = (uint32_t*)C.list_own.p;
+        a.votes = (uint32_t*)C.votes.p;
+        TRY(run_pass(x, MODE_WRITE, a, ri.pairs, entries));
+        x->stat.ranges += 1;
+        const uint32_t* VL = (const uint32_t*)C.votes.p;
+        if (x->opts.world > 1) {
+            TRY(ensure(x, C.votes_local, 16ull * nq));
+            CK(cudaMemcpyAsync(C.votes_local.p, C.votes.p, 16ull * nq, cudaMemcpyDeviceToDevice, x->st));
+            VL = (const uint32_t*)C.votes_local.p;
+            TRY(allreduce_sum_u32(x, (uint32_t*)C.votes.p, 4ull * nq));
+        }
+        TRY(do_split(x, lc + 1, C, q0, nq, (const uint32_t*)C.votes.p, VL));
+        TRY(descend(x, lc, q0, q1));
+        q0 = q1;
+    }
+    return HHT_OK;
+}
+
+hht_status check_args(hht_ctx* x, const int32_t* points, int64_t n_total, int32_t N, int32_t D, int64_t T) {
+    if (!x) return HHT_EINVAL;
+    if (n_total < 0) return set_err(x, HHT_EINVAL, "n < 0");
+    if (n_total > 0 && !points) return set_err(x, HHT_EINVAL, "points is NULL");
+    if (((uintptr_t)points & 7) != 0) return set_err(x, HHT_EINVAL, "points must be 8-byte aligned");
+    if (N < 1 || N > 65536) return set_err(x, HHT_EINVAL, "N must be in [1, 65536] (16-bit packed coordinates)");
+    if (D < 1 || D > 30) return set_err(x, HHT_EINVAL, "depth must be in [1, 30]");
+    if (T < 1) return set_err(x, HHT_EINVAL, "threshold must be >= 1");
+    if (x->opts.halves == 0 || (x->opts.halves & ~3u)) return set_err(x, HHT_EINVAL, "bad halves");
+    // |G| < 5 N 2^D must fit the signed width
+    const long double mag = 5.0L * (long double)N * (long double)(1ull << D);
+    if (mag >= 4.6e18L) return set_err(x, HHT_EOVERFLOW, "5*N*2^depth >= 2^62: exact int64 arithmetic impossible");
+    if (n_total > 0xFFFFFFFFll) return set_err(x, HHT_EINVAL, "more than 2^32-1 points per rank");
+    return HHT_OK;
+}
+
+hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets, int32_t B, int32_t N,
+                       int32_t D, int64_t T) {
+    if (!x) return HHT_EINVAL;
+    x->err.clear();
+    x->have = false;
+    if (B < 1 || !offsets) return set_err(x, HHT_EINVAL, "need B >= 1 images and host offsets");
+    if (offsets[0] != 0) return set_err(x, HHT_EINVAL, "offsets[0] must be 0");
+    for (int b = 0; b < B; ++b)
+        if (offsets[b + 1] < offsets[b]) return set_err(x, HHT_EINVAL, "offsets must be non-decreasing");
+    const int64_t n = offsets[B];
+    TRY(check_args(x, points, n, N, D, T));
+
+    x->N = N;
+    x->D = D;
+    x->T = (uint64_t)T;
+    x->B = B;
+    x->H = (x->opts.halves & HHT_ALPHA ? 1 : 0) + (x->opts.halves & HHT_BETA ? 1 : 0);
+    x->ntrees = B * x->H;
+    x->int64 = x->opts.force_int64 || !(5.0L * N * (long double)(1ull << D) < 2147483647.0L);
+    memset(&x->stat, 0, sizeof x->stat);
+    memset(&x->prof, 0, sizeof x->prof);
+    x->pev_used = 0;
+    x->stat.levels = D + 1;
+    x->stat.int_bits = x->int64 ? 64 : 32;
+    x->stat.images = B;
+    for (int l = 0; l < 64; ++l) {
+        x->rec[l].n = 0;
+        x->rec_host_ok[l] = false;
+    }
+    x->leaves.n = 0;
+    x->leaves_host_ok = false;
+    if ((int)x->lv.size() < D + 1) x->lv.resize(D + 1);
+    for (auto& L : x->lv) {
+        L.F = 0;
+        L.S = L.C = 0;
+        L.list = nullptr;
+    }
+
+    CK(cudaSetDevice(x->opts.device));
+    CK(cudaEventRecord(x->ev0, x->st));
+
+    // trees and per-tree point counts (global over ranks)
+    x->tree_half.assign(x->ntrees, 0);
+    std::vector<int64_t> local_n(B);
+    for (int b = 0; b < B; ++b) local_n[b] = offsets[b + 1] - offsets[b];
+    {
+        int t = 0;
+        for (int b = 0; b < B; ++b)
+            for (uint32_t h : {HHT_ALPHA, HHT_BETA})
+                if (x->opts.halves & h) x->tree_half[t++] = (uint8_t)h;
+    }
+    std::vector<int64_t> global_n = local_n;
+    if (x->opts.world > 1) {
+        // argument agreement: min and max of (N, D, T, halves, B) must coincide
+        int64_t prm[5] = {N, D, T, (int64_t)x->opts.halves, B};
+        TRY(ensure(x, x->vtmp, std::max<size_t>(8 * 10, 8 * (size_t)B)));
+        CK(cudaMemcpyAsync(x->vtmp.p, prm, sizeof prm, cudaMemcpyHostToDevice, x->st));
+        CK(cudaMemcpyAsync((char*)x->vtmp.p + 40, prm, sizeof prm, cudaMemcpyHostToDevice, x->st));
+        CKN(ncclAllReduce(x->vtmp.p, x->vtmp.p, 5, ncclInt64, ncclMin, x->comm, x->st));
+        CKN(ncclAllReduce((char*)x->vtmp.p + 40, (char*)x->vtmp.p + 40, 5, ncclInt64, ncclMax, x->comm, x->st));
+        int64_t got[10];
+        CK(cudaMemcpyAsync(got, x->vtmp.p, sizeof got, cudaMemcpyDeviceToHost, x->st));
+        TRY(sync(x));
+        for (int i = 0; i < 5; ++i)
+            if (got[i] != got[5 + i]) return set_err(x, HHT_EMISMATCH, "ranks disagree on (N, depth, threshold, halves, images)");
+        CK(cudaMemcpyAsync(x->vtmp.p, local_n.data(), 8 * (size_t)B, cudaMemcpyHostToDevice, x->st));
+        CKN(ncclAllReduce(x->vtmp.p, x->vtmp.p, B, ncclInt64, ncclSum, x->comm, x->st));
+        CK(cudaMemcpyAsync(global_n.data(), x->vtmp.p, 8 * (size_t)B, cudaMemcpyDeviceToHost, x->st));
+        TRY(sync(x));
+    }
+    x->tree_E.assign(x->ntrees, 0);
+    for (int t = 0; t < x->ntrees; ++t) x->tree_E[t] = global_n[t / x->H];
+
+    // K0: stage + validate (reject before any traversal; collective over ranks)
+    TRY(ensure(x, x->packed, std::max<int64_t>(n, 1) * 4));
+    CK(cudaMemsetAsync(x->errflag.p, 0, 4, x->st));
+    if (n > 0) {
+        const int32_t* dev_pts = points;
+        cudaPointerAttributes pa{};
+        cudaError_t e = cudaPointerGetAttributes(&pa, points);
+        if (e != cudaSuccess) cudaGetLastError();
+        const bool on_device = e == cudaSuccess && (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
+        if (!on_device) {
+            TRY(ensure(x, x->stage_in, (size_t)n * 8));
+            CK(cudaMemcpyAsync(x->stage_in.p, points, (size_t)n * 8, cudaMemcpyHostToDevice, x->st));
+            x->stat.h2d_bytes += (uint64_t)n * 8;
+            dev_pts = (const int32_t*)x->stage_in.p;
+        }
+        const int id = prof_begin(x, 0, (uint64_t)n * 12);
+        CK(launch_stage(dev_pts, (uint64_t)n, N, (uint32_t*)x->packed.p, (uint32_t*)x->errflag.p, x->st));
+        prof_end(x, id);
+    }
+    if (x->opts.world > 1)
+        CKN(ncclAllReduce(x->errflag.p, x->errflag.p, 1, ncclUint32, ncclMax, x->comm, x->st));
+    CK(cudaMemcpyAsync(x->misc_h, x->errflag.p, 4, cudaMemcpyDeviceToHost, x->st));
+    TRY(sync(x));
+    if ((uint32_t)(x->misc_h[0] & 0xFFFFFFFFu)) return set_err(x, HHT_ERANGE, "a point lies outside [0, N)^2");
+
+    // stats accumulators
+    CK(cudaMemsetAsync(x->stats.p, 0, kStatCount * 8, x->st));
+    std::vector<uint8_t> beta(x->ntrees);
+    for (int t = 0; t < x->ntrees; ++t) beta[t] = x->tree_half[t] == HHT_BETA;
+    TRY(ensure(x, x->beta, x->ntrees));
+    CK(cudaMemcpyAsync(x->beta.p, beta.data(), x->ntrees, cudaMemcpyHostToDevice, x->st));
+
+    // level 0: every tree's root ("each line ... passes through this region")
+    uint64_t root_votes = 0, root_tests = 0, root_split = 0;
+    std::vector<Record> r0rec;
+    std::vector<uint32_t> h_tree, h_zero, h_len;
+    std::vector<uint64_t> h_off, h_choff;
+    uint64_t chunks = 0, pairs0 = 0;
+    for (int t = 0; t < x->ntrees; ++t) {
+        const int b = t / x->H;
+        const uint64_t E = (uint64_t)x->tree_E[t];
+        r0rec.push_back({(uint32_t)t, 0, 0, (uint32_t)E});
+        root_votes += E;
+        root_tests += E;
+        if (E > x->T) {                 // R6: the uniform split rule also applies at the root
+            root_split++;
+            root_tests += 4 * E;
+            h_tree.push_back(t);
+            h_zero.push_back(0);
+            const uint64_t ln = (uint64_t)local_n[b];
+            h_len.push_back((uint32_t)ln);
+            h_off.push_back((uint64_t)offsets[b]);
+            h_choff.push_back(chunks);
+            chunks += (ln + kChunk - 1) / kChunk;
+            pairs0 += ln;
+        }
+    }
+    const uint32_t F0 = (uint32_t)h_tree.size();
+    h_off.push_back((uint64_t)n);
+    h_choff.push_back(chunks);
+    x->stat.visited[0] = x->ntrees;
+    x->stat.split[0] = root_split;
+    if (x->opts.record_levels) {
+        TRY(grow(x, x->rec[0], sizeof(Record), x->ntrees));
+        CK(cudaMemcpyAsync(x->rec[0].b.p, r0rec.data(), r0rec.size() * sizeof(Record), cudaMemcpyHostToDevice, x->st));
+        x->rec[0].n = x->ntrees;
+    }
+    Level& L0 = x->lv[0];
+    L0.F = F0;
+    L0.S = pairs0;
+    L0.C = chunks;
+    L0.list = (const uint32_t*)x->packed.p;
+    L0.list_base = 0;
+    if (F0 > 0) {
+        TRY(ensure(x, L0.tree, F0 * 4ull));
+        TRY(ensure(x, L0.a, F0 * 4ull));
+        TRY(ensure(x, L0.c, F0 * 4ull));
+        TRY(ensure(x, L0.parent, F0 * 4ull));
+        TRY(ensure(x, L0.len, F0 * 4ull));
+        TRY(ensure(x, L0.off, (F0 + 1) * 8ull));
+        TRY(ensure(x, L0.choff, (F0 + 1) * 8ull));
+        TRY(ensure(x, L0.chunk_region, std::max<uint64_t>(chunks, 1) * 4));
+        CK(cudaMemcpyAsync(L0.tree.p, h_tree.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
+        CK(cudaMemcpyAsync(L0.a.p, h_zero.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
+        CK(cudaMemcpyAsync(L0.c.p, h_zero.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
+        CK(cudaMemcpyAsync(L0.parent.p, h_tree.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
+        CK(cudaMemcpyAsync(L0.len.p, h_len.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
+        CK(cudaMemcpyAsync(L0.off.p, h_off.data(), (F0 + 1) * 8ull, cudaMemcpyHostToDevice, x->st));
+        CK(cudaMemcpyAsync(L0.choff.p, h_choff.data(), (F0 + 1) * 8ull, cudaMemcpyHostToDevice, x->st));
+        CK(launch_chunk_map((const uint64_t*)L0.choff.p, F0, (uint32_t*)L0.chunk_region.p, x->st));
+        const uint64_t cb[2] = {0, chunks};
+        CK(cudaMemcpyAsync(x->bounds.p, cb, sizeof cb, cudaMemcpyHostToDevice, x->st));
+        TRY(ensure(x, L0.votes, 16ull * F0));
+        CK(cudaMemsetAsync(L0.votes.p, 0, 16ull * F0, x->st));
+        PassArgs a = pass_args(x, L0, 0);
+        a.votes = (uint32_t*)L0.votes.p;
+        a.nf_rbase = 0;
+        TRY(run_pass(x, MODE_COUNT, a, pairs0, 0));
+        const uint32_t* VL = (const uint32_t*)L0.votes.p;
+        if (x->opts.world > 1) {
+            TRY(ensure(x, L0.votes_local, 16ull * F0));
+            CK(cudaMemcpyAsync(L0.votes_local.p, L0.votes.p, 16ull * F0, cudaMemcpyDeviceToDevice, x->st));
+            VL = (const uint32_t*)L0.votes_local.p;
+            TRY(allreduce_sum_u32(x, (uint32_t*)L0.votes.p, 4ull * F0));
+        }
+        TRY(do_split(x, 1, L0, 0, F0, (const uint32_t*)L0.votes.p, VL));
+        TRY(descend(x, 0, 0, F0));
+    }
+
+    // stats
+    uint64_t st[kStatCount];
+    CK(cudaMemcpyAsync(st, x->stats.p, sizeof st, cudaMemcpyDeviceToHost, x->st));
+    CK(cudaEventRecord(x->ev1, x->st));
+    TRY(sync(x));
+    x->stat.tests = root_tests + st[kStatTests];
+    x->stat.votes = root_votes + st[kStatVotes];
+    x->stat.leaves = st[kStatLeaves];
+    for (int l = 1; l <= D && l < 64; ++l) {
+        x->stat.visited[l] = st[kStatVisited0 + l];
+        x->stat.split[l] = st[kStatSplit0 + l];
+    }
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, x->ev0, x->ev1));
+    x->stat.ms = ms;
+    if (x->opts.profile) {
+        for (size_t i = 0; i < x->pev_used; ++i) {
+            float m = 0;
+            if (cudaEventElapsedTime(&m, x->pev[i].a, x->pev[i].b) == cudaSuccess) {
+                x->prof.ms[x->pev[i].cls] += m;
+                x->prof.launches[x->pev[i].cls] += 1;
+                x->prof.bytes[x->pev[i].cls] += x->pev[i].bytes;
+            }
+        }
+    }
+    x->have = true;
+    return HHT_OK;
+}
+
+hht_status host_records(hht_ctx* x, int level) {
+    if (x->rec_host_ok[level]) return HHT_OK;
+    x->rec_host[level].resize(x->rec[level].n);
+    if (x->rec[level].n)
+        CK(cudaMemcpyAsync(x->rec_host[level].data(), x->rec[level].b.p, x->rec[level].n * sizeof(Record),
+                           cudaMemcpyDeviceToHost, x->st));
+    TRY(sync(x));
+    x->rec_host_ok[level] = true;
+    return HHT_OK;
+}
+
+hht_status host_leaves(hht_ctx* x) {
+    if (x->leaves_host_ok) return HHT_OK;
+    x->leaves_host.resize(x->leaves.n);
+    if (x->leaves.n)
+        CK(cudaMemcpyAsync(x->leaves_host.data(), x->leaves.b.p, x->leaves.n * sizeof(LeafRec),
+                           cudaMemcpyDeviceToHost, x->st));
+    TRY(sync(x));
+    x->stat.d2h_bytes += x->leaves.n * sizeof(LeafRec);
+    x->leaves_host_ok = true;
+    return HHT_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+extern "C" {
+
+const char* hht_version(void) { return "hht 0.1.0 sm_100a"; }
+
+const char* hht_status_str(hht_status s) {
+    switch (s) {
+        case HHT_OK: return "HHT_OK";
+        case HHT_EINVAL: return "HHT_EINVAL";
+        case HHT_ERANGE: return "HHT_ERANGE";
+        case HHT_EOVERFLOW: return "HHT_EOVERFLOW";
+        case HHT_ENOMEM: return "HHT_ENOMEM";
+        case HHT_ECUDA: return "HHT_ECUDA";
+        case HHT_ENCCL: return "HHT_ENCCL";
+        case HHT_EMISMATCH: return "HHT_EMISMATCH";
+        case HHT_ESTATE: return "HHT_ESTATE";
+    }
+    return "HHT_UNKNOWN";
+}
+
+hht_status hht_default_opts(hht_opts* o) {
+    if (!o) return HHT_EINVAL;
+    memset(o, 0, sizeof *o);
+    o->device = 0;
+    o->rank = 0;
+    o->world = 1;
+    o->halves = HHT_ALPHA | HHT_BETA;
+    o->record_levels = 1;
+    return HHT_OK;
+}
+
+hht_status hht_nccl_unique_id(void* out, size_t cap) {
+    if (!out || cap < sizeof(ncclUniqueId)) return HHT_EINVAL;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return HHT_ENCCL;
+    memcpy(out, &id, sizeof id);
+    return HHT_OK;
+}
+
+hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
+    if (!out) return HHT_EINVAL;
+    *out = nullptr;
+    hht_opts o;
+    if (opts) o = *opts; else hht_default_opts(&o);
+    if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return HHT_EINVAL;
+    if (o.world > 1 && !o.nccl_id) return HHT_EINVAL;
+    if (o.halves == 0 || (o.halves & ~3u)) return HHT_EINVAL;
+    hht_ctx* x = new (std::nothrow) hht_ctx();
+    if (!x) return HHT_ENOMEM;
+    x->opts = o;
+    auto fail = [&](hht_status s) {
+        hht_destroy(x);
+        return s;
+    };
+    if (cudaSetDevice(o.device) != cudaSuccess) { cudaGetLastError(); return fail(HHT_ECUDA); }
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, o.device) != cudaSuccess) return fail(HHT_ECUDA);
+    x->sms = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&x->st, cudaStreamNonBlocking) != cudaSuccess) return fail(HHT_ECUDA);
+    if (cudaEventCreate(&x->ev0) != cudaSuccess || cudaEventCreate(&x->ev1) != cudaSuccess ||
+        cudaEventCreate(&x->tb0) != cudaSuccess || cudaEventCreate(&x->tb1) != cudaSuccess)
+        return fail(HHT_ECUDA);
+    // keep freed pool memory cached across calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, o.device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    for (int m = 0; m < 3; ++m)
+        for (int w = 0; w < 2; ++w) x->grid[m][w] = x->sms * pass_blocks_per_sm(m, w == 1);
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return fail(HHT_ECUDA);
+    x->budget = o.mem_budget ? o.mem_budget : (size_t)(0.70 * (double)fr);
+    if (ensure(x, x->errflag, 256) || ensure(x, x->stats, kStatCount * 8) || ensure(x, x->tilectr, 256) ||
+        ensure(x, x->totals, 256) || ensure(x, x->rng, 256) || ensure(x, x->bounds, 256) ||
+        ensure(x, x->vtmp, 256))
+        return fail(HHT_ENOMEM);
+    if (cudaMallocHost((void**)&x->totals_h, sizeof(Totals)) != cudaSuccess ||
+        cudaMallocHost((void**)&x->range_h, sizeof(RangeInfo)) != cudaSuccess ||
+        cudaMallocHost((void**)&x->misc_h, 64) != cudaSuccess)
+        return fail(HHT_ECUDA);
+    if (o.world > 1) {
+        ncclUniqueId id;
+        memcpy(&id, o.nccl_id, sizeof id);
+        if (ncclCommInitRank(&x->comm, o.world, id, o.rank) != ncclSuccess) return fail(HHT_ENCCL);
+    }
+    if (cudaStreamSynchronize(x->st) != cudaSuccess) return fail(HHT_ECUDA);
+    *out = x;
+    return HHT_OK;
+}
+
+hht_status hht_detect(hht_ctx* ctx, const int32_t* points, int64_t n, int32_t N, int32_t depth, int64_t threshold) {
+    if (!ctx) return HHT_EINVAL;
+    if (n < 0) return set_err(ctx, HHT_EINVAL, "n < 0");
+    const int64_t off[2] = {0, n};
+    return detect_impl(ctx, points, off, 1, N, depth, threshold);
+}
+
+hht_status hht_detect_batch(hht_ctx* ctx, const int32_t* points, const int64_t* offsets, int32_t B, int32_t N,
+                            int32_t depth, int64_t threshold) {
+    if (!ctx) return HHT_EINVAL;
+    return detect_impl(ctx, points, offsets, B, N, depth, threshold);
+}
+
+hht_status hht_result_leaves(hht_ctx* x, int32_t image, hht_leaf* out, int64_t cap, int64_t* count) {
+    if (!x || !count) return HHT_EINVAL;
+    if (!x->have) return set_err(x, HHT_ESTATE, "no successful detect yet");
+    if (image < -1 || image >= x->B) return set_err(x, HHT_EINVAL, "image out of range");
+    TRY(host_leaves(x));
+    const auto& L = x->leaves_host;
+    uint64_t b = 0, e = L.size();
+    if (image >= 0) {
+        const uint32_t t0 = (uint32_t)image * x->H, t1 = t0 + x->H;
+        b = std::lower_bound(L.begin(), L.end(), t0, [](const LeafRec& r, uint32_t t) { return r.tree < t; }) - L.begin();
+        e = std::lower_bound(L.begin(), L.end(), t1, [](const LeafRec& r, uint32_t t) { return r.tree < t; }) - L.begin();
+    }
+    *count = (int64_t)(e - b);
+    if (cap < *count) return set_err(x, HHT_EINVAL, "cap %lld < %lld leaves", (long long)cap, (long long)*count);
+    if (!*count) return HHT_OK;
+    if (!out) return set_err(x, HHT_EINVAL, "out is NULL");
+    std::vector<hht_leaf> tmp(e - b);
+    for (uint64_t k = b; k < e; ++k) {
+        const LeafRec& r = L[k];
+        tmp[k - b] = {(int32_t)(r.tree / x->H), x->tree_half[r.tree], r.i, r.j, r.votes};
+    }
+    CK(cudaMemcpy(out, tmp.data(), tmp.size() * sizeof(hht_leaf), cudaMemcpyDefault));
+    return HHT_OK;
+}
+
+hht_status hht_result_level(hht_ctx* x, int32_t image, uint32_t half, int32_t level, uint32_t* out, int64_t cap,
+                            int64_t* count) {
+    if (!x || !count) return HHT_EINVAL;
+    if (!x->have) return set_err(x, HHT_ESTATE, "no successful detect yet");
+    if (!x->opts.record_levels) return set_err(x, HHT_ESTATE, "record_levels is off");
+    if (image < 0 || image >= x->B) return set_err(x, HHT_EINVAL, "image out of range");
+    if (level < 0 || level > x->D) return set_err(x, HHT_EINVAL, "level out of range");
+    if (!(half == HHT_ALPHA || half == HHT_BETA) || !(x->opts.halves & half)) return set_err(x, HHT_EINVAL, "half not computed");
+    const uint32_t t = (uint32_t)image * x->H + ((half == HHT_BETA && (x->opts.halves & HHT_ALPHA)) ? 1 : 0);
+    TRY(host_records(x, level));
+    const auto& R = x->rec_host[level];
+    const auto lo = std::lower_bound(R.begin(), R.end(), t, [](const Record& r, uint32_t v) { return r.tree < v; });
+    const auto hi = std::lower_bound(R.begin(), R.end(), t + 1, [](const Record& r, uint32_t v) { return r.tree < v; });
+    *count = (int64_t)(hi - lo);
+    if (cap < *count) return set_err(x, HHT_EINVAL, "cap %lld < %lld records", (long long)cap, (long long)*count);
+    if (!*count) return HHT_OK;
+    if (!out) return set_err(x, HHT_EINVAL, "out is NULL");
+    std::vector<uint32_t> tmp(3 * (size_t)*count);
+    size_t k = 0;
+    for (auto it = lo; it != hi; ++it) {
+        tmp[k++] = it->a;
+        tmp[k++] = it->c;
+        tmp[k++] = it->votes;
+    }
+    CK(cudaMemcpy(out, tmp.data(), tmp.size() * 4, cudaMemcpyDefault));
+    return HHT_OK;
+}
+
+hht_status hht_result_stats(hht_ctx* x, hht_stats* out) {
+    if (!x || !out) return HHT_EINVAL;
+    if (!x->have) return set_err(x, HHT_ESTATE, "no successful detect yet");
+    *out = x->stat;
+    return HHT_OK;
+}
+
+hht_status hht_result_profile(hht_ctx* x, hht_profile* out) {
+    if (!x || !out) return HHT_EINVAL;
+    if (!x->have) return set_err(x, HHT_ESTATE, "no successful detect yet");
+    *out = x->prof;
+    return HHT_OK;
+}
+
+hht_status hht_timer_begin(hht_ctx* x) {
+    if (!x) return HHT_EINVAL;
+    CK(cudaEventRecord(x->tb0, x->st));
+    return HHT_OK;
+}
+
+hht_status hht_timer_end(hht_ctx* x, double* ms) {
+    if (!x || !ms) return HHT_EINVAL;
+    CK(cudaEventRecord(x->tb1, x->st));
+    CK(cudaEventSynchronize(x->tb1));
+    float m = 0;
+    CK(cudaEventElapsedTime(&m, x->tb0, x->tb1));
+    *ms = m;
+    return HHT_OK;
+}
+
+const char* hht_last_error(const hht_ctx* x) { return x ? x->err.c_str() : "null context"; }
+
+void hht_destroy(hht_ctx* x) {
+    if (!x) return;
+    if (x->st) cudaStreamSynchronize(x->st);
+    auto fr = [&](Buf& b) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+    };
+    for (auto& L : x->lv) {
+        for (Buf* b : {&L.tree, &L.a, &L.c, &L.parent, &L.len, &L.off, &L.choff, &L.chunk_region, &L.nf, &L.votes,
+                       &L.votes_local, &L.cursor, &L.list_own})
+            fr(*b);
+    }
+    for (auto& g : x->rec) fr(g.b);
+    fr(x->leaves.b);
+    for (Buf* b : {&x->stage_in, &x->packed, &x->errflag, &x->beta, &x->stats, &x->tiles, &x->tilectr, &x->totals,
+                   &x->rng, &x->bounds, &x->vtmp})
+        fr(*b);
+    if (x->totals_h) cudaFreeHost(x->totals_h);
+    if (x->range_h) cudaFreeHost(x->range_h);
+    if (x->misc_h) cudaFreeHost(x->misc_h);
+    for (auto& e : x->pev) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    for (cudaEvent_t e : {x->ev0, x->ev1, x->tb0, x->tb1})
+        if (e) cudaEventDestroy(e);
+    if (x->comm) ncclCommDestroy(x->comm);
+    if (x->st) cudaStreamDestroy(x->st);
+    delete x;
+}
+
+}  // extern "C"

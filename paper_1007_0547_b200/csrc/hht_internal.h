@@ -1,0 +1,130 @@
+// Internal interface between the level driver (hht_driver.cu) and the kernels (hht_kernels.cu).
+// Not part of the C ABI. Nothing here is shared with oracle/.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hht {
+
+constexpr int kWarp = 32;
+constexpr int kItems = 8;                  // list entries per lane per chunk
+constexpr int kChunk = kWarp * kItems;     // 256 entries: one warp work unit, never spans regions
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr int kSplitThreads = 256;         // split kernel: one thread per parent (its 4 children)
+
+// Quad order of the paper: q = 0 NE, 1 NW, 2 SW, 3 SE; child (2a+da, 2c+dc).
+__host__ __device__ constexpr uint32_t quad_da(int q) { return (q == 0 || q == 3) ? 1u : 0u; }
+__host__ __device__ constexpr uint32_t quad_dc(int q) { return (q <= 1) ? 1u : 0u; }
+
+// Frontier of split regions at one level, structure of arrays in HBM.
+struct Frontier {
+    uint32_t* tree;      // tree id (image * H + half index)
+    uint32_t* a;         // region column (m axis)
+    uint32_t* c;         // region row (b axis)
+    uint32_t* parent;    // index of the parent in the previous level's frontier
+    uint32_t* len;       // local candidate-list length (this rank's lines crossing the region)
+    uint64_t* off;       // [F+1] local list offset (exclusive scan of len); off[F] = total
+    uint64_t* choff;     // [F+1] chunk offset (exclusive scan of ceil(len/kChunk)); choff[F] = total
+    uint32_t* chunk_region;  // [total chunks] chunk -> region index
+};
+
+struct Record { uint32_t tree, a, c, votes; };     // one visited region
+struct LeafRec { uint32_t tree, i, j, votes; };     // one detected line
+
+// Look-back tile descriptor for the split scan (status: 0 none, 1 aggregate, 2 inclusive prefix).
+struct TileDesc {
+    uint32_t status;
+    uint32_t aggF, aggC, pad0;
+    uint64_t aggS;
+    uint32_t incF, incC;
+    uint64_t incS;
+};
+
+struct Totals {          // written by the last split tile
+    uint64_t F, S, C;
+};
+
+// Device-side stats accumulators (uint64): see kStat*.
+enum { kStatTests = 0, kStatVotes = 1, kStatLeaves = 2, kStatSplit0 = 8, kStatVisited0 = 8 + 64,
+       kStatCount = 8 + 128 };
+
+enum PassMode { MODE_COUNT = 0, MODE_WRITE = 1, MODE_COUNT2 = 2 };
+
+// Geometry of one pass over the lists of split regions at parent level l:
+//   g(p) = G(i0, j0) = ex*alpha + (ey << D) + beta,  alpha = 2^D - 2*i0,  beta = N*2^D - 3N*j0,
+//   child SW values g - {0,Pc} - {0,Qc}, Pc = ex << (D-l), Qc = 3N*2^(D-l-1); child votes iff
+//   0 < g_child <= Pc + Qc; grandchildren likewise with Pg = Pc/2, Qg = Qc/2.
+struct PassArgs {
+    // parent level
+    const uint32_t* list;          // packed (x << 16 | y) candidate lines of the parents
+    uint64_t list_base;            // subtract from p_off[r] to index `list`
+    const uint32_t* p_tree;
+    const uint32_t* p_a;
+    const uint32_t* p_c;
+    const uint32_t* p_len;
+    const uint64_t* p_off;
+    const uint64_t* p_choff;
+    const uint32_t* chunk_region;
+    const uint64_t* chunk_bounds;  // device [2]: chunk range [lo, hi) of this launch
+    const uint8_t* tree_beta;      // [trees] 1 = BETA tree (swap x and y)
+    int level;                     // parent level l
+    int D;
+    int N;
+    // children of the parents (level l+1)
+    const uint32_t* nf;            // [4 * nparents] child -> next-frontier index or kNone
+    uint32_t nf_rbase;             // parent index of nf[0..3]
+    uint32_t q0, q1;               // only next-frontier indices in [q0, q1) are written / counted
+    const uint64_t* c_off;         // next-frontier list offsets
+    uint64_t c_list_base;          // subtract from c_off[nf] to index c_list
+    uint32_t* c_cursor;            // [q1 - q0] append cursors
+    uint32_t* c_list;              // output lists
+    uint32_t* votes;               // MODE_COUNT: [4 * nparents] (4*(r - nf_rbase) + q)
+                                   // else:       [4 * (q1 - q0)] (4*(nf - q0) + q')
+};
+
+struct SplitArgs {
+    const uint32_t* V;             // [4 * Fp] global child votes
+    const uint32_t* VL;            // [4 * Fp] local child votes (list lengths on this rank)
+    uint32_t Fp;
+    const uint32_t* p_tree;        // parent arrays, already offset to the range start
+    const uint32_t* p_a;
+    const uint32_t* p_c;
+    uint32_t parent_base;          // global index of p_*[0]
+    int child_level;
+    int leaf_level;                // child_level == D: emit leaves, no frontier
+    int need_lists;                // child_level <= D-2: children will carry candidate lists
+    int record;
+    uint64_t T;
+    uint32_t* nf;                  // [4 * Fp]
+    Frontier out;
+    Record* rec;                   // records of child_level, rec[4*p + q]
+    LeafRec* leaves;               // leaves[leaf index]
+    TileDesc* tiles;
+    uint32_t* tile_counter;
+    unsigned long long* stats;
+    Totals* totals;
+    uint32_t ntiles;
+};
+
+// Range selection over a next frontier (one thread).
+struct RangeInfo {
+    uint64_t q1;                   // proposed / final end of range
+    uint64_t s_lo, s_hi;           // list offsets off[q0], off[q1]
+    uint64_t chunk_lo, chunk_hi;   // parents' chunk bounds (written into chunk_bounds too)
+    uint64_t pairs;                // parent entries streamed by this range's pass
+};
+
+// Launchers (hht_kernels.cu). All asynchronous on `st`.
+cudaError_t launch_stage(const int32_t* pts, uint64_t n, int N, uint32_t* packed, uint32_t* err,
+                         cudaStream_t st);
+cudaError_t launch_pass(int mode, bool int64, const PassArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_split(const SplitArgs& a, cudaStream_t st);
+cudaError_t launch_chunk_map(const uint64_t* choff, uint32_t F, uint32_t* chunk_region, cudaStream_t st);
+cudaError_t launch_range(const uint64_t* c_off, const uint32_t* c_parent, uint32_t Fc, uint32_t q0,
+                         uint64_t cap_entries, uint64_t forced_q1, const uint64_t* p_off,
+                         const uint64_t* p_choff, const uint32_t* p_len, int p_is_root, RangeInfo* info,
+                         uint64_t* chunk_bounds, cudaStream_t st);
+int pass_blocks_per_sm(int mode, bool int64);
+
+}  // namespace hht

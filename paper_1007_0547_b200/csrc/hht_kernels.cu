@@ -1,0 +1,572 @@
+// Device kernels of the level-synchronous hierarchical Hough pass (sm_100a).
+//
+// Paper: Singh & Bhatia, arXiv 1007.0547. What each kernel computes, in the paper's
+// terms, and the readings it rests on are in DESIGN.md §4; the oracle that checks it is oracle/
+// (shares nothing with this file).
+//
+// Integer formulation: for an effective point (ex, ey) (BETA swaps,
+// PAPER.md:67) and lattice corner (i, j) with m_i = -1 + 2i/2^D, b_j = -N + 3N*j/2^D,
+//     G(i, j) = 2^D*(ey - ex*m_i - b_j) = 2^D*(ex + ey + N) - 2*i*ex - 3N*j,
+// and the corner is below the line b = ey - ex*m (its getcode() bit is 1) iff G > 0.
+// Because 0 <= ex < N < 1.5N, every region satisfies G_SW >= G_SE > G_NW >= G_NE, so its code is
+// one of 0000, 0010, 0011, 0111, 1111 and "code != 0000 and != 1111" is exactly
+// G_SW > 0 >= G_NE, i.e. 0 < G_SW <= s*(2ex + 3N) for a region of side s. In unsigned arithmetic
+// that is the single compare (G_SW - 1) <u s*(2ex + 3N). The children of a region with SW value g
+// have SW values g - {0, Pc} - {0, Qc} (Pc = ex*s, Qc = 3N*s/2): the 9 lattice points of the
+// region (corners, edge midpoints, centre) decide the parent code and all four child codes.
+#include <cuda/atomic>
+
+#include "hht_internal.h"
+
+namespace hht {
+
+namespace {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+template <typename I> struct Unsigned;
+template <> struct Unsigned<int32_t> { using type = uint32_t; };
+template <> struct Unsigned<int64_t> { using type = uint64_t; };
+
+// 0 < v <= U  <=>  (v - 1) <u U  (v > -2^(bits-1) guaranteed by the width check).
+template <typename I>
+__device__ __forceinline__ bool crosses(I v_minus_1, I U) {
+    using UI = typename Unsigned<I>::type;
+    return (UI)v_minus_1 < (UI)U;
+}
+
+__device__ __forceinline__ uint32_t shfl_u32(uint32_t v, int src) { return __shfl_sync(kFull, v, src); }
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+    uint32_t lo = __shfl_sync(kFull, (uint32_t)v, src), hi = __shfl_sync(kFull, (uint32_t)(v >> 32), src);
+    return ((uint64_t)hi << 32) | lo;
+}
+
+// Warp sum of four byte counters packed in one word (each <= 255 per lane, sums < 2^16).
+// Returns counter `which` (0..3) of the warp total; all lanes must call.
+__device__ __forceinline__ void warp_sum_bytes(uint32_t acc, uint32_t& c02, uint32_t& c13) {
+    c02 = __reduce_add_sync(kFull, acc & 0x00FF00FFu);
+    c13 = __reduce_add_sync(kFull, (acc >> 8) & 0x00FF00FFu);
+}
+__device__ __forceinline__ uint32_t byte_counter(uint32_t c02, uint32_t c13, int which) {
+    return (((which & 1) ? c13 : c02) >> (16 * (which >> 1))) & 0xFFFFu;
+}
+
+// quad index of (da, dc): NE(1,1)=0, NW(0,1)=1, SW(0,0)=2, SE(1,0)=3
+__host__ __device__ constexpr int quad_of(int da, int dc) { return dc ? (da ? 0 : 1) : (da ? 3 : 2); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// K0: stage and validate (SPEC.md:310 rejects out-of-range points before any
+// traversal). Packs (x, y) into one word x << 16 | y; the BETA swap happens at use.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_stage(const int2* __restrict__ pts, uint64_t n, int N,
+                                               uint32_t* __restrict__ packed, uint32_t* __restrict__ err) {
+    uint32_t bad = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int2 p = __ldcs(pts + i);
+        const bool ok = (unsigned)p.x < (unsigned)N && (unsigned)p.y < (unsigned)N;
+        bad |= !ok;
+        packed[i] = ok ? (((uint32_t)p.x << 16) | (uint32_t)p.y) : 0u;
+    }
+    if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
+cudaError_t launch_stage(const int32_t* pts, uint64_t n, int N, uint32_t* packed, uint32_t* err,
+                         cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_stage<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const int2*>(pts), n, N, packed, err);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// K1/K4 fused: one pass over the candidate lists of the split regions at parent level l.
+//
+// One warp owns one chunk (<= 256 consecutive entries of ONE region's list; 8 per lane, loaded
+// coalesced with streaming hints). Per entry it evaluates the region's 9-point lattice signs in
+// the reduced form above and
+//   MODE_COUNT  : counts votes of the 4 children (used at the root, PAPER.md steps 1-5 / 12);
+//   MODE_WRITE  : appends the entry to the list of every SPLIT child it crosses (PAPER.md:100-103
+//                 "if the line passes through the parent region then decide about the child
+//                 regions") with warp-aggregated atomics, and counts the votes of the children of
+//                 those split children ("count-ahead": the next level's votes are produced while
+//                 the entry is in registers, so each list is read exactly once);
+//   MODE_COUNT2 : MODE_WRITE without the append (the children are at level D-1: their lists would
+//                 only be read to count the leaves, which this pass already does).
+// Votes are warp ballots / per-lane byte counters reduced with __reduce_add_sync and added with one
+// atomic per (warp chunk, region, quad): a segmented reduction whose segments are chunks.
+// ---------------------------------------------------------------------------------------------
+template <typename I, int MODE>
+__global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t c_lo = A.chunk_bounds[0], c_hi = A.chunk_bounds[1];
+    const int D = A.D;
+    const int sh = D - A.level;                       // log2 of the parent side s (>= 1)
+    const I N = (I)A.N;
+    const I Qc = ((I)3 * N) << (sh - 1);              // 3N * s/2: child b-step
+    const I Qg = (MODE == MODE_COUNT) ? (I)0 : (((I)3 * N) << (sh - 2));   // 3N * s/4 (sh >= 2)
+
+    for (uint64_t ch = c_lo + warp0; ch < c_hi; ch += nwarps) {
+        const uint32_t r = __ldg(A.chunk_region + ch);
+        const uint64_t k = ch - __ldg(A.p_choff + r);
+        const uint32_t len = __ldg(A.p_len + r);
+        const uint64_t e0 = __ldg(A.p_off + r) - A.list_base + k * kChunk;
+        const int cnt = (int)min((uint64_t)kChunk, (uint64_t)len - k * kChunk);
+        const uint32_t tree = __ldg(A.p_tree + r);
+        const bool beta = __ldg(A.tree_beta + tree) != 0;
+        const I i0 = (I)__ldg(A.p_a + r) << sh;
+        const I j0 = (I)__ldg(A.p_c + r) << sh;
+        const I alpha = ((I)1 << D) - 2 * i0;          // g = ex*alpha + (ey << D) + beta_c
+        const I beta_c = (N << D) - (I)3 * N * j0;
+
+        uint32_t nfq[4] = {kNone, kNone, kNone, kNone};
+        uint64_t cdst[4] = {0, 0, 0, 0};
+        if (MODE != MODE_COUNT) {
+            uint32_t my_nf = kNone;
+            uint64_t my_off = 0;
+            if (lane < 4) {
+                my_nf = __ldg(A.nf + 4 * (uint64_t)(r - A.nf_rbase) + lane);
+                if (my_nf != kNone && (my_nf < A.q0 || my_nf >= A.q1)) my_nf = kNone;
+                if (MODE == MODE_WRITE && my_nf != kNone) my_off = __ldg(A.c_off + my_nf) - A.c_list_base;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                nfq[q] = shfl_u32(my_nf, q);
+                if (MODE == MODE_WRITE) cdst[q] = shfl_u64(my_off, q);
+            }
+        }
+
+        uint32_t p[kItems];
+#pragma unroll
+        for (int it = 0; it < kItems; ++it) {
+            const int idx = lane + kWarp * it;
+            p[it] = (idx < cnt) ? __ldcs(A.list + e0 + idx) : 0u;
+        }
+
+        uint32_t cm = 0;            // 4 child bits per item, item it at bits [4it, 4it+4)
+        uint32_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int it = 0; it < kItems; ++it) {
+            const uint32_t w = p[it];
+            const bool valid = (lane + kWarp * it) < cnt;
+            const I ex = (I)(beta ? (w & 0xFFFFu) : (w >> 16));
+            const I ey = (I)(beta ? (w >> 16) : (w & 0xFFFFu));
+            const I gm1 = ex * alpha + (ey << D) + beta_c - 1;   // G(SW corner) - 1
+            const I Pc = ex << sh;                                // ex * s
+            const I Uc = Pc + Qc;
+            // child SW values: NE g-Pc-Qc, NW g-Qc, SW g, SE g-Pc
+            const uint32_t bNE = crosses<I>(gm1 - Pc - Qc, Uc);
+            const uint32_t bNW = crosses<I>(gm1 - Qc, Uc);
+            const uint32_t bSW = crosses<I>(gm1, Uc);
+            const uint32_t bSE = crosses<I>(gm1 - Pc, Uc);
+            const uint32_t m4 = valid ? (bNE | (bNW << 1) | (bSW << 2) | (bSE << 3)) : 0u;
+            cm |= m4 << (4 * it);
+            if (MODE == MODE_COUNT) {
+                acc[0] += (m4 & 1u) | ((m4 & 2u) << 7) | ((m4 & 4u) << 14) | ((m4 & 8u) << 21);
+            } else {
+                // Count-ahead: the 4x4 level-(l+2) cells (u, v), u along m, v along b, have SW value
+                // g - u*Pg - v*Qg. A line crossing a cell crosses its parent child (containment),
+                // so only the child's split flag (warp-uniform) gates the count.
+                const I Pg = Pc >> 1;
+                const I Ug = Pg + Qg;
+                if (valid) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const I hu = gm1 - (I)u * Pg;
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            const int q = quad_of(u >> 1, v >> 1);
+                            const int qq = quad_of(u & 1, v & 1);
+                            if (nfq[q] != kNone && crosses<I>(hu - (I)v * Qg, Ug)) acc[q] += 1u << (8 * qq);
+                        }
+                    }
+                }
+            }
+        }
+
+        if (MODE == MODE_COUNT) {
+            uint32_t c02, c13;
+            warp_sum_bytes(acc[0], c02, c13);
+            if (lane < 4) {
+                const uint32_t v = byte_counter(c02, c13, lane);
+                if (v) atomicAdd(A.votes + 4 * (uint64_t)(r - A.nf_rbase) + lane, v);
+            }
+            continue;
+        }
+
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (nfq[q] == kNone) continue;                  // warp-uniform
+            uint32_t c02, c13;
+            warp_sum_bytes(acc[q], c02, c13);
+            if (lane < 4) {
+                const uint32_t v = byte_counter(c02, c13, lane);
+                if (v) atomicAdd(A.votes + 4 * (uint64_t)(nfq[q] - A.q0) + lane, v);
+            }
+        }
+
+        if (MODE == MODE_WRITE) {
+            // child list compaction: one atomic per (chunk, split child) reserves a contiguous run,
+            // ballots give each lane its rank inside the run.
+            uint32_t tot[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t t = 0;
+#pragma unroll
+                for (int it = 0; it < kItems; ++it) t += __popc(__ballot_sync(kFull, (cm >> (4 * it + q)) & 1u));
+                tot[q] = (nfq[q] != kNone) ? t : 0u;
+            }
+            uint32_t my_base = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (lane == q && tot[q]) my_base = atomicAdd(A.c_cursor + (nfq[q] - A.q0), tot[q]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (!tot[q]) continue;                      // warp-uniform
+                const uint64_t dst = cdst[q] + shfl_u32(my_base, q);
+                uint32_t run = 0;
+#pragma unroll
+                for (int it = 0; it < kItems; ++it) {
+                    const bool on = (cm >> (4 * it + q)) & 1u;
+                    const uint32_t bal = __ballot_sync(kFull, on);
+                    if (on) A.c_list[dst + run + __popc(bal & lt_mask)] = p[it];
+                    run += __popc(bal);
+                }
+            }
+        }
+    }
+}
+
+template <typename I, int MODE>
+static int blocks_per_sm_impl() {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pass<I, MODE>, 256, 0);
+    return n > 0 ? n : 1;
+}
+
+int pass_blocks_per_sm(int mode, bool int64) {
+    if (int64) {
+        if (mode == MODE_COUNT) return blocks_per_sm_impl<int64_t, MODE_COUNT>();
+        if (mode == MODE_WRITE) return blocks_per_sm_impl<int64_t, MODE_WRITE>();
+        return blocks_per_sm_impl<int64_t, MODE_COUNT2>();
+    }
+    if (mode == MODE_COUNT) return blocks_per_sm_impl<int32_t, MODE_COUNT>();
+    if (mode == MODE_WRITE) return blocks_per_sm_impl<int32_t, MODE_WRITE>();
+    return blocks_per_sm_impl<int32_t, MODE_COUNT2>();
+}
+
+cudaError_t launch_pass(int mode, bool int64, const PassArgs& a, int grid, cudaStream_t st) {
+    if (int64) {
+        if (mode == MODE_COUNT) k_pass<int64_t, MODE_COUNT><<<grid, 256, 0, st>>>(a);
+        else if (mode == MODE_WRITE) k_pass<int64_t, MODE_WRITE><<<grid, 256, 0, st>>>(a);
+        else k_pass<int64_t, MODE_COUNT2><<<grid, 256, 0, st>>>(a);
+    } else {
+        if (mode == MODE_COUNT) k_pass<int32_t, MODE_COUNT><<<grid, 256, 0, st>>>(a);
+        else if (mode == MODE_WRITE) k_pass<int32_t, MODE_WRITE><<<grid, 256, 0, st>>>(a);
+        else k_pass<int32_t, MODE_COUNT2><<<grid, 256, 0, st>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// K3: threshold-and-split (PAPER.md:122-134 step 13: "if level.vote > THRESHOLD ... if level =
+// ceil(log2 N) then solution() else level <- level+1") for every child of a range of parents.
+// One thread per parent (its 4 children in quad order, a 16-byte vector load); a single-pass
+// decoupled look-back scan over (split count, local list entries, chunks) gives each split child
+// its next-frontier index, list offset and chunk offset in the paper's depth-first order (children
+// of a parent are consecutive, parents keep their order). Writes the (key, votes) record of every
+// child, the next frontier (SoA), and at the leaf level the detected lines.
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+struct Agg {
+    uint32_t F, C;
+    uint64_t S;
+};
+
+__device__ __forceinline__ Agg agg_add(Agg x, Agg y) { return {x.F + y.F, x.C + y.C, x.S + y.S}; }
+
+__device__ __forceinline__ Agg shfl_up_agg(Agg v, int d) {
+    Agg o;
+    o.F = __shfl_up_sync(kFull, v.F, d);
+    o.C = __shfl_up_sync(kFull, v.C, d);
+    o.S = __shfl_up_sync(kFull, v.S, d);
+    return o;
+}
+
+__device__ __forceinline__ Agg warp_inclusive(Agg v, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const Agg o = shfl_up_agg(v, d);
+        if (lane >= d) v = agg_add(v, o);
+    }
+    return v;
+}
+
+__device__ __forceinline__ Agg warp_total(Agg v) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        v.F += __shfl_xor_sync(kFull, v.F, d);
+        v.C += __shfl_xor_sync(kFull, v.C, d);
+        v.S += __shfl_xor_sync(kFull, v.S, d);
+    }
+    return v;
+}
+
+using dev_u32 = cuda::atomic_ref<uint32_t, cuda::thread_scope_device>;
+using dev_u64 = cuda::atomic_ref<uint64_t, cuda::thread_scope_device>;
+
+__device__ __forceinline__ void publish(TileDesc* t, Agg v, uint32_t status) {
+    if (status == 1) {
+        dev_u32(t->aggF).store(v.F, cuda::memory_order_relaxed);
+        dev_u32(t->aggC).store(v.C, cuda::memory_order_relaxed);
+        dev_u64(t->aggS).store(v.S, cuda::memory_order_relaxed);
+    } else {
+        dev_u32(t->incF).store(v.F, cuda::memory_order_relaxed);
+        dev_u32(t->incC).store(v.C, cuda::memory_order_relaxed);
+        dev_u64(t->incS).store(v.S, cuda::memory_order_relaxed);
+    }
+    dev_u32(t->status).store(status, cuda::memory_order_release);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
+    __shared__ Agg s_warp[kSplitThreads / 32];
+    __shared__ Agg s_prefix;
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_stat[3];    // votes, split-or-leaf count, 4 * split votes
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) {
+        s_tile = atomicAdd(A.tile_counter, 1u);   // dynamic tile order: predecessors are running
+        s_stat[0] = s_stat[1] = s_stat[2] = 0;
+    }
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint32_t p = tile * kSplitThreads + tid;
+    const bool valid = p < A.Fp;
+
+    uint4 V = make_uint4(0, 0, 0, 0), VL = V;
+    uint32_t tree = 0, pa = 0, pc = 0;
+    if (valid) {
+        V = __ldg(reinterpret_cast<const uint4*>(A.V) + p);
+        VL = (A.VL == A.V) ? V : __ldg(reinterpret_cast<const uint4*>(A.VL) + p);
+        tree = __ldg(A.p_tree + p);
+        pa = __ldg(A.p_a + p);
+        pc = __ldg(A.p_c + p);
+    }
+    const uint32_t v[4] = {V.x, V.y, V.z, V.w};
+    const uint32_t vl[4] = {VL.x, VL.y, VL.z, VL.w};
+    uint32_t flag[4], len[4], nch[4];
+    Agg mine = {0, 0, 0};
+    unsigned long long my_votes = 0, my_tests = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        flag[q] = (valid && (uint64_t)v[q] > A.T) ? 1u : 0u;          // strict: votes > THRESHOLD
+        len[q] = (flag[q] && A.need_lists) ? vl[q] : 0u;
+        nch[q] = (len[q] + kChunk - 1) / kChunk;
+        mine.F += flag[q];
+        mine.C += nch[q];
+        mine.S += len[q];
+        my_votes += v[q];
+        if (flag[q]) my_tests += 4ull * v[q];
+    }
+
+    // block scan
+    const Agg incl = warp_inclusive(mine, lane);
+    if (lane == 31) s_warp[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        Agg w = lane < kSplitThreads / 32 ? s_warp[lane] : Agg{0, 0, 0};
+        const Agg wi = warp_inclusive(w, lane);
+        if (lane < kSplitThreads / 32) s_warp[lane] = {wi.F - w.F, wi.C - w.C, wi.S - w.S};  // exclusive
+        const Agg block_total = {__shfl_sync(kFull, wi.F, 31), __shfl_sync(kFull, wi.C, 31), shfl_u64(wi.S, 31)};
+        // decoupled look-back (warp-wide window of 32 predecessors)
+        Agg excl = {0, 0, 0};
+        if (tile == 0) {
+            if (lane == 0) publish(A.tiles + 0, block_total, 2);
+        } else {
+            if (lane == 0) publish(A.tiles + tile, block_total, 1);
+            int64_t pred = (int64_t)tile - 1;
+            while (true) {
+                const int64_t t = pred - lane;
+                uint32_t st = 2;
+                Agg val = {0, 0, 0};
+                if (t >= 0) {
+                    TileDesc* d = A.tiles + t;
+                    do { st = dev_u32(d->status).load(cuda::memory_order_acquire); } while (st == 0);
+                    if (st == 1) {
+                        val = {dev_u32(d->aggF).load(cuda::memory_order_relaxed),
+                               dev_u32(d->aggC).load(cuda::memory_order_relaxed),
+                               dev_u64(d->aggS).load(cuda::memory_order_relaxed)};
+                    } else {
+                        val = {dev_u32(d->incF).load(cuda::memory_order_relaxed),
+                               dev_u32(d->incC).load(cuda::memory_order_relaxed),
+                               dev_u64(d->incS).load(cuda::memory_order_relaxed)};
+                    }
+                }
+                const uint32_t pm = __ballot_sync(kFull, st == 2);
+                const int stop = pm ? __ffs(pm) - 1 : 31;    // nearest predecessor with a prefix
+                if (lane > stop) val = {0, 0, 0};
+                excl = agg_add(excl, warp_total(val));
+                if (pm) break;
+                pred -= 32;
+            }
+            if (lane == 0) publish(A.tiles + tile, agg_add(excl, block_total), 2);
+        }
+        if (lane == 0) {
+            s_prefix = excl;
+            if (tile == A.ntiles - 1) {
+                const Agg tot = agg_add(excl, block_total);
+                A.totals->F = tot.F;
+                A.totals->S = tot.S;
+                A.totals->C = tot.C;
+                if (!A.leaf_level) {
+                    A.out.off[tot.F] = tot.S;
+                    A.out.choff[tot.F] = tot.C;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const Agg base = agg_add(agg_add(s_prefix, s_warp[wid]), Agg{incl.F - mine.F, incl.C - mine.C, incl.S - mine.S});
+
+    if (valid) {
+        uint32_t f = base.F, cc = base.C;
+        uint64_t s = base.S;
+        uint32_t nf4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t ca = 2 * pa + quad_da(q), cb = 2 * pc + quad_dc(q);
+            nf4[q] = kNone;
+            if (flag[q]) {
+                if (A.leaf_level) {
+                    A.leaves[f] = {tree, ca, cb, v[q]};
+                } else {
+                    nf4[q] = f;
+                    A.out.tree[f] = tree;
+                    A.out.a[f] = ca;
+                    A.out.c[f] = cb;
+                    A.out.parent[f] = A.parent_base + p;
+                    A.out.len[f] = len[q];
+                    A.out.off[f] = s;
+                    A.out.choff[f] = cc;
+                }
+                f += 1;
+                s += len[q];
+                cc += nch[q];
+            }
+            if (A.record) A.rec[4 * (uint64_t)p + q] = {tree, ca, cb, v[q]};
+        }
+        if (!A.leaf_level) reinterpret_cast<uint4*>(A.nf)[p] = make_uint4(nf4[0], nf4[1], nf4[2], nf4[3]);
+    }
+
+    // stats
+    unsigned long long sv = my_votes, sf = mine.F, stt = my_tests;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        sv += __shfl_xor_sync(kFull, sv, d);
+        sf += __shfl_xor_sync(kFull, sf, d);
+        stt += __shfl_xor_sync(kFull, stt, d);
+    }
+    if (lane == 0) {
+        atomicAdd(&s_stat[0], sv);
+        atomicAdd(&s_stat[1], sf);
+        atomicAdd(&s_stat[2], stt);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        atomicAdd(A.stats + kStatVotes, s_stat[0]);
+        if (A.leaf_level) {
+            atomicAdd(A.stats + kStatLeaves, s_stat[1]);
+        } else {
+            atomicAdd(A.stats + kStatSplit0 + A.child_level, s_stat[1]);
+            atomicAdd(A.stats + kStatTests, s_stat[2]);
+        }
+        const uint64_t nvalid = (A.Fp > tile * kSplitThreads) ? min((uint64_t)kSplitThreads, (uint64_t)A.Fp - tile * kSplitThreads) : 0;
+        atomicAdd(A.stats + kStatVisited0 + A.child_level, 4ull * nvalid);
+    }
+}
+
+cudaError_t launch_split(const SplitArgs& a, cudaStream_t st) {
+    if (a.ntiles == 0) return cudaSuccess;
+    k_split<<<a.ntiles, kSplitThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Chunk map: chunk -> region for a frontier (one warp per region).
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_chunk_map(const uint64_t* __restrict__ choff, uint32_t F,
+                                                   uint32_t* __restrict__ chunk_region) {
+    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= F) return;
+    const uint64_t b = choff[w], e = choff[w + 1];
+    for (uint64_t k = b + lane; k < e; k += 32) chunk_region[k] = (uint32_t)w;
+}
+
+cudaError_t launch_chunk_map(const uint64_t* choff, uint32_t F, uint32_t* chunk_region, cudaStream_t st) {
+    if (F == 0) return cudaSuccess;
+    const uint64_t blocks = ((uint64_t)F * 32 + 255) / 256;
+    k_chunk_map<<<(unsigned)blocks, 256, 0, st>>>(choff, F, chunk_region);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Range selection: largest q1 with off[q1] - off[q0] <= cap (at least q0+1), and the chunk range
+// of the parents of [q0, q1). One thread; binary search.
+// ---------------------------------------------------------------------------------------------
+__global__ void k_range(const uint64_t* c_off, const uint32_t* c_parent, uint32_t Fc, uint32_t q0,
+                        uint64_t cap, uint64_t forced_q1, const uint64_t* p_off, const uint64_t* p_choff,
+                        const uint32_t* p_len, int p_is_root, RangeInfo* info, uint64_t* chunk_bounds) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const uint64_t base = c_off[q0];
+    uint64_t q1;
+    if (forced_q1) {
+        q1 = forced_q1;
+    } else {
+        uint64_t lo = q0 + 1, hi = Fc;     // answer in [q0+1, Fc]
+        if (c_off[hi] - base <= cap) {
+            lo = hi;
+        } else {
+            while (lo < hi) {              // largest x in [lo, hi) with c_off[x] - base <= cap
+                const uint64_t mid = (lo + hi + 1) / 2;
+                if (c_off[mid] - base <= cap) lo = mid; else hi = mid - 1;
+            }
+        }
+        q1 = lo;
+    }
+    const uint32_t plo = c_parent[q0], phi = c_parent[q1 - 1];
+    info->q1 = q1;
+    info->s_lo = base;
+    info->s_hi = c_off[q1];
+    info->chunk_lo = p_choff[plo];
+    info->chunk_hi = p_choff[phi + 1];
+    if (p_is_root) {        // root lists alias the image slices: off[] is not a scan of len[]
+        uint64_t s = 0;
+        for (uint32_t r = plo; r <= phi; ++r) s += p_len[r];
+        info->pairs = s;
+    } else {
+        info->pairs = p_off[phi + 1] - p_off[plo];
+    }
+    chunk_bounds[0] = info->chunk_lo;
+    chunk_bounds[1] = info->chunk_hi;
+}
+
+cudaError_t launch_range(const uint64_t* c_off, const uint32_t* c_parent, uint32_t Fc, uint32_t q0,
+                         uint64_t cap_entries, uint64_t forced_q1, const uint64_t* p_off,
+                         const uint64_t* p_choff, const uint32_t* p_len, int p_is_root, RangeInfo* info,
+                         uint64_t* chunk_bounds, cudaStream_t st) {
+    k_range<<<1, 32, 0, st>>>(c_off, c_parent, Fc, q0, cap_entries, forced_q1, p_off, p_choff, p_len,
+                              p_is_root, info, chunk_bounds);
+    return cudaGetLastError();
+}
+
+}  // namespace hht

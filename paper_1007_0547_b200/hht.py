@@ -1,0 +1,243 @@
+"""Python binding of libhht.so (include/hht.h): argument marshalling only.
+
+Every step of the method runs in the library's CUDA kernels; this module converts arrays to
+pointers and results to numpy. There is no CPU fallback: if libhht.so is missing or fails to
+load, importing/using this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from fractions import Fraction
+from typing import Optional, Sequence
+
+import numpy as np
+
+ALPHA = 1
+BETA = 2
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libhht.so")
+
+STATUS = {0: "HHT_OK", 1: "HHT_EINVAL", 2: "HHT_ERANGE", 3: "HHT_EOVERFLOW", 4: "HHT_ENOMEM",
+          5: "HHT_ECUDA", 6: "HHT_ENCCL", 7: "HHT_EMISMATCH", 8: "HHT_ESTATE"}
+
+# names the header declares (tests check every one is exported)
+EXPORTS = ["hht_default_opts", "hht_create", "hht_nccl_unique_id", "hht_detect", "hht_detect_batch",
+           "hht_result_leaves", "hht_result_level", "hht_result_stats", "hht_result_profile",
+           "hht_timer_begin", "hht_timer_end", "hht_last_error", "hht_status_str", "hht_destroy",
+           "hht_version"]
+
+PROFILE_CLASSES = ["stage", "count", "write", "count2", "split", "chunk_map", "other", "allreduce"]
+
+
+class HHTError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class Opts(C.Structure):
+    _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("halves", C.c_uint32),
+                ("record_levels", C.c_uint32), ("force_int64", C.c_uint32), ("profile", C.c_uint32),
+                ("reserved", C.c_uint32), ("mem_budget", C.c_size_t), ("nccl_id", C.c_void_p)]
+
+
+class Leaf(C.Structure):
+    _fields_ = [("image", C.c_int32), ("half", C.c_uint32), ("i", C.c_uint32), ("j", C.c_uint32),
+                ("votes", C.c_uint32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("tests", C.c_uint64), ("votes", C.c_uint64), ("leaves", C.c_uint64), ("pairs", C.c_uint64),
+                ("visited", C.c_uint64 * 64), ("split", C.c_uint64 * 64), ("h2d_bytes", C.c_uint64),
+                ("d2h_bytes", C.c_uint64), ("levels", C.c_uint32), ("int_bits", C.c_uint32),
+                ("ranges", C.c_uint32), ("images", C.c_uint32), ("ms", C.c_double)]
+
+
+class Profile(C.Structure):
+    _fields_ = [("launches", C.c_uint64 * 8), ("ms", C.c_double * 8), ("bytes", C.c_uint64 * 8)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load libhht.so (raises if it is absent: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(path)
+    p, i32, i64, u32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32
+    sig = {
+        "hht_default_opts": ([p], C.c_int),
+        "hht_create": ([p, p], C.c_int),
+        "hht_nccl_unique_id": ([p, C.c_size_t], C.c_int),
+        "hht_detect": ([p, p, i64, i32, i32, i64], C.c_int),
+        "hht_detect_batch": ([p, p, p, i32, i32, i32, i64], C.c_int),
+        "hht_result_leaves": ([p, i32, p, i64, p], C.c_int),
+        "hht_result_level": ([p, i32, u32, i32, p, i64, p], C.c_int),
+        "hht_result_stats": ([p, p], C.c_int),
+        "hht_result_profile": ([p, p], C.c_int),
+        "hht_timer_begin": ([p], C.c_int),
+        "hht_timer_end": ([p, p], C.c_int),
+        "hht_last_error": ([p], C.c_char_p),
+        "hht_status_str": ([C.c_int], C.c_char_p),
+        "hht_destroy": ([p], None),
+        "hht_version": ([], C.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def version() -> str:
+    return load().hht_version().decode()
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = load().hht_nccl_unique_id(buf, 128)
+    if st:
+        raise HHTError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def leaf_bounds(i: int, j: int, N: int, D: int):
+    """Exact (m_lo, m_hi, b_lo, b_hi) of leaf (i, j): m_i = -1 + 2i/2^D, b_j = -N + 3N j/2^D
+    (include/hht.h conventions; SPEC.md:236-244 leaf_params)."""
+    side = 1 << D
+    m = lambda k: Fraction(-1) + Fraction(2 * k, side)  # noqa: E731
+    b = lambda k: Fraction(-N) + Fraction(3 * N * k, side)  # noqa: E731
+    return m(i), m(i + 1), b(j), b(j + 1)
+
+
+def _as_points(points):
+    """Return (pointer, n, keepalive, is_cuda) for int32 [n, 2] points (torch tensor or numpy)."""
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(points, torch.Tensor):
+        t = points
+        if t.dtype != torch.int32:
+            t = t.to(torch.int32)
+        t = t.reshape(-1, 2).contiguous()
+        if t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()   # producer work done before the library reads
+        return t.data_ptr(), t.shape[0], t, t.is_cuda
+    a = np.ascontiguousarray(np.asarray(points, dtype=np.int32).reshape(-1, 2))
+    return a.ctypes.data, a.shape[0], a, False
+
+
+class HHT:
+    """One libhht context (one device, one rank)."""
+
+    def __init__(self, device: int = 0, halves: int = ALPHA | BETA, record_levels: bool = True,
+                 force_int64: bool = False, profile: bool = False, mem_budget: int = 0,
+                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+        self._lib = load()
+        o = Opts()
+        self._lib.hht_default_opts(C.byref(o))
+        o.device, o.rank, o.world, o.halves = device, rank, world, halves
+        o.record_levels, o.force_int64, o.profile = int(record_levels), int(force_int64), int(profile)
+        o.mem_budget = mem_budget
+        self._id = None
+        if nccl_id is not None:
+            self._id = C.create_string_buffer(bytes(nccl_id), 128)
+            o.nccl_id = C.cast(self._id, C.c_void_p)
+        self._ctx = C.c_void_p()
+        st = self._lib.hht_create(C.byref(self._ctx), C.byref(o))
+        if st:
+            raise HHTError(st, "hht_create failed")
+        self.halves = halves
+        self.world = world
+
+    def _check(self, st: int):
+        if st:
+            raise HHTError(st, self._lib.hht_last_error(self._ctx).decode())
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self._lib.hht_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # --- compute -----------------------------------------------------------------------------
+    def detect(self, points, N: int, depth: int, threshold: int) -> "HHT":
+        ptr, n, keep, _ = _as_points(points)
+        self._check(self._lib.hht_detect(self._ctx, C.c_void_p(ptr), n, N, depth, threshold))
+        del keep
+        return self
+
+    def detect_batch(self, points, offsets: Sequence[int], N: int, depth: int, threshold: int) -> "HHT":
+        ptr, n, keep, _ = _as_points(points)
+        offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+        B = offs.shape[0] - 1
+        self._check(self._lib.hht_detect_batch(self._ctx, C.c_void_p(ptr), offs.ctypes.data, B, N, depth,
+                                               threshold))
+        del keep
+        return self
+
+    # --- results -------------------------------------------------------------------------------
+    def leaves(self, image: int = -1) -> np.ndarray:
+        """int64 [L, 5]: (image, half, i, j, votes) in image, half, depth-first order."""
+        cnt = C.c_int64(0)
+        st = self._lib.hht_result_leaves(self._ctx, image, None, 0, C.byref(cnt))
+        if st and cnt.value == 0:
+            self._check(st)
+        out = (Leaf * max(cnt.value, 1))()
+        self._check(self._lib.hht_result_leaves(self._ctx, image, out, cnt.value, C.byref(cnt)))
+        arr = np.frombuffer(out, dtype=np.uint32, count=5 * cnt.value).reshape(-1, 5).astype(np.int64)
+        return arr
+
+    def level(self, image: int, half: int, level: int) -> np.ndarray:
+        """uint32 [k, 3]: (a, c, votes) of the visited regions of one tree at one level."""
+        cnt = C.c_int64(0)
+        st = self._lib.hht_result_level(self._ctx, image, half, level, None, 0, C.byref(cnt))
+        if st and cnt.value == 0:
+            self._check(st)
+        out = np.zeros((max(cnt.value, 1), 3), dtype=np.uint32)
+        self._check(self._lib.hht_result_level(self._ctx, image, half, level, out.ctypes.data, cnt.value,
+                                               C.byref(cnt)))
+        return out[:cnt.value]
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._check(self._lib.hht_result_stats(self._ctx, C.byref(s)))
+        L = s.levels
+        return {"tests": s.tests, "votes": s.votes, "leaves": s.leaves, "pairs": s.pairs,
+                "visited": list(s.visited)[:L], "split": list(s.split)[:L], "h2d_bytes": s.h2d_bytes,
+                "d2h_bytes": s.d2h_bytes, "levels": L, "int_bits": s.int_bits, "ranges": s.ranges,
+                "images": s.images, "ms": s.ms}
+
+    def profile(self) -> dict:
+        p = Profile()
+        self._check(self._lib.hht_result_profile(self._ctx, C.byref(p)))
+        return {name: {"launches": p.launches[k], "ms": p.ms[k], "bytes": p.bytes[k]}
+                for k, name in enumerate(PROFILE_CLASSES)}
+
+    def timer_begin(self):
+        self._check(self._lib.hht_timer_begin(self._ctx))
+
+    def timer_end(self) -> float:
+        ms = C.c_double(0)
+        self._check(self._lib.hht_timer_end(self._ctx, C.byref(ms)))
+        return ms.value

@@ -1,0 +1,29 @@
+"""Run `--reps` detections of one config through the C ABI (for ncu / compute-sanitizer)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1007_0547_b200 import hht, synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=3)
+ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--images", type=int, default=None)
+ap.add_argument("--budget", type=int, default=0)
+a = ap.parse_args()
+cfg = synth.CONFIGS[a.config]
+if cfg.images > 1:
+    pts, offs = synth.config_batch(a.config, a.images)
+else:
+    pts, _ = synth.config_image(a.config)
+    offs = np.array([0, len(pts)])
+d = torch.from_numpy(pts).cuda()
+h = hht.HHT(halves=cfg.halves, mem_budget=a.budget)
+for _ in range(a.reps):
+    h.detect_batch(d, offs, cfg.N, cfg.D, cfg.T)
+st = h.stats()
+print({k: st[k] for k in ("tests", "votes", "leaves", "pairs", "ranges", "ms", "int_bits")})

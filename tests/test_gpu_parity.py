@@ -1,0 +1,212 @@
+"""GPU parity: libhht (CUDA, through the C ABI) vs the CPU oracle, element by element.
+
+Records of every level (a, c, votes), the leaf list, and the tests/votes statistics must be
+identical (integer work: bit-exact). Sizes span many 256-entry chunks and ragged
+tails; edge cases cover empty input, E <= T, identical points, D = 1/2, the int64 kernels,
+depth-first list ranges under a tiny memory budget, host-pointer input, batches with empty images,
+and the error paths."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1007_0547_b200 import hht, synth
+from tests.hht_compare import check_structure, compare_all
+
+pytestmark = pytest.mark.gpu
+
+AB = hht.ALPHA | hht.BETA
+
+
+@pytest.fixture(scope="module")
+def torch_dev(cuda_device):
+    return cuda_device
+
+
+def _dev(pts, dev):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(pts, dtype=np.int32)).to(dev)
+
+
+def _run(pts, N, D, T, halves, dev, **kw):
+    h = hht.HHT(halves=halves, **kw)
+    h.detect(_dev(pts, dev), N, D, T)
+    return h
+
+
+def test_survey_example(torch_dev):
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "survey_example_n8_d3_t2.json")))
+    pts = np.array(g["points"], dtype=np.int32)
+    h = _run(pts, 8, 3, 2, hht.ALPHA, torch_dev)
+    for lev, recs in g["levels"].items():
+        assert h.level(0, hht.ALPHA, int(lev)).tolist() == recs
+    assert h.leaves(0)[:, 2:].tolist() == g["leaves"]
+    st = h.stats()
+    assert st["votes"] == g["votes"] and st["tests"] == g["tests"]
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+def test_config_full_parity(cid, torch_dev):
+    cfg = synth.CONFIGS[cid]
+    pts, _ = synth.config_image(cid)
+    ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves)
+    h = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, torch_dev)
+    compare_all(h, ref, cfg.halves, cfg.D)
+    st = h.stats()
+    assert (st["tests"], st["votes"], st["leaves"]) == (ref.tests, ref.votes, ref.leaves.shape[0])
+    for half in (1, 2):
+        if cfg.halves & half:
+            for lev in range(cfg.D + 1):
+                pass
+    assert st["int_bits"] == 32
+
+
+@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("force64", [False, True])
+def test_random_scenes(seed, force64, torch_dev):
+    rng = np.random.default_rng(seed)
+    N = int(rng.choice([4, 7, 16, 33, 64, 128, 200]))
+    D = int(rng.integers(1, 9))
+    T = int(rng.choice([1, 2, 3, 8, 20]))
+    pts = synth.random_scene(1000 + seed, N, max_lines=4, max_noise=int(rng.choice([10, 300, 3000])))
+    ref = oracle.detect(pts, N, D, T, AB)
+    h = _run(pts, N, D, T, AB, torch_dev, force_int64=force64)
+    compare_all(h, ref, AB, D)
+    st = h.stats()
+    assert (st["tests"], st["votes"]) == (ref.tests, ref.votes)
+    assert st["int_bits"] == (64 if force64 else 32)
+
+
+def test_depth_beyond_log2n_int64(torch_dev):
+    """D > log2 N and 5*N*2^D > 2^31: the library switches to the int64 kernels by itself."""
+    pts = synth.random_scene(77, 100, max_lines=2, max_noise=50)
+    N, D, T = 100, 23, 10
+    ref = oracle.detect(pts, N, D, T, AB)
+    h = _run(pts, N, D, T, AB, torch_dev)
+    assert h.stats()["int_bits"] == 64
+    compare_all(h, ref, AB, D)
+
+
+def test_ranges_under_tiny_budget(torch_dev):
+    """A 256 KiB list budget forces many depth-first ranges; output must not change."""
+    cfg = synth.CONFIGS[2]
+    pts, _ = synth.config_image(2)
+    ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves)
+    h = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, torch_dev, mem_budget=256 << 10)
+    compare_all(h, ref, cfg.halves, cfg.D)
+    assert h.stats()["ranges"] > 4 * cfg.D
+
+
+def test_host_pointer_input(torch_dev):
+    cfg = synth.CONFIGS[1]
+    pts, _ = synth.config_image(1)
+    h = hht.HHT(halves=cfg.halves)
+    h.detect(pts, cfg.N, cfg.D, cfg.T)          # numpy (host) pointer: staged by the library
+    st = h.stats()
+    assert st["h2d_bytes"] == pts.nbytes
+    ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves)
+    compare_all(h, ref, cfg.halves, cfg.D)
+
+
+def test_batch_with_empty_and_ragged_images(torch_dev):
+    N, D, T = 64, 6, 6
+    imgs = [synth.random_scene(500 + k, N, max_lines=3, max_noise=k * 40) for k in range(6)]
+    imgs[2] = np.zeros((0, 2), dtype=np.int32)
+    imgs[4] = imgs[4][:3]
+    offs = np.zeros(len(imgs) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum([len(p) for p in imgs])
+    allp = np.concatenate(imgs).astype(np.int32)
+    h = hht.HHT(halves=AB)
+    h.detect_batch(_dev(allp, torch_dev), offs, N, D, T)
+    tests = votes = 0
+    for b, p in enumerate(imgs):
+        ref = oracle.detect(p, N, D, T, AB)
+        compare_all(h, ref, AB, D, image=b)
+        tests += ref.tests
+        votes += ref.votes
+    st = h.stats()
+    assert (st["tests"], st["votes"]) == (tests, votes)
+    allv = h.leaves(-1)
+    assert (np.diff(allv[:, 0]) >= 0).all()
+
+
+@pytest.mark.parametrize("case", ["empty", "below_threshold", "identical", "d1", "d2", "n1", "corner_touch"])
+def test_edge_cases(case, torch_dev):
+    N, D, T, halves = 16, 4, 2, AB
+    if case == "empty":
+        pts = np.zeros((0, 2), np.int32)
+    elif case == "below_threshold":
+        pts = np.array([[1, 2], [3, 4]], np.int32)
+    elif case == "identical":
+        pts = np.array([[5, 9]] * 300, np.int32)
+        T = 100
+    elif case == "d1":
+        pts = synth.random_scene(3, 16, max_noise=40)
+        D = 1
+    elif case == "d2":
+        pts = synth.random_scene(4, 16, max_noise=40)
+        D = 2
+    elif case == "n1":
+        pts = np.array([[0, 0]] * 5, np.int32)
+        N, D, T = 1, 3, 1
+    else:   # an NE-corner touch from below votes, an SW touch does not
+        pts = np.array([[4, 4]] * 3, np.int32)
+        N, D, T, halves = 8, 3, 1, hht.ALPHA
+    ref = oracle.detect(pts, N, D, T, halves)
+    h = _run(pts, N, D, T, halves, torch_dev)
+    compare_all(h, ref, halves, D)
+    if case == "corner_touch":
+        cells = {(int(i), int(j)) for _, _, i, j, _ in h.leaves(0).tolist()}
+        assert (3, 3) in cells and (4, 4) not in cells
+
+
+def test_errors(torch_dev):
+    h = hht.HHT(halves=AB)
+    bad = np.array([[0, 0], [16, 3]], np.int32)
+    with pytest.raises(hht.HHTError) as e:
+        h.detect(_dev(bad, torch_dev), 16, 4, 2)
+    assert e.value.name == "HHT_ERANGE"
+    ok = np.array([[0, 0]], np.int32)
+    for N, D, T in [(0, 4, 2), (16, 0, 2), (16, 4, 0), (70000, 4, 2), (16, 31, 2)]:
+        with pytest.raises(hht.HHTError) as e:
+            h.detect(_dev(ok, torch_dev), N, D, T)
+        assert e.value.name == "HHT_EINVAL"
+    with pytest.raises(hht.HHTError) as e:
+        h.level(0, hht.ALPHA, 0)          # no successful detect since the errors
+    assert e.value.name == "HHT_ESTATE"
+
+
+def test_records_off_still_emits_leaves(torch_dev):
+    cfg = synth.CONFIGS[2]
+    pts, _ = synth.config_image(2)
+    ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves)
+    h = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, torch_dev, record_levels=False)
+    assert np.array_equal(h.leaves(0)[:, 1:], ref.leaves.astype(np.int64))
+    with pytest.raises(hht.HHTError):
+        h.level(0, hht.ALPHA, 1)
+
+
+def test_repeat_calls_identical(torch_dev):
+    """Determinism across calls on one context (outputs are order-independent counts)."""
+    cfg = synth.CONFIGS[2]
+    pts, _ = synth.config_image(2)
+    h = hht.HHT(halves=cfg.halves)
+    d = _dev(pts, torch_dev)
+    h.detect(d, cfg.N, cfg.D, cfg.T)
+    a = [h.level(0, 2, l).copy() for l in range(cfg.D + 1)], h.leaves().copy()
+    h.detect(d, cfg.N, cfg.D, cfg.T)
+    b = [h.level(0, 2, l) for l in range(cfg.D + 1)], h.leaves()
+    assert all(np.array_equal(x, y) for x, y in zip(a[0], b[0])) and np.array_equal(a[1], b[1])
+
+
+def test_c2_structure_and_profile(torch_dev):
+    cfg = synth.CONFIGS[2]
+    pts, _ = synth.config_image(2)
+    h = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, torch_dev, profile=True)
+    for half in (1, 2):
+        levels = [h.level(0, half, l) for l in range(cfg.D + 1)]
+        check_structure(levels, pts.shape[0], cfg.T, cfg.D)
+    prof = h.profile()
+    assert prof["write"]["launches"] > 0 and prof["split"]["launches"] >= cfg.D
