@@ -68,7 +68,6 @@ struct hht_ctx {
     ncclComm_t comm = nullptr;
     std::string err;
     size_t budget = 0;
-    size_t list_used = 0;
     int grid[3][2] = {};
 
     // last call
@@ -364,10 +363,12 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
 
     uint32_t q0 = 0;
     while (q0 < Fc) {
-        // list budget left for this level: everything not held by the other levels' buffers
-        // (their capacities persist across ranges and calls, so steady state does no allocation)
-        const size_t others = x->list_used - C.list_own.cap;
-        const size_t avail = x->budget > others ? x->budget - others : 0;
+        // list budget left for this level: everything not held by the active ancestor levels.
+        // Buffer capacities persist across ranges and calls (steady state allocates nothing);
+        // idle deeper buffers are released only under budget pressure.
+        size_t active = 0;
+        for (int k = 1; k < lc; ++k) active += x->lv[k].list_own.cap;
+        const size_t avail = x->budget > active ? x->budget - active : 0;
         const uint64_t cap = (lc == x->D - 2 ? avail : avail / 3) / 4;
         RangeInfo ri{};
         TRY(choose_range(x, lc, q0, cap, false, &ri));
@@ -377,10 +378,12 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
             return set_err(x, HHT_ENOMEM, "level %d region list of %llu entries exceeds the list budget (%zu B free)",
                            lc, (unsigned long long)entries, avail);
         if (entries * 4 > C.list_own.cap) {
-            x->list_used -= C.list_own.cap;
+            size_t deeper = 0;
+            for (int k = lc + 1; k < (int)x->lv.size(); ++k) deeper += x->lv[k].list_own.cap;
+            if (active + entries * 4 + deeper > x->budget)
+                for (int k = lc + 1; k < (int)x->lv.size(); ++k) TRY(release(x, x->lv[k].list_own));
             TRY(release(x, C.list_own));
             TRY(ensure(x, C.list_own, std::max<uint64_t>(entries, 1) * 4, true));
-            x->list_used += C.list_own.cap;
         }
         C.list = (const uint32_t*)C.list_own.p;
         C.list_base = ri.s_lo;

@@ -99,10 +99,57 @@ cudaError_t launch_stage(const int32_t* pts, uint64_t n, int N, uint32_t* packed
 // Votes are warp ballots / per-lane byte counters reduced with __reduce_add_sync and added with one
 // atomic per (warp chunk, region, quad): a segmented reduction whose segments are chunks.
 // ---------------------------------------------------------------------------------------------
+// Per-entry arithmetic of one chunk (8 entries per lane). Invalid lanes (past the chunk's end) get
+// g - 1 = -1, which crosses nothing, so the body is branch-free.
+//   cm  : 4 child bits per item (MODE_COUNT / MODE_WRITE), item it at bits [4it, 4it+4)
+//   acc : MODE_COUNT: acc[0] byte q = votes of child q; else acc[q] byte q' = votes of grandchild
+//         q' of child q (count-ahead over the 4x4 level-(l+2) cells (u, v), SW value
+//         g - u*Pg - v*Qg; containment makes the child's own crossing implied).
+template <typename I, int MODE, bool BETA>
+__device__ __forceinline__ void chunk_math(const uint32_t (&p)[kItems], int cnt, int lane, I alpha, I beta_m1,
+                                           int D, int sh, I Qc, I Qg, uint32_t& cm, uint32_t (&acc)[4]) {
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+        const uint32_t w = p[it];
+        const I ex = (I)(BETA ? (w & 0xFFFFu) : (w >> 16));
+        const I ey = (I)(BETA ? (w >> 16) : (w & 0xFFFFu));
+        I gm1 = ex * alpha + (ey << D) + beta_m1;            // G(SW corner) - 1
+        if (lane + kWarp * it >= cnt) gm1 = (I)-1;
+        const I Pc = ex << sh;                                // ex * s
+        if (MODE != MODE_COUNT2) {
+            const I Uc = Pc + Qc;
+            // child SW values: NE g-Pc-Qc, NW g-Qc, SW g, SE g-Pc
+            const uint32_t bNE = crosses<I>(gm1 - Pc - Qc, Uc);
+            const uint32_t bNW = crosses<I>(gm1 - Qc, Uc);
+            const uint32_t bSW = crosses<I>(gm1, Uc);
+            const uint32_t bSE = crosses<I>(gm1 - Pc, Uc);
+            if (MODE == MODE_COUNT) {
+                acc[0] += bNE | (bNW << 8) | (bSW << 16) | (bSE << 24);
+            } else {
+                cm |= (bNE | (bNW << 1) | (bSW << 2) | (bSE << 3)) << (4 * it);
+            }
+        }
+        if (MODE != MODE_COUNT) {
+            const I Pg = Pc >> 1;
+            const I Ug = Pg + Qg;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const I hu = gm1 - (I)u * Pg;
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int q = quad_of(u >> 1, v >> 1);
+                    const int qq = quad_of(u & 1, v & 1);
+                    if (crosses<I>(hu - (I)v * Qg, Ug)) acc[q] += 1u << (8 * qq);
+                }
+            }
+        }
+    }
+}
+
 template <typename I, int MODE>
 __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
+    __shared__ uint32_t s_stage[MODE == MODE_WRITE ? 8 * 4 * kChunk : 1];   // 4 KB per warp
     const int lane = threadIdx.x & 31;
-    const uint32_t lt_mask = (1u << lane) - 1u;
     const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t c_lo = A.chunk_bounds[0], c_hi = A.chunk_bounds[1];
@@ -123,12 +170,12 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
         const I i0 = (I)__ldg(A.p_a + r) << sh;
         const I j0 = (I)__ldg(A.p_c + r) << sh;
         const I alpha = ((I)1 << D) - 2 * i0;          // g = ex*alpha + (ey << D) + beta_c
-        const I beta_c = (N << D) - (I)3 * N * j0;
+        const I beta_m1 = (N << D) - (I)3 * N * j0 - 1;
 
         uint32_t nfq[4] = {kNone, kNone, kNone, kNone};
         uint64_t cdst[4] = {0, 0, 0, 0};
+        uint32_t my_nf = kNone;            // lanes 0..3: next-frontier index of child `lane`
         if (MODE != MODE_COUNT) {
-            uint32_t my_nf = kNone;
             uint64_t my_off = 0;
             if (lane < 4) {
                 my_nf = __ldg(A.nf + 4 * (uint64_t)(r - A.nf_rbase) + lane);
@@ -149,46 +196,10 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
             p[it] = (idx < cnt) ? __ldcs(A.list + e0 + idx) : 0u;
         }
 
-        uint32_t cm = 0;            // 4 child bits per item, item it at bits [4it, 4it+4)
+        uint32_t cm = 0;
         uint32_t acc[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int it = 0; it < kItems; ++it) {
-            const uint32_t w = p[it];
-            const bool valid = (lane + kWarp * it) < cnt;
-            const I ex = (I)(beta ? (w & 0xFFFFu) : (w >> 16));
-            const I ey = (I)(beta ? (w >> 16) : (w & 0xFFFFu));
-            const I gm1 = ex * alpha + (ey << D) + beta_c - 1;   // G(SW corner) - 1
-            const I Pc = ex << sh;                                // ex * s
-            const I Uc = Pc + Qc;
-            // child SW values: NE g-Pc-Qc, NW g-Qc, SW g, SE g-Pc
-            const uint32_t bNE = crosses<I>(gm1 - Pc - Qc, Uc);
-            const uint32_t bNW = crosses<I>(gm1 - Qc, Uc);
-            const uint32_t bSW = crosses<I>(gm1, Uc);
-            const uint32_t bSE = crosses<I>(gm1 - Pc, Uc);
-            const uint32_t m4 = valid ? (bNE | (bNW << 1) | (bSW << 2) | (bSE << 3)) : 0u;
-            cm |= m4 << (4 * it);
-            if (MODE == MODE_COUNT) {
-                acc[0] += (m4 & 1u) | ((m4 & 2u) << 7) | ((m4 & 4u) << 14) | ((m4 & 8u) << 21);
-            } else {
-                // Count-ahead: the 4x4 level-(l+2) cells (u, v), u along m, v along b, have SW value
-                // g - u*Pg - v*Qg. A line crossing a cell crosses its parent child (containment),
-                // so only the child's split flag (warp-uniform) gates the count.
-                const I Pg = Pc >> 1;
-                const I Ug = Pg + Qg;
-                if (valid) {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const I hu = gm1 - (I)u * Pg;
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) {
-                            const int q = quad_of(u >> 1, v >> 1);
-                            const int qq = quad_of(u & 1, v & 1);
-                            if (nfq[q] != kNone && crosses<I>(hu - (I)v * Qg, Ug)) acc[q] += 1u << (8 * qq);
-                        }
-                    }
-                }
-            }
-        }
+        if (beta) chunk_math<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, cm, acc);
+        else chunk_math<I, MODE, false>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, cm, acc);
 
         if (MODE == MODE_COUNT) {
             uint32_t c02, c13;
@@ -212,33 +223,46 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
         }
 
         if (MODE == MODE_WRITE) {
-            // child list compaction: one atomic per (chunk, split child) reserves a contiguous run,
-            // ballots give each lane its rank inside the run.
-            uint32_t tot[4];
+            // Child list compaction (warp-private, order within a child list is irrelevant to the
+            // counts): per-lane per-child counts -> one packed warp exclusive scan -> entries staged
+            // in shared memory per child -> one atomic per (chunk, split child) reserves a run ->
+            // fully coalesced copy-out.
+            uint32_t splitm = 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t t = 0;
+            for (int q = 0; q < 4; ++q) splitm |= (nfq[q] != kNone ? 1u : 0u) << q;
+            cm &= splitm * 0x11111111u;
+            const uint32_t c0 = __popc(cm & 0x11111111u), c1 = __popc(cm & 0x22222222u);
+            const uint32_t c2 = __popc(cm & 0x44444444u), c3 = __popc(cm & 0x88888888u);
+            uint32_t s02 = c0 | (c2 << 16), s13 = c1 | (c3 << 16);     // 16-bit fields: sums <= 256
 #pragma unroll
-                for (int it = 0; it < kItems; ++it) t += __popc(__ballot_sync(kFull, (cm >> (4 * it + q)) & 1u));
-                tot[q] = (nfq[q] != kNone) ? t : 0u;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t t02 = __shfl_up_sync(kFull, s02, d), t13 = __shfl_up_sync(kFull, s13, d);
+                if (lane >= d) { s02 += t02; s13 += t13; }
             }
-            uint32_t my_base = 0;
+            const uint32_t tot02 = __shfl_sync(kFull, s02, 31), tot13 = __shfl_sync(kFull, s13, 31);
+            uint32_t pos[4] = {(s02 & 0xFFFFu) - c0, (s13 & 0xFFFFu) - c1, (s02 >> 16) - c2, (s13 >> 16) - c3};
+            uint32_t* stage = s_stage + (threadIdx.x >> 5) * (4 * kChunk);
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (lane == q && tot[q]) my_base = atomicAdd(A.c_cursor + (nfq[q] - A.q0), tot[q]);
+            for (int it = 0; it < kItems; ++it) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (!tot[q]) continue;                      // warp-uniform
-                const uint64_t dst = cdst[q] + shfl_u32(my_base, q);
-                uint32_t run = 0;
-#pragma unroll
-                for (int it = 0; it < kItems; ++it) {
-                    const bool on = (cm >> (4 * it + q)) & 1u;
-                    const uint32_t bal = __ballot_sync(kFull, on);
-                    if (on) A.c_list[dst + run + __popc(bal & lt_mask)] = p[it];
-                    run += __popc(bal);
+                for (int q = 0; q < 4; ++q) {
+                    if ((cm >> (4 * it + q)) & 1u) stage[q * kChunk + pos[q]++] = p[it];
                 }
             }
+            const uint32_t tq[4] = {tot02 & 0xFFFFu, tot13 & 0xFFFFu, tot02 >> 16, tot13 >> 16};
+            uint32_t my_base = 0;
+            if (lane < 4) {
+                const uint32_t t = lane == 0 ? tq[0] : lane == 1 ? tq[1] : lane == 2 ? tq[2] : tq[3];
+                if (t) my_base = atomicAdd(A.c_cursor + (my_nf - A.q0), t);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (tq[q] == 0) continue;                   // warp-uniform
+                uint32_t* dst = A.c_list + cdst[q] + shfl_u32(my_base, q);
+                for (uint32_t i = lane; i < tq[q]; i += kWarp) dst[i] = stage[q * kChunk + i];
+            }
+            __syncwarp();
         }
     }
 }
