@@ -97,9 +97,10 @@ typedef struct {
 
 /* Per-kernel-class timings of the last detect (opts.profile = 1), CUDA events per launch. */
 typedef struct {
-    uint64_t launches[8];    /* 0 stage, 1 count pass, 2 write pass (list compaction + count-ahead),
-                                3 count-only pass, 4 split (threshold + scan), 5 chunk map,
-                                6 other (memsets, range selection), 7 allreduce */
+    uint64_t launches[8];    /* 0 stage, 1 root count pass, 2 write pass (list compaction +
+                                count-ahead), 3 dense tail (levels D-1, D) or count-only pass (D = 2),
+                                4 split (threshold + scan), 5 chunk map / tail gather,
+                                6 other (range selection), 7 allreduce */
     double ms[8];
     uint64_t bytes[8];       /* algorithmic HBM bytes moved by that class */
 } hht_profile;

@@ -69,6 +69,7 @@ struct hht_ctx {
     std::string err;
     size_t budget = 0;
     int grid[3][2] = {};
+    int tail_grid[2] = {};
 
     // last call
     int N = 0, D = 0, B = 0, H = 0, ntrees = 0;
@@ -78,7 +79,7 @@ struct hht_ctx {
     std::vector<uint8_t> tree_half;         // HHT_ALPHA / HHT_BETA per tree
     std::vector<int64_t> tree_E;            // global points per tree
 
-    Buf stage_in, packed, errflag, beta, stats, tiles, tilectr, totals, rng, bounds, vtmp;
+    Buf stage_in, packed, errflag, beta, stats, tiles, tilectr, totals, rng, bounds, vtmp, dense, gv;
     Totals* totals_h = nullptr;
     RangeInfo* range_h = nullptr;
     uint64_t* misc_h = nullptr;
@@ -211,7 +212,9 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
     if (Fp == 0) return HHT_OK;
     Level& C = x->lv[child_level];
     const bool leaf = child_level == x->D;
-    const bool need_lists = child_level <= x->D - 2;
+    // lists are read by write passes (levels <= D-4) and the dense tail (level D-3); for D = 2 the
+    // count-only pass reads the roots' lists (the points themselves)
+    const bool need_lists = child_level <= x->D - 3;
     const uint64_t nch = 4ull * Fp;
     if (!leaf) {
         TRY(ensure(x, C.tree, nch * 4));
@@ -333,16 +336,61 @@ hht_status choose_range(hht_ctx* x, int lc, uint32_t q0, uint64_t cap_entries, b
     return HHT_OK;
 }
 
+// Dense tail at level L = D-3 (D >= 3): lv[L] holds the lists of R_L[r0, r1) and lv[L+1] holds
+// R_(D-2) (its split children, without lists). Counts the level D-1 and D grids of every R_L
+// region in one pass, then splits level D-1 and emits the leaves from the gathered votes.
+hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
+    Level& P = x->lv[L];
+    const uint32_t n = r1 - r0;
+    if (n == 0) return HHT_OK;
+    TRY(ensure(x, x->dense, (size_t)n * kTailCells * 4));
+    CK(cudaMemsetAsync(x->dense.p, 0, (size_t)n * kTailCells * 4, x->st));
+    CK(launch_bounds((const uint64_t*)P.off.p, (const uint64_t*)P.choff.p, (const uint32_t*)P.len.p, r0, r1, L == 0,
+                     (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->st));
+    CK(cudaMemcpyAsync(x->range_h, x->rng.p, sizeof(RangeInfo), cudaMemcpyDeviceToHost, x->st));
+    PassArgs a = pass_args(x, P, L);
+    a.nf_rbase = r0;
+    a.votes = (uint32_t*)x->dense.p;
+    const int id = prof_begin(x, 3, 0);
+    CK(launch_tail(x->int64, a, x->tail_grid[x->int64 ? 1 : 0], x->st));
+    prof_end(x, id);
+    TRY(sync(x));
+    const uint64_t pairs = x->range_h->pairs;
+    if (id >= 0) x->pev[id].bytes = pairs * 4 + (uint64_t)n * kTailCells * 4;
+    x->stat.pairs += pairs;
+    TRY(allreduce_sum_u32(x, (uint32_t*)x->dense.p, (size_t)n * kTailCells));
+    // level D-1: parents R_(D-2), votes from the 4x4 grids
+    Level& P1 = x->lv[L + 1];
+    if (P1.F == 0) return HHT_OK;
+    TRY(ensure(x, x->gv, 16ull * P1.F));
+    const int g1 = prof_begin(x, 5, 16ull * P1.F + 32ull * P1.F);
+    CK(launch_gather((const uint32_t*)x->dense.p, r0, (const uint32_t*)P.a.p, (const uint32_t*)P.c.p,
+                     (const uint32_t*)P1.a.p, (const uint32_t*)P1.c.p, (const uint32_t*)P1.parent.p, nullptr, 1, P1.F,
+                     (uint32_t*)x->gv.p, x->st));
+    prof_end(x, g1);
+    TRY(do_split(x, L + 2, P1, 0, P1.F, (const uint32_t*)x->gv.p, (const uint32_t*)x->gv.p));
+    // level D: parents R_(D-1), votes from the 8x8 grids
+    Level& P2 = x->lv[L + 2];
+    if (P2.F == 0) return HHT_OK;
+    TRY(ensure(x, x->gv, 16ull * P2.F));
+    const int g2 = prof_begin(x, 5, 16ull * P2.F + 36ull * P2.F);
+    CK(launch_gather((const uint32_t*)x->dense.p, r0, (const uint32_t*)P.a.p, (const uint32_t*)P.c.p,
+                     (const uint32_t*)P2.a.p, (const uint32_t*)P2.c.p, (const uint32_t*)P2.parent.p,
+                     (const uint32_t*)P1.parent.p, 2, P2.F, (uint32_t*)x->gv.p, x->st));
+    prof_end(x, g2);
+    return do_split(x, L + 3, P2, 0, P2.F, (const uint32_t*)x->gv.p, (const uint32_t*)x->gv.p);
+}
+
 // Preconditions: lv[l] holds the lists of R_l[r0, r1) and lv[l+1] holds R_(l+1) = the split
 // children of R_l[r0, r1) with NF_(l+1). Processes everything below.
 hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
     const int lc = l + 1;
     if (lc >= x->D) return HHT_OK;
+    if (x->D >= 3 && l == x->D - 3) return tail(x, l, r0, r1);
     Level& P = x->lv[l];
     Level& C = x->lv[lc];
     const uint32_t Fc = C.F;
     if (Fc == 0) return HHT_OK;
-    (void)r1;
 
     if (lc == x->D - 1) {
         // count-only pass: level-D votes of the children of R_(D-1), then the leaves.
@@ -742,6 +790,7 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     }
     for (int m = 0; m < 3; ++m)
         for (int w = 0; w < 2; ++w) x->grid[m][w] = x->sms * pass_blocks_per_sm(m, w == 1);
+    for (int w = 0; w < 2; ++w) x->tail_grid[w] = x->sms * tail_blocks_per_sm(w == 1);
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return fail(HHT_ECUDA);
     x->budget = o.mem_budget ? o.mem_budget : (size_t)(0.70 * (double)fr);
@@ -876,7 +925,7 @@ void hht_destroy(hht_ctx* x) {
     for (auto& g : x->rec) fr(g.b);
     fr(x->leaves.b);
     for (Buf* b : {&x->stage_in, &x->packed, &x->errflag, &x->beta, &x->stats, &x->tiles, &x->tilectr, &x->totals,
-                   &x->rng, &x->bounds, &x->vtmp})
+                   &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv})
         fr(*b);
     if (x->totals_h) cudaFreeHost(x->totals_h);
     if (x->range_h) cudaFreeHost(x->range_h);

@@ -12,6 +12,7 @@ constexpr int kItems = 8;                  // list entries per lane per chunk
 constexpr int kChunk = kWarp * kItems;     // 256 entries: one warp work unit, never spans regions
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr int kSplitThreads = 256;         // split kernel: one thread per parent (its 4 children)
+constexpr int kTailCells = 80;             // dense tail grids per level-(D-3) region: 4x4 + 8x8
 
 // Quad order of the paper: q = 0 NE, 1 NW, 2 SW, 3 SE; child (2a+da, 2c+dc).
 __host__ __device__ constexpr uint32_t quad_da(int q) { return (q == 0 || q == 3) ? 1u : 0u; }
@@ -126,5 +127,12 @@ cudaError_t launch_range(const uint64_t* c_off, const uint32_t* c_parent, uint32
                          const uint64_t* p_choff, const uint32_t* p_len, int p_is_root, RangeInfo* info,
                          uint64_t* chunk_bounds, cudaStream_t st);
 int pass_blocks_per_sm(int mode, bool int64);
+int tail_blocks_per_sm(bool int64);
+cudaError_t launch_tail(bool int64, const PassArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_gather(const uint32_t* dense, uint32_t anc_base, const uint32_t* anc_a, const uint32_t* anc_c,
+                          const uint32_t* p_a, const uint32_t* p_c, const uint32_t* p_parent,
+                          const uint32_t* pp_parent, int kk, uint32_t Fp, uint32_t* V, cudaStream_t st);
+cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
+                          int is_root, RangeInfo* info, uint64_t* chunk_bounds, cudaStream_t st);
 
 }  // namespace hht

@@ -267,6 +267,192 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Dense raster tail: one pass over the lists of the split regions R at level L = D-3 counts the
+// votes of every level-(D-1) and level-D region inside R (a 4x4 and an 8x8 grid). A region's
+// votes are the number of lines crossing it (containment: a line crossing a region crosses all of
+// its ancestors, so R's list holds every line that can vote below R), so the split kernels then
+// read the visited regions' votes from these grids. Level D-2 lists are never materialised.
+//
+// Raster of one line over the 8x8 leaf grid of R (cell side = 1 lattice step): with
+// y_w = G(i0+w, j0) - 1 (w = 0..8, y_(w+1) = y_w - 2ex) and k_w = #{v in 0..8 : 3N*v <= y_w},
+// cell (u, v) is crossed iff v < k_u and v >= k_(u+1) - 1, i.e. the column's rows run from
+// k_(u+1)-1 to min(k_u, 8)-1. Since 2ex < 3N, k drops by at most 1 per column: a one-hot byte mask
+// B of row k-1 (plus a flag for k = 9, row 8 outside the grid) shifts down one byte on a drop,
+// and the column's row mask is B | B_next. A level-(D-1) cell is crossed iff one of its four
+// leaf cells is (parent crossed => its SW or NE child crossed, by the corner ordering), so the
+// 4x4 grid is the OR of 2x2 blocks of the 8x8 masks. Per-lane byte counters (<= 8 per chunk).
+// ---------------------------------------------------------------------------------------------
+template <typename I, bool BETA>
+__device__ __forceinline__ void tail_math(const uint32_t (&p)[kItems], int cnt, int lane, I alpha, I beta_m1,
+                                          int D, I N3, uint32_t (&a4)[4], uint32_t (&a8)[16]) {
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+        const uint32_t w = p[it];
+        const I ex = (I)(BETA ? (w & 0xFFFFu) : (w >> 16));
+        const I ey = (I)(BETA ? (w >> 16) : (w & 0xFFFFu));
+        I y = ex * alpha + (ey << D) + beta_m1;            // G(SW corner of R) - 1
+        if (lane + kWarp * it >= cnt) y = (I)-1;            // crosses nothing
+        const I P8 = 2 * ex;
+        // f = min(floor(y / 3N), 8) for y >= 0 (binary search); k0 = f + 1
+        I f = 0;
+        if (y >= (I)8 * N3) {
+            f = 8;
+        } else {
+            if (y >= (I)4 * N3) f = 4;
+            if (y >= (f + 2) * N3) f += 2;
+            if (y >= (f + 1) * N3) f += 1;
+        }
+        I Kq = f * N3;                                       // (k - 1) * 3N: drop threshold
+        uint32_t f9 = (y >= (I)8 * N3) ? 0x01000000u : 0u;  // k == 9 (row 8, outside the grid)
+        uint32_t Blo = 0, Bhi = 0;                           // one-hot byte of row k-1 (rows 0..7)
+        if (y >= 0 && f < 8) {
+            const uint32_t fs = (uint32_t)f;
+            Blo = fs < 4 ? (1u << (8 * fs)) : 0u;
+            Bhi = fs >= 4 ? (1u << (8 * (fs - 4))) : 0u;
+        }
+        uint32_t Mlo_prev = 0, Mhi_prev = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            y -= P8;
+            const bool drop = y < Kq;
+            uint32_t Nlo = Blo, Nhi = Bhi;
+            if (drop) {
+                Kq -= N3;
+                Nlo = __funnelshift_r(Blo, Bhi, 8);
+                Nhi = (Bhi >> 8) | f9;
+                f9 = 0;
+            }
+            const uint32_t Mlo = Blo | Nlo, Mhi = Bhi | Nhi;    // rows crossed in column u
+            a8[2 * u] += Mlo;
+            a8[2 * u + 1] += Mhi;
+            if (u & 1) {
+                const uint32_t clo = Mlo | Mlo_prev, chi = Mhi | Mhi_prev;
+                const uint32_t plo = clo | __funnelshift_r(clo, chi, 8), phi = chi | (chi >> 8);
+                a4[u >> 1] += __byte_perm(plo, phi, 0x6420);  // rows (0,1),(2,3),(4,5),(6,7)
+            }
+            Mlo_prev = Mlo;
+            Mhi_prev = Mhi;
+            Blo = Nlo;
+            Bhi = Nhi;
+        }
+    }
+}
+
+template <typename I>
+__global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t c_lo = A.chunk_bounds[0], c_hi = A.chunk_bounds[1];
+    const int D = A.D;
+    const int sh = D - A.level;                       // == 3
+    const I N = (I)A.N;
+    const I N3 = (I)3 * N;
+
+    for (uint64_t ch = c_lo + warp0; ch < c_hi; ch += nwarps) {
+        const uint32_t r = __ldg(A.chunk_region + ch);
+        const uint64_t k = ch - __ldg(A.p_choff + r);
+        const uint32_t len = __ldg(A.p_len + r);
+        const uint64_t e0 = __ldg(A.p_off + r) - A.list_base + k * kChunk;
+        const int cnt = (int)min((uint64_t)kChunk, (uint64_t)len - k * kChunk);
+        const uint32_t tree = __ldg(A.p_tree + r);
+        const bool beta = __ldg(A.tree_beta + tree) != 0;
+        const I i0 = (I)__ldg(A.p_a + r) << sh;
+        const I j0 = (I)__ldg(A.p_c + r) << sh;
+        const I alpha = ((I)1 << D) - 2 * i0;
+        const I beta_m1 = (N << D) - N3 * j0 - 1;
+
+        uint32_t p[kItems];
+#pragma unroll
+        for (int it = 0; it < kItems; ++it) {
+            const int idx = lane + kWarp * it;
+            p[it] = (idx < cnt) ? __ldcs(A.list + e0 + idx) : 0u;
+        }
+        uint32_t a4[4] = {0, 0, 0, 0};
+        uint32_t a8[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) a8[i] = 0;
+        if (beta) tail_math<I, true>(p, cnt, lane, alpha, beta_m1, D, N3, a4, a8);
+        else tail_math<I, false>(p, cnt, lane, alpha, beta_m1, D, N3, a4, a8);
+
+        // dense[(r - nf_rbase) * 80 + 4*w + b]: w 0..3 = 4x4 column w; w = 4 + 2u + h = 8x8 column u, rows 4h..4h+3
+        uint32_t* dst = A.votes + (uint64_t)(r - A.nf_rbase) * kTailCells;
+#pragma unroll
+        for (int wi = 0; wi < 20; ++wi) {
+            uint32_t c02, c13;
+            warp_sum_bytes(wi < 4 ? a4[wi] : a8[wi - 4], c02, c13);
+            if (lane < 4) {
+                const uint32_t v = byte_counter(c02, c13, lane);
+                if (v) atomicAdd(dst + 4 * wi + lane, v);
+            }
+        }
+    }
+}
+
+int tail_blocks_per_sm(bool int64) {
+    int n = 0;
+    if (int64) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tail<int64_t>, 256, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tail<int32_t>, 256, 0);
+    return n > 0 ? n : 1;
+}
+
+cudaError_t launch_tail(bool int64, const PassArgs& a, int grid, cudaStream_t st) {
+    if (int64) k_tail<int64_t><<<grid, 256, 0, st>>>(a);
+    else k_tail<int32_t><<<grid, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// Gather the 4 child votes of each parent (level D-2 parents: 4x4 grid, kk = 1; level D-1
+// parents: 8x8 grid, kk = 2) from the dense grids of their level-(D-3) ancestor.
+__global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ dense, uint32_t anc_base,
+                                                const uint32_t* __restrict__ anc_a, const uint32_t* __restrict__ anc_c,
+                                                const uint32_t* __restrict__ p_a, const uint32_t* __restrict__ p_c,
+                                                const uint32_t* __restrict__ p_parent,
+                                                const uint32_t* __restrict__ pp_parent, int kk, uint32_t Fp,
+                                                uint32_t* __restrict__ V) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= Fp) return;
+    uint32_t A = p_parent[p];
+    if (kk == 2) A = pp_parent[A];
+    const uint32_t la = p_a[p] - (anc_a[A] << kk), lc = p_c[p] - (anc_c[A] << kk);
+    const uint32_t G = 2u << kk;                   // grid side: 4 or 8
+    const uint32_t* g = dense + (uint64_t)(A - anc_base) * kTailCells + (kk == 1 ? 0 : 16);
+    uint32_t v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = g[(2 * la + quad_da(q)) * G + 2 * lc + quad_dc(q)];
+    reinterpret_cast<uint4*>(V)[p] = make_uint4(v[0], v[1], v[2], v[3]);
+}
+
+cudaError_t launch_gather(const uint32_t* dense, uint32_t anc_base, const uint32_t* anc_a, const uint32_t* anc_c,
+                          const uint32_t* p_a, const uint32_t* p_c, const uint32_t* p_parent,
+                          const uint32_t* pp_parent, int kk, uint32_t Fp, uint32_t* V, cudaStream_t st) {
+    if (Fp == 0) return cudaSuccess;
+    k_gather<<<(Fp + 255) / 256, 256, 0, st>>>(dense, anc_base, anc_a, anc_c, p_a, p_c, p_parent, pp_parent, kk, Fp, V);
+    return cudaGetLastError();
+}
+
+// Chunk bounds and streamed pairs of a parent range [r0, r1) (one thread).
+__global__ void k_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
+                         int is_root, RangeInfo* info, uint64_t* chunk_bounds) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint64_t pairs = 0;
+    if (is_root) {
+        for (uint32_t r = r0; r < r1; ++r) pairs += len[r];
+    } else {
+        pairs = off[r1] - off[r0];
+    }
+    info->pairs = pairs;
+    info->chunk_lo = chunk_bounds[0] = choff[r0];
+    info->chunk_hi = chunk_bounds[1] = choff[r1];
+}
+
+cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
+                          int is_root, RangeInfo* info, uint64_t* chunk_bounds, cudaStream_t st) {
+    k_bounds<<<1, 32, 0, st>>>(off, choff, len, r0, r1, is_root, info, chunk_bounds);
+    return cudaGetLastError();
+}
+
 template <typename I, int MODE>
 static int blocks_per_sm_impl() {
     int n = 0;

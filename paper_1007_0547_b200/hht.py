@@ -28,7 +28,7 @@ EXPORTS = ["hht_default_opts", "hht_create", "hht_nccl_unique_id", "hht_detect",
            "hht_timer_begin", "hht_timer_end", "hht_last_error", "hht_status_str", "hht_destroy",
            "hht_version"]
 
-PROFILE_CLASSES = ["stage", "count", "write", "count2", "split", "chunk_map", "other", "allreduce"]
+PROFILE_CLASSES = ["stage", "count", "write", "tail", "split", "gather", "other", "allreduce"]
 
 
 class HHTError(RuntimeError):
