@@ -12,7 +12,7 @@ constexpr int kItems = 8;                  // list entries per lane per chunk
 constexpr int kChunk = kWarp * kItems;     // 256 entries: one warp work unit, never spans regions
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr int kSplitThreads = 256;         // split kernel: one thread per parent (its 4 children)
-constexpr int kTailCells = 80;             // dense tail grids per level-(D-3) region: 4x4 + 8x8
+constexpr int kTailCells = 64;             // dense tail grid per level-(D-3) region: 8x8 leaves
 
 // Quad order of the paper: q = 0 NE, 1 NW, 2 SW, 3 SE; child (2a+da, 2c+dc).
 __host__ __device__ constexpr uint32_t quad_da(int q) { return (q == 0 || q == 3) ? 1u : 0u; }

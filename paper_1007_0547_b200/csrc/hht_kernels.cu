@@ -269,23 +269,41 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
 
 // ---------------------------------------------------------------------------------------------
 // Dense raster tail: one pass over the lists of the split regions R at level L = D-3 counts the
-// votes of every level-(D-1) and level-D region inside R (a 4x4 and an 8x8 grid). A region's
-// votes are the number of lines crossing it (containment: a line crossing a region crosses all of
-// its ancestors, so R's list holds every line that can vote below R), so the split kernels then
-// read the visited regions' votes from these grids. Level D-2 lists are never materialised.
+// votes of every level-D region inside R (an 8x8 grid); the visited level-(D-1) and level-D
+// regions' votes are then gathered from the grid. A region's votes are the number of lines
+// crossing it, and R's list holds every line that crosses anything inside R (containment), so the
+// grid counts are exactly the paper's votes. Level D-2 lists are never materialised.
+//
+// Level D-1 from level D: with G_SW >= G_centre >= G_NE for every region, a line crosses region C
+// iff it crosses exactly one of C's SW child (G_SW > 0 >= G_centre) and NE child
+// (G_centre > 0 >= G_NE), so votes(C) = votes(SW child) + votes(NE child).
 //
 // Raster of one line over the 8x8 leaf grid of R (cell side = 1 lattice step): with
 // y_w = G(i0+w, j0) - 1 (w = 0..8, y_(w+1) = y_w - 2ex) and k_w = #{v in 0..8 : 3N*v <= y_w},
-// cell (u, v) is crossed iff v < k_u and v >= k_(u+1) - 1, i.e. the column's rows run from
-// k_(u+1)-1 to min(k_u, 8)-1. Since 2ex < 3N, k drops by at most 1 per column: a one-hot byte mask
-// B of row k-1 (plus a flag for k = 9, row 8 outside the grid) shifts down one byte on a drop,
-// and the column's row mask is B | B_next. A level-(D-1) cell is crossed iff one of its four
-// leaf cells is (parent crossed => its SW or NE child crossed, by the corner ordering), so the
-// 4x4 grid is the OR of 2x2 blocks of the 8x8 masks. Per-lane byte counters (<= 8 per chunk).
+// cell (u, v) is crossed iff v < k_u and v >= k_(u+1) - 1: the rows of column u run from
+// k_(u+1)-1 to min(k_u, 8)-1. Since 2ex < 3N, k drops by at most 1 per column (drop <=> y_(u+1) <
+// (k_u - 1)*3N), so the column's crossed-row byte mask depends only on (k_u, drop) and comes from a
+// 36-entry shared-memory table (k in -8..9: a line below the grid keeps "dropping" harmlessly into
+// all-zero entries). Per column: one subtract, one compare, one 8-byte table load, two adds.
 // ---------------------------------------------------------------------------------------------
+constexpr int kTab8 = 36;   // (k + 8) * 2 + drop, k in -8..9
+
+__device__ __forceinline__ uint2 tab8_entry(int t) {
+    const int k = t / 2 - 8, d = t & 1;
+    uint32_t lo = 0, hi = 0;
+    if (k >= 1) {
+        const int vhi = min(k, 8) - 1, vlo = max(k - d - 1, 0);
+        for (int v = vlo; v <= vhi; ++v) {
+            if (v < 4) lo |= 1u << (8 * v);
+            else hi |= 1u << (8 * (v - 4));
+        }
+    }
+    return make_uint2(lo, hi);
+}
+
 template <typename I, bool BETA>
 __device__ __forceinline__ void tail_math(const uint32_t (&p)[kItems], int cnt, int lane, I alpha, I beta_m1,
-                                          int D, I N3, uint32_t (&a4)[4], uint32_t (&a8)[16]) {
+                                          int D, I N3, const uint2* __restrict__ tab, uint32_t (&a8)[16]) {
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
         const uint32_t w = p[it];
@@ -294,53 +312,34 @@ __device__ __forceinline__ void tail_math(const uint32_t (&p)[kItems], int cnt, 
         I y = ex * alpha + (ey << D) + beta_m1;            // G(SW corner of R) - 1
         if (lane + kWarp * it >= cnt) y = (I)-1;            // crosses nothing
         const I P8 = 2 * ex;
-        // f = min(floor(y / 3N), 8) for y >= 0 (binary search); k0 = f + 1
-        I f = 0;
-        if (y >= (I)8 * N3) {
-            f = 8;
-        } else {
-            if (y >= (I)4 * N3) f = 4;
-            if (y >= (f + 2) * N3) f += 2;
-            if (y >= (f + 1) * N3) f += 1;
-        }
-        I Kq = f * N3;                                       // (k - 1) * 3N: drop threshold
-        uint32_t f9 = (y >= (I)8 * N3) ? 0x01000000u : 0u;  // k == 9 (row 8, outside the grid)
-        uint32_t Blo = 0, Bhi = 0;                           // one-hot byte of row k-1 (rows 0..7)
-        if (y >= 0 && f < 8) {
-            const uint32_t fs = (uint32_t)f;
-            Blo = fs < 4 ? (1u << (8 * fs)) : 0u;
-            Bhi = fs >= 4 ? (1u << (8 * (fs - 4))) : 0u;
-        }
-        uint32_t Mlo_prev = 0, Mhi_prev = 0;
+        // f = min(floor(y / 3N), 8) for y >= 0 (branch-free binary search); k0 = f + 1 (0 if y < 0)
+        I f = (y >= (I)4 * N3) ? (I)4 : (I)0;
+        f += (y >= (f + 2) * N3) ? (I)2 : (I)0;
+        f += (y >= (f + 1) * N3) ? (I)1 : (I)0;
+        f = (y >= (I)8 * N3) ? (I)8 : f;
+        const bool below = y < 0;
+        I Kq = below ? -N3 : f * N3;                         // (k - 1) * 3N: drop threshold
+        int kk = below ? 16 : 2 * (int)f + 18;               // table index of (k, 0): 2 * (k + 8)
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             y -= P8;
             const bool drop = y < Kq;
-            uint32_t Nlo = Blo, Nhi = Bhi;
+            const uint2 m = tab[kk + (drop ? 1 : 0)];
+            a8[2 * u] += m.x;
+            a8[2 * u + 1] += m.y;
             if (drop) {
+                kk -= 2;
                 Kq -= N3;
-                Nlo = __funnelshift_r(Blo, Bhi, 8);
-                Nhi = (Bhi >> 8) | f9;
-                f9 = 0;
             }
-            const uint32_t Mlo = Blo | Nlo, Mhi = Bhi | Nhi;    // rows crossed in column u
-            a8[2 * u] += Mlo;
-            a8[2 * u + 1] += Mhi;
-            if (u & 1) {
-                const uint32_t clo = Mlo | Mlo_prev, chi = Mhi | Mhi_prev;
-                const uint32_t plo = clo | __funnelshift_r(clo, chi, 8), phi = chi | (chi >> 8);
-                a4[u >> 1] += __byte_perm(plo, phi, 0x6420);  // rows (0,1),(2,3),(4,5),(6,7)
-            }
-            Mlo_prev = Mlo;
-            Mhi_prev = Mhi;
-            Blo = Nlo;
-            Bhi = Nhi;
         }
     }
 }
 
 template <typename I>
 __global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
+    __shared__ uint2 s_tab[kTab8];
+    if (threadIdx.x < kTab8) s_tab[threadIdx.x] = tab8_entry(threadIdx.x);
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -369,22 +368,21 @@ __global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
             const int idx = lane + kWarp * it;
             p[it] = (idx < cnt) ? __ldcs(A.list + e0 + idx) : 0u;
         }
-        uint32_t a4[4] = {0, 0, 0, 0};
         uint32_t a8[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) a8[i] = 0;
-        if (beta) tail_math<I, true>(p, cnt, lane, alpha, beta_m1, D, N3, a4, a8);
-        else tail_math<I, false>(p, cnt, lane, alpha, beta_m1, D, N3, a4, a8);
+        if (beta) tail_math<I, true>(p, cnt, lane, alpha, beta_m1, D, N3, s_tab, a8);
+        else tail_math<I, false>(p, cnt, lane, alpha, beta_m1, D, N3, s_tab, a8);
 
-        // dense[(r - nf_rbase) * 80 + 4*w + b]: w 0..3 = 4x4 column w; w = 4 + 2u + h = 8x8 column u, rows 4h..4h+3
+        // grid[(r - nf_rbase) * 64 + 8u + v]: a8[2u] byte b = row b, a8[2u+1] byte b = row 4+b
         uint32_t* dst = A.votes + (uint64_t)(r - A.nf_rbase) * kTailCells;
 #pragma unroll
-        for (int wi = 0; wi < 20; ++wi) {
+        for (int wi = 0; wi < 16; ++wi) {
             uint32_t c02, c13;
-            warp_sum_bytes(wi < 4 ? a4[wi] : a8[wi - 4], c02, c13);
+            warp_sum_bytes(a8[wi], c02, c13);
             if (lane < 4) {
                 const uint32_t v = byte_counter(c02, c13, lane);
-                if (v) atomicAdd(dst + 4 * wi + lane, v);
+                if (v) atomicAdd(dst + 8 * (wi >> 1) + 4 * (wi & 1) + lane, v);
             }
         }
     }
@@ -416,11 +414,17 @@ __global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ den
     uint32_t A = p_parent[p];
     if (kk == 2) A = pp_parent[A];
     const uint32_t la = p_a[p] - (anc_a[A] << kk), lc = p_c[p] - (anc_c[A] << kk);
-    const uint32_t G = 2u << kk;                   // grid side: 4 or 8
-    const uint32_t* g = dense + (uint64_t)(A - anc_base) * kTailCells + (kk == 1 ? 0 : 16);
+    const uint32_t* g = dense + (uint64_t)(A - anc_base) * kTailCells;   // 8x8 leaf grid, [8u + v]
     uint32_t v[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = g[(2 * la + quad_da(q)) * G + 2 * lc + quad_dc(q)];
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t u = 2 * la + quad_da(q), w = 2 * lc + quad_dc(q);
+        if (kk == 2) {
+            v[q] = g[8 * u + w];
+        } else {   // level D-1 cell (u, w): votes = SW leaf (2u, 2w) + NE leaf (2u+1, 2w+1)
+            v[q] = g[8 * (2 * u) + 2 * w] + g[8 * (2 * u + 1) + 2 * w + 1];
+        }
+    }
     reinterpret_cast<uint4*>(V)[p] = make_uint4(v[0], v[1], v[2], v[3]);
 }
 
