@@ -174,22 +174,14 @@ def main():
     else:
         pts, _ = synth.config_image(a.config)
         offs = np.array([0, pts.shape[0]], dtype=np.int64)
-    # shard: images across ranks for batches (independent trees), points within the image otherwise
-    if cfg.images > 1 and world > 1:
-        lo, hi = synth.shard(cfg.images, rank, world)
-        my = pts[offs[lo]:offs[hi]]
-        my_offs = offs[lo:hi + 1] - offs[lo]
-        comm_world = 1
-    else:
-        lo, hi = synth.shard(pts.shape[0], rank, world)
-        my = pts[lo:hi]
-        my_offs = np.array([0, my.shape[0]], dtype=np.int64)
-        comm_world = world
+    # shard: whole images across ranks for batches (independent trees), points within the image otherwise
+    from paper_1007_0547_b200 import dist as hdist
+    sh = hdist.make_shard(pts, offs, rank, world)
+    my, my_offs, comm_world = sh.points, sh.offsets, sh.comm_world
     nccl_id = None
     if comm_world > 1:
-        obj = [hht.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        hdist.check_consistent(cfg.N, cfg.D, cfg.T, cfg.halves, 1)
+        nccl_id = hdist.broadcast_bytes(hht.nccl_unique_id() if rank == 0 else None)
     h = hht.HHT(device=local, halves=cfg.halves, record_levels=True, profile=True,
                 rank=rank if comm_world > 1 else 0, world=comm_world, nccl_id=nccl_id)
     d_pts = torch.from_numpy(np.ascontiguousarray(my)).to(dev)

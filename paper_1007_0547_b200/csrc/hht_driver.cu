@@ -31,7 +31,7 @@ struct Buf {
 };
 
 struct Level {
-    Buf tree, a, c, parent, len, off, choff, chunk_region;   // frontier R_l
+    Buf tree, a, c, parent, len, votes_g, off, choff, chunk_region;   // frontier R_l
     Buf nf;                                                   // children of R_(l-1) range -> R_l
     Buf votes, votes_local;                                   // votes of R_l's children (range)
     Buf cursor;                                               // append cursors of R_l lists (range)
@@ -43,7 +43,7 @@ struct Level {
 
     Frontier frontier() {
         return {(uint32_t*)tree.p, (uint32_t*)a.p, (uint32_t*)c.p, (uint32_t*)parent.p, (uint32_t*)len.p,
-                (uint64_t*)off.p, (uint64_t*)choff.p, (uint32_t*)chunk_region.p};
+                (uint32_t*)votes_g.p, (uint64_t*)off.p, (uint64_t*)choff.p, (uint32_t*)chunk_region.p};
     }
 };
 
@@ -208,7 +208,7 @@ hht_status sync(hht_ctx* x) {
 // split: threshold the votes of the children of parents P[r0, r0+Fp) into level child_level.
 // ---------------------------------------------------------------------------------------------
 hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t Fp, const uint32_t* V,
-                    const uint32_t* VL) {
+                    const uint32_t* VL, bool derive_ne = false) {
     if (Fp == 0) return HHT_OK;
     Level& C = x->lv[child_level];
     const bool leaf = child_level == x->D;
@@ -222,6 +222,7 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
         TRY(ensure(x, C.c, nch * 4));
         TRY(ensure(x, C.parent, nch * 4));
         TRY(ensure(x, C.len, nch * 4));
+        TRY(ensure(x, C.votes_g, nch * 4));
         TRY(ensure(x, C.off, (nch + 1) * 8));
         TRY(ensure(x, C.choff, (nch + 1) * 8));
         TRY(ensure(x, C.nf, nch * 4));
@@ -243,6 +244,9 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
     a.p_a = (const uint32_t*)P.a.p + r0;
     a.p_c = (const uint32_t*)P.c.p + r0;
     a.parent_base = r0;
+    a.derive_ne = derive_ne;
+    a.p_votes = derive_ne ? (const uint32_t*)P.votes_g.p + r0 : nullptr;
+    a.p_len = derive_ne ? (const uint32_t*)P.len.p + r0 : nullptr;
     a.child_level = child_level;
     a.leaf_level = leaf;
     a.need_lists = need_lists;
@@ -298,6 +302,7 @@ PassArgs pass_args(hht_ctx* x, Level& P, int level) {
     a.level = level;
     a.D = x->D;
     a.N = x->N;
+    a.one = 1;
     return a;
 }
 
@@ -406,7 +411,7 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         a.votes = (uint32_t*)C.votes.p;
         TRY(run_pass(x, MODE_COUNT2, a, ri.pairs, 0));
         TRY(allreduce_sum_u32(x, (uint32_t*)C.votes.p, 4ull * Fc));
-        return do_split(x, x->D, C, 0, Fc, (const uint32_t*)C.votes.p, (const uint32_t*)C.votes.p);
+        return do_split(x, x->D, C, 0, Fc, (const uint32_t*)C.votes.p, (const uint32_t*)C.votes.p, true);
     }
 
     uint32_t q0 = 0;
@@ -459,7 +464,7 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
             VL = (const uint32_t*)C.votes_local.p;
             TRY(allreduce_sum_u32(x, (uint32_t*)C.votes.p, 4ull * nq));
         }
-        TRY(do_split(x, lc + 1, C, q0, nq, (const uint32_t*)C.votes.p, VL));
+        TRY(do_split(x, lc + 1, C, q0, nq, (const uint32_t*)C.votes.p, VL, true));
         TRY(descend(x, lc, q0, q1));
         q0 = q1;
     }
@@ -590,7 +595,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     // level 0: every tree's root ("each line ... passes through this region")
     uint64_t root_votes = 0, root_tests = 0, root_split = 0;
     std::vector<Record> r0rec;
-    std::vector<uint32_t> h_tree, h_zero, h_len;
+    std::vector<uint32_t> h_tree, h_zero, h_len, h_votes;
     std::vector<uint64_t> h_off, h_choff;
     uint64_t chunks = 0, pairs0 = 0;
     for (int t = 0; t < x->ntrees; ++t) {
@@ -606,6 +611,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
             h_zero.push_back(0);
             const uint64_t ln = (uint64_t)local_n[b];
             h_len.push_back((uint32_t)ln);
+            h_votes.push_back((uint32_t)E);
             h_off.push_back((uint64_t)offsets[b]);
             h_choff.push_back(chunks);
             chunks += (ln + kChunk - 1) / kChunk;
@@ -634,6 +640,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         TRY(ensure(x, L0.c, F0 * 4ull));
         TRY(ensure(x, L0.parent, F0 * 4ull));
         TRY(ensure(x, L0.len, F0 * 4ull));
+        TRY(ensure(x, L0.votes_g, F0 * 4ull));
         TRY(ensure(x, L0.off, (F0 + 1) * 8ull));
         TRY(ensure(x, L0.choff, (F0 + 1) * 8ull));
         TRY(ensure(x, L0.chunk_region, std::max<uint64_t>(chunks, 1) * 4));
@@ -642,6 +649,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         CK(cudaMemcpyAsync(L0.c.p, h_zero.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
         CK(cudaMemcpyAsync(L0.parent.p, h_tree.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
         CK(cudaMemcpyAsync(L0.len.p, h_len.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
+        CK(cudaMemcpyAsync(L0.votes_g.p, h_votes.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
         CK(cudaMemcpyAsync(L0.off.p, h_off.data(), (F0 + 1) * 8ull, cudaMemcpyHostToDevice, x->st));
         CK(cudaMemcpyAsync(L0.choff.p, h_choff.data(), (F0 + 1) * 8ull, cudaMemcpyHostToDevice, x->st));
         CK(launch_chunk_map((const uint64_t*)L0.choff.p, F0, (uint32_t*)L0.chunk_region.p, x->st));
@@ -918,7 +926,7 @@ void hht_destroy(hht_ctx* x) {
         b.p = nullptr;
     };
     for (auto& L : x->lv) {
-        for (Buf* b : {&L.tree, &L.a, &L.c, &L.parent, &L.len, &L.off, &L.choff, &L.chunk_region, &L.nf, &L.votes,
+        for (Buf* b : {&L.tree, &L.a, &L.c, &L.parent, &L.len, &L.votes_g, &L.off, &L.choff, &L.chunk_region, &L.nf, &L.votes,
                        &L.votes_local, &L.cursor, &L.list_own})
             fr(*b);
     }

@@ -24,7 +24,8 @@ struct Frontier {
     uint32_t* a;         // region column (m axis)
     uint32_t* c;         // region row (b axis)
     uint32_t* parent;    // index of the parent in the previous level's frontier
-    uint32_t* len;       // local candidate-list length (this rank's lines crossing the region)
+    uint32_t* len;       // local votes = local candidate-list length (this rank's lines crossing it)
+    uint32_t* votes;     // global votes (all ranks)
     uint64_t* off;       // [F+1] local list offset (exclusive scan of len); off[F] = total
     uint64_t* choff;     // [F+1] chunk offset (exclusive scan of ceil(len/kChunk)); choff[F] = total
     uint32_t* chunk_region;  // [total chunks] chunk -> region index
@@ -80,6 +81,7 @@ struct PassArgs {
     uint64_t c_list_base;          // subtract from c_off[nf] to index c_list
     uint32_t* c_cursor;            // [q1 - q0] append cursors
     uint32_t* c_list;              // output lists
+    uint32_t one;                  // == 1 (runtime value: keeps the count adds on the FMA pipe)
     uint32_t* votes;               // MODE_COUNT: [4 * nparents] (4*(r - nf_rbase) + q)
                                    // else:       [4 * (q1 - q0)] (4*(nf - q0) + q')
 };
@@ -97,6 +99,9 @@ struct SplitArgs {
     int need_lists;                // child_level <= D-2: children will carry candidate lists
     int record;
     uint64_t T;
+    const uint32_t* p_votes;       // derive_ne: parents' global votes (range start)
+    const uint32_t* p_len;         // derive_ne: parents' local votes (range start)
+    int derive_ne;                 // V/VL hold no NE counts: NE = parent - SW (votes identity)
     uint32_t* nf;                  // [4 * Fp]
     Frontier out;
     Record* rec;                   // records of child_level, rec[4*p + q]

@@ -51,6 +51,13 @@ __device__ __forceinline__ uint32_t byte_counter(uint32_t c02, uint32_t c13, int
     return (((which & 1) ? c13 : c02) >> (16 * (which >> 1))) & 0xFFFFu;
 }
 
+// if (c) acc += one * k, as a predicated integer multiply-add (issued on the FMA pipe; `one` is a
+// runtime 1 so ptxas cannot strength-reduce it to an ALU add).
+__device__ __forceinline__ void mad_if(bool c, uint32_t& acc, uint32_t one, uint32_t k) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p mad.lo.u32 %0, %2, %3, %0;\n\t}"
+        : "+r"(acc) : "r"((uint32_t)c), "r"(one), "r"(k));
+}
+
 // quad index of (da, dc): NE(1,1)=0, NW(0,1)=1, SW(0,0)=2, SE(1,0)=3
 __host__ __device__ constexpr int quad_of(int da, int dc) { return dc ? (da ? 0 : 1) : (da ? 3 : 2); }
 
@@ -107,7 +114,8 @@ cudaError_t launch_stage(const int32_t* pts, uint64_t n, int N, uint32_t* packed
 //         g - u*Pg - v*Qg; containment makes the child's own crossing implied).
 template <typename I, int MODE, bool BETA>
 __device__ __forceinline__ void chunk_math(const uint32_t (&p)[kItems], int cnt, int lane, I alpha, I beta_m1,
-                                           int D, int sh, I Qc, I Qg, uint32_t& cm, uint32_t (&acc)[4]) {
+                                           int D, int sh, I Qc, I Qg, uint32_t one, uint32_t& cm,
+                                           uint32_t (&acc)[4]) {
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
         const uint32_t w = p[it];
@@ -130,16 +138,25 @@ __device__ __forceinline__ void chunk_math(const uint32_t (&p)[kItems], int cnt,
             }
         }
         if (MODE != MODE_COUNT) {
+            // 12 of the 16 cells: the NE grandchild of each child is derived later from
+            // votes(child) = votes(SW grandchild) + votes(NE grandchild).
             const I Pg = Pc >> 1;
             const I Ug = Pg + Qg;
+            int n = 0;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const I hu = gm1 - (I)u * Pg;
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
+                    if ((u & 1) && (v & 1)) continue;
                     const int q = quad_of(u >> 1, v >> 1);
                     const int qq = quad_of(u & 1, v & 1);
-                    if (crosses<I>(hu - (I)v * Qg, Ug)) acc[q] += 1u << (8 * qq);
+                    const bool c = crosses<I>(hu - (I)v * Qg, Ug);
+                    if ((n++ & 1) == 0) {
+                        if (c) acc[q] += 1u << (8 * qq);                   // ALU pipe
+                    } else {
+                        mad_if(c, acc[q], one, 1u << (8 * qq));            // FMA pipe
+                    }
                 }
             }
         }
@@ -198,8 +215,8 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
 
         uint32_t cm = 0;
         uint32_t acc[4] = {0, 0, 0, 0};
-        if (beta) chunk_math<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, cm, acc);
-        else chunk_math<I, MODE, false>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, cm, acc);
+        if (beta) chunk_math<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc);
+        else chunk_math<I, MODE, false>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc);
 
         if (MODE == MODE_COUNT) {
             uint32_t c02, c13;
@@ -216,7 +233,7 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
             if (nfq[q] == kNone) continue;                  // warp-uniform
             uint32_t c02, c13;
             warp_sum_bytes(acc[q], c02, c13);
-            if (lane < 4) {
+            if (lane >= 1 && lane < 4) {             // NE (lane 0) is derived in the split
                 const uint32_t v = byte_counter(c02, c13, lane);
                 if (v) atomicAdd(A.votes + 4 * (uint64_t)(nfq[q] - A.q0) + lane, v);
             }
@@ -575,6 +592,10 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
         pa = __ldg(A.p_a + p);
         pc = __ldg(A.p_c + p);
     }
+    if (valid && A.derive_ne) {   // votes(parent) = votes(SW child) + votes(NE child)
+        V.x = __ldg(A.p_votes + p) - V.z;
+        VL.x = __ldg(A.p_len + p) - VL.z;
+    }
     const uint32_t v[4] = {V.x, V.y, V.z, V.w};
     const uint32_t vl[4] = {VL.x, VL.y, VL.z, VL.w};
     uint32_t flag[4], len[4], nch[4];
@@ -583,7 +604,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         flag[q] = (valid && (uint64_t)v[q] > A.T) ? 1u : 0u;          // strict: votes > THRESHOLD
-        len[q] = (flag[q] && A.need_lists) ? vl[q] : 0u;
+        len[q] = (flag[q] && A.need_lists) ? vl[q] : 0u;   // list entries on this rank
         nch[q] = (len[q] + kChunk - 1) / kChunk;
         mine.F += flag[q];
         mine.C += nch[q];
@@ -668,7 +689,8 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
                     A.out.a[f] = ca;
                     A.out.c[f] = cb;
                     A.out.parent[f] = A.parent_base + p;
-                    A.out.len[f] = len[q];
+                    A.out.len[f] = vl[q];
+                    A.out.votes[f] = v[q];
                     A.out.off[f] = s;
                     A.out.choff[f] = cc;
                 }

@@ -30,7 +30,8 @@ def compare_all(h, ref, halves, D, image=0):
 def check_structure(levels, E, T, D):
     """levels[l] = uint32 [k, 3] records (a, c, votes) of one tree in depth-first order. Checks:
     root = E; the visited set at l+1 is exactly the children (NE,NW,SW,SE) of the regions at l with
-    votes > T, in order; child <= parent; parent <= sum(children) <= 3*parent.
+    votes > T, in order; child <= parent; parent <= sum(children) <= 3*parent (SURVEY.md §0 L5-L7);
+    votes(parent) = votes(SW child) + votes(NE child).
     Returns (tests, votes) recomputed from the records."""
     assert levels[0].tolist() == [[0, 0, E]]
     tests, votes = E, int(levels[0][:, 2].sum())
@@ -49,6 +50,7 @@ def check_structure(levels, E, T, D):
         assert (cv.max(axis=1) <= Ps[:, 2]).all(), f"child > parent at level {lev + 1}"
         s = cv.sum(axis=1)
         assert (s >= Ps[:, 2]).all() and (s <= 3 * Ps[:, 2]).all(), f"sum of children at level {lev + 1}"
+        assert np.array_equal(cv[:, 0] + cv[:, 2], Ps[:, 2]), f"votes != SW + NE at level {lev}"
         tests += 4 * int(Ps[:, 2].sum())
         votes += int(Cn[:, 2].sum())
     return tests, votes

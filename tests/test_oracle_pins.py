@@ -211,6 +211,9 @@ def _check_tree(pts, N, D, T, half, r):
                 ch = [next(kids)[2] for _ in range(4)]
                 assert max(ch) <= v
                 assert v <= sum(ch) <= 3 * v
+                # G_SW >= G_centre >= G_NE: a line crosses R iff it crosses exactly one of R's SW
+                # child (G_SW > 0 >= G_centre) and NE child (G_centre > 0 >= G_NE)
+                assert v == ch[2] + ch[0]
     # leaves = {leaf : brute votes > T} (removal off)
     leaves = {(int(i), int(j)) for h, i, j, _ in r.leaves.tolist() if h == half}
     brute = {(a, c) for c, a in zip(*np.nonzero(dense[D] > T))}
