@@ -242,15 +242,22 @@ def main():
     d = prof_tot[dom]
     avg_ms = d["ms"] / max(d["launches"], 1)
     achieved = (d["bytes"] / max(d["launches"], 1)) / (avg_ms / 1e3) / 1e9 if d["launches"] else 0.0
-    traffic = None
+    # traffic: DRAM bytes of one launch of the same kernel class from the committed ncu --set full
+    # capture (profiles/ncu_traffic.json), with that launch's algorithmic bytes beside it
+    traffic, cap = None, {}
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"config{cfg.cid}", {}).get(dom)
+            cap = json.load(open(tpath)).get(f"config{cfg.cid}", {}).get(dom, {}) or {}
+            traffic = cap.get("traffic")
         except Exception:
-            traffic = None
+            cap = {}
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                "traffic_launch_algorithmic_bytes": cap.get("algorithmic_bytes"),
+                "binding_unit": ("SM integer pipes (ncu: issue active %.0f%%, ALU pipe %.0f%%, FMA pipe %.0f%%, DRAM %.0f%%)"
+                                 % (cap["issue_active_pct"], cap["alu_pipe_pct"], cap["fma_pipe_pct"], cap["dram_pct"])
+                                 if cap.get("issue_active_pct") is not None else None),
                 "kernel_share_of_step": d["ms"] / max(sum(step_ms), 1e-9),
                 "launches": d["launches"], "avg_launch_ms": avg_ms,
                 "algorithmic_bytes_per_launch": d["bytes"] / max(d["launches"], 1)}
@@ -258,11 +265,12 @@ def main():
     e2e = None
     if not a.no_e2e:
         host = torch.from_numpy(np.ascontiguousarray(my)).pin_memory()
-        h2 = hht.HHT(device=local, halves=cfg.halves, record_levels=True,
-                     rank=rank if comm_world > 1 else 0, world=comm_world, nccl_id=None) if comm_world == 1 else h
+        h2 = h
         hnp = host.numpy()
         h2.detect_batch(hnp, my_offs, cfg.N, cfg.D, cfg.T)   # warm
-        h2.leaves()
+        nleaf = h2.stats()["leaves"]
+        lbuf = torch.empty((max(int(nleaf * 1.1) + 1024, 1024), 5), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+        h2.leaves_into(lbuf)
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -270,8 +278,8 @@ def main():
         d2h = 0
         for _ in range(e_steps):
             h2.detect_batch(hnp, my_offs, cfg.N, cfg.D, cfg.T)   # H2D inside the call
-            lv = h2.leaves()                                       # D2H of the detected lines
-            d2h = lv.shape[0] * 16
+            nl = h2.leaves_into(lbuf)                              # D2H of the detected lines
+            d2h = nl * 20
         torch.cuda.synchronize()
         et = time.perf_counter() - t0
         if world > 1:
@@ -280,7 +288,7 @@ def main():
             et = float(t.item())
         e2e = {"value": tests_tot / a.steps * e_steps / et, "unit": UNIT,
                "h2d_bytes_per_step": int(hnp.nbytes), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": 1e3 * et / e_steps, "timing": "wall clock around detect(host points) + leaves()"}
+               "ms_per_step": 1e3 * et / e_steps, "timing": "wall clock around detect_batch(pinned host points) + leaves_into(pinned buffer)"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

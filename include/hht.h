@@ -140,6 +140,17 @@ hht_status hht_result_level(hht_ctx* ctx, int32_t image, uint32_t half, int32_t 
 hht_status hht_result_stats(hht_ctx* ctx, hht_stats* out);
 hht_status hht_result_profile(hht_ctx* ctx, hht_profile* out);
 
+/* One kernel launch of the last detect (opts.profile = 1), in launch order. */
+typedef struct {
+    uint32_t cls;            /* hht_profile class index */
+    uint32_t reserved;
+    uint64_t bytes;          /* algorithmic HBM bytes of this launch */
+    double ms;               /* CUDA-event duration */
+} hht_launch;
+
+/* Per-launch log of the last detect (opts.profile = 1); same cap/count protocol as the getters. */
+hht_status hht_result_launches(hht_ctx* ctx, hht_launch* out, int64_t cap, int64_t* count);
+
 /* Device-time bracket on the ctx stream (CUDA events): begin records, end records, synchronises
  * and returns the milliseconds between the two. */
 hht_status hht_timer_begin(hht_ctx* ctx);

@@ -79,7 +79,7 @@ struct hht_ctx {
     std::vector<uint8_t> tree_half;         // HHT_ALPHA / HHT_BETA per tree
     std::vector<int64_t> tree_E;            // global points per tree
 
-    Buf stage_in, packed, errflag, beta, stats, tiles, tilectr, totals, rng, bounds, vtmp, dense, gv;
+    Buf stage_in, packed, errflag, beta, stats, tiles, tilectr, totals, rng, bounds, vtmp, dense, gv, leafrows;
     Totals* totals_h = nullptr;
     RangeInfo* range_h = nullptr;
     uint64_t* misc_h = nullptr;
@@ -94,6 +94,7 @@ struct hht_ctx {
     hht_profile prof{};
     std::vector<ProfEv> pev;
     size_t pev_used = 0;
+    std::vector<hht_launch> launch_log;
 };
 
 namespace {
@@ -687,6 +688,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, x->ev0, x->ev1));
     x->stat.ms = ms;
+    x->launch_log.clear();
     if (x->opts.profile) {
         for (size_t i = 0; i < x->pev_used; ++i) {
             float m = 0;
@@ -694,6 +696,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
                 x->prof.ms[x->pev[i].cls] += m;
                 x->prof.launches[x->pev[i].cls] += 1;
                 x->prof.bytes[x->pev[i].cls] += x->pev[i].bytes;
+                x->launch_log.push_back({(uint32_t)x->pev[i].cls, 0, x->pev[i].bytes, (double)m});
             }
         }
     }
@@ -837,6 +840,20 @@ hht_status hht_result_leaves(hht_ctx* x, int32_t image, hht_leaf* out, int64_t c
     if (!x || !count) return HHT_EINVAL;
     if (!x->have) return set_err(x, HHT_ESTATE, "no successful detect yet");
     if (image < -1 || image >= x->B) return set_err(x, HHT_EINVAL, "image out of range");
+    if (image == -1) {
+        // every leaf: convert on the device, then one copy into the caller's buffer
+        *count = (int64_t)x->leaves.n;
+        if (cap < *count) return set_err(x, HHT_EINVAL, "cap %lld < %lld leaves", (long long)cap, (long long)*count);
+        if (!*count) return HHT_OK;
+        if (!out) return set_err(x, HHT_EINVAL, "out is NULL");
+        TRY(ensure(x, x->leafrows, x->leaves.n * sizeof(hht_leaf)));
+        CK(launch_leaf_rows((const LeafRec*)x->leaves.b.p, x->leaves.n, (const uint8_t*)x->beta.p, x->H,
+                            (uint32_t*)x->leafrows.p, x->st));
+        CK(cudaMemcpyAsync(out, x->leafrows.p, x->leaves.n * sizeof(hht_leaf), cudaMemcpyDefault, x->st));
+        TRY(sync(x));
+        x->stat.d2h_bytes += x->leaves.n * sizeof(hht_leaf);
+        return HHT_OK;
+    }
     TRY(host_leaves(x));
     const auto& L = x->leaves_host;
     uint64_t b = 0, e = L.size();
@@ -900,6 +917,16 @@ hht_status hht_result_profile(hht_ctx* x, hht_profile* out) {
     return HHT_OK;
 }
 
+hht_status hht_result_launches(hht_ctx* x, hht_launch* out, int64_t cap, int64_t* count) {
+    if (!x || !count) return HHT_EINVAL;
+    if (!x->have) return set_err(x, HHT_ESTATE, "no successful detect yet");
+    *count = (int64_t)x->launch_log.size();
+    if (cap < *count) return set_err(x, HHT_EINVAL, "cap %lld < %lld launches", (long long)cap, (long long)*count);
+    if (*count && !out) return set_err(x, HHT_EINVAL, "out is NULL");
+    for (int64_t i = 0; i < *count; ++i) out[i] = x->launch_log[i];
+    return HHT_OK;
+}
+
 hht_status hht_timer_begin(hht_ctx* x) {
     if (!x) return HHT_EINVAL;
     CK(cudaEventRecord(x->tb0, x->st));
@@ -933,7 +960,7 @@ void hht_destroy(hht_ctx* x) {
     for (auto& g : x->rec) fr(g.b);
     fr(x->leaves.b);
     for (Buf* b : {&x->stage_in, &x->packed, &x->errflag, &x->beta, &x->stats, &x->tiles, &x->tilectr, &x->totals,
-                   &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv})
+                   &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv, &x->leafrows})
         fr(*b);
     if (x->totals_h) cudaFreeHost(x->totals_h);
     if (x->range_h) cudaFreeHost(x->range_h);

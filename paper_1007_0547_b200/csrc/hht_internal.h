@@ -133,6 +133,8 @@ cudaError_t launch_range(const uint64_t* c_off, const uint32_t* c_parent, uint32
                          uint64_t* chunk_bounds, cudaStream_t st);
 int pass_blocks_per_sm(int mode, bool int64);
 int tail_blocks_per_sm(bool int64);
+cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_beta, uint32_t H, uint32_t* out,
+                             cudaStream_t st);
 cudaError_t launch_tail(bool int64, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_gather(const uint32_t* dense, uint32_t anc_base, const uint32_t* anc_a, const uint32_t* anc_c,
                           const uint32_t* p_a, const uint32_t* p_c, const uint32_t* p_parent,

@@ -474,6 +474,31 @@ cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint
     return cudaGetLastError();
 }
 
+// Leaf records (tree, i, j, votes) -> the ABI's hht_leaf rows (image, half, i, j, votes).
+__global__ void __launch_bounds__(256) k_leaf_rows(const LeafRec* __restrict__ in, uint64_t n,
+                                                   const uint8_t* __restrict__ tree_beta, uint32_t H,
+                                                   uint32_t* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += stride) {
+        const LeafRec r = in[k];
+        uint32_t* o = out + 5 * k;
+        o[0] = r.tree / H;
+        o[1] = tree_beta[r.tree] ? 2u : 1u;
+        o[2] = r.i;
+        o[3] = r.j;
+        o[4] = r.votes;
+    }
+}
+
+cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_beta, uint32_t H, uint32_t* out,
+                             cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_leaf_rows<<<(unsigned)blocks, 256, 0, st>>>(in, n, tree_beta, H, out);
+    return cudaGetLastError();
+}
+
 template <typename I, int MODE>
 static int blocks_per_sm_impl() {
     int n = 0;

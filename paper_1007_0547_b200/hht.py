@@ -25,8 +25,8 @@ STATUS = {0: "HHT_OK", 1: "HHT_EINVAL", 2: "HHT_ERANGE", 3: "HHT_EOVERFLOW", 4: 
 # names the header declares (tests check every one is exported)
 EXPORTS = ["hht_default_opts", "hht_create", "hht_nccl_unique_id", "hht_detect", "hht_detect_batch",
            "hht_result_leaves", "hht_result_level", "hht_result_stats", "hht_result_profile",
-           "hht_timer_begin", "hht_timer_end", "hht_last_error", "hht_status_str", "hht_destroy",
-           "hht_version"]
+           "hht_result_launches", "hht_timer_begin", "hht_timer_end", "hht_last_error", "hht_status_str",
+           "hht_destroy", "hht_version"]
 
 PROFILE_CLASSES = ["stage", "count", "write", "tail", "split", "gather", "other", "allreduce"]
 
@@ -56,6 +56,10 @@ class Stats(C.Structure):
                 ("ranges", C.c_uint32), ("images", C.c_uint32), ("ms", C.c_double)]
 
 
+class Launch(C.Structure):
+    _fields_ = [("cls", C.c_uint32), ("reserved", C.c_uint32), ("bytes", C.c_uint64), ("ms", C.c_double)]
+
+
 class Profile(C.Structure):
     _fields_ = [("launches", C.c_uint64 * 8), ("ms", C.c_double * 8), ("bytes", C.c_uint64 * 8)]
 
@@ -82,6 +86,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hht_result_level": ([p, i32, u32, i32, p, i64, p], C.c_int),
         "hht_result_stats": ([p, p], C.c_int),
         "hht_result_profile": ([p, p], C.c_int),
+        "hht_result_launches": ([p, p, i64, p], C.c_int),
         "hht_timer_begin": ([p], C.c_int),
         "hht_timer_end": ([p, p], C.c_int),
         "hht_last_error": ([p], C.c_char_p),
@@ -197,8 +202,25 @@ class HHT:
         return self
 
     # --- results -------------------------------------------------------------------------------
+    def leaves_into(self, out: np.ndarray) -> int:
+        """Copy every image's leaves as uint32 rows (image, half, i, j, votes) into `out` (a C-contiguous
+        uint32 [cap, 5] array, e.g. a pinned buffer); returns the count."""
+        assert out.dtype == np.uint32 and out.ndim == 2 and out.shape[1] == 5 and out.flags.c_contiguous
+        cnt = C.c_int64(0)
+        self._check(self._lib.hht_result_leaves(self._ctx, -1, C.c_void_p(out.ctypes.data), out.shape[0],
+                                                C.byref(cnt)))
+        return cnt.value
+
     def leaves(self, image: int = -1) -> np.ndarray:
         """int64 [L, 5]: (image, half, i, j, votes) in image, half, depth-first order."""
+        if image == -1:
+            cnt = C.c_int64(0)
+            st = self._lib.hht_result_leaves(self._ctx, -1, None, 0, C.byref(cnt))
+            if st and cnt.value == 0:
+                self._check(st)
+            buf = np.empty((max(cnt.value, 1), 5), dtype=np.uint32)
+            n = self.leaves_into(buf)
+            return buf[:n].astype(np.int64)
         cnt = C.c_int64(0)
         st = self._lib.hht_result_leaves(self._ctx, image, None, 0, C.byref(cnt))
         if st and cnt.value == 0:
@@ -233,6 +255,16 @@ class HHT:
         self._check(self._lib.hht_result_profile(self._ctx, C.byref(p)))
         return {name: {"launches": p.launches[k], "ms": p.ms[k], "bytes": p.bytes[k]}
                 for k, name in enumerate(PROFILE_CLASSES)}
+
+    def launches(self) -> list:
+        """Per-launch log of the last detect (profile=True): [(class name, algorithmic bytes, ms)]."""
+        cnt = C.c_int64(0)
+        st = self._lib.hht_result_launches(self._ctx, None, 0, C.byref(cnt))
+        if st and cnt.value == 0:
+            self._check(st)
+        out = (Launch * max(cnt.value, 1))()
+        self._check(self._lib.hht_result_launches(self._ctx, out, cnt.value, C.byref(cnt)))
+        return [(PROFILE_CLASSES[out[i].cls], out[i].bytes, out[i].ms) for i in range(cnt.value)]
 
     def timer_begin(self):
         self._check(self._lib.hht_timer_begin(self._ctx))

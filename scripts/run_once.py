@@ -22,8 +22,18 @@ else:
     pts, _ = synth.config_image(a.config)
     offs = np.array([0, len(pts)])
 d = torch.from_numpy(pts).cuda()
-h = hht.HHT(halves=cfg.halves, mem_budget=a.budget)
+h = hht.HHT(halves=cfg.halves, mem_budget=a.budget, profile=True)
 for _ in range(a.reps):
     h.detect_batch(d, offs, cfg.N, cfg.D, cfg.T)
 st = h.stats()
 print({k: st[k] for k in ("tests", "votes", "leaves", "pairs", "ranges", "ms", "int_bits")})
+# per-launch algorithmic bytes, to pair with an ncu capture of the same launch (ncu -k regex:k_tail -c 1
+# is the first "tail" launch; ncu -k regex:k_pass -s S -c 1 is k_pass launch S counting the root count)
+log = h.launches()
+by = {}
+for cls, b, ms in log:
+    by.setdefault(cls, []).append((b, ms))
+for cls in ("count", "write", "tail"):
+    xs = by.get(cls, [])
+    if xs:
+        print(cls, "launches", len(xs), "first bytes", xs[0][0], "bytes[:16]", [b for b, _ in xs[:16]])
