@@ -64,7 +64,8 @@ typedef struct {
     uint32_t record_levels;  /* 1 (default): keep every level's (a, c, votes) records */
     uint32_t force_int64;    /* 1: use the int64 kernels even where int32 is exact (testing) */
     uint32_t profile;        /* 1: time every kernel launch with CUDA events (hht_result_profile) */
-    uint32_t reserved;
+    uint32_t tail_depth;     /* levels counted by the dense leaf-grid tail: 0 = auto (4 when
+                                depth >= 4, else 3), 3 or 4 to force (results are identical) */
     size_t mem_budget;       /* device bytes for candidate lists; 0 = 80% of free memory at create.
                                 Levels whose lists do not fit are processed in depth-first ranges. */
     const void* nccl_id;     /* world > 1: 128-byte ncclUniqueId from hht_nccl_unique_id on rank 0,

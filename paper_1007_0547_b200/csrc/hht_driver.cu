@@ -70,6 +70,7 @@ struct hht_ctx {
     size_t budget = 0;
     int grid[3][2] = {};
     int tail_grid[2] = {};
+    int tail16_grid[2] = {};
 
     // last call
     int N = 0, D = 0, B = 0, H = 0, ntrees = 0;
@@ -98,6 +99,13 @@ struct hht_ctx {
 };
 
 namespace {
+
+
+// Levels covered by the dense tail: a 16x16 leaf grid under level D-4 when D >= 4, else 8x8.
+int tail_depth(const hht_ctx* x) {
+    const int want = x->opts.tail_depth ? (int)x->opts.tail_depth : 4;
+    return (want >= 4 && x->D >= 4) ? 4 : 3;
+}
 
 hht_status set_err(hht_ctx* x, hht_status s, const char* fmt, ...) {
     char buf[512];
@@ -213,9 +221,9 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
     if (Fp == 0) return HHT_OK;
     Level& C = x->lv[child_level];
     const bool leaf = child_level == x->D;
-    // lists are read by write passes (levels <= D-4) and the dense tail (level D-3); for D = 2 the
+    // lists are read by write passes (levels < D-TK) and the dense tail (level D-TK); for D = 2 the
     // count-only pass reads the roots' lists (the points themselves)
-    const bool need_lists = child_level <= x->D - 3;
+    const bool need_lists = child_level <= x->D - tail_depth(x);
     const uint64_t nch = 4ull * Fp;
     if (!leaf) {
         TRY(ensure(x, C.tree, nch * 4));
@@ -342,15 +350,18 @@ hht_status choose_range(hht_ctx* x, int lc, uint32_t q0, uint64_t cap_entries, b
     return HHT_OK;
 }
 
-// Dense tail at level L = D-3 (D >= 3): lv[L] holds the lists of R_L[r0, r1) and lv[L+1] holds
-// R_(D-2) (its split children, without lists). Counts the level D-1 and D grids of every R_L
-// region in one pass, then splits level D-1 and emits the leaves from the gathered votes.
+// Dense tail at level L = D-TK (D >= 3): lv[L] holds the lists of R_L[r0, r1) and lv[L+1] holds
+// R_(L+1) (its split children, without lists). One pass counts the 2^TK x 2^TK leaf grid of every
+// R_L region; every deeper level is then split from votes gathered out of the grids (a region's
+// votes = the sum of its diagonal leaves), down to the leaves.
 hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
+    const int TK = x->D - L;
+    const uint32_t cells = 1u << (2 * TK);
     Level& P = x->lv[L];
     const uint32_t n = r1 - r0;
     if (n == 0) return HHT_OK;
-    TRY(ensure(x, x->dense, (size_t)n * kTailCells * 4));
-    CK(cudaMemsetAsync(x->dense.p, 0, (size_t)n * kTailCells * 4, x->st));
+    TRY(ensure(x, x->dense, (size_t)n * cells * 4));
+    CK(cudaMemsetAsync(x->dense.p, 0, (size_t)n * cells * 4, x->st));
     CK(launch_bounds((const uint64_t*)P.off.p, (const uint64_t*)P.choff.p, (const uint32_t*)P.len.p, r0, r1, L == 0,
                      (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->st));
     CK(cudaMemcpyAsync(x->range_h, x->rng.p, sizeof(RangeInfo), cudaMemcpyDeviceToHost, x->st));
@@ -358,33 +369,30 @@ hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
     a.nf_rbase = r0;
     a.votes = (uint32_t*)x->dense.p;
     const int id = prof_begin(x, 3, 0);
-    CK(launch_tail(x->int64, a, x->tail_grid[x->int64 ? 1 : 0], x->st));
+    if (TK == 4) CK(launch_tail16(x->int64, a, x->tail16_grid[x->int64 ? 1 : 0], x->st));
+    else CK(launch_tail(x->int64, a, x->tail_grid[x->int64 ? 1 : 0], x->st));
     prof_end(x, id);
     TRY(sync(x));
     const uint64_t pairs = x->range_h->pairs;
-    if (id >= 0) x->pev[id].bytes = pairs * 4 + (uint64_t)n * kTailCells * 4;
+    if (id >= 0) x->pev[id].bytes = pairs * 4 + (uint64_t)n * cells * 4;
     x->stat.pairs += pairs;
-    TRY(allreduce_sum_u32(x, (uint32_t*)x->dense.p, (size_t)n * kTailCells));
-    // level D-1: parents R_(D-2), votes from the 4x4 grids
-    Level& P1 = x->lv[L + 1];
-    if (P1.F == 0) return HHT_OK;
-    TRY(ensure(x, x->gv, 16ull * P1.F));
-    const int g1 = prof_begin(x, 5, 16ull * P1.F + 32ull * P1.F);
-    CK(launch_gather((const uint32_t*)x->dense.p, r0, (const uint32_t*)P.a.p, (const uint32_t*)P.c.p,
-                     (const uint32_t*)P1.a.p, (const uint32_t*)P1.c.p, (const uint32_t*)P1.parent.p, nullptr, 1, P1.F,
-                     (uint32_t*)x->gv.p, x->st));
-    prof_end(x, g1);
-    TRY(do_split(x, L + 2, P1, 0, P1.F, (const uint32_t*)x->gv.p, (const uint32_t*)x->gv.p));
-    // level D: parents R_(D-1), votes from the 8x8 grids
-    Level& P2 = x->lv[L + 2];
-    if (P2.F == 0) return HHT_OK;
-    TRY(ensure(x, x->gv, 16ull * P2.F));
-    const int g2 = prof_begin(x, 5, 16ull * P2.F + 36ull * P2.F);
-    CK(launch_gather((const uint32_t*)x->dense.p, r0, (const uint32_t*)P.a.p, (const uint32_t*)P.c.p,
-                     (const uint32_t*)P2.a.p, (const uint32_t*)P2.c.p, (const uint32_t*)P2.parent.p,
-                     (const uint32_t*)P1.parent.p, 2, P2.F, (uint32_t*)x->gv.p, x->st));
-    prof_end(x, g2);
-    return do_split(x, L + 3, P2, 0, P2.F, (const uint32_t*)x->gv.p, (const uint32_t*)x->gv.p);
+    TRY(allreduce_sum_u32(x, (uint32_t*)x->dense.p, (size_t)n * cells));
+    // levels L+2 .. D: parents R_(c-1), votes gathered from the grids
+    for (int c = L + 2; c <= x->D; ++c) {
+        Level& Pc = x->lv[c - 1];
+        if (Pc.F == 0) return HHT_OK;
+        const int hops = c - 1 - L;
+        GatherChain chain{};
+        for (int h = 0; h < hops; ++h) chain.parent[h] = (const uint32_t*)x->lv[c - 1 - h].parent.p;
+        TRY(ensure(x, x->gv, 16ull * Pc.F));
+        const int g = prof_begin(x, 5, (16ull + 8 + 4ull * hops + 16ull * (1u << (x->D - c))) * Pc.F);
+        CK(launch_gather((const uint32_t*)x->dense.p, r0, (const uint32_t*)P.a.p, (const uint32_t*)P.c.p,
+                         (const uint32_t*)Pc.a.p, (const uint32_t*)Pc.c.p, chain, hops, TK, x->D - c, Pc.F,
+                         (uint32_t*)x->gv.p, x->st));
+        prof_end(x, g);
+        TRY(do_split(x, c, Pc, 0, Pc.F, (const uint32_t*)x->gv.p, (const uint32_t*)x->gv.p));
+    }
+    return HHT_OK;
 }
 
 // Preconditions: lv[l] holds the lists of R_l[r0, r1) and lv[l+1] holds R_(l+1) = the split
@@ -392,7 +400,7 @@ hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
 hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
     const int lc = l + 1;
     if (lc >= x->D) return HHT_OK;
-    if (x->D >= 3 && l == x->D - 3) return tail(x, l, r0, r1);
+    if (x->D >= 3 && l == x->D - tail_depth(x)) return tail(x, l, r0, r1);
     Level& P = x->lv[l];
     Level& C = x->lv[lc];
     const uint32_t Fc = C.F;
@@ -778,6 +786,7 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return HHT_EINVAL;
     if (o.world > 1 && !o.nccl_id) return HHT_EINVAL;
     if (o.halves == 0 || (o.halves & ~3u)) return HHT_EINVAL;
+    if (!(o.tail_depth == 0 || o.tail_depth == 3 || o.tail_depth == 4)) return HHT_EINVAL;
     hht_ctx* x = new (std::nothrow) hht_ctx();
     if (!x) return HHT_ENOMEM;
     x->opts = o;
@@ -802,6 +811,7 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     for (int m = 0; m < 3; ++m)
         for (int w = 0; w < 2; ++w) x->grid[m][w] = x->sms * pass_blocks_per_sm(m, w == 1);
     for (int w = 0; w < 2; ++w) x->tail_grid[w] = x->sms * tail_blocks_per_sm(w == 1);
+    for (int w = 0; w < 2; ++w) x->tail16_grid[w] = x->sms * tail16_blocks_per_sm(w == 1);
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return fail(HHT_ECUDA);
     x->budget = o.mem_budget ? o.mem_budget : (size_t)(0.70 * (double)fr);

@@ -12,7 +12,8 @@ constexpr int kItems = 8;                  // list entries per lane per chunk
 constexpr int kChunk = kWarp * kItems;     // 256 entries: one warp work unit, never spans regions
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr int kSplitThreads = 256;         // split kernel: one thread per parent (its 4 children)
-constexpr int kTailCells = 64;             // dense tail grid per level-(D-3) region: 8x8 leaves
+constexpr int kTailCells = 64;             // 8x8 tail: leaf grid per level-(D-3) region
+constexpr int kTail16Cells = 256;          // 16x16 tail: leaf grid per level-(D-4) region
 
 // Quad order of the paper: q = 0 NE, 1 NW, 2 SW, 3 SE; child (2a+da, 2c+dc).
 __host__ __device__ constexpr uint32_t quad_da(int q) { return (q == 0 || q == 3) ? 1u : 0u; }
@@ -136,9 +137,12 @@ int tail_blocks_per_sm(bool int64);
 cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_beta, uint32_t H, uint32_t* out,
                              cudaStream_t st);
 cudaError_t launch_tail(bool int64, const PassArgs& a, int grid, cudaStream_t st);
+struct GatherChain { const uint32_t* parent[3]; };   // parent-index arrays, nearest level first
 cudaError_t launch_gather(const uint32_t* dense, uint32_t anc_base, const uint32_t* anc_a, const uint32_t* anc_c,
-                          const uint32_t* p_a, const uint32_t* p_c, const uint32_t* p_parent,
-                          const uint32_t* pp_parent, int kk, uint32_t Fp, uint32_t* V, cudaStream_t st);
+                          const uint32_t* p_a, const uint32_t* p_c, const GatherChain& chain, int hops, int tk,
+                          int j, uint32_t Fp, uint32_t* V, cudaStream_t st);
+int tail16_blocks_per_sm(bool int64);
+cudaError_t launch_tail16(bool int64, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
                           int is_root, RangeInfo* info, uint64_t* chunk_bounds, cudaStream_t st);
 

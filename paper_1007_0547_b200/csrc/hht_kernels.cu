@@ -341,7 +341,7 @@ __device__ __forceinline__ void tail_math(const uint32_t (&p)[kItems], int cnt, 
         for (int u = 0; u < 8; ++u) {
             y -= P8;
             const bool drop = y < Kq;
-            const uint2 m = tab[kk + (drop ? 1 : 0)];
+            const uint2 m = tab[16 * (kk + (drop ? 1 : 0))];
             a8[2 * u] += m.x;
             a8[2 * u + 1] += m.y;
             if (drop) {
@@ -352,10 +352,11 @@ __device__ __forceinline__ void tail_math(const uint32_t (&p)[kItems], int cnt, 
     }
 }
 
+// Table replicated 16x (an LDS.64 serves 16 lanes per wavefront): lane l reads copy (l & 15).
 template <typename I>
 __global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
-    __shared__ uint2 s_tab[kTab8];
-    if (threadIdx.x < kTab8) s_tab[threadIdx.x] = tab8_entry(threadIdx.x);
+    __shared__ uint2 s_tab[kTab8 * 16];
+    for (int t = threadIdx.x; t < kTab8 * 16; t += blockDim.x) s_tab[t] = tab8_entry(t >> 4);
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -388,8 +389,8 @@ __global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
         uint32_t a8[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) a8[i] = 0;
-        if (beta) tail_math<I, true>(p, cnt, lane, alpha, beta_m1, D, N3, s_tab, a8);
-        else tail_math<I, false>(p, cnt, lane, alpha, beta_m1, D, N3, s_tab, a8);
+        if (beta) tail_math<I, true>(p, cnt, lane, alpha, beta_m1, D, N3, s_tab + (lane & 15), a8);
+        else tail_math<I, false>(p, cnt, lane, alpha, beta_m1, D, N3, s_tab + (lane & 15), a8);
 
         // grid[(r - nf_rbase) * 64 + 8u + v]: a8[2u] byte b = row b, a8[2u+1] byte b = row 4+b
         uint32_t* dst = A.votes + (uint64_t)(r - A.nf_rbase) * kTailCells;
@@ -405,6 +406,166 @@ __global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// 16x16 dense tail (level L = D-4): the same raster over a 16x16 leaf grid. Every level below L+1
+// then comes from the leaf grid: a line crosses a region iff it crosses exactly one of the region's
+// diagonal (SW..NE) leaves (the SW+NE identity applied recursively), so
+// votes(region of side 2^j leaves) = sum of its 2^j diagonal leaf counts.
+// The 64 per-lane counter words do not fit in registers, so the grid is processed in 4 column
+// blocks of 4 columns; each line's raster state (y, k, threshold) is carried across blocks, and
+// each block's 16 counter words are reduced across the warp with a butterfly reduce-scatter
+// (16 shuffles) that leaves every lane with the warp totals of 2 cells.
+// ---------------------------------------------------------------------------------------------
+constexpr int kTab16 = 68;  // (k + 16) * 2 + drop, k in -16..17
+
+__device__ __forceinline__ uint4 tab16_entry(int t) {
+    const int k = t / 2 - 16, d = t & 1;
+    uint32_t w[4] = {0, 0, 0, 0};
+    if (k >= 1) {
+        const int vhi = min(k, 16) - 1, vlo = max(k - d - 1, 0);
+        for (int v = vlo; v <= vhi; ++v) w[v >> 2] |= 1u << (8 * (v & 3));
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// The mask table is replicated 8x, entry e of copy c at slot 8e + c: an LDS.128 serves 8 lanes per
+// shared-memory wavefront, and lane l reads copy (l & 7), i.e. its own bank group, so lookups are
+// bank-conflict-free whatever entries the lanes need.
+template <typename I>
+__global__ void __launch_bounds__(256, 3) k_tail16(const PassArgs A) {
+    __shared__ uint4 s_tab[kTab16 * 8];
+    for (int t = threadIdx.x; t < kTab16 * 8; t += blockDim.x) s_tab[t] = tab16_entry(t >> 3);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint4* tabl = s_tab + (lane & 7);
+    const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t c_lo = A.chunk_bounds[0], c_hi = A.chunk_bounds[1];
+    const int D = A.D;
+    const int sh = D - A.level;                       // == 4
+    const I N = (I)A.N;
+    const I N3 = (I)3 * N;
+
+    for (uint64_t ch = c_lo + warp0; ch < c_hi; ch += nwarps) {
+        const uint32_t r = __ldg(A.chunk_region + ch);
+        const uint64_t k = ch - __ldg(A.p_choff + r);
+        const uint32_t len = __ldg(A.p_len + r);
+        const uint64_t e0 = __ldg(A.p_off + r) - A.list_base + k * kChunk;
+        const int cnt = (int)min((uint64_t)kChunk, (uint64_t)len - k * kChunk);
+        const uint32_t tree = __ldg(A.p_tree + r);
+        const bool beta = __ldg(A.tree_beta + tree) != 0;
+        const I i0 = (I)__ldg(A.p_a + r) << sh;
+        const I j0 = (I)__ldg(A.p_c + r) << sh;
+        const I alpha = ((I)1 << D) - 2 * i0;
+        const I beta_m1 = (N << D) - N3 * j0 - 1;
+
+        // per-line raster state carried across the 4 column blocks: z = y - (k-1)*3N (height of the
+        // line above its row's floor at the current lattice column; a column drops iff z < 0),
+        // the table index of (k, 0), and the column step 2ex
+        I z[kItems], P8[kItems];
+        int kk[kItems];
+#pragma unroll
+        for (int it = 0; it < kItems; ++it) {
+            const int idx = lane + kWarp * it;
+            const uint32_t w = (idx < cnt) ? __ldcs(A.list + e0 + idx) : 0u;
+            const I ex = (I)(beta ? (w & 0xFFFFu) : (w >> 16));
+            const I ey = (I)(beta ? (w >> 16) : (w & 0xFFFFu));
+            I yy = ex * alpha + (ey << D) + beta_m1;          // G(SW corner of R) - 1
+            if (idx >= cnt) yy = (I)-1;
+            // f = min(floor(y / 3N), 16) for y >= 0 (branch-free binary search)
+            I f = (yy >= (I)8 * N3) ? (I)8 : (I)0;
+            f += (yy >= (f + 4) * N3) ? (I)4 : (I)0;
+            f += (yy >= (f + 2) * N3) ? (I)2 : (I)0;
+            f += (yy >= (f + 1) * N3) ? (I)1 : (I)0;
+            f = (yy >= (I)16 * N3) ? (I)16 : f;
+            const bool below = yy < 0;
+            P8[it] = 2 * ex;
+            z[it] = below ? yy + N3 : yy - f * N3;
+            kk[it] = below ? 32 : 2 * (int)f + 34;           // table index of (k, 0): 2 * (k + 16)
+        }
+        uint32_t* dst = A.votes + (uint64_t)(r - A.nf_rbase) * kTail16Cells;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            uint32_t acc[16];                                 // [4 * column-in-block + row word]
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] = 0;
+#pragma unroll
+            for (int it = 0; it < kItems; ++it) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    z[it] -= P8[it];
+                    const bool drop = z[it] < 0;
+                    const uint4 m = tabl[8 * (kk[it] + (drop ? 1 : 0))];
+                    acc[4 * u + 0] += m.x;
+                    acc[4 * u + 1] += m.y;
+                    acc[4 * u + 2] += m.z;
+                    acc[4 * u + 3] += m.w;
+                    if (drop) {
+                        kk[it] -= 2;
+                        z[it] += N3;
+                    }
+                }
+            }
+            // butterfly reduce-scatter of 16 words of byte counters (<= 8 each per lane): after
+            // 4 halving steps lane L holds word (L >> 1) summed over a lane group; byte pairs are then
+            // split into 16-bit fields and one more step gives each lane 2 cells' warp totals.
+            uint32_t v8[8], v4[4], v2[2], v1;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {                     // step 16: keep half by lane bit 4
+                const bool hiH = lane & 16;
+                const uint32_t send = hiH ? acc[i] : acc[i + 8];
+                const uint32_t keep = hiH ? acc[i + 8] : acc[i];
+                v8[i] = keep + __shfl_xor_sync(kFull, send, 16);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {                     // step 8
+                const bool hiH = lane & 8;
+                const uint32_t send = hiH ? v8[i] : v8[i + 4];
+                const uint32_t keep = hiH ? v8[i + 4] : v8[i];
+                v4[i] = keep + __shfl_xor_sync(kFull, send, 8);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {                     // step 4
+                const bool hiH = lane & 4;
+                const uint32_t send = hiH ? v4[i] : v4[i + 2];
+                const uint32_t keep = hiH ? v4[i + 2] : v4[i];
+                v2[i] = keep + __shfl_xor_sync(kFull, send, 4);
+            }
+            {                                                 // step 2 (bytes <= 128 after this)
+                const bool hiH = lane & 2;
+                const uint32_t send = hiH ? v2[0] : v2[1];
+                const uint32_t keep = hiH ? v2[1] : v2[0];
+                v1 = keep + __shfl_xor_sync(kFull, send, 2);
+            }
+            // word index held by this lane: bits 4,3,2,1 of the lane select halves of 16 words
+            const uint32_t word = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                                  ((lane >> 1) & 1);
+            // step 1: split bytes into two 16-bit-field halves; lane keeps bytes (0,2) or (1,3)
+            const uint32_t ev = v1 & 0x00FF00FFu, od = (v1 >> 8) & 0x00FF00FFu;
+            const bool odd = lane & 1;
+            const uint32_t tot = (odd ? od : ev) + __shfl_xor_sync(kFull, odd ? ev : od, 1);
+            // cells: column 4b + (word >> 2), rows 4*(word & 3) + {0, 2} (even lane) or {1, 3} (odd)
+            const uint32_t col = 4 * b + (word >> 2), row0 = 4 * (word & 3) + (odd ? 1 : 0);
+            const uint32_t c0 = tot & 0xFFFFu, c1 = tot >> 16;
+            if (c0) atomicAdd(dst + 16 * col + row0, c0);
+            if (c1) atomicAdd(dst + 16 * col + row0 + 2, c1);
+        }
+    }
+}
+
+int tail16_blocks_per_sm(bool int64) {
+    int n = 0;
+    if (int64) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tail16<int64_t>, 256, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tail16<int32_t>, 256, 0);
+    return n > 0 ? n : 1;
+}
+
+cudaError_t launch_tail16(bool int64, const PassArgs& a, int grid, cudaStream_t st) {
+    if (int64) k_tail16<int64_t><<<grid, 256, 0, st>>>(a);
+    else k_tail16<int32_t><<<grid, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
 int tail_blocks_per_sm(bool int64) {
     int n = 0;
     if (int64) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tail<int64_t>, 256, 0);
@@ -418,38 +579,37 @@ cudaError_t launch_tail(bool int64, const PassArgs& a, int grid, cudaStream_t st
     return cudaGetLastError();
 }
 
-// Gather the 4 child votes of each parent (level D-2 parents: 4x4 grid, kk = 1; level D-1
-// parents: 8x8 grid, kk = 2) from the dense grids of their level-(D-3) ancestor.
+// Gather the 4 child votes of each parent at level c-1 from the leaf grid (side G = 2^tk leaves) of
+// its ancestor at the tail level L = c-1-hops: a child region of side 2^j leaves (j = D - c) has
+// votes = sum of its 2^j diagonal leaf counts (diagonal identity, see the tail kernels).
 __global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ dense, uint32_t anc_base,
                                                 const uint32_t* __restrict__ anc_a, const uint32_t* __restrict__ anc_c,
                                                 const uint32_t* __restrict__ p_a, const uint32_t* __restrict__ p_c,
-                                                const uint32_t* __restrict__ p_parent,
-                                                const uint32_t* __restrict__ pp_parent, int kk, uint32_t Fp,
+                                                GatherChain chain, int hops, int tk, int j, uint32_t Fp,
                                                 uint32_t* __restrict__ V) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= Fp) return;
-    uint32_t A = p_parent[p];
-    if (kk == 2) A = pp_parent[A];
-    const uint32_t la = p_a[p] - (anc_a[A] << kk), lc = p_c[p] - (anc_c[A] << kk);
-    const uint32_t* g = dense + (uint64_t)(A - anc_base) * kTailCells;   // 8x8 leaf grid, [8u + v]
+    uint32_t A = p;
+    for (int h = 0; h < hops; ++h) A = chain.parent[h][A];
+    const uint32_t la = p_a[p] - (anc_a[A] << hops), lc = p_c[p] - (anc_c[A] << hops);
+    const uint32_t G = 1u << tk, S = 1u << j;
+    const uint32_t* g = dense + (uint64_t)(A - anc_base) * (G * G);   // leaf grid, [G*u + v]
     uint32_t v[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        const uint32_t u = 2 * la + quad_da(q), w = 2 * lc + quad_dc(q);
-        if (kk == 2) {
-            v[q] = g[8 * u + w];
-        } else {   // level D-1 cell (u, w): votes = SW leaf (2u, 2w) + NE leaf (2u+1, 2w+1)
-            v[q] = g[8 * (2 * u) + 2 * w] + g[8 * (2 * u + 1) + 2 * w + 1];
-        }
+        const uint32_t u0 = (2 * la + quad_da(q)) * S, w0 = (2 * lc + quad_dc(q)) * S;
+        uint32_t sum = 0;
+        for (uint32_t t = 0; t < S; ++t) sum += g[G * (u0 + t) + w0 + t];
+        v[q] = sum;
     }
     reinterpret_cast<uint4*>(V)[p] = make_uint4(v[0], v[1], v[2], v[3]);
 }
 
 cudaError_t launch_gather(const uint32_t* dense, uint32_t anc_base, const uint32_t* anc_a, const uint32_t* anc_c,
-                          const uint32_t* p_a, const uint32_t* p_c, const uint32_t* p_parent,
-                          const uint32_t* pp_parent, int kk, uint32_t Fp, uint32_t* V, cudaStream_t st) {
+                          const uint32_t* p_a, const uint32_t* p_c, const GatherChain& chain, int hops, int tk,
+                          int j, uint32_t Fp, uint32_t* V, cudaStream_t st) {
     if (Fp == 0) return cudaSuccess;
-    k_gather<<<(Fp + 255) / 256, 256, 0, st>>>(dense, anc_base, anc_a, anc_c, p_a, p_c, p_parent, pp_parent, kk, Fp, V);
+    k_gather<<<(Fp + 255) / 256, 256, 0, st>>>(dense, anc_base, anc_a, anc_c, p_a, p_c, chain, hops, tk, j, Fp, V);
     return cudaGetLastError();
 }
 

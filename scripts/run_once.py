@@ -14,6 +14,7 @@ ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--images", type=int, default=None)
 ap.add_argument("--budget", type=int, default=0)
+ap.add_argument("--tail", type=int, default=0)
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 if cfg.images > 1:
@@ -22,10 +23,12 @@ else:
     pts, _ = synth.config_image(a.config)
     offs = np.array([0, len(pts)])
 d = torch.from_numpy(pts).cuda()
-h = hht.HHT(halves=cfg.halves, mem_budget=a.budget, profile=True)
+h = hht.HHT(halves=cfg.halves, mem_budget=a.budget, profile=True, tail_depth=a.tail)
 for _ in range(a.reps):
     h.detect_batch(d, offs, cfg.N, cfg.D, cfg.T)
 st = h.stats()
+prof = h.profile()
+print({k: round(v["ms"], 2) for k, v in prof.items() if v["ms"] > 0})
 print({k: st[k] for k in ("tests", "votes", "leaves", "pairs", "ranges", "ms", "int_bits")})
 # per-launch algorithmic bytes, to pair with an ncu capture of the same launch (ncu -k regex:k_tail -c 1
 # is the first "tail" launch; ncu -k regex:k_pass -s S -c 1 is k_pass launch S counting the root count)

@@ -210,3 +210,18 @@ def test_c2_structure_and_profile(torch_dev):
         check_structure(levels, pts.shape[0], cfg.T, cfg.D)
     prof = h.profile()
     assert prof["write"]["launches"] > 0 and prof["split"]["launches"] >= cfg.D
+
+
+@pytest.mark.parametrize("tail_depth", [3, 4])
+@pytest.mark.parametrize("seed", range(8))
+def test_tail_depth_variants(seed, tail_depth, torch_dev):
+    """The 8x8 (D-3) and 16x16 (D-4) leaf-grid tails give identical records and leaves."""
+    rng = np.random.default_rng(100 + seed)
+    N = int(rng.choice([16, 33, 64, 200]))
+    D = int(rng.integers(3, 9))
+    T = int(rng.choice([1, 2, 5, 12]))
+    pts = synth.random_scene(3000 + seed, N, max_lines=4, max_noise=int(rng.choice([50, 500, 4000])))
+    ref = oracle.detect(pts, N, D, T, AB)
+    h = _run(pts, N, D, T, AB, torch_dev, tail_depth=tail_depth)
+    compare_all(h, ref, AB, D)
+    assert (h.stats()["tests"], h.stats()["votes"]) == (ref.tests, ref.votes)
