@@ -69,7 +69,8 @@ typedef struct {
     size_t mem_budget;       /* device bytes for candidate lists; 0 = 80% of free memory at create.
                                 Levels whose lists do not fit are processed in depth-first ranges. */
     const void* nccl_id;     /* world > 1: 128-byte ncclUniqueId from hht_nccl_unique_id on rank 0,
-                                identical on every rank; NULL when world == 1 */
+                                identical on every rank. NULL when world == 1; a non-NULL id with
+                                world == 1 runs every collective on a 1-rank communicator (tests) */
 } hht_opts;
 
 /* One detected line: leaf (i, j) of tree (image, half) with votes > threshold. */

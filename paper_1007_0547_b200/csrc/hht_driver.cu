@@ -201,7 +201,7 @@ void prof_end(hht_ctx* x, int id) {
 }
 
 hht_status allreduce_sum_u32(hht_ctx* x, uint32_t* buf, size_t count) {
-    if (x->opts.world <= 1 || count == 0) return HHT_OK;
+    if (!x->comm || count == 0) return HHT_OK;
     const int id = prof_begin(x, 7, count * 4);
     CKN(ncclAllReduce(buf, buf, count, ncclUint32, ncclSum, x->comm, x->st));
     prof_end(x, id);
@@ -333,7 +333,7 @@ hht_status choose_range(hht_ctx* x, int lc, uint32_t q0, uint64_t cap_entries, b
                     all ? C.F : 0, (const uint64_t*)P.off.p, (const uint64_t*)P.choff.p,
                     (const uint32_t*)P.len.p, lc == 1, (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->st));
     prof_end(x, id);
-    if (x->opts.world > 1 && !all) {
+    if (x->comm && !all) {
         // min over ranks of the proposed end, then recompute with the agreed end
         CKN(ncclAllReduce((const char*)x->rng.p + offsetof(RangeInfo, q1), (char*)x->vtmp.p, 1, ncclUint64,
                           ncclMin, x->comm, x->st));
@@ -467,7 +467,7 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         TRY(run_pass(x, MODE_WRITE, a, ri.pairs, entries));
         x->stat.ranges += 1;
         const uint32_t* VL = (const uint32_t*)C.votes.p;
-        if (x->opts.world > 1) {
+        if (x->comm) {
             TRY(ensure(x, C.votes_local, 16ull * nq));
             CK(cudaMemcpyAsync(C.votes_local.p, C.votes.p, 16ull * nq, cudaMemcpyDeviceToDevice, x->st));
             VL = (const uint32_t*)C.votes_local.p;
@@ -548,7 +548,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
                 if (x->opts.halves & h) x->tree_half[t++] = (uint8_t)h;
     }
     std::vector<int64_t> global_n = local_n;
-    if (x->opts.world > 1) {
+    if (x->comm) {
         // argument agreement: min and max of (N, D, T, halves, B) must coincide
         int64_t prm[5] = {N, D, T, (int64_t)x->opts.halves, B};
         TRY(ensure(x, x->vtmp, std::max<size_t>(8 * 10, 8 * (size_t)B)));
@@ -588,7 +588,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         CK(launch_stage(dev_pts, (uint64_t)n, N, (uint32_t*)x->packed.p, (uint32_t*)x->errflag.p, x->st));
         prof_end(x, id);
     }
-    if (x->opts.world > 1)
+    if (x->comm)
         CKN(ncclAllReduce(x->errflag.p, x->errflag.p, 1, ncclUint32, ncclMax, x->comm, x->st));
     CK(cudaMemcpyAsync(x->misc_h, x->errflag.p, 4, cudaMemcpyDeviceToHost, x->st));
     TRY(sync(x));
@@ -671,7 +671,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         a.nf_rbase = 0;
         TRY(run_pass(x, MODE_COUNT, a, pairs0, 0));
         const uint32_t* VL = (const uint32_t*)L0.votes.p;
-        if (x->opts.world > 1) {
+        if (x->comm) {
             TRY(ensure(x, L0.votes_local, 16ull * F0));
             CK(cudaMemcpyAsync(L0.votes_local.p, L0.votes.p, 16ull * F0, cudaMemcpyDeviceToDevice, x->st));
             VL = (const uint32_t*)L0.votes_local.p;
@@ -823,7 +823,7 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
         cudaMallocHost((void**)&x->range_h, sizeof(RangeInfo)) != cudaSuccess ||
         cudaMallocHost((void**)&x->misc_h, 64) != cudaSuccess)
         return fail(HHT_ECUDA);
-    if (o.world > 1) {
+    if (o.nccl_id) {   // world > 1, or world == 1 with an id: every collective runs (1-rank comm)
         ncclUniqueId id;
         memcpy(&id, o.nccl_id, sizeof id);
         if (ncclCommInitRank(&x->comm, o.world, id, o.rank) != ncclSuccess) return fail(HHT_ENCCL);

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round profiling run on one B200 (see /opt/skills/guides/B200_PROFILING.md):
 #   1. the default bench line, 2. the ncu launch list of the same command,
-#   3. full ncu captures of the dominant kernels (tail, write pass) on config 5, with the
+#   3. full ncu captures of the dominant kernels (tail, largest write pass) on config 5, with the
 #      library's per-launch algorithmic bytes of the same run (run_once.py prints them).
 set -x
 mkdir -p gpurun_out
@@ -9,10 +9,17 @@ python bench.py > gpurun_out/bench_default.log 2> gpurun_out/bench_default.err &
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_c5.csv python bench.py > gpurun_out/ncu_launches.log 2>&1
 echo "launch list rc=$?"
-python scripts/run_once.py --config 5 > gpurun_out/plain_c5.log 2>&1 && \
+python scripts/run_once.py --config 5 > gpurun_out/plain_c5.log 2>&1
+# k_pass launch index of the largest write pass (k_pass launch 0 is the root count pass)
+WSKIP=$(python -c "
+import ast,re
+t=open('gpurun_out/plain_c5.log').read()
+b=ast.literal_eval(re.search(r'^write launches \d+ first bytes \d+ bytes\[:16\] (\[.*\])$', t, re.M).group(1))
+print(1 + max(range(len(b)), key=lambda i: b[i]))")
+echo "write capture index $WSKIP" > gpurun_out/write_skip.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_tail -c 1 \
     -o gpurun_out/c5_tail python scripts/run_once.py --config 5 > gpurun_out/ncu_tail.log 2>&1
 echo "tail capture rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pass -s 14 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pass -s $WSKIP -c 1 \
     -o gpurun_out/c5_write python scripts/run_once.py --config 5 > gpurun_out/ncu_write.log 2>&1
 echo "write capture rc=$?"

@@ -86,7 +86,11 @@ def main():
     lb = launch_bytes()
     traffic = {"config5": {}, "source": "ncu --set full --clock-control none, one launch per kernel class "
                "(scripts/gpu_profile.sh); algorithmic bytes of the same launch from hht_result_launches"}
-    caps = {"tail": ("c5_tail", 0), "write": ("c5_write", 13)}
+    wskip = 14
+    wf = os.path.join(G, "write_skip.txt")
+    if os.path.exists(wf):
+        wskip = int(open(wf).read().split()[-1])
+    caps = {"tail": ("c5_tail", 0), "write": ("c5_write", wskip - 1)}   # write launch index = k_pass index - 1
     for cls, (f, idx) in caps.items():
         rep = os.path.join(G, f + ".ncu-rep")
         if not os.path.exists(rep):

@@ -225,3 +225,26 @@ def test_tail_depth_variants(seed, tail_depth, torch_dev):
     h = _run(pts, N, D, T, AB, torch_dev, tail_depth=tail_depth)
     compare_all(h, ref, AB, D)
     assert (h.stats()["tests"], h.stats()["votes"]) == (ref.tests, ref.votes)
+
+
+def test_nccl_collectives_one_rank(torch_dev):
+    """world = 1 with an NCCL id runs every collective call site (argument check, per-image
+    counts, range agreement, per-level vote allreduce, error flag) on a 1-rank communicator;
+    results must equal the oracle's."""
+    cfg = synth.CONFIGS[2]
+    pts, _ = synth.config_image(2)
+    ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves)
+    h = hht.HHT(halves=cfg.halves, nccl_id=hht.nccl_unique_id(), world=1, rank=0, mem_budget=1 << 20)
+    h.detect(_dev(pts, torch_dev), cfg.N, cfg.D, cfg.T)
+    compare_all(h, ref, cfg.halves, cfg.D)
+    assert h.stats()["ranges"] > cfg.D
+    imgs = [synth.random_scene(900 + k, 64, max_noise=200) for k in range(3)]
+    offs = np.zeros(4, dtype=np.int64)
+    offs[1:] = np.cumsum([len(p) for p in imgs])
+    h.detect_batch(_dev(np.concatenate(imgs), torch_dev), offs, 64, 6, 5)
+    for b, p in enumerate(imgs):
+        compare_all(h, oracle.detect(p, 64, 6, 5, AB), AB, 6, image=b)
+    bad = np.array([[0, 0], [70, 3]], np.int32)
+    with pytest.raises(hht.HHTError) as e:
+        h.detect(_dev(bad, torch_dev), 64, 6, 5)
+    assert e.value.name == "HHT_ERANGE"
