@@ -418,26 +418,29 @@ __global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
 // ---------------------------------------------------------------------------------------------
 constexpr int kTab16 = 68;  // (k + 16) * 2 + drop, k in -16..17
 
-__device__ __forceinline__ uint4 tab16_entry(int t) {
+// Column mask of the 16x16 tail as 4-bit counters: row v at nibble (v & 7) of word (v >> 3).
+// A lane adds at most kItems = 8 per cell per block, so nibbles do not overflow; they are widened
+// to bytes right before the warp reduction.
+__device__ __forceinline__ uint2 tab16_entry(int t) {
     const int k = t / 2 - 16, d = t & 1;
-    uint32_t w[4] = {0, 0, 0, 0};
+    uint32_t w[2] = {0, 0};
     if (k >= 1) {
         const int vhi = min(k, 16) - 1, vlo = max(k - d - 1, 0);
-        for (int v = vlo; v <= vhi; ++v) w[v >> 2] |= 1u << (8 * (v & 3));
+        for (int v = vlo; v <= vhi; ++v) w[v >> 3] |= 1u << (4 * (v & 7));
     }
-    return make_uint4(w[0], w[1], w[2], w[3]);
+    return make_uint2(w[0], w[1]);
 }
 
-// The mask table is replicated 8x, entry e of copy c at slot 8e + c: an LDS.128 serves 8 lanes per
-// shared-memory wavefront, and lane l reads copy (l & 7), i.e. its own bank group, so lookups are
-// bank-conflict-free whatever entries the lanes need.
+// The mask table is replicated 16x, entry e of copy c at slot 16e + c: an LDS.64 serves 16 lanes
+// per shared-memory wavefront, and lane l reads copy (l & 15), i.e. its own bank pair, so lookups
+// are bank-conflict-free whatever entries the lanes need.
 template <typename I>
 __global__ void __launch_bounds__(256, 3) k_tail16(const PassArgs A) {
-    __shared__ uint4 s_tab[kTab16 * 8];
-    for (int t = threadIdx.x; t < kTab16 * 8; t += blockDim.x) s_tab[t] = tab16_entry(t >> 3);
+    __shared__ uint2 s_tab[kTab16 * 16];
+    for (int t = threadIdx.x; t < kTab16 * 16; t += blockDim.x) s_tab[t] = tab16_entry(t >> 4);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const uint4* tabl = s_tab + (lane & 7);
+    const uint2* tabl = s_tab + (lane & 15);
     const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t c_lo = A.chunk_bounds[0], c_hi = A.chunk_bounds[1];
@@ -486,35 +489,40 @@ __global__ void __launch_bounds__(256, 3) k_tail16(const PassArgs A) {
         uint32_t* dst = A.votes + (uint64_t)(r - A.nf_rbase) * kTail16Cells;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            uint32_t acc[16];                                 // [4 * column-in-block + row word]
+            uint32_t acc[8];                                  // [2 * column-in-block + row half], nibbles
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[i] = 0;
+            for (int i = 0; i < 8; ++i) acc[i] = 0;
 #pragma unroll
             for (int it = 0; it < kItems; ++it) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     z[it] -= P8[it];
                     const bool drop = z[it] < 0;
-                    const uint4 m = tabl[8 * (kk[it] + (drop ? 1 : 0))];
-                    acc[4 * u + 0] += m.x;
-                    acc[4 * u + 1] += m.y;
-                    acc[4 * u + 2] += m.z;
-                    acc[4 * u + 3] += m.w;
+                    const uint2 m = tabl[16 * (kk[it] + (drop ? 1 : 0))];
+                    acc[2 * u + 0] += m.x;
+                    acc[2 * u + 1] += m.y;
                     if (drop) {
                         kk[it] -= 2;
                         z[it] += N3;
                     }
                 }
             }
+            // widen nibbles to bytes: word 4u + 2w + par holds rows 8w + 2b + par in byte b
+            uint32_t acc16[16];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                acc16[2 * i] = acc[i] & 0x0F0F0F0Fu;
+                acc16[2 * i + 1] = (acc[i] >> 4) & 0x0F0F0F0Fu;
+            }
             // butterfly reduce-scatter of 16 words of byte counters (<= 8 each per lane): after
-            // 4 halving steps lane L holds word (L >> 1) summed over a lane group; byte pairs are then
+            // 4 halving steps lane L holds word (L >> 1) summed over 16 lanes; byte pairs are then
             // split into 16-bit fields and one more step gives each lane 2 cells' warp totals.
             uint32_t v8[8], v4[4], v2[2], v1;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {                     // step 16: keep half by lane bit 4
                 const bool hiH = lane & 16;
-                const uint32_t send = hiH ? acc[i] : acc[i + 8];
-                const uint32_t keep = hiH ? acc[i + 8] : acc[i];
+                const uint32_t send = hiH ? acc16[i] : acc16[i + 8];
+                const uint32_t keep = hiH ? acc16[i + 8] : acc16[i];
                 v8[i] = keep + __shfl_xor_sync(kFull, send, 16);
             }
 #pragma unroll
@@ -544,11 +552,12 @@ __global__ void __launch_bounds__(256, 3) k_tail16(const PassArgs A) {
             const uint32_t ev = v1 & 0x00FF00FFu, od = (v1 >> 8) & 0x00FF00FFu;
             const bool odd = lane & 1;
             const uint32_t tot = (odd ? od : ev) + __shfl_xor_sync(kFull, odd ? ev : od, 1);
-            // cells: column 4b + (word >> 2), rows 4*(word & 3) + {0, 2} (even lane) or {1, 3} (odd)
-            const uint32_t col = 4 * b + (word >> 2), row0 = 4 * (word & 3) + (odd ? 1 : 0);
+            // word = 4u + 2w + par: column 4b + u; byte bb -> row 8w + 2bb + par, bb in {odd, odd + 2}
+            const uint32_t col = 4 * b + (word >> 2);
+            const uint32_t row0 = 8 * ((word >> 1) & 1) + 2 * (odd ? 1 : 0) + (word & 1);
             const uint32_t c0 = tot & 0xFFFFu, c1 = tot >> 16;
             if (c0) atomicAdd(dst + 16 * col + row0, c0);
-            if (c1) atomicAdd(dst + 16 * col + row0 + 2, c1);
+            if (c1) atomicAdd(dst + 16 * col + row0 + 4, c1);
         }
     }
 }
