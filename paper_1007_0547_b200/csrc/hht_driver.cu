@@ -312,6 +312,7 @@ PassArgs pass_args(hht_ctx* x, Level& P, int level) {
     a.D = x->D;
     a.N = x->N;
     a.one = 1;
+    a.tab_stride = 128;
     return a;
 }
 

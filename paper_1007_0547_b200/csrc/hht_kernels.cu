@@ -58,6 +58,30 @@ __device__ __forceinline__ void mad_if(bool c, uint32_t& acc, uint32_t one, uint
         : "+r"(acc) : "r"((uint32_t)c), "r"(one), "r"(k));
 }
 
+// a*b + c as an integer multiply-add: keeps pointer / threshold updates on the FMA pipe (the ALU pipe
+// is the binding unit of the raster loops); b is a runtime value so ptxas cannot turn it into a
+// shift + add on the ALU pipe.
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+__device__ __forceinline__ int32_t mad_i(uint32_t a, int32_t b, int32_t c) {
+    int32_t r;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+__device__ __forceinline__ int64_t mad_i(uint32_t a, int64_t b, int64_t c) {
+    int64_t r;
+    asm("mad.lo.s64 %0, %1, %2, %3;" : "=l"(r) : "l"((int64_t)a), "l"(b), "l"(c));
+    return r;
+}
+template <typename I>
+__device__ __forceinline__ uint32_t sign_bit(I v) {
+    using UI = typename Unsigned<I>::type;
+    return (uint32_t)((UI)v >> (8 * sizeof(I) - 1));
+}
+
 // quad index of (da, dc): NE(1,1)=0, NW(0,1)=1, SW(0,0)=2, SE(1,0)=3
 __host__ __device__ constexpr int quad_of(int da, int dc) { return dc ? (da ? 0 : 1) : (da ? 3 : 2); }
 
@@ -440,7 +464,8 @@ __global__ void __launch_bounds__(256, 3) k_tail16(const PassArgs A) {
     for (int t = threadIdx.x; t < kTab16 * 16; t += blockDim.x) s_tab[t] = tab16_entry(t >> 4);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const uint2* tabl = s_tab + (lane & 15);
+    const uint32_t tab_sm = (uint32_t)__cvta_generic_to_shared(s_tab + (lane & 15));
+    const uint32_t c128 = A.tab_stride, c256n = 0u - 2u * A.tab_stride;   // 128, -256 (runtime)
     const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t c_lo = A.chunk_bounds[0], c_hi = A.chunk_bounds[1];
@@ -463,10 +488,10 @@ __global__ void __launch_bounds__(256, 3) k_tail16(const PassArgs A) {
         const I beta_m1 = (N << D) - N3 * j0 - 1;
 
         // per-line raster state carried across the 4 column blocks: z = y - (k-1)*3N (height of the
-        // line above its row's floor at the current lattice column; a column drops iff z < 0),
-        // the table index of (k, 0), and the column step 2ex
+        // line above its row's floor at the current lattice column; a column drops iff z < 0), the
+        // shared-memory address of table entry (k, 0) in this lane's copy, and the column step 2ex
         I z[kItems], P8[kItems];
-        int kk[kItems];
+        uint32_t ta[kItems];
 #pragma unroll
         for (int it = 0; it < kItems; ++it) {
             const int idx = lane + kWarp * it;
@@ -484,7 +509,7 @@ __global__ void __launch_bounds__(256, 3) k_tail16(const PassArgs A) {
             const bool below = yy < 0;
             P8[it] = 2 * ex;
             z[it] = below ? yy + N3 : yy - f * N3;
-            kk[it] = below ? 32 : 2 * (int)f + 34;           // table index of (k, 0): 2 * (k + 16)
+            ta[it] = tab_sm + 128u * (below ? 32u : 2u * (uint32_t)f + 34u);   // entry 2 * (k + 16)
         }
         uint32_t* dst = A.votes + (uint64_t)(r - A.nf_rbase) * kTail16Cells;
 #pragma unroll
@@ -496,15 +521,15 @@ __global__ void __launch_bounds__(256, 3) k_tail16(const PassArgs A) {
             for (int it = 0; it < kItems; ++it) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    z[it] -= P8[it];
-                    const bool drop = z[it] < 0;
-                    const uint2 m = tabl[16 * (kk[it] + (drop ? 1 : 0))];
-                    acc[2 * u + 0] += m.x;
-                    acc[2 * u + 1] += m.y;
-                    if (drop) {
-                        kk[it] -= 2;
-                        z[it] += N3;
-                    }
+                    const I zz = z[it] - P8[it];
+                    const uint32_t d = sign_bit<I>(zz);                 // drop: the line left its row
+                    uint32_t mx, my;
+                    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mx), "=r"(my)
+                                 : "r"(mad_u32(d, c128, ta[it])));
+                    acc[2 * u + 0] += mx;
+                    acc[2 * u + 1] += my;
+                    ta[it] = mad_u32(d, c256n, ta[it]);                 // k -= drop
+                    z[it] = mad_i(d, N3, zz);                           // threshold -= drop * 3N
                 }
             }
             // widen nibbles to bytes: word 4u + 2w + par holds rows 8w + 2b + par in byte b
