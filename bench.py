@@ -35,6 +35,7 @@ def _args():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="hht", choices=["hht", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--prefetch", type=int, default=0, help="0 auto, 1 descriptor only, 2 descriptor + entries")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-tests", type=float, default=4e8, help="bounded oracle sample (code evaluations)")
     return ap.parse_args()
@@ -183,7 +184,7 @@ def main():
         hdist.check_consistent(cfg.N, cfg.D, cfg.T, cfg.halves, 1)
         nccl_id = hdist.broadcast_bytes(hht.nccl_unique_id() if rank == 0 else None)
     h = hht.HHT(device=local, halves=cfg.halves, record_levels=True, profile=True,
-                rank=rank if comm_world > 1 else 0, world=comm_world, nccl_id=nccl_id)
+                rank=rank if comm_world > 1 else 0, world=comm_world, nccl_id=nccl_id, prefetch=a.prefetch)
     d_pts = torch.from_numpy(np.ascontiguousarray(my)).to(dev)
     B = my_offs.shape[0] - 1
 

@@ -66,6 +66,8 @@ typedef struct {
     uint32_t profile;        /* 1: time every kernel launch with CUDA events (hht_result_profile) */
     uint32_t tail_depth;     /* levels counted by the dense leaf-grid tail: 0 = auto (4 when
                                 depth >= 4, else 3), 3 or 4 to force (results are identical) */
+    uint32_t prefetch;       /* pass/tail kernels: 0 = auto, 1 = fetch the next chunk's descriptor
+                                only, 2 = also its list entries (more registers); identical results */
     size_t mem_budget;       /* device bytes for candidate lists; 0 = 80% of free memory at create.
                                 Levels whose lists do not fit are processed in depth-first ranges. */
     const void* nccl_id;     /* world > 1: 128-byte ncclUniqueId from hht_nccl_unique_id on rank 0,

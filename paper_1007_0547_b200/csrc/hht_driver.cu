@@ -31,8 +31,8 @@ struct Buf {
 };
 
 struct Level {
-    Buf tree, a, c, parent, len, votes_g, off, choff, chunk_region;   // frontier R_l
-    Buf nf;                                                   // children of R_(l-1) range -> R_l
+    Buf tree, a, c, parent, len, votes_g, off, choff, chunks;   // frontier R_l
+    Buf nf, nfoff;                                            // children of R_(l-1) range -> R_l
     Buf votes, votes_local;                                   // votes of R_l's children (range)
     Buf cursor;                                               // append cursors of R_l lists (range)
     Buf list_own;                                             // R_l candidate lists (range)
@@ -43,7 +43,7 @@ struct Level {
 
     Frontier frontier() {
         return {(uint32_t*)tree.p, (uint32_t*)a.p, (uint32_t*)c.p, (uint32_t*)parent.p, (uint32_t*)len.p,
-                (uint32_t*)votes_g.p, (uint64_t*)off.p, (uint64_t*)choff.p, (uint32_t*)chunk_region.p};
+                (uint32_t*)votes_g.p, (uint64_t*)off.p, (uint64_t*)choff.p, (ChunkDesc*)chunks.p};
     }
 };
 
@@ -71,6 +71,7 @@ struct hht_ctx {
     int grid[3][2] = {};
     int tail_grid[2] = {};
     int tail16_grid[2] = {};
+    bool pref_pass = true, pref_tail = true;   // opts.prefetch (0 = auto)
 
     // last call
     int N = 0, D = 0, B = 0, H = 0, ntrees = 0;
@@ -235,6 +236,7 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
         TRY(ensure(x, C.off, (nch + 1) * 8));
         TRY(ensure(x, C.choff, (nch + 1) * 8));
         TRY(ensure(x, C.nf, nch * 4));
+        if (need_lists) TRY(ensure(x, C.nfoff, nch * 8));
     } else {
         TRY(grow(x, x->leaves, sizeof(LeafRec), x->leaves.n + nch));
     }
@@ -262,6 +264,7 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
     a.record = record;
     a.T = x->T;
     a.nf = (uint32_t*)C.nf.p;
+    a.nfoff = need_lists ? (uint64_t*)C.nfoff.p : nullptr;
     a.out = C.frontier();
     a.rec = record ? (Record*)x->rec[child_level].b.p + x->rec[child_level].n : nullptr;
     a.leaves = leaf ? (LeafRec*)x->leaves.b.p + x->leaves.n : nullptr;
@@ -287,9 +290,11 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
     C.C = t.C;
     if (x->opts.profile) x->prof.bytes[4] += (uint64_t)C.F * 36;
     if (need_lists && C.F) {
-        TRY(ensure(x, C.chunk_region, std::max<uint64_t>(C.C, 1) * 4));
-        const int id2 = prof_begin(x, 5, C.C * 4 + (uint64_t)C.F * 16);
-        CK(launch_chunk_map((const uint64_t*)C.choff.p, C.F, (uint32_t*)C.chunk_region.p, x->st));
+        TRY(ensure(x, C.chunks, std::max<uint64_t>(C.C, 1) * sizeof(ChunkDesc)));
+        const int id2 = prof_begin(x, 5, C.C * sizeof(ChunkDesc) + (uint64_t)C.F * 36);
+        CK(launch_chunk_map((const uint64_t*)C.choff.p, (const uint64_t*)C.off.p, (const uint32_t*)C.len.p,
+                            (const uint32_t*)C.a.p, (const uint32_t*)C.c.p, (const uint32_t*)C.tree.p,
+                            (const uint8_t*)x->beta.p, C.F, (ChunkDesc*)C.chunks.p, x->st));
         prof_end(x, id2);
     }
     return HHT_OK;
@@ -299,27 +304,29 @@ PassArgs pass_args(hht_ctx* x, Level& P, int level) {
     PassArgs a{};
     a.list = P.list;
     a.list_base = P.list_base;
-    a.p_tree = (const uint32_t*)P.tree.p;
-    a.p_a = (const uint32_t*)P.a.p;
-    a.p_c = (const uint32_t*)P.c.p;
-    a.p_len = (const uint32_t*)P.len.p;
-    a.p_off = (const uint64_t*)P.off.p;
-    a.p_choff = (const uint64_t*)P.choff.p;
-    a.chunk_region = (const uint32_t*)P.chunk_region.p;
+    a.chunks = (const ChunkDesc*)P.chunks.p;
     a.chunk_bounds = (const uint64_t*)x->bounds.p;
-    a.tree_beta = (const uint8_t*)x->beta.p;
     a.level = level;
     a.D = x->D;
     a.N = x->N;
     a.one = 1;
     a.tab_stride = 128;
+    // floor(y / 3N) = umulhi(y, m) >> (l - 1) for 0 <= y < 2^31, with l = ceil(log2 3N) and
+    // m = ceil(2^(31+l) / 3N) < 2^32 (3N is never a power of two); see floor_div3n_clamp16
+    {
+        const uint64_t n3 = 3ull * (uint64_t)x->N;
+        int l = 0;
+        while ((1ull << l) < n3) ++l;
+        a.div_m = (uint32_t)(((1ull << (31 + l)) + n3 - 1) / n3);
+        a.div_s = (uint32_t)(l - 1);
+    }
     return a;
 }
 
 hht_status run_pass(hht_ctx* x, int mode, const PassArgs& a, uint64_t pairs, uint64_t written) {
     const int cls = mode == MODE_COUNT ? 1 : (mode == MODE_WRITE ? 2 : 3);
     const int id = prof_begin(x, cls, pairs * 4 + written * 4);
-    CK(launch_pass(mode, x->int64, a, x->grid[mode][x->int64 ? 1 : 0], x->st));
+    CK(launch_pass(mode, x->int64, x->pref_pass, a, x->grid[mode][x->int64 ? 1 : 0], x->st));
     prof_end(x, id);
     x->stat.pairs += pairs;
     return HHT_OK;
@@ -370,7 +377,7 @@ hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
     a.nf_rbase = r0;
     a.votes = (uint32_t*)x->dense.p;
     const int id = prof_begin(x, 3, 0);
-    if (TK == 4) CK(launch_tail16(x->int64, a, x->tail16_grid[x->int64 ? 1 : 0], x->st));
+    if (TK == 4) CK(launch_tail16(x->int64, x->pref_tail, a, x->tail16_grid[x->int64 ? 1 : 0], x->st));
     else CK(launch_tail(x->int64, a, x->tail_grid[x->int64 ? 1 : 0], x->st));
     prof_end(x, id);
     TRY(sync(x));
@@ -460,7 +467,7 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         a.nf_rbase = r0;
         a.q0 = q0;
         a.q1 = q1;
-        a.c_off = (const uint64_t*)C.off.p;
+        a.nfoff = (const uint64_t*)C.nfoff.p;
         a.c_list_base = ri.s_lo;
         a.c_cursor = (uint32_t*)C.cursor.p;
         a.c_list = (uint32_t*)C.list_own.p;
@@ -653,7 +660,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         TRY(ensure(x, L0.votes_g, F0 * 4ull));
         TRY(ensure(x, L0.off, (F0 + 1) * 8ull));
         TRY(ensure(x, L0.choff, (F0 + 1) * 8ull));
-        TRY(ensure(x, L0.chunk_region, std::max<uint64_t>(chunks, 1) * 4));
+        TRY(ensure(x, L0.chunks, std::max<uint64_t>(chunks, 1) * sizeof(ChunkDesc)));
         CK(cudaMemcpyAsync(L0.tree.p, h_tree.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
         CK(cudaMemcpyAsync(L0.a.p, h_zero.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
         CK(cudaMemcpyAsync(L0.c.p, h_zero.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
@@ -662,7 +669,9 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         CK(cudaMemcpyAsync(L0.votes_g.p, h_votes.data(), F0 * 4ull, cudaMemcpyHostToDevice, x->st));
         CK(cudaMemcpyAsync(L0.off.p, h_off.data(), (F0 + 1) * 8ull, cudaMemcpyHostToDevice, x->st));
         CK(cudaMemcpyAsync(L0.choff.p, h_choff.data(), (F0 + 1) * 8ull, cudaMemcpyHostToDevice, x->st));
-        CK(launch_chunk_map((const uint64_t*)L0.choff.p, F0, (uint32_t*)L0.chunk_region.p, x->st));
+        CK(launch_chunk_map((const uint64_t*)L0.choff.p, (const uint64_t*)L0.off.p, (const uint32_t*)L0.len.p,
+                            (const uint32_t*)L0.a.p, (const uint32_t*)L0.c.p, (const uint32_t*)L0.tree.p,
+                            (const uint8_t*)x->beta.p, F0, (ChunkDesc*)L0.chunks.p, x->st));
         const uint64_t cb[2] = {0, chunks};
         CK(cudaMemcpyAsync(x->bounds.p, cb, sizeof cb, cudaMemcpyHostToDevice, x->st));
         TRY(ensure(x, L0.votes, 16ull * F0));
@@ -809,10 +818,12 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
+    if (o.prefetch == 1) x->pref_pass = x->pref_tail = false;
+    if (o.prefetch == 2) x->pref_pass = x->pref_tail = true;
     for (int m = 0; m < 3; ++m)
-        for (int w = 0; w < 2; ++w) x->grid[m][w] = x->sms * pass_blocks_per_sm(m, w == 1);
+        for (int w = 0; w < 2; ++w) x->grid[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, x->pref_pass);
     for (int w = 0; w < 2; ++w) x->tail_grid[w] = x->sms * tail_blocks_per_sm(w == 1);
-    for (int w = 0; w < 2; ++w) x->tail16_grid[w] = x->sms * tail16_blocks_per_sm(w == 1);
+    for (int w = 0; w < 2; ++w) x->tail16_grid[w] = x->sms * tail16_blocks_per_sm(w == 1, x->pref_tail);
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return fail(HHT_ECUDA);
     x->budget = o.mem_budget ? o.mem_budget : (size_t)(0.70 * (double)fr);
@@ -964,7 +975,7 @@ void hht_destroy(hht_ctx* x) {
         b.p = nullptr;
     };
     for (auto& L : x->lv) {
-        for (Buf* b : {&L.tree, &L.a, &L.c, &L.parent, &L.len, &L.votes_g, &L.off, &L.choff, &L.chunk_region, &L.nf, &L.votes,
+        for (Buf* b : {&L.tree, &L.a, &L.c, &L.parent, &L.len, &L.votes_g, &L.off, &L.choff, &L.chunks, &L.nf, &L.nfoff, &L.votes,
                        &L.votes_local, &L.cursor, &L.list_own})
             fr(*b);
     }

@@ -19,6 +19,18 @@ constexpr int kTail16Cells = 256;          // 16x16 tail: leaf grid per level-(D
 __host__ __device__ constexpr uint32_t quad_da(int q) { return (q == 0 || q == 3) ? 1u : 0u; }
 __host__ __device__ constexpr uint32_t quad_dc(int q) { return (q <= 1) ? 1u : 0u; }
 
+// One warp work unit of a pass: <= kChunk consecutive entries of ONE region's candidate list, with
+// everything the pass needs about the region, so that a chunk costs one 32-byte load before its
+// entries can be fetched (and that load is issued one chunk ahead).
+struct alignas(16) ChunkDesc {
+    uint32_t r;          // region index in its level's frontier
+    uint32_t cnt;        // entries in this chunk (1..kChunk)
+    uint32_t a, c;       // region lattice coordinates
+    uint64_t e0;         // absolute list offset of the first entry
+    uint32_t beta;       // 1 = BETA tree (swap x and y)
+    uint32_t pad;
+};
+
 // Frontier of split regions at one level, structure of arrays in HBM.
 struct Frontier {
     uint32_t* tree;      // tree id (image * H + half index)
@@ -29,7 +41,7 @@ struct Frontier {
     uint32_t* votes;     // global votes (all ranks)
     uint64_t* off;       // [F+1] local list offset (exclusive scan of len); off[F] = total
     uint64_t* choff;     // [F+1] chunk offset (exclusive scan of ceil(len/kChunk)); choff[F] = total
-    uint32_t* chunk_region;  // [total chunks] chunk -> region index
+    ChunkDesc* chunks;   // [total chunks] work-unit descriptors (k_chunk_map)
 };
 
 struct Record { uint32_t tree, a, c, votes; };     // one visited region
@@ -61,29 +73,23 @@ enum PassMode { MODE_COUNT = 0, MODE_WRITE = 1, MODE_COUNT2 = 2 };
 struct PassArgs {
     // parent level
     const uint32_t* list;          // packed (x << 16 | y) candidate lines of the parents
-    uint64_t list_base;            // subtract from p_off[r] to index `list`
-    const uint32_t* p_tree;
-    const uint32_t* p_a;
-    const uint32_t* p_c;
-    const uint32_t* p_len;
-    const uint64_t* p_off;
-    const uint64_t* p_choff;
-    const uint32_t* chunk_region;
+    uint64_t list_base;            // subtract from ChunkDesc::e0 to index `list`
+    const ChunkDesc* chunks;       // parents' chunk descriptors
     const uint64_t* chunk_bounds;  // device [2]: chunk range [lo, hi) of this launch
-    const uint8_t* tree_beta;      // [trees] 1 = BETA tree (swap x and y)
     int level;                     // parent level l
     int D;
     int N;
     // children of the parents (level l+1)
     const uint32_t* nf;            // [4 * nparents] child -> next-frontier index or kNone
+    const uint64_t* nfoff;         // [4 * nparents] list offset of each split child (next frontier)
     uint32_t nf_rbase;             // parent index of nf[0..3]
     uint32_t q0, q1;               // only next-frontier indices in [q0, q1) are written / counted
-    const uint64_t* c_off;         // next-frontier list offsets
-    uint64_t c_list_base;          // subtract from c_off[nf] to index c_list
+    uint64_t c_list_base;          // subtract from nfoff[] to index c_list
     uint32_t* c_cursor;            // [q1 - q0] append cursors
     uint32_t* c_list;              // output lists
     uint32_t one;                  // == 1 (runtime value: keeps the count adds on the FMA pipe)
     uint32_t tab_stride;           // == 128 (runtime value, see mad_u32)
+    uint32_t div_m, div_s;         // floor(y / 3N) = umulhi(y, div_m) >> div_s for 0 <= y < 2^31
     uint32_t* votes;               // MODE_COUNT: [4 * nparents] (4*(r - nf_rbase) + q)
                                    // else:       [4 * (q1 - q0)] (4*(nf - q0) + q')
 };
@@ -105,6 +111,7 @@ struct SplitArgs {
     const uint32_t* p_len;         // derive_ne: parents' local votes (range start)
     int derive_ne;                 // V/VL hold no NE counts: NE = parent - SW (votes identity)
     uint32_t* nf;                  // [4 * Fp]
+    uint64_t* nfoff;               // [4 * Fp] list offset of each split child (need_lists)
     Frontier out;
     Record* rec;                   // records of child_level, rec[4*p + q]
     LeafRec* leaves;               // leaves[leaf index]
@@ -126,14 +133,16 @@ struct RangeInfo {
 // Launchers (hht_kernels.cu). All asynchronous on `st`.
 cudaError_t launch_stage(const int32_t* pts, uint64_t n, int N, uint32_t* packed, uint32_t* err,
                          cudaStream_t st);
-cudaError_t launch_pass(int mode, bool int64, const PassArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_pass(int mode, bool int64, bool pref, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_split(const SplitArgs& a, cudaStream_t st);
-cudaError_t launch_chunk_map(const uint64_t* choff, uint32_t F, uint32_t* chunk_region, cudaStream_t st);
+cudaError_t launch_chunk_map(const uint64_t* choff, const uint64_t* off, const uint32_t* len, const uint32_t* a,
+                             const uint32_t* c, const uint32_t* tree, const uint8_t* tree_beta, uint32_t F,
+                             ChunkDesc* chunks, cudaStream_t st);
 cudaError_t launch_range(const uint64_t* c_off, const uint32_t* c_parent, uint32_t Fc, uint32_t q0,
                          uint64_t cap_entries, uint64_t forced_q1, const uint64_t* p_off,
                          const uint64_t* p_choff, const uint32_t* p_len, int p_is_root, RangeInfo* info,
                          uint64_t* chunk_bounds, cudaStream_t st);
-int pass_blocks_per_sm(int mode, bool int64);
+int pass_blocks_per_sm(int mode, bool int64, bool pref);
 int tail_blocks_per_sm(bool int64);
 cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_beta, uint32_t H, uint32_t* out,
                              cudaStream_t st);
@@ -142,8 +151,8 @@ struct GatherChain { const uint32_t* parent[3]; };   // parent-index arrays, nea
 cudaError_t launch_gather(const uint32_t* dense, uint32_t anc_base, const uint32_t* anc_a, const uint32_t* anc_c,
                           const uint32_t* p_a, const uint32_t* p_c, const GatherChain& chain, int hops, int tk,
                           int j, uint32_t Fp, uint32_t* V, cudaStream_t st);
-int tail16_blocks_per_sm(bool int64);
-cudaError_t launch_tail16(bool int64, const PassArgs& a, int grid, cudaStream_t st);
+int tail16_blocks_per_sm(bool int64, bool pref);
+cudaError_t launch_tail16(bool int64, bool pref, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
                           int is_root, RangeInfo* info, uint64_t* chunk_bounds, cudaStream_t st);
 

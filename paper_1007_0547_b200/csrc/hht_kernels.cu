@@ -187,59 +187,97 @@ __device__ __forceinline__ void chunk_math(const uint32_t (&p)[kItems], int cnt,
     }
 }
 
-template <typename I, int MODE>
-__global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
-    __shared__ uint32_t s_stage[MODE == MODE_WRITE ? 8 * 4 * kChunk : 1];   // 4 KB per warp
-    const int lane = threadIdx.x & 31;
+// Chunk descriptor (32 B, one broadcast load per warp) and the chunk's entries. Lanes past `cnt`
+// load nothing; a descriptor past the launch's chunk range reads as cnt = 0.
+__device__ __forceinline__ ChunkDesc load_desc(const ChunkDesc* __restrict__ d, uint64_t ch, uint64_t c_hi) {
+    ChunkDesc z;
+    if (ch < c_hi) {
+        const uint4* q = reinterpret_cast<const uint4*>(d + ch);
+        const uint4 u0 = __ldg(q), u1 = __ldg(q + 1);
+        z.r = u0.x; z.cnt = u0.y; z.a = u0.z; z.c = u0.w;
+        z.e0 = ((uint64_t)u1.y << 32) | u1.x;
+        z.beta = u1.z; z.pad = 0;
+    } else {
+        z.r = 0; z.cnt = 0; z.a = 0; z.c = 0; z.e0 = 0; z.beta = 0; z.pad = 0;
+    }
+    return z;
+}
+
+__device__ __forceinline__ void load_items(uint32_t (&p)[kItems], const uint32_t* __restrict__ list, uint64_t base,
+                                           const ChunkDesc& d, int lane) {
+    const uint32_t* src = list + (d.e0 - base) + lane;       // one 64-bit address, immediate offsets
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) p[it] = (lane + kWarp * it < (int)d.cnt) ? __ldcs(src + kWarp * it) : 0u;
+}
+
+// if (m != 0) { shared[sa] = v; sa += 4; }  -- predicated STS (the staging of the list compaction)
+__device__ __forceinline__ void sts_if(uint32_t m, uint32_t& sa, uint32_t v) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p st.shared.u32 [%0], %2;\n\t@p add.u32 %0, %0, 4;\n\t}"
+                 : "+r"(sa) : "r"(m), "r"(v) : "memory");
+}
+
+// Work loop of the pass and tail kernels: each warp walks chunks c_lo + warp0, + nwarps, ...; the
+// next chunk's descriptor and entries are in flight while the current chunk is processed
+// (PREF = true), or only the descriptor is (PREF = false, fewer registers).
+template <bool PREF, typename Body>
+__device__ __forceinline__ void chunk_loop(const PassArgs& A, int lane, Body body) {
     const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t c_lo = A.chunk_bounds[0], c_hi = A.chunk_bounds[1];
+    uint64_t ch = c_lo + warp0;
+    ChunkDesc d = load_desc(A.chunks, ch, c_hi);
+    ChunkDesc dn = load_desc(A.chunks, ch + nwarps, c_hi);
+    uint32_t p[kItems];
+    load_items(p, A.list, A.list_base, d, lane);
+    for (; ch < c_hi; ch += nwarps) {
+        if (PREF) {
+            uint32_t pn[kItems];
+            load_items(pn, A.list, A.list_base, dn, lane);
+            const ChunkDesc dnn = load_desc(A.chunks, ch + 2 * nwarps, c_hi);
+            body(d, p);
+#pragma unroll
+            for (int it = 0; it < kItems; ++it) p[it] = pn[it];
+            d = dn;
+            dn = dnn;
+        } else {
+            body(d, p);
+            d = dn;
+            dn = load_desc(A.chunks, ch + 2 * nwarps, c_hi);
+            load_items(p, A.list, A.list_base, d, lane);
+        }
+    }
+}
+
+template <typename I, int MODE, bool PREF>
+__global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
+    __shared__ uint32_t s_stage[MODE == MODE_WRITE ? 8 * 4 * kChunk : 1];   // 4 KB per warp
+    const int lane = threadIdx.x & 31;
     const int D = A.D;
     const int sh = D - A.level;                       // log2 of the parent side s (>= 1)
     const I N = (I)A.N;
     const I Qc = ((I)3 * N) << (sh - 1);              // 3N * s/2: child b-step
     const I Qg = (MODE == MODE_COUNT) ? (I)0 : (((I)3 * N) << (sh - 2));   // 3N * s/4 (sh >= 2)
+    const uint32_t stage_sa = (uint32_t)__cvta_generic_to_shared(s_stage) + (threadIdx.x >> 5) * (4 * kChunk * 4);
 
-    for (uint64_t ch = c_lo + warp0; ch < c_hi; ch += nwarps) {
-        const uint32_t r = __ldg(A.chunk_region + ch);
-        const uint64_t k = ch - __ldg(A.p_choff + r);
-        const uint32_t len = __ldg(A.p_len + r);
-        const uint64_t e0 = __ldg(A.p_off + r) - A.list_base + k * kChunk;
-        const int cnt = (int)min((uint64_t)kChunk, (uint64_t)len - k * kChunk);
-        const uint32_t tree = __ldg(A.p_tree + r);
-        const bool beta = __ldg(A.tree_beta + tree) != 0;
-        const I i0 = (I)__ldg(A.p_a + r) << sh;
-        const I j0 = (I)__ldg(A.p_c + r) << sh;
+    chunk_loop<PREF>(A, lane, [&](const ChunkDesc& d, const uint32_t (&p)[kItems]) {
+        const int cnt = (int)d.cnt;
+        const I i0 = (I)d.a << sh;
+        const I j0 = (I)d.c << sh;
         const I alpha = ((I)1 << D) - 2 * i0;          // g = ex*alpha + (ey << D) + beta_c
         const I beta_m1 = (N << D) - (I)3 * N * j0 - 1;
 
-        uint32_t nfq[4] = {kNone, kNone, kNone, kNone};
-        uint64_t cdst[4] = {0, 0, 0, 0};
-        uint32_t my_nf = kNone;            // lanes 0..3: next-frontier index of child `lane`
-        if (MODE != MODE_COUNT) {
-            uint64_t my_off = 0;
-            if (lane < 4) {
-                my_nf = __ldg(A.nf + 4 * (uint64_t)(r - A.nf_rbase) + lane);
-                if (my_nf != kNone && (my_nf < A.q0 || my_nf >= A.q1)) my_nf = kNone;
-                if (MODE == MODE_WRITE && my_nf != kNone) my_off = __ldg(A.c_off + my_nf) - A.c_list_base;
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                nfq[q] = shfl_u32(my_nf, q);
-                if (MODE == MODE_WRITE) cdst[q] = shfl_u64(my_off, q);
-            }
-        }
-
-        uint32_t p[kItems];
-#pragma unroll
-        for (int it = 0; it < kItems; ++it) {
-            const int idx = lane + kWarp * it;
-            p[it] = (idx < cnt) ? __ldcs(A.list + e0 + idx) : 0u;
+        // lanes 0..3: next-frontier index and list offset of child `lane` (split children only)
+        uint32_t my_nf = kNone;
+        uint64_t my_off = 0;
+        if (MODE != MODE_COUNT && lane < 4) {
+            const uint64_t k = 4 * (uint64_t)(d.r - A.nf_rbase) + lane;
+            my_nf = __ldg(A.nf + k);
+            if (MODE == MODE_WRITE) my_off = __ldg(A.nfoff + k);
         }
 
         uint32_t cm = 0;
         uint32_t acc[4] = {0, 0, 0, 0};
-        if (beta) chunk_math<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc);
+        if (d.beta) chunk_math<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc);
         else chunk_math<I, MODE, false>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc);
 
         if (MODE == MODE_COUNT) {
@@ -247,10 +285,15 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
             warp_sum_bytes(acc[0], c02, c13);
             if (lane < 4) {
                 const uint32_t v = byte_counter(c02, c13, lane);
-                if (v) atomicAdd(A.votes + 4 * (uint64_t)(r - A.nf_rbase) + lane, v);
+                if (v) atomicAdd(A.votes + 4 * (uint64_t)(d.r - A.nf_rbase) + lane, v);
             }
-            continue;
+            return;
         }
+
+        if (my_nf != kNone && (my_nf < A.q0 || my_nf >= A.q1)) my_nf = kNone;
+        uint32_t nfq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) nfq[q] = shfl_u32(my_nf, q);
 
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -265,9 +308,9 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
 
         if (MODE == MODE_WRITE) {
             // Child list compaction (warp-private, order within a child list is irrelevant to the
-            // counts): per-lane per-child counts -> one packed warp exclusive scan -> entries staged
-            // in shared memory per child -> one atomic per (chunk, split child) reserves a run ->
-            // fully coalesced copy-out.
+            // counts): per-lane per-child counts -> one packed warp exclusive scan -> predicated
+            // stores into a per-child shared-memory staging area -> one atomic per (chunk, split
+            // child) reserves a run -> fully coalesced copy-out.
             uint32_t splitm = 0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) splitm |= (nfq[q] != kNone ? 1u : 0u) << q;
@@ -276,19 +319,18 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
             const uint32_t c2 = __popc(cm & 0x44444444u), c3 = __popc(cm & 0x88888888u);
             uint32_t s02 = c0 | (c2 << 16), s13 = c1 | (c3 << 16);     // 16-bit fields: sums <= 256
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t t02 = __shfl_up_sync(kFull, s02, d), t13 = __shfl_up_sync(kFull, s13, d);
-                if (lane >= d) { s02 += t02; s13 += t13; }
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const uint32_t t02 = __shfl_up_sync(kFull, s02, dd), t13 = __shfl_up_sync(kFull, s13, dd);
+                if (lane >= dd) { s02 += t02; s13 += t13; }
             }
             const uint32_t tot02 = __shfl_sync(kFull, s02, 31), tot13 = __shfl_sync(kFull, s13, 31);
-            uint32_t pos[4] = {(s02 & 0xFFFFu) - c0, (s13 & 0xFFFFu) - c1, (s02 >> 16) - c2, (s13 >> 16) - c3};
-            uint32_t* stage = s_stage + (threadIdx.x >> 5) * (4 * kChunk);
+            uint32_t sa[4] = {stage_sa + 4 * ((s02 & 0xFFFFu) - c0), stage_sa + 4 * (kChunk + (s13 & 0xFFFFu) - c1),
+                              stage_sa + 4 * (2 * kChunk + (s02 >> 16) - c2),
+                              stage_sa + 4 * (3 * kChunk + (s13 >> 16) - c3)};
 #pragma unroll
             for (int it = 0; it < kItems; ++it) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if ((cm >> (4 * it + q)) & 1u) stage[q * kChunk + pos[q]++] = p[it];
-                }
+                for (int q = 0; q < 4; ++q) sts_if(cm & (1u << (4 * it + q)), sa[q], p[it]);
             }
             const uint32_t tq[4] = {tot02 & 0xFFFFu, tot13 & 0xFFFFu, tot02 >> 16, tot13 >> 16};
             uint32_t my_base = 0;
@@ -296,16 +338,18 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
                 const uint32_t t = lane == 0 ? tq[0] : lane == 1 ? tq[1] : lane == 2 ? tq[2] : tq[3];
                 if (t) my_base = atomicAdd(A.c_cursor + (my_nf - A.q0), t);
             }
+            const uint64_t my_dst = my_off - A.c_list_base + my_base;
             __syncwarp();
+            const uint32_t* stage = s_stage + (threadIdx.x >> 5) * (4 * kChunk);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 if (tq[q] == 0) continue;                   // warp-uniform
-                uint32_t* dst = A.c_list + cdst[q] + shfl_u32(my_base, q);
+                uint32_t* dst = A.c_list + shfl_u64(my_dst, q);
                 for (uint32_t i = lane; i < tq[q]; i += kWarp) dst[i] = stage[q * kChunk + i];
             }
             __syncwarp();
         }
-    }
+    });
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -383,41 +427,25 @@ __global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
     for (int t = threadIdx.x; t < kTab8 * 16; t += blockDim.x) s_tab[t] = tab8_entry(t >> 4);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t c_lo = A.chunk_bounds[0], c_hi = A.chunk_bounds[1];
     const int D = A.D;
     const int sh = D - A.level;                       // == 3
     const I N = (I)A.N;
     const I N3 = (I)3 * N;
 
-    for (uint64_t ch = c_lo + warp0; ch < c_hi; ch += nwarps) {
-        const uint32_t r = __ldg(A.chunk_region + ch);
-        const uint64_t k = ch - __ldg(A.p_choff + r);
-        const uint32_t len = __ldg(A.p_len + r);
-        const uint64_t e0 = __ldg(A.p_off + r) - A.list_base + k * kChunk;
-        const int cnt = (int)min((uint64_t)kChunk, (uint64_t)len - k * kChunk);
-        const uint32_t tree = __ldg(A.p_tree + r);
-        const bool beta = __ldg(A.tree_beta + tree) != 0;
-        const I i0 = (I)__ldg(A.p_a + r) << sh;
-        const I j0 = (I)__ldg(A.p_c + r) << sh;
+    chunk_loop<false>(A, lane, [&](const ChunkDesc& d, const uint32_t (&p)[kItems]) {
+        const int cnt = (int)d.cnt;
+        const I i0 = (I)d.a << sh;
+        const I j0 = (I)d.c << sh;
         const I alpha = ((I)1 << D) - 2 * i0;
         const I beta_m1 = (N << D) - N3 * j0 - 1;
-
-        uint32_t p[kItems];
-#pragma unroll
-        for (int it = 0; it < kItems; ++it) {
-            const int idx = lane + kWarp * it;
-            p[it] = (idx < cnt) ? __ldcs(A.list + e0 + idx) : 0u;
-        }
         uint32_t a8[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) a8[i] = 0;
-        if (beta) tail_math<I, true>(p, cnt, lane, alpha, beta_m1, D, N3, s_tab + (lane & 15), a8);
+        if (d.beta) tail_math<I, true>(p, cnt, lane, alpha, beta_m1, D, N3, s_tab + (lane & 15), a8);
         else tail_math<I, false>(p, cnt, lane, alpha, beta_m1, D, N3, s_tab + (lane & 15), a8);
 
         // grid[(r - nf_rbase) * 64 + 8u + v]: a8[2u] byte b = row b, a8[2u+1] byte b = row 4+b
-        uint32_t* dst = A.votes + (uint64_t)(r - A.nf_rbase) * kTailCells;
+        uint32_t* dst = A.votes + (uint64_t)(d.r - A.nf_rbase) * kTailCells;
 #pragma unroll
         for (int wi = 0; wi < 16; ++wi) {
             uint32_t c02, c13;
@@ -427,7 +455,7 @@ __global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
                 if (v) atomicAdd(dst + 8 * (wi >> 1) + 4 * (wi & 1) + lane, v);
             }
         }
-    }
+    });
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -458,34 +486,50 @@ __device__ __forceinline__ uint2 tab16_entry(int t) {
 // The mask table is replicated 16x, entry e of copy c at slot 16e + c: an LDS.64 serves 16 lanes
 // per shared-memory wavefront, and lane l reads copy (l & 15), i.e. its own bank pair, so lookups
 // are bank-conflict-free whatever entries the lanes need.
+// Per-line raster state at the SW corner of R: y = G_SW - 1 (>= 0 for every listed line: it crosses
+// R), f = min(floor(y / 3N), 16) (for int32, a multiply-high by the host-computed reciprocal, exact
+// for 0 <= y < 2^31; for int64 a branch-free binary search), then z = y - f*3N and the table
+// address of entry (k = f + 1, drop 0) in this lane's copy. Lanes past the chunk's end point at
+// the all-zero entries of k = 0.
 template <typename I>
-__global__ void __launch_bounds__(256, 3) k_tail16(const PassArgs A) {
+__device__ __forceinline__ I floor_div3n_clamp16(I y, I N3, uint32_t div_m, uint32_t div_s) {
+    if (sizeof(I) == 4) {
+        const uint32_t q = __umulhi((uint32_t)y, div_m) >> div_s;
+        return (I)min(q, 16u);
+    } else {
+        I f = (y >= (I)8 * N3) ? (I)8 : (I)0;
+        f += (y >= (f + 4) * N3) ? (I)4 : (I)0;
+        f += (y >= (f + 2) * N3) ? (I)2 : (I)0;
+        f += (y >= (f + 1) * N3) ? (I)1 : (I)0;
+        return (y >= (I)16 * N3) ? (I)16 : f;
+    }
+}
+
+template <typename I, bool PREF>
+__global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) {
     __shared__ uint2 s_tab[kTab16 * 16];
     for (int t = threadIdx.x; t < kTab16 * 16; t += blockDim.x) s_tab[t] = tab16_entry(t >> 4);
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint32_t tab_sm = (uint32_t)__cvta_generic_to_shared(s_tab + (lane & 15));
     const uint32_t c128 = A.tab_stride, c256n = 0u - 2u * A.tab_stride;   // 128, -256 (runtime)
-    const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t c_lo = A.chunk_bounds[0], c_hi = A.chunk_bounds[1];
+    const uint32_t c256 = 2u * A.tab_stride;
+    const uint32_t ta_zero = tab_sm + 128u * 32u;                          // entry (k = 0, drop 0)
+    const uint32_t ta_base = tab_sm + 128u * 34u;                          // entry (k = 1, drop 0)
     const int D = A.D;
     const int sh = D - A.level;                       // == 4
     const I N = (I)A.N;
     const I N3 = (I)3 * N;
+    const uint32_t div_m = A.div_m, div_s = A.div_s;
 
-    for (uint64_t ch = c_lo + warp0; ch < c_hi; ch += nwarps) {
-        const uint32_t r = __ldg(A.chunk_region + ch);
-        const uint64_t k = ch - __ldg(A.p_choff + r);
-        const uint32_t len = __ldg(A.p_len + r);
-        const uint64_t e0 = __ldg(A.p_off + r) - A.list_base + k * kChunk;
-        const int cnt = (int)min((uint64_t)kChunk, (uint64_t)len - k * kChunk);
-        const uint32_t tree = __ldg(A.p_tree + r);
-        const bool beta = __ldg(A.tree_beta + tree) != 0;
-        const I i0 = (I)__ldg(A.p_a + r) << sh;
-        const I j0 = (I)__ldg(A.p_c + r) << sh;
+    chunk_loop<PREF>(A, lane, [&](const ChunkDesc& d, const uint32_t (&p)[kItems]) {
+        const int cnt = (int)d.cnt;
+        const I i0 = (I)d.a << sh;
+        const I j0 = (I)d.c << sh;
         const I alpha = ((I)1 << D) - 2 * i0;
         const I beta_m1 = (N << D) - N3 * j0 - 1;
+        // byte selectors: ex = low half-word of the packed entry for BETA (x <-> y), high for ALPHA
+        const uint32_t sel_ex = d.beta ? 0x4410u : 0x4432u, sel_ey = d.beta ? 0x4432u : 0x4410u;
 
         // per-line raster state carried across the 4 column blocks: z = y - (k-1)*3N (height of the
         // line above its row's floor at the current lattice column; a column drops iff z < 0), the
@@ -494,24 +538,16 @@ __global__ void __launch_bounds__(256, 3) k_tail16(const PassArgs A) {
         uint32_t ta[kItems];
 #pragma unroll
         for (int it = 0; it < kItems; ++it) {
-            const int idx = lane + kWarp * it;
-            const uint32_t w = (idx < cnt) ? __ldcs(A.list + e0 + idx) : 0u;
-            const I ex = (I)(beta ? (w & 0xFFFFu) : (w >> 16));
-            const I ey = (I)(beta ? (w >> 16) : (w & 0xFFFFu));
-            I yy = ex * alpha + (ey << D) + beta_m1;          // G(SW corner of R) - 1
-            if (idx >= cnt) yy = (I)-1;
-            // f = min(floor(y / 3N), 16) for y >= 0 (branch-free binary search)
-            I f = (yy >= (I)8 * N3) ? (I)8 : (I)0;
-            f += (yy >= (f + 4) * N3) ? (I)4 : (I)0;
-            f += (yy >= (f + 2) * N3) ? (I)2 : (I)0;
-            f += (yy >= (f + 1) * N3) ? (I)1 : (I)0;
-            f = (yy >= (I)16 * N3) ? (I)16 : f;
-            const bool below = yy < 0;
+            const uint32_t w = p[it];
+            const I ex = (I)__byte_perm(w, 0, sel_ex);
+            const I ey = (I)__byte_perm(w, 0, sel_ey);
+            const I yy = ex * alpha + (ey << D) + beta_m1;         // G(SW corner of R) - 1 >= 0
+            const I f = floor_div3n_clamp16<I>(yy, N3, div_m, div_s);
             P8[it] = 2 * ex;
-            z[it] = below ? yy + N3 : yy - f * N3;
-            ta[it] = tab_sm + 128u * (below ? 32u : 2u * (uint32_t)f + 34u);   // entry 2 * (k + 16)
+            z[it] = yy - f * N3;
+            ta[it] = (lane + kWarp * it < cnt) ? mad_u32((uint32_t)f, c256, ta_base) : ta_zero;
         }
-        uint32_t* dst = A.votes + (uint64_t)(r - A.nf_rbase) * kTail16Cells;
+        uint32_t* dst = A.votes + (uint64_t)(d.r - A.nf_rbase) * kTail16Cells;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             uint32_t acc[8];                                  // [2 * column-in-block + row half], nibbles
@@ -522,14 +558,14 @@ __global__ void __launch_bounds__(256, 3) k_tail16(const PassArgs A) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const I zz = z[it] - P8[it];
-                    const uint32_t d = sign_bit<I>(zz);                 // drop: the line left its row
+                    const uint32_t dr = sign_bit<I>(zz);                // drop: the line left its row
                     uint32_t mx, my;
                     asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mx), "=r"(my)
-                                 : "r"(mad_u32(d, c128, ta[it])));
+                                 : "r"(mad_u32(dr, c128, ta[it])));
                     acc[2 * u + 0] += mx;
                     acc[2 * u + 1] += my;
-                    ta[it] = mad_u32(d, c256n, ta[it]);                 // k -= drop
-                    z[it] = mad_i(d, N3, zz);                           // threshold -= drop * 3N
+                    ta[it] = mad_u32(dr, c256n, ta[it]);                // k -= drop
+                    z[it] = mad_i(dr, N3, zz);                          // threshold -= drop * 3N
                 }
             }
             // widen nibbles to bytes: word 4u + 2w + par holds rows 8w + 2b + par in byte b
@@ -584,19 +620,24 @@ __global__ void __launch_bounds__(256, 3) k_tail16(const PassArgs A) {
             if (c0) atomicAdd(dst + 16 * col + row0, c0);
             if (c1) atomicAdd(dst + 16 * col + row0 + 4, c1);
         }
-    }
+    });
 }
 
-int tail16_blocks_per_sm(bool int64) {
+using PassKernel = void (*)(const PassArgs);
+
+static PassKernel tail16_kernel(bool int64, bool pref) {
+    if (int64) return pref ? k_tail16<int64_t, true> : k_tail16<int64_t, false>;
+    return pref ? k_tail16<int32_t, true> : k_tail16<int32_t, false>;
+}
+
+int tail16_blocks_per_sm(bool int64, bool pref) {
     int n = 0;
-    if (int64) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tail16<int64_t>, 256, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tail16<int32_t>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tail16_kernel(int64, pref), 256, 0);
     return n > 0 ? n : 1;
 }
 
-cudaError_t launch_tail16(bool int64, const PassArgs& a, int grid, cudaStream_t st) {
-    if (int64) k_tail16<int64_t><<<grid, 256, 0, st>>>(a);
-    else k_tail16<int32_t><<<grid, 256, 0, st>>>(a);
+cudaError_t launch_tail16(bool int64, bool pref, const PassArgs& a, int grid, cudaStream_t st) {
+    tail16_kernel(int64, pref)<<<grid, 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -693,34 +734,26 @@ cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_
     return cudaGetLastError();
 }
 
-template <typename I, int MODE>
-static int blocks_per_sm_impl() {
+template <typename I, bool P>
+static PassKernel pass_kernel_t(int mode) {
+    if (mode == MODE_COUNT) return k_pass<I, MODE_COUNT, P>;
+    if (mode == MODE_WRITE) return k_pass<I, MODE_WRITE, P>;
+    return k_pass<I, MODE_COUNT2, P>;
+}
+
+static PassKernel pass_kernel(int mode, bool int64, bool pref) {
+    if (int64) return pref ? pass_kernel_t<int64_t, true>(mode) : pass_kernel_t<int64_t, false>(mode);
+    return pref ? pass_kernel_t<int32_t, true>(mode) : pass_kernel_t<int32_t, false>(mode);
+}
+
+int pass_blocks_per_sm(int mode, bool int64, bool pref) {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pass<I, MODE>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, pass_kernel(mode, int64, pref), 256, 0);
     return n > 0 ? n : 1;
 }
 
-int pass_blocks_per_sm(int mode, bool int64) {
-    if (int64) {
-        if (mode == MODE_COUNT) return blocks_per_sm_impl<int64_t, MODE_COUNT>();
-        if (mode == MODE_WRITE) return blocks_per_sm_impl<int64_t, MODE_WRITE>();
-        return blocks_per_sm_impl<int64_t, MODE_COUNT2>();
-    }
-    if (mode == MODE_COUNT) return blocks_per_sm_impl<int32_t, MODE_COUNT>();
-    if (mode == MODE_WRITE) return blocks_per_sm_impl<int32_t, MODE_WRITE>();
-    return blocks_per_sm_impl<int32_t, MODE_COUNT2>();
-}
-
-cudaError_t launch_pass(int mode, bool int64, const PassArgs& a, int grid, cudaStream_t st) {
-    if (int64) {
-        if (mode == MODE_COUNT) k_pass<int64_t, MODE_COUNT><<<grid, 256, 0, st>>>(a);
-        else if (mode == MODE_WRITE) k_pass<int64_t, MODE_WRITE><<<grid, 256, 0, st>>>(a);
-        else k_pass<int64_t, MODE_COUNT2><<<grid, 256, 0, st>>>(a);
-    } else {
-        if (mode == MODE_COUNT) k_pass<int32_t, MODE_COUNT><<<grid, 256, 0, st>>>(a);
-        else if (mode == MODE_WRITE) k_pass<int32_t, MODE_WRITE><<<grid, 256, 0, st>>>(a);
-        else k_pass<int32_t, MODE_COUNT2><<<grid, 256, 0, st>>>(a);
-    }
+cudaError_t launch_pass(int mode, bool int64, bool pref, const PassArgs& a, int grid, cudaStream_t st) {
+    pass_kernel(mode, int64, pref)<<<grid, 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -904,6 +937,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
                     A.leaves[f] = {tree, ca, cb, v[q]};
                 } else {
                     nf4[q] = f;
+                    if (A.need_lists) A.nfoff[4 * (uint64_t)p + q] = s;
                     A.out.tree[f] = tree;
                     A.out.a[f] = ca;
                     A.out.c[f] = cb;
@@ -958,19 +992,32 @@ cudaError_t launch_split(const SplitArgs& a, cudaStream_t st) {
 // ---------------------------------------------------------------------------------------------
 // Chunk map: chunk -> region for a frontier (one warp per region).
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_chunk_map(const uint64_t* __restrict__ choff, uint32_t F,
-                                                   uint32_t* __restrict__ chunk_region) {
+__global__ void __launch_bounds__(256) k_chunk_map(const uint64_t* __restrict__ choff, const uint64_t* __restrict__ off,
+                                                   const uint32_t* __restrict__ len, const uint32_t* __restrict__ ra,
+                                                   const uint32_t* __restrict__ rc, const uint32_t* __restrict__ tree,
+                                                   const uint8_t* __restrict__ tree_beta, uint32_t F,
+                                                   ChunkDesc* __restrict__ chunks) {
     const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= F) return;
-    const uint64_t b = choff[w], e = choff[w + 1];
-    for (uint64_t k = b + lane; k < e; k += 32) chunk_region[k] = (uint32_t)w;
+    const uint64_t b = choff[w], e = choff[w + 1], o = off[w];
+    const uint32_t n = len[w], a = ra[w], c = rc[w], beta = tree_beta[tree[w]];
+    for (uint64_t k = b + lane; k < e; k += 32) {
+        const uint64_t j = (k - b) * kChunk;
+        const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, (uint64_t)n - j);
+        uint4* q = reinterpret_cast<uint4*>(chunks + k);
+        q[0] = make_uint4((uint32_t)w, cnt, a, c);
+        const uint64_t e0 = o + j;
+        q[1] = make_uint4((uint32_t)e0, (uint32_t)(e0 >> 32), beta, 0u);
+    }
 }
 
-cudaError_t launch_chunk_map(const uint64_t* choff, uint32_t F, uint32_t* chunk_region, cudaStream_t st) {
+cudaError_t launch_chunk_map(const uint64_t* choff, const uint64_t* off, const uint32_t* len, const uint32_t* a,
+                             const uint32_t* c, const uint32_t* tree, const uint8_t* tree_beta, uint32_t F,
+                             ChunkDesc* chunks, cudaStream_t st) {
     if (F == 0) return cudaSuccess;
     const uint64_t blocks = ((uint64_t)F * 32 + 255) / 256;
-    k_chunk_map<<<(unsigned)blocks, 256, 0, st>>>(choff, F, chunk_region);
+    k_chunk_map<<<(unsigned)blocks, 256, 0, st>>>(choff, off, len, a, c, tree, tree_beta, F, chunks);
     return cudaGetLastError();
 }
 

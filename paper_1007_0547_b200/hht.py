@@ -41,7 +41,8 @@ class HHTError(RuntimeError):
 class Opts(C.Structure):
     _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("halves", C.c_uint32),
                 ("record_levels", C.c_uint32), ("force_int64", C.c_uint32), ("profile", C.c_uint32),
-                ("tail_depth", C.c_uint32), ("mem_budget", C.c_size_t), ("nccl_id", C.c_void_p)]
+                ("tail_depth", C.c_uint32), ("prefetch", C.c_uint32), ("mem_budget", C.c_size_t),
+                ("nccl_id", C.c_void_p)]
 
 
 class Leaf(C.Structure):
@@ -146,7 +147,8 @@ class HHT:
 
     def __init__(self, device: int = 0, halves: int = ALPHA | BETA, record_levels: bool = True,
                  force_int64: bool = False, profile: bool = False, mem_budget: int = 0,
-                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, tail_depth: int = 0):
+                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, tail_depth: int = 0,
+                 prefetch: int = 0):
         self._lib = load()
         o = Opts()
         self._lib.hht_default_opts(C.byref(o))
@@ -154,6 +156,7 @@ class HHT:
         o.record_levels, o.force_int64, o.profile = int(record_levels), int(force_int64), int(profile)
         o.mem_budget = mem_budget
         o.tail_depth = tail_depth
+        o.prefetch = prefetch
         self._id = None
         if nccl_id is not None:
             self._id = C.create_string_buffer(bytes(nccl_id), 128)
