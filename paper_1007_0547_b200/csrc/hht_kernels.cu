@@ -258,6 +258,8 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
     const I Qc = ((I)3 * N) << (sh - 1);              // 3N * s/2: child b-step
     const I Qg = (MODE == MODE_COUNT) ? (I)0 : (((I)3 * N) << (sh - 2));   // 3N * s/4 (sh >= 2)
     const uint32_t stage_sa = (uint32_t)__cvta_generic_to_shared(s_stage) + (threadIdx.x >> 5) * (4 * kChunk * 4);
+    const uint32_t cell_q = ((uint32_t)lane * 11u) >> 5;          // lane L < 12: child q = L / 3
+    const uint32_t cell_qq = (uint32_t)lane - 3u * cell_q + 1u;    // grandchild qq = 1 + L % 3
 
     chunk_loop<PREF>(A, lane, [&](const ChunkDesc& d, const uint32_t (&p)[kItems]) {
         const int cnt = (int)d.cnt;
@@ -291,48 +293,61 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
         }
 
         if (my_nf != kNone && (my_nf < A.q0 || my_nf >= A.q1)) my_nf = kNone;
-        uint32_t nfq[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) nfq[q] = shfl_u32(my_nf, q);
 
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (nfq[q] == kNone) continue;                  // warp-uniform
-            uint32_t c02, c13;
-            warp_sum_bytes(acc[q], c02, c13);
-            if (lane >= 1 && lane < 4) {             // NE (lane 0) is derived in the split
-                const uint32_t v = byte_counter(c02, c13, lane);
-                if (v) atomicAdd(A.votes + 4 * (uint64_t)(nfq[q] - A.q0) + lane, v);
-            }
+        // Count-ahead votes: the 12 derived-free cells (child q, grandchild qq = NW, SW, SE) in
+        // 16-bit fields of 6 words (cell L = 3q + qq - 1 at field L & 1 of word L >> 1), one warp
+        // sum per word; lane L < 12 then adds cell L to its split child's vote counter.
+        {
+            const uint32_t w0 = ((acc[0] >> 8) & 0xFFu) | (acc[0] & 0xFF0000u);
+            const uint32_t w1 = (acc[0] >> 24) | ((acc[1] << 8) & 0xFF0000u);
+            const uint32_t w2 = ((acc[1] >> 16) & 0xFFu) | ((acc[1] >> 8) & 0xFF0000u);
+            const uint32_t w3 = ((acc[2] >> 8) & 0xFFu) | (acc[2] & 0xFF0000u);
+            const uint32_t w4 = (acc[2] >> 24) | ((acc[3] << 8) & 0xFF0000u);
+            const uint32_t w5 = ((acc[3] >> 16) & 0xFFu) | ((acc[3] >> 8) & 0xFF0000u);
+            const uint32_t s0 = __reduce_add_sync(kFull, w0), s1 = __reduce_add_sync(kFull, w1);
+            const uint32_t s2 = __reduce_add_sync(kFull, w2), s3 = __reduce_add_sync(kFull, w3);
+            const uint32_t s4 = __reduce_add_sync(kFull, w4), s5 = __reduce_add_sync(kFull, w5);
+            const uint32_t t0 = (lane & 2) ? s1 : s0, t1 = (lane & 2) ? s3 : s2, t2 = (lane & 2) ? s5 : s4;
+            const uint32_t sw = (lane & 8) ? t2 : ((lane & 4) ? t1 : t0);      // word lane >> 1 (lane < 12)
+            const uint32_t v = (sw >> (16 * (lane & 1))) & 0xFFFFu;
+            const uint32_t nf_l = __shfl_sync(kFull, my_nf, cell_q);
+            if (lane < 12 && nf_l != kNone && v) atomicAdd(A.votes + 4 * (uint64_t)(nf_l - A.q0) + cell_qq, v);
         }
 
         if (MODE == MODE_WRITE) {
             // Child list compaction (warp-private, order within a child list is irrelevant to the
-            // counts): per-lane per-child counts -> one packed warp exclusive scan -> predicated
-            // stores into a per-child shared-memory staging area -> one atomic per (chunk, split
-            // child) reserves a run -> fully coalesced copy-out.
+            // counts): per-lane per-child counts -> one packed warp scan -> predicated stores into a
+            // per-child shared-memory staging area -> one atomic per (chunk, split child) reserves a
+            // run -> coalesced copy-out.
             uint32_t splitm = 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) splitm |= (nfq[q] != kNone ? 1u : 0u) << q;
+            for (int q = 0; q < 4; ++q) splitm |= (__shfl_sync(kFull, my_nf, q) != kNone ? 1u : 0u) << q;
             cm &= splitm * 0x11111111u;
             const uint32_t c0 = __popc(cm & 0x11111111u), c1 = __popc(cm & 0x22222222u);
             const uint32_t c2 = __popc(cm & 0x44444444u), c3 = __popc(cm & 0x88888888u);
-            uint32_t s02 = c0 | (c2 << 16), s13 = c1 | (c3 << 16);     // 16-bit fields: sums <= 256
+            // inclusive scan of the 4 counts in byte fields: a lane's inclusive sum <= 31*8 except
+            // lane 31's, whose wrap is undone exactly by the modular subtraction below
+            const uint32_t own = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+            uint32_t inc = own;
 #pragma unroll
             for (int dd = 1; dd < 32; dd <<= 1) {
-                const uint32_t t02 = __shfl_up_sync(kFull, s02, dd), t13 = __shfl_up_sync(kFull, s13, dd);
-                if (lane >= dd) { s02 += t02; s13 += t13; }
+                uint32_t t;
+                asm volatile("{\n\t.reg .pred p;\n\tshfl.sync.up.b32 %0|p, %1, %2, 0, 0xffffffff;\n\t@!p mov.b32 %0, 0;\n\t}"
+                             : "=r"(t) : "r"(inc), "r"(dd));
+                inc += t;
             }
-            const uint32_t tot02 = __shfl_sync(kFull, s02, 31), tot13 = __shfl_sync(kFull, s13, 31);
-            uint32_t sa[4] = {stage_sa + 4 * ((s02 & 0xFFFFu) - c0), stage_sa + 4 * (kChunk + (s13 & 0xFFFFu) - c1),
-                              stage_sa + 4 * (2 * kChunk + (s02 >> 16) - c2),
-                              stage_sa + 4 * (3 * kChunk + (s13 >> 16) - c3)};
+            const uint32_t exc = inc - own;
+            const uint32_t t02 = __reduce_add_sync(kFull, c0 | (c2 << 16));
+            const uint32_t t13 = __reduce_add_sync(kFull, c1 | (c3 << 16));
+            const uint32_t tq[4] = {t02 & 0xFFFFu, t13 & 0xFFFFu, t02 >> 16, t13 >> 16};
+            uint32_t sa[4] = {stage_sa + 4 * (exc & 0xFFu), stage_sa + 4 * (kChunk + ((exc >> 8) & 0xFFu)),
+                              stage_sa + 4 * (2 * kChunk + ((exc >> 16) & 0xFFu)),
+                              stage_sa + 4 * (3 * kChunk + (exc >> 24))};
 #pragma unroll
             for (int it = 0; it < kItems; ++it) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) sts_if(cm & (1u << (4 * it + q)), sa[q], p[it]);
             }
-            const uint32_t tq[4] = {tot02 & 0xFFFFu, tot13 & 0xFFFFu, tot02 >> 16, tot13 >> 16};
             uint32_t my_base = 0;
             if (lane < 4) {
                 const uint32_t t = lane == 0 ? tq[0] : lane == 1 ? tq[1] : lane == 2 ? tq[2] : tq[3];
@@ -343,9 +358,15 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
             const uint32_t* stage = s_stage + (threadIdx.x >> 5) * (4 * kChunk);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                if (tq[q] == 0) continue;                   // warp-uniform
-                uint32_t* dst = A.c_list + shfl_u64(my_dst, q);
-                for (uint32_t i = lane; i < tq[q]; i += kWarp) dst[i] = stage[q * kChunk + i];
+                const uint32_t n = tq[q];
+                if (n == 0) continue;                       // warp-uniform
+                uint32_t* dst = A.c_list + shfl_u64(my_dst, q) + lane;     // immediate offsets below
+                const uint32_t* src = stage + q * kChunk + lane;
+#pragma unroll
+                for (int it = 0; it < kItems; ++it) {
+                    if ((uint32_t)(kWarp * it) >= n) break;                 // warp-uniform
+                    if ((uint32_t)(lane + kWarp * it) < n) dst[kWarp * it] = src[kWarp * it];
+                }
             }
             __syncwarp();
         }
