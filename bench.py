@@ -50,6 +50,18 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _issue_clock(dev):
+    """SM count and SM clock for the integer-issue peak: MEASURED_PEAKS.json's max SM clock (the
+    clock sampled under load is reported beside it in `clocks`), else the device's rated clock."""
+    import torch
+    prop = torch.cuda.get_device_properties(dev)
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return prop.multi_processor_count, float(json.load(f)["sm_max_mhz"]), "MEASURED_PEAKS.json sm_max_mhz"
+    except Exception:
+        return prop.multi_processor_count, 1965.0, "B200 max SM clock (fallback)"
+
+
 def _workload(cfg):
     return {"workload": f"config{cfg.cid}: {cfg.text}", "N": cfg.N, "depth": cfg.D, "threshold": cfg.T,
             "images": cfg.images, "halves": "both" if cfg.halves == 3 else "alpha",
@@ -215,10 +227,11 @@ def main():
             step_ms.append(st["ms"])
             tests_tot += st["tests"]
             for k, v in h.profile().items():
-                p = prof_tot.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0})
+                p = prof_tot.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0, "ops": 0})
                 p["launches"] += v["launches"]
                 p["ms"] += v["ms"]
                 p["bytes"] += v["bytes"]
+                p["ops"] += v.get("ops", 0)
         ms = h.timer_end()
         torch.cuda.synchronize()
         barrier()
@@ -241,8 +254,9 @@ def main():
     peak, peak_kind = _peaks()
     dom = max((k for k in prof_tot if k not in ("allreduce",)), key=lambda k: prof_tot[k]["ms"])
     d = prof_tot[dom]
-    avg_ms = d["ms"] / max(d["launches"], 1)
-    achieved = (d["bytes"] / max(d["launches"], 1)) / (avg_ms / 1e3) / 1e9 if d["launches"] else 0.0
+    nl = max(d["launches"], 1)
+    avg_ms = d["ms"] / nl
+    achieved_gbs = (d["bytes"] / nl) / (avg_ms / 1e3) / 1e9 if d["launches"] else 0.0
     # traffic: DRAM bytes of one launch of the same kernel class from the committed ncu --set full
     # capture (profiles/ncu_traffic.json), with that launch's algorithmic bytes beside it
     traffic, cap = None, {}
@@ -253,15 +267,27 @@ def main():
             traffic = cap.get("traffic")
         except Exception:
             cap = {}
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                "traffic_launch_algorithmic_bytes": cap.get("algorithmic_bytes"),
-                "binding_unit": ("SM integer pipes (ncu: issue active %.0f%%, ALU pipe %.0f%%, FMA pipe %.0f%%, DRAM %.0f%%)"
-                                 % (cap["issue_active_pct"], cap["alu_pipe_pct"], cap["fma_pipe_pct"], cap["dram_pct"])
-                                 if cap.get("issue_active_pct") is not None else None),
-                "kernel_share_of_step": d["ms"] / max(sum(step_ms), 1e-9),
-                "launches": d["launches"], "avg_launch_ms": avg_ms,
-                "algorithmic_bytes_per_launch": d["bytes"] / max(d["launches"], 1)}
+    hbm = {"achieved": achieved_gbs, "peak": peak, "unit": "GB/s", "frac": achieved_gbs / peak,
+           "peak_source": peak_kind, "algorithmic_bytes_per_launch": d["bytes"] / nl, "traffic": traffic,
+           "traffic_launch_algorithmic_bytes": cap.get("algorithmic_bytes")}
+    ncu_pipes = ("ncu: issue active %.0f%%, ALU pipe %.0f%%, FMA pipe %.0f%%, DRAM %.0f%%"
+                 % (cap["issue_active_pct"], cap["alu_pipe_pct"], cap["fma_pipe_pct"], cap["dram_pct"])
+                 if cap.get("issue_active_pct") is not None else None)
+    common = {"kernel": dom, "kernel_share_of_step": d["ms"] / max(sum(step_ms), 1e-9),
+              "launches": d["launches"], "avg_launch_ms": avg_ms, "ncu": ncu_pipes}
+    if d.get("ops"):
+        # integer-issue bound: algorithmic instructions of the raster steps per launch
+        # over the launch time, against the SM issue rate (1 warp instruction / clock / SMSP)
+        sms, mhz, mhz_src = _issue_clock(local)
+        ipeak = sms * 4 * 32 * mhz * 1e6 / 1e12
+        ach = (d["ops"] / nl) / (avg_ms / 1e3) / 1e12
+        roofline = {"bound": "alu", "achieved": ach, "peak": ipeak, "unit": "Tinstr/s", "frac": ach / ipeak,
+                    "traffic": traffic, "peak_source": f"{sms} SMs x 4 SMSP x 32 lanes x {mhz:.0f} MHz ({mhz_src})",
+                    "algorithmic_instr_per_launch": d["ops"] / nl, **common, "hbm": hbm}
+    else:
+        roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+                    "frac": achieved_gbs / peak, "traffic": traffic, "peak_source": peak_kind,
+                    "algorithmic_bytes_per_launch": d["bytes"] / nl, **common}
 
     e2e = None
     if not a.no_e2e:

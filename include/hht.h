@@ -107,6 +107,8 @@ typedef struct {
                                 6 other (range selection), 7 allreduce */
     double ms[8];
     uint64_t bytes[8];       /* algorithmic HBM bytes moved by that class */
+    uint64_t ops[8];         /* algorithmic integer instructions (thread-level) of that class where
+                                it is issue-bound: the dense tail's raster steps; 0 else */
 } hht_profile;
 
 /* Fill opts with defaults (device 0, rank 0 of 1, both halves, records on). */

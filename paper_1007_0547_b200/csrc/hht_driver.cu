@@ -56,6 +56,7 @@ struct ProfEv {
     cudaEvent_t a, b;
     int cls;
     uint64_t bytes;
+    uint64_t ops;
 };
 
 }  // namespace
@@ -194,6 +195,7 @@ int prof_begin(hht_ctx* x, int cls, uint64_t bytes) {
     ProfEv& e = x->pev[x->pev_used];
     e.cls = cls;
     e.bytes = bytes;
+    e.ops = 0;
     cudaEventRecord(e.a, x->st);
     return (int)x->pev_used++;
 }
@@ -310,7 +312,7 @@ PassArgs pass_args(hht_ctx* x, Level& P, int level) {
     a.D = x->D;
     a.N = x->N;
     a.one = 1;
-    a.tab_stride = 128;
+    a.tab_stride = 256;   // k_tail16: table slot stride per entry (32 lane copies x 8 B)
     // floor(y / 3N) = umulhi(y, m) >> (l - 1) for 0 <= y < 2^31, with l = ceil(log2 3N) and
     // m = ceil(2^(31+l) / 3N) < 2^32 (3N is never a power of two); see floor_div3n_clamp16
     {
@@ -382,7 +384,12 @@ hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
     prof_end(x, id);
     TRY(sync(x));
     const uint64_t pairs = x->range_h->pairs;
-    if (id >= 0) x->pev[id].bytes = pairs * 4 + (uint64_t)n * cells * 4;
+    if (id >= 0) {
+        x->pev[id].bytes = pairs * 4 + (uint64_t)n * cells * 4;
+        // raster step = 8 instructions per (line, leaf column): advance the height, extract the
+        // drop, form the table address, load the column mask, two counter adds, two state updates
+        x->pev[id].ops = pairs * (1ull << TK) * 8;
+    }
     x->stat.pairs += pairs;
     TRY(allreduce_sum_u32(x, (uint32_t*)x->dense.p, (size_t)n * cells));
     // levels L+2 .. D: parents R_(c-1), votes gathered from the grids
@@ -714,6 +721,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
                 x->prof.ms[x->pev[i].cls] += m;
                 x->prof.launches[x->pev[i].cls] += 1;
                 x->prof.bytes[x->pev[i].cls] += x->pev[i].bytes;
+                x->prof.ops[x->pev[i].cls] += x->pev[i].ops;
                 x->launch_log.push_back({(uint32_t)x->pev[i].cls, 0, x->pev[i].bytes, (double)m});
             }
         }

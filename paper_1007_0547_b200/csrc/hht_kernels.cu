@@ -491,22 +491,27 @@ __global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
 // ---------------------------------------------------------------------------------------------
 constexpr int kTab16 = 68;  // (k + 16) * 2 + drop, k in -16..17
 
-// Column mask of the 16x16 tail as 4-bit counters: row v at nibble (v & 7) of word (v >> 3).
-// A lane adds at most kItems = 8 per cell per block, so nibbles do not overflow; they are widened
-// to bytes right before the warp reduction.
-__device__ __forceinline__ uint2 tab16_entry(int t) {
+// Column mask of the 16x16 tail as 4-bit counters, one table copy per lane. Logical row
+// v = 8h + 2b + par (h: word, b: byte, par: nibble within the byte) is stored at word h ^ L4, byte
+// b ^ L0, nibble par ^ L3, where Lx is bit x of the lane that owns the copy: the three lane-bit
+// swaps are exactly the register swaps the butterfly reduce-scatter in k_tail16 would otherwise do
+// with selects (levels xor 16, xor 8 and the final xor 1). A lane adds at most kItems = 8 per cell
+// per column block, so nibbles do not overflow; they are widened to bytes before the reduction.
+__device__ __forceinline__ uint2 tab16_entry(int t, int lane) {
     const int k = t / 2 - 16, d = t & 1;
     uint32_t w[2] = {0, 0};
     if (k >= 1) {
         const int vhi = min(k, 16) - 1, vlo = max(k - d - 1, 0);
-        for (int v = vlo; v <= vhi; ++v) w[v >> 3] |= 1u << (4 * (v & 7));
+        for (int v = vlo; v <= vhi; ++v) {
+            const int hp = (v >> 3) ^ ((lane >> 4) & 1);
+            const int bp = ((v >> 1) & 3) ^ (lane & 1);
+            const int np = (v & 1) ^ ((lane >> 3) & 1);
+            w[hp] |= 1u << (4 * (2 * bp + np));
+        }
     }
     return make_uint2(w[0], w[1]);
 }
 
-// The mask table is replicated 16x, entry e of copy c at slot 16e + c: an LDS.64 serves 16 lanes
-// per shared-memory wavefront, and lane l reads copy (l & 15), i.e. its own bank pair, so lookups
-// are bank-conflict-free whatever entries the lanes need.
 // Per-line raster state at the SW corner of R: y = G_SW - 1 (>= 0 for every listed line: it crosses
 // R), f = min(floor(y / 3N), 16) (for int32, a multiply-high by the host-computed reciprocal, exact
 // for 0 <= y < 2^31; for int64 a branch-free binary search), then z = y - f*3N and the table
@@ -528,15 +533,21 @@ __device__ __forceinline__ I floor_div3n_clamp16(I y, I N3, uint32_t div_m, uint
 
 template <typename I, bool PREF>
 __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) {
-    __shared__ uint2 s_tab[kTab16 * 16];
-    for (int t = threadIdx.x; t < kTab16 * 16; t += blockDim.x) s_tab[t] = tab16_entry(t >> 4);
+    // table entry e of lane copy c at slot 32e + c: an LDS.64 serves 16 lanes per wavefront and
+    // every lane reads its own bank pair, so lookups never conflict whatever entries lanes need
+    __shared__ uint2 s_tab[kTab16 * 32];
+    for (int t = threadIdx.x; t < kTab16 * 32; t += blockDim.x) s_tab[t] = tab16_entry(t >> 5, t & 31);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const uint32_t tab_sm = (uint32_t)__cvta_generic_to_shared(s_tab + (lane & 15));
-    const uint32_t c128 = A.tab_stride, c256n = 0u - 2u * A.tab_stride;   // 128, -256 (runtime)
-    const uint32_t c256 = 2u * A.tab_stride;
-    const uint32_t ta_zero = tab_sm + 128u * 32u;                          // entry (k = 0, drop 0)
-    const uint32_t ta_base = tab_sm + 128u * 34u;                          // entry (k = 1, drop 0)
+    const uint32_t tab_sm = (uint32_t)__cvta_generic_to_shared(s_tab + lane);
+    const uint32_t cdrop = A.tab_stride, ck2n = 0u - 2u * A.tab_stride;   // 256, -512 (runtime)
+    const uint32_t ck2 = 2u * A.tab_stride;
+    const uint32_t ta_zero = tab_sm + 256u * 32u;                          // entry (k = 0, drop 0)
+    const uint32_t ta_base = tab_sm + 256u * 34u;                          // entry (k = 1, drop 0)
+    // cells this lane holds after the reduce-scatter: column 4b + u, u = L1 + 2 L2; rows
+    // 8 L4 + 2 L0 + L3 (+ 4)
+    const uint32_t red_u = ((lane >> 1) & 1) + 2 * ((lane >> 2) & 1);
+    const uint32_t red_row = 8 * ((lane >> 4) & 1) + 2 * (lane & 1) + ((lane >> 3) & 1);
     const int D = A.D;
     const int sh = D - A.level;                       // == 4
     const I N = (I)A.N;
@@ -566,7 +577,7 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
             const I f = floor_div3n_clamp16<I>(yy, N3, div_m, div_s);
             P8[it] = 2 * ex;
             z[it] = yy - f * N3;
-            ta[it] = (lane + kWarp * it < cnt) ? mad_u32((uint32_t)f, c256, ta_base) : ta_zero;
+            ta[it] = (lane + kWarp * it < cnt) ? mad_u32((uint32_t)f, ck2, ta_base) : ta_zero;
         }
         uint32_t* dst = A.votes + (uint64_t)(d.r - A.nf_rbase) * kTail16Cells;
 #pragma unroll
@@ -582,64 +593,43 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
                     const uint32_t dr = sign_bit<I>(zz);                // drop: the line left its row
                     uint32_t mx, my;
                     asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mx), "=r"(my)
-                                 : "r"(mad_u32(dr, c128, ta[it])));
+                                 : "r"(mad_u32(dr, cdrop, ta[it])));
                     acc[2 * u + 0] += mx;
                     acc[2 * u + 1] += my;
-                    ta[it] = mad_u32(dr, c256n, ta[it]);                // k -= drop
+                    ta[it] = mad_u32(dr, ck2n, ta[it]);                 // k -= drop
                     z[it] = mad_i(dr, N3, zz);                          // threshold -= drop * 3N
                 }
             }
-            // widen nibbles to bytes: word 4u + 2w + par holds rows 8w + 2b + par in byte b
-            uint32_t acc16[16];
+            // widen nibbles to bytes (physical nibble 0 / 1 of each byte), then a butterfly
+            // reduce-scatter over the lanes: xor 16 pairs the two physical words of a column, xor 8
+            // the two nibble parities, xor 4 and xor 2 the columns (selects), xor 1 the byte pairs
+            // (0,2) / (1,3) split into 16-bit fields (sums <= 256). The per-lane table layout makes
+            // "keep the first, send the second" correct for the select-free levels.
+            uint32_t e1[4], o1[4];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                acc16[2 * i] = acc[i] & 0x0F0F0F0Fu;
-                acc16[2 * i + 1] = (acc[i] >> 4) & 0x0F0F0F0Fu;
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t e0 = acc[2 * u] & 0x0F0F0F0Fu, eh = acc[2 * u + 1] & 0x0F0F0F0Fu;
+                const uint32_t q0 = (acc[2 * u] >> 4) & 0x0F0F0F0Fu, qh = (acc[2 * u + 1] >> 4) & 0x0F0F0F0Fu;
+                e1[u] = e0 + __shfl_xor_sync(kFull, eh, 16);
+                o1[u] = q0 + __shfl_xor_sync(kFull, qh, 16);
             }
-            // butterfly reduce-scatter of 16 words of byte counters (<= 8 each per lane): after
-            // 4 halving steps lane L holds word (L >> 1) summed over 16 lanes; byte pairs are then
-            // split into 16-bit fields and one more step gives each lane 2 cells' warp totals.
-            uint32_t v8[8], v4[4], v2[2], v1;
+            uint32_t w4[4];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {                     // step 16: keep half by lane bit 4
-                const bool hiH = lane & 16;
-                const uint32_t send = hiH ? acc16[i] : acc16[i + 8];
-                const uint32_t keep = hiH ? acc16[i + 8] : acc16[i];
-                v8[i] = keep + __shfl_xor_sync(kFull, send, 16);
-            }
+            for (int u = 0; u < 4; ++u) w4[u] = e1[u] + __shfl_xor_sync(kFull, o1[u], 8);
+            uint32_t x2[2];
+            const bool b2 = lane & 4, b1 = lane & 2;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {                     // step 8
-                const bool hiH = lane & 8;
-                const uint32_t send = hiH ? v8[i] : v8[i + 4];
-                const uint32_t keep = hiH ? v8[i + 4] : v8[i];
-                v4[i] = keep + __shfl_xor_sync(kFull, send, 8);
+            for (int j = 0; j < 2; ++j) {
+                const uint32_t send = b2 ? w4[j] : w4[j + 2];
+                const uint32_t keep = b2 ? w4[j + 2] : w4[j];
+                x2[j] = keep + __shfl_xor_sync(kFull, send, 4);
             }
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {                     // step 4
-                const bool hiH = lane & 4;
-                const uint32_t send = hiH ? v4[i] : v4[i + 2];
-                const uint32_t keep = hiH ? v4[i + 2] : v4[i];
-                v2[i] = keep + __shfl_xor_sync(kFull, send, 4);
-            }
-            {                                                 // step 2 (bytes <= 128 after this)
-                const bool hiH = lane & 2;
-                const uint32_t send = hiH ? v2[0] : v2[1];
-                const uint32_t keep = hiH ? v2[1] : v2[0];
-                v1 = keep + __shfl_xor_sync(kFull, send, 2);
-            }
-            // word index held by this lane: bits 4,3,2,1 of the lane select halves of 16 words
-            const uint32_t word = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
-                                  ((lane >> 1) & 1);
-            // step 1: split bytes into two 16-bit-field halves; lane keeps bytes (0,2) or (1,3)
-            const uint32_t ev = v1 & 0x00FF00FFu, od = (v1 >> 8) & 0x00FF00FFu;
-            const bool odd = lane & 1;
-            const uint32_t tot = (odd ? od : ev) + __shfl_xor_sync(kFull, odd ? ev : od, 1);
-            // word = 4u + 2w + par: column 4b + u; byte bb -> row 8w + 2bb + par, bb in {odd, odd + 2}
-            const uint32_t col = 4 * b + (word >> 2);
-            const uint32_t row0 = 8 * ((word >> 1) & 1) + 2 * (odd ? 1 : 0) + (word & 1);
+            const uint32_t v1 = (b1 ? x2[1] : x2[0]) + __shfl_xor_sync(kFull, b1 ? x2[0] : x2[1], 2);
+            const uint32_t tot = (v1 & 0x00FF00FFu) + __shfl_xor_sync(kFull, (v1 >> 8) & 0x00FF00FFu, 1);
+            const uint32_t col = 4 * b + red_u;
             const uint32_t c0 = tot & 0xFFFFu, c1 = tot >> 16;
-            if (c0) atomicAdd(dst + 16 * col + row0, c0);
-            if (c1) atomicAdd(dst + 16 * col + row0 + 4, c1);
+            if (c0) atomicAdd(dst + 16 * col + red_row, c0);
+            if (c1) atomicAdd(dst + 16 * col + red_row + 4, c1);
         }
     });
 }

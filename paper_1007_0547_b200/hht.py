@@ -62,7 +62,8 @@ class Launch(C.Structure):
 
 
 class Profile(C.Structure):
-    _fields_ = [("launches", C.c_uint64 * 8), ("ms", C.c_double * 8), ("bytes", C.c_uint64 * 8)]
+    _fields_ = [("launches", C.c_uint64 * 8), ("ms", C.c_double * 8), ("bytes", C.c_uint64 * 8),
+                ("ops", C.c_uint64 * 8)]
 
 
 _lib = None
@@ -257,7 +258,7 @@ class HHT:
     def profile(self) -> dict:
         p = Profile()
         self._check(self._lib.hht_result_profile(self._ctx, C.byref(p)))
-        return {name: {"launches": p.launches[k], "ms": p.ms[k], "bytes": p.bytes[k]}
+        return {name: {"launches": p.launches[k], "ms": p.ms[k], "bytes": p.bytes[k], "ops": p.ops[k]}
                 for k, name in enumerate(PROFILE_CLASSES)}
 
     def launches(self) -> list:
