@@ -44,8 +44,8 @@ struct Frontier {
     ChunkDesc* chunks;   // [total chunks] work-unit descriptors (k_chunk_map)
 };
 
-struct Record { uint32_t tree, a, c, votes; };     // one visited region
-struct LeafRec { uint32_t tree, i, j, votes; };     // one detected line
+struct alignas(16) Record { uint32_t tree, a, c, votes; };     // one visited region
+struct alignas(16) LeafRec { uint32_t tree, i, j, votes; };     // one detected line
 
 // Look-back tile descriptor for the split scan (status: 0 none, 1 aggregate, 2 inclusive prefix).
 struct TileDesc {

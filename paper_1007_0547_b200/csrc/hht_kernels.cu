@@ -836,6 +836,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
     __shared__ Agg s_prefix;
     __shared__ uint32_t s_tile;
     __shared__ unsigned long long s_stat[3];    // votes, split-or-leaf count, 4 * split votes
+    __shared__ uint4 s_rec[kSplitThreads / 32][128];   // per-warp record staging (4 per parent)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) {
         s_tile = atomicAdd(A.tile_counter, 1u);   // dynamic tile order: predecessors are running
@@ -898,7 +899,10 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
                 Agg val = {0, 0, 0};
                 if (t >= 0) {
                     TileDesc* d = A.tiles + t;
-                    do { st = dev_u32(d->status).load(cuda::memory_order_acquire); } while (st == 0);
+                    // relaxed spin (no L1 invalidation per poll), then one acquire fence: the
+                    // payload was stored before the status with release semantics
+                    do { st = dev_u32(d->status).load(cuda::memory_order_relaxed); } while (st == 0);
+                    cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
                     if (st == 1) {
                         val = {dev_u32(d->aggF).load(cuda::memory_order_relaxed),
                                dev_u32(d->aggC).load(cuda::memory_order_relaxed),
@@ -939,16 +943,17 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
         uint32_t f = base.F, cc = base.C;
         uint64_t s = base.S;
         uint32_t nf4[4];
+        uint64_t so[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const uint32_t ca = 2 * pa + quad_da(q), cb = 2 * pc + quad_dc(q);
             nf4[q] = kNone;
+            so[q] = s;
             if (flag[q]) {
                 if (A.leaf_level) {
                     A.leaves[f] = {tree, ca, cb, v[q]};
                 } else {
                     nf4[q] = f;
-                    if (A.need_lists) A.nfoff[4 * (uint64_t)p + q] = s;
                     A.out.tree[f] = tree;
                     A.out.a[f] = ca;
                     A.out.c[f] = cb;
@@ -962,9 +967,28 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
                 s += len[q];
                 cc += nch[q];
             }
-            if (A.record) A.rec[4 * (uint64_t)p + q] = {tree, ca, cb, v[q]};
+            if (A.record) s_rec[wid][4 * lane + q] = make_uint4(tree, ca, cb, v[q]);
         }
-        if (!A.leaf_level) reinterpret_cast<uint4*>(A.nf)[p] = make_uint4(nf4[0], nf4[1], nf4[2], nf4[3]);
+        if (!A.leaf_level) {
+            reinterpret_cast<uint4*>(A.nf)[p] = make_uint4(nf4[0], nf4[1], nf4[2], nf4[3]);
+            if (A.need_lists) {
+                ulonglong2* o = reinterpret_cast<ulonglong2*>(A.nfoff + 4 * (uint64_t)p);
+                o[0] = make_ulonglong2(so[0], so[1]);
+                o[1] = make_ulonglong2(so[2], so[3]);
+            }
+        }
+    }
+    if (A.record) {
+        // the warp's 4 x 32 records (2 KB, contiguous in HBM) go out as fully coalesced 16-byte stores
+        __syncwarp();
+        const uint32_t p0 = tile * kSplitThreads + wid * 32;
+        const uint32_t nrec = p0 < A.Fp ? 4 * min(32u, A.Fp - p0) : 0;
+        uint4* dst = reinterpret_cast<uint4*>(A.rec) + 4 * (uint64_t)p0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t k = lane + 32 * i;
+            if (k < nrec) dst[k] = s_rec[wid][k];
+        }
     }
 
     // stats
