@@ -36,6 +36,8 @@ def _args():
     ap.add_argument("--impl", default="hht", choices=["hht", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--prefetch", type=int, default=0, help="0 auto, 1 descriptor only, 2 descriptor + entries")
+    ap.add_argument("--variant", default="exact", choices=["exact", "fht"],
+                    help="membership test: the paper's exact corner code, or the FHT circumcircle comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-tests", type=float, default=4e8, help="bounded oracle sample (code evaluations)")
     return ap.parse_args()
@@ -196,7 +198,8 @@ def main():
         hdist.check_consistent(cfg.N, cfg.D, cfg.T, cfg.halves, 1)
         nccl_id = hdist.broadcast_bytes(hht.nccl_unique_id() if rank == 0 else None)
     h = hht.HHT(device=local, halves=cfg.halves, record_levels=True, profile=True,
-                rank=rank if comm_world > 1 else 0, world=comm_world, nccl_id=nccl_id, prefetch=a.prefetch)
+                rank=rank if comm_world > 1 else 0, world=comm_world, nccl_id=nccl_id, prefetch=a.prefetch,
+                variant=hht.FHT_CIRCLE if a.variant == "fht" else hht.EXACT)
     d_pts = torch.from_numpy(np.ascontiguousarray(my)).to(dev)
     B = my_offs.shape[0] - 1
 
@@ -329,6 +332,8 @@ def main():
     if rank == 0:
         wl = _workload(cfg)
         wl["points_per_image"] = int(offs[1] - offs[0])
+        if a.variant == "fht":
+            wl["variant"] = "FHT circumcircle membership test (comparison, PAPER.md:45)"
         wl["parallelism"] = (f"points sharded x{world}, per-level NCCL allreduce" if comm_world > 1 else
                              (f"images sharded x{world}" if world > 1 else "single GPU"))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,

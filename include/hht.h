@@ -54,6 +54,9 @@ typedef enum {
 #define HHT_ALPHA 1u    /* |m| <= 1 set: point (x, y) */
 #define HHT_BETA 2u     /* |m| > 1 set: point taken as (y, x) */
 
+#define HHT_EXACT 0u       /* opts.variant: the paper's exact corner-code test             */
+#define HHT_FHT_CIRCLE 1u  /* opts.variant: FHT circumcircle test (comparison) */
+
 typedef struct hht_ctx hht_ctx;   /* opaque */
 
 typedef struct {
@@ -68,6 +71,10 @@ typedef struct {
                                 depth >= 4, else 3), 3 or 4 to force (results are identical) */
     uint32_t prefetch;       /* pass/tail kernels: 0 = auto, 1 = fetch the next chunk's descriptor
                                 only, 2 = also its list entries (more registers); identical results */
+    uint32_t variant;        /* membership test: HHT_EXACT (0, default) = the paper's 4-bit corner
+                                code; HHT_FHT_CIRCLE (1) = the FHT comparison: the line meets the
+                                region's circumscribing circle (exact integers, see
+                                DESIGN.md). HHT_EOVERFLOW if 13 N^2 2^(2 depth - 1) >= 2^63 */
     size_t mem_budget;       /* device bytes for candidate lists; 0 = 80% of free memory at create.
                                 Levels whose lists do not fit are processed in depth-first ranges. */
     const void* nccl_id;     /* world > 1: 128-byte ncclUniqueId from hht_nccl_unique_id on rank 0,

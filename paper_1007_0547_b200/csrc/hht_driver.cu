@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <cmath>
+
 #include "hht.h"
 #include "hht_internal.h"
 
@@ -73,6 +75,8 @@ struct hht_ctx {
     int tail_grid[2] = {};
     int tail16_grid[2] = {};
     bool pref_pass = true, pref_tail = true;   // opts.prefetch (0 = auto)
+    bool circle = false;                       // opts.variant == HHT_FHT_CIRCLE
+    int grid_circle[3][2] = {};
 
     // last call
     int N = 0, D = 0, B = 0, H = 0, ntrees = 0;
@@ -226,7 +230,7 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
     const bool leaf = child_level == x->D;
     // lists are read by write passes (levels < D-TK) and the dense tail (level D-TK); for D = 2 the
     // count-only pass reads the roots' lists (the points themselves)
-    const bool need_lists = child_level <= x->D - tail_depth(x);
+    const bool need_lists = child_level <= x->D - (x->circle ? 2 : tail_depth(x));
     const uint64_t nch = 4ull * Fp;
     if (!leaf) {
         TRY(ensure(x, C.tree, nch * 4));
@@ -328,7 +332,8 @@ PassArgs pass_args(hht_ctx* x, Level& P, int level) {
 hht_status run_pass(hht_ctx* x, int mode, const PassArgs& a, uint64_t pairs, uint64_t written) {
     const int cls = mode == MODE_COUNT ? 1 : (mode == MODE_WRITE ? 2 : 3);
     const int id = prof_begin(x, cls, pairs * 4 + written * 4);
-    CK(launch_pass(mode, x->int64, x->pref_pass, a, x->grid[mode][x->int64 ? 1 : 0], x->st));
+    const int grid = x->circle ? x->grid_circle[mode][x->int64 ? 1 : 0] : x->grid[mode][x->int64 ? 1 : 0];
+    CK(launch_pass(mode, x->int64, x->pref_pass || x->circle, x->circle, a, grid, x->st));
     prof_end(x, id);
     x->stat.pairs += pairs;
     return HHT_OK;
@@ -415,7 +420,7 @@ hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
 hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
     const int lc = l + 1;
     if (lc >= x->D) return HHT_OK;
-    if (x->D >= 3 && l == x->D - tail_depth(x)) return tail(x, l, r0, r1);
+    if (!x->circle && x->D >= 3 && l == x->D - tail_depth(x)) return tail(x, l, r0, r1);
     Level& P = x->lv[l];
     Level& C = x->lv[lc];
     const uint32_t Fc = C.F;
@@ -435,7 +440,7 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         a.votes = (uint32_t*)C.votes.p;
         TRY(run_pass(x, MODE_COUNT2, a, ri.pairs, 0));
         TRY(allreduce_sum_u32(x, (uint32_t*)C.votes.p, 4ull * Fc));
-        return do_split(x, x->D, C, 0, Fc, (const uint32_t*)C.votes.p, (const uint32_t*)C.votes.p, true);
+        return do_split(x, x->D, C, 0, Fc, (const uint32_t*)C.votes.p, (const uint32_t*)C.votes.p, !x->circle);
     }
 
     uint32_t q0 = 0;
@@ -488,7 +493,7 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
             VL = (const uint32_t*)C.votes_local.p;
             TRY(allreduce_sum_u32(x, (uint32_t*)C.votes.p, 4ull * nq));
         }
-        TRY(do_split(x, lc + 1, C, q0, nq, (const uint32_t*)C.votes.p, VL, true));
+        TRY(do_split(x, lc + 1, C, q0, nq, (const uint32_t*)C.votes.p, VL, !x->circle));
         TRY(descend(x, lc, q0, q1));
         q0 = q1;
     }
@@ -508,6 +513,10 @@ hht_status check_args(hht_ctx* x, const int32_t* points, int64_t n_total, int32_
     const long double mag = 5.0L * (long double)N * (long double)(1ull << D);
     if (mag >= 4.6e18L) return set_err(x, HHT_EOVERFLOW, "5*N*2^depth >= 2^62: exact int64 arithmetic impossible");
     if (n_total > 0xFFFFFFFFll) return set_err(x, HHT_EINVAL, "more than 2^32-1 points per rank");
+    if (x->opts.variant > HHT_FHT_CIRCLE) return set_err(x, HHT_EINVAL, "unknown variant");
+    // circle test: the squared radius 2 s^2 (4 ex^2 + 9 N^2) of a child of the root must fit 63 bits
+    if (x->opts.variant == HHT_FHT_CIRCLE && 13.0L * N * (long double)N * powl(2.0L, 2.0L * D - 1) >= 9.2e18L)
+        return set_err(x, HHT_EOVERFLOW, "13 N^2 2^(2 depth - 1) >= 2^63: circle radius overflows 64 bits");
     return HHT_OK;
 }
 
@@ -529,7 +538,8 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     x->B = B;
     x->H = (x->opts.halves & HHT_ALPHA ? 1 : 0) + (x->opts.halves & HHT_BETA ? 1 : 0);
     x->ntrees = B * x->H;
-    x->int64 = x->opts.force_int64 || !(5.0L * N * (long double)(1ull << D) < 2147483647.0L);
+    // |G| < 5 N 2^D (exact test); the circle test also squares 2 G(centre): |L2| < 10 N 2^D
+    x->int64 = x->opts.force_int64 || !((x->circle ? 10.0L : 5.0L) * N * (long double)(1ull << D) < 2147483647.0L);
     memset(&x->stat, 0, sizeof x->stat);
     memset(&x->prof, 0, sizeof x->prof);
     x->pev_used = 0;
@@ -829,7 +839,10 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     if (o.prefetch == 1) x->pref_pass = x->pref_tail = false;
     if (o.prefetch == 2) x->pref_pass = x->pref_tail = true;
     for (int m = 0; m < 3; ++m)
-        for (int w = 0; w < 2; ++w) x->grid[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, x->pref_pass);
+        for (int w = 0; w < 2; ++w) x->grid[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, x->pref_pass, false);
+    x->circle = o.variant == HHT_FHT_CIRCLE;
+    for (int m = 0; m < 3; ++m)
+        for (int w = 0; w < 2; ++w) x->grid_circle[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, true, true);
     for (int w = 0; w < 2; ++w) x->tail_grid[w] = x->sms * tail_blocks_per_sm(w == 1);
     for (int w = 0; w < 2; ++w) x->tail16_grid[w] = x->sms * tail16_blocks_per_sm(w == 1, x->pref_tail);
     size_t fr = 0, tot = 0;

@@ -133,7 +133,7 @@ struct RangeInfo {
 // Launchers (hht_kernels.cu). All asynchronous on `st`.
 cudaError_t launch_stage(const int32_t* pts, uint64_t n, int N, uint32_t* packed, uint32_t* err,
                          cudaStream_t st);
-cudaError_t launch_pass(int mode, bool int64, bool pref, const PassArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_pass(int mode, bool int64, bool pref, bool circle, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_split(const SplitArgs& a, cudaStream_t st);
 cudaError_t launch_chunk_map(const uint64_t* choff, const uint64_t* off, const uint32_t* len, const uint32_t* a,
                              const uint32_t* c, const uint32_t* tree, const uint8_t* tree_beta, uint32_t F,
@@ -142,7 +142,7 @@ cudaError_t launch_range(const uint64_t* c_off, const uint32_t* c_parent, uint32
                          uint64_t cap_entries, uint64_t forced_q1, const uint64_t* p_off,
                          const uint64_t* p_choff, const uint32_t* p_len, int p_is_root, RangeInfo* info,
                          uint64_t* chunk_bounds, cudaStream_t st);
-int pass_blocks_per_sm(int mode, bool int64, bool pref);
+int pass_blocks_per_sm(int mode, bool int64, bool pref, bool circle);
 int tail_blocks_per_sm(bool int64);
 cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_beta, uint32_t H, uint32_t* out,
                              cudaStream_t st);

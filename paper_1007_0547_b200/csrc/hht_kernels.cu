@@ -35,7 +35,6 @@ __device__ __forceinline__ bool crosses(I v_minus_1, I U) {
     return (UI)v_minus_1 < (UI)U;
 }
 
-__device__ __forceinline__ uint32_t shfl_u32(uint32_t v, int src) { return __shfl_sync(kFull, v, src); }
 __device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
     uint32_t lo = __shfl_sync(kFull, (uint32_t)v, src), hi = __shfl_sync(kFull, (uint32_t)(v >> 32), src);
     return ((uint64_t)hi << 32) | lo;
@@ -248,7 +247,72 @@ __device__ __forceinline__ void chunk_loop(const PassArgs& A, int lane, Body bod
     }
 }
 
-template <typename I, int MODE, bool PREF>
+// ---------------------------------------------------------------------------------------------
+// FHT circumcircle variant ("calculates the perpendicular
+// distance to the line from the center of the region and compares it with the radius of the
+// circle circumscribing the region"). Same lists and passes, membership test replaced: with
+// L(i, j) = G(i, j) (the line's signed lattice value) and a region of side s' with doubled centre
+// (i2, j2), the line meets the circumcircle iff (L2)^2 <= 2 s'^2 (4ex^2 + 9N^2), L2 = 2 L(centre),
+// exactly in integers (the oracle's form). A child (da, dc) of a parent of side s with SW value g
+// has L2 = 2g - Pc(2da+1) - Qc(2dc+1) (Pc = ex s, Qc = 3N s/2); a grandchild (u, v) has
+// L2 = 2g - Pg(2u+1) - Qg(2v+1) (Pg = ex s/2, Qg = 3N s/4). Circles are nested (a child's
+// circumcircle lies inside its parent's), so a child's votes are again counted over the parent's
+// list; but the SW+NE identity of the exact test does not hold, so all 16 grandchildren are
+// counted and the dense tail is not used. int32 when 10 N 2^D < 2^31 (|L2| < 2^31, L2^2 < 2^62);
+// int64 otherwise, with a 128-bit square.
+// ---------------------------------------------------------------------------------------------
+template <typename I>
+__device__ __forceinline__ bool circle_in(I L2, uint64_t rhs) {
+    if (sizeof(I) == 4) {
+        const int64_t l = (int64_t)L2;
+        return (uint64_t)(l * l) <= rhs;
+    } else {
+        const uint64_t a = (uint64_t)(L2 < 0 ? -L2 : L2);
+        return __umul64hi(a, a) == 0 && a * a <= rhs;
+    }
+}
+
+template <typename I, int MODE, bool BETA>
+__device__ __forceinline__ void chunk_math_circle(const uint32_t (&p)[kItems], int cnt, int lane, I alpha, I beta_m1,
+                                                  int D, int sh, I N, I Qc, I Qg, uint32_t& cm, uint32_t (&acc)[4]) {
+    const uint64_t nn9 = 9ull * (uint64_t)N * (uint64_t)N;
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+        const uint32_t w = p[it];
+        const I ex = (I)(BETA ? (w & 0xFFFFu) : (w >> 16));
+        const I ey = (I)(BETA ? (w >> 16) : (w & 0xFFFFu));
+        const bool valid = lane + kWarp * it < cnt;
+        // invalid lanes: L2 odd (2g = 1, ex = 0) against rhs = 0 never passes
+        const I twog = valid ? 2 * (ex * alpha + (ey << D) + beta_m1 + 1) : (I)1;
+        const uint64_t K = valid ? 4ull * (uint64_t)ex * (uint64_t)ex + nn9 : 0ull;   // 4ex^2 + 9N^2
+        const I Pc = ex << sh;
+        if (MODE != MODE_COUNT2) {
+            const uint64_t rc = K << (2 * sh - 1);                  // 2 (s/2)^2 K
+            uint32_t b = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const I L2 = twog - Pc * (I)(2 * quad_da(q) + 1) - Qc * (I)(2 * quad_dc(q) + 1);
+                b |= (circle_in<I>(L2, rc) ? 1u : 0u) << (MODE == MODE_COUNT ? 8 * q : q);
+            }
+            if (MODE == MODE_COUNT) acc[0] += b;
+            else cm |= b << (4 * it);
+        }
+        if (MODE != MODE_COUNT) {
+            const uint64_t rg = K << (2 * sh - 3);                  // 2 (s/4)^2 K
+            const I Pg = Pc >> 1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const I L2 = twog - Pg * (I)(2 * u + 1) - Qg * (I)(2 * v + 1);
+                    if (circle_in<I>(L2, rg)) acc[quad_of(u >> 1, v >> 1)] += 1u << (8 * quad_of(u & 1, v & 1));
+                }
+            }
+        }
+    }
+}
+
+template <typename I, int MODE, bool PREF, bool CIRCLE>
 __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
     __shared__ uint32_t s_stage[MODE == MODE_WRITE ? 8 * 4 * kChunk : 1];   // 4 KB per warp
     const int lane = threadIdx.x & 31;
@@ -279,8 +343,13 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
 
         uint32_t cm = 0;
         uint32_t acc[4] = {0, 0, 0, 0};
-        if (d.beta) chunk_math<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc);
-        else chunk_math<I, MODE, false>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc);
+        if (CIRCLE) {
+            if (d.beta) chunk_math_circle<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, N, Qc, Qg, cm, acc);
+            else chunk_math_circle<I, MODE, false>(p, cnt, lane, alpha, beta_m1, D, sh, N, Qc, Qg, cm, acc);
+        } else {
+            if (d.beta) chunk_math<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc);
+            else chunk_math<I, MODE, false>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc);
+        }
 
         if (MODE == MODE_COUNT) {
             uint32_t c02, c13;
@@ -294,6 +363,21 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
 
         if (my_nf != kNone && (my_nf < A.q0 || my_nf >= A.q1)) my_nf = kNone;
 
+        if (CIRCLE) {
+            // all 16 grandchild cells (no derivation for circles): cell L = 4q + qq at field L & 1
+            // of word L >> 1, one warp sum per word; lane L < 16 adds cell L
+            uint32_t sw = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t lo = (acc[q] & 0xFFu) | ((acc[q] << 8) & 0xFF0000u);
+                const uint32_t hi = ((acc[q] >> 16) & 0xFFu) | ((acc[q] >> 8) & 0xFF0000u);
+                const uint32_t slo = __reduce_add_sync(kFull, lo), shi = __reduce_add_sync(kFull, hi);
+                if ((lane >> 2) == q) sw = (lane & 2) ? shi : slo;
+            }
+            const uint32_t v = (sw >> (16 * (lane & 1))) & 0xFFFFu;
+            const uint32_t nf_l = __shfl_sync(kFull, my_nf, (lane >> 2) & 3);
+            if (lane < 16 && nf_l != kNone && v) atomicAdd(A.votes + 4 * (uint64_t)(nf_l - A.q0) + (lane & 3), v);
+        } else
         // Count-ahead votes: the 12 derived-free cells (child q, grandchild qq = NW, SW, SE) in
         // 16-bit fields of 6 words (cell L = 3q + qq - 1 at field L & 1 of word L >> 1), one warp
         // sum per word; lane L < 12 then adds cell L to its split child's vote counter.
@@ -745,26 +829,28 @@ cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_
     return cudaGetLastError();
 }
 
-template <typename I, bool P>
+template <typename I, bool P, bool C>
 static PassKernel pass_kernel_t(int mode) {
-    if (mode == MODE_COUNT) return k_pass<I, MODE_COUNT, P>;
-    if (mode == MODE_WRITE) return k_pass<I, MODE_WRITE, P>;
-    return k_pass<I, MODE_COUNT2, P>;
+    if (mode == MODE_COUNT) return k_pass<I, MODE_COUNT, P, C>;
+    if (mode == MODE_WRITE) return k_pass<I, MODE_WRITE, P, C>;
+    return k_pass<I, MODE_COUNT2, P, C>;
 }
 
-static PassKernel pass_kernel(int mode, bool int64, bool pref) {
-    if (int64) return pref ? pass_kernel_t<int64_t, true>(mode) : pass_kernel_t<int64_t, false>(mode);
-    return pref ? pass_kernel_t<int32_t, true>(mode) : pass_kernel_t<int32_t, false>(mode);
+// The circumcircle variant is instantiated with the prefetching loop only.
+static PassKernel pass_kernel(int mode, bool int64, bool pref, bool circle = false) {
+    if (circle) return int64 ? pass_kernel_t<int64_t, true, true>(mode) : pass_kernel_t<int32_t, true, true>(mode);
+    if (int64) return pref ? pass_kernel_t<int64_t, true, false>(mode) : pass_kernel_t<int64_t, false, false>(mode);
+    return pref ? pass_kernel_t<int32_t, true, false>(mode) : pass_kernel_t<int32_t, false, false>(mode);
 }
 
-int pass_blocks_per_sm(int mode, bool int64, bool pref) {
+int pass_blocks_per_sm(int mode, bool int64, bool pref, bool circle) {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, pass_kernel(mode, int64, pref), 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, pass_kernel(mode, int64, pref, circle), 256, 0);
     return n > 0 ? n : 1;
 }
 
-cudaError_t launch_pass(int mode, bool int64, bool pref, const PassArgs& a, int grid, cudaStream_t st) {
-    pass_kernel(mode, int64, pref)<<<grid, 256, 0, st>>>(a);
+cudaError_t launch_pass(int mode, bool int64, bool pref, bool circle, const PassArgs& a, int grid, cudaStream_t st) {
+    pass_kernel(mode, int64, pref, circle)<<<grid, 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -15,6 +15,8 @@ import numpy as np
 
 ALPHA = 1
 BETA = 2
+EXACT = 0          # opts.variant: the paper's exact 4-bit corner-code test
+FHT_CIRCLE = 1     # opts.variant: FHT circumcircle test (the paper's comparison)
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libhht.so")
@@ -41,7 +43,8 @@ class HHTError(RuntimeError):
 class Opts(C.Structure):
     _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("halves", C.c_uint32),
                 ("record_levels", C.c_uint32), ("force_int64", C.c_uint32), ("profile", C.c_uint32),
-                ("tail_depth", C.c_uint32), ("prefetch", C.c_uint32), ("mem_budget", C.c_size_t),
+                ("tail_depth", C.c_uint32), ("prefetch", C.c_uint32), ("variant", C.c_uint32),
+                ("mem_budget", C.c_size_t),
                 ("nccl_id", C.c_void_p)]
 
 
@@ -149,7 +152,7 @@ class HHT:
     def __init__(self, device: int = 0, halves: int = ALPHA | BETA, record_levels: bool = True,
                  force_int64: bool = False, profile: bool = False, mem_budget: int = 0,
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, tail_depth: int = 0,
-                 prefetch: int = 0):
+                 prefetch: int = 0, variant: int = 0):
         self._lib = load()
         o = Opts()
         self._lib.hht_default_opts(C.byref(o))
@@ -158,6 +161,7 @@ class HHT:
         o.mem_budget = mem_budget
         o.tail_depth = tail_depth
         o.prefetch = prefetch
+        o.variant = variant
         self._id = None
         if nccl_id is not None:
             self._id = C.create_string_buffer(bytes(nccl_id), 128)

@@ -16,6 +16,7 @@ ap.add_argument("--images", type=int, default=None)
 ap.add_argument("--budget", type=int, default=0)
 ap.add_argument("--tail", type=int, default=0)
 ap.add_argument("--prefetch", type=int, default=0)
+ap.add_argument("--variant", type=int, default=0, help="0 exact, 1 FHT circumcircle")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 if cfg.images > 1:
@@ -24,7 +25,7 @@ else:
     pts, _ = synth.config_image(a.config)
     offs = np.array([0, len(pts)])
 d = torch.from_numpy(pts).cuda()
-h = hht.HHT(halves=cfg.halves, mem_budget=a.budget, profile=True, tail_depth=a.tail, prefetch=a.prefetch)
+h = hht.HHT(halves=cfg.halves, mem_budget=a.budget, profile=True, tail_depth=a.tail, prefetch=a.prefetch, variant=a.variant)
 for _ in range(a.reps):
     h.detect_batch(d, offs, cfg.N, cfg.D, cfg.T)
 st = h.stats()

@@ -1,0 +1,106 @@
+"""GPU parity of the FHT circumcircle variant: the same
+level-synchronous pipeline with the membership test "the line meets the region's circumscribing
+circle", compared bit-exactly with the oracle's variant 1 (oracle/hht_oracle.c
+oracle_circle_passes, pinned in tests/test_oracle_pins.py), plus the paper's claim that the circle
+test casts extra (false) votes: at every region both runs visit, circle votes >= exact votes."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1007_0547_b200 import hht, synth
+from tests.hht_compare import compare_all
+
+pytestmark = pytest.mark.gpu
+
+AB = hht.ALPHA | hht.BETA
+
+
+def _dev(pts, dev):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(pts, dtype=np.int32)).to(dev)
+
+
+def _run(pts, N, D, T, halves, dev, **kw):
+    h = hht.HHT(halves=halves, variant=hht.FHT_CIRCLE, **kw)
+    h.detect(_dev(pts, dev), N, D, T)
+    return h
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+def test_config_parity_circle(cid, cuda_device):
+    cfg = synth.CONFIGS[cid]
+    pts, _ = synth.config_image(cid)
+    ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves, variant=1)
+    h = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, cuda_device)
+    compare_all(h, ref, cfg.halves, cfg.D)
+    st = h.stats()
+    assert (st["tests"], st["votes"], st["leaves"]) == (ref.tests, ref.votes, ref.leaves.shape[0])
+
+
+@pytest.mark.parametrize("seed", range(20))
+@pytest.mark.parametrize("force64", [False, True])
+def test_random_scenes_circle(seed, force64, cuda_device):
+    rng = np.random.default_rng(7000 + seed)
+    N = int(rng.choice([4, 7, 16, 33, 64, 128, 200]))
+    D = int(rng.integers(1, 9))
+    T = int(rng.choice([1, 2, 3, 8, 20]))
+    pts = synth.random_scene(8000 + seed, N, max_lines=4, max_noise=int(rng.choice([10, 300, 3000])))
+    ref = oracle.detect(pts, N, D, T, AB, variant=1)
+    h = _run(pts, N, D, T, AB, cuda_device, force_int64=force64)
+    compare_all(h, ref, AB, D)
+    st = h.stats()
+    assert (st["tests"], st["votes"]) == (ref.tests, ref.votes)
+    assert st["int_bits"] == (64 if force64 else 32)
+
+
+def test_circle_ranges_under_tiny_budget(cuda_device):
+    cfg = synth.CONFIGS[2]
+    pts, _ = synth.config_image(2)
+    ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves, variant=1)
+    h = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, cuda_device, mem_budget=256 << 10)
+    compare_all(h, ref, cfg.halves, cfg.D)
+    assert h.stats()["ranges"] > 4 * cfg.D
+
+
+@pytest.mark.parametrize("case", ["empty", "identical", "d1", "d2", "d3", "n1"])
+def test_circle_edge_cases(case, cuda_device):
+    N, D, T = 16, 4, 2
+    if case == "empty":
+        pts = np.zeros((0, 2), np.int32)
+    elif case == "identical":
+        pts, T = np.array([[5, 9]] * 300, np.int32), 100
+    elif case == "n1":
+        pts, N, D, T = np.array([[0, 0]] * 5, np.int32), 1, 3, 1
+    else:
+        D = int(case[1])
+        pts = synth.random_scene(30 + D, 16, max_noise=60)
+    ref = oracle.detect(pts, N, D, T, AB, variant=1)
+    h = _run(pts, N, D, T, AB, cuda_device)
+    compare_all(h, ref, AB, D)
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+def test_circle_casts_extra_votes(cid, cuda_device):
+    """North star: the circumcircle test (FHT) votes wherever the exact test does and more: at every
+    region visited by both runs, votes_circle >= votes_exact; strictly more votes in total."""
+    cfg = synth.CONFIGS[cid]
+    pts, _ = synth.config_image(cid)
+    he = hht.HHT(halves=cfg.halves)
+    he.detect(_dev(pts, cuda_device), cfg.N, cfg.D, cfg.T)
+    hc = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, cuda_device)
+    for half in (1, 2):
+        if not cfg.halves & half:
+            continue
+        for lev in range(cfg.D + 1):
+            e = {(a, c): v for a, c, v in he.level(0, half, lev).tolist()}
+            c = {(a, c): v for a, c, v in hc.level(0, half, lev).tolist()}
+            assert set(e) <= set(c), f"level {lev}: exact visits a region the circle run does not"
+            assert all(c[k] >= v for k, v in e.items()), f"level {lev}: circle votes < exact votes"
+    assert hc.stats()["votes"] > he.stats()["votes"]
+
+
+def test_circle_overflow_rejected(cuda_device):
+    h = hht.HHT(halves=AB, variant=hht.FHT_CIRCLE)
+    with pytest.raises(hht.HHTError) as e:
+        h.detect(_dev(np.array([[0, 0]], np.int32), cuda_device), 65536, 30, 2)
+    assert e.value.name == "HHT_EOVERFLOW"
