@@ -104,7 +104,17 @@ typedef struct {
     uint32_t ranges;         /* list ranges processed (1 per level when everything fits) */
     uint32_t images;
     double ms;               /* device time of the call (CUDA events on the ctx stream) */
+    uint64_t leaves_streamed;   /* leaf rows written to the leaf sink (hht_set_leaf_sink) */
 } hht_stats;
+
+/* Leaf sink: while a detect runs, the detected lines are converted to hht_leaf rows and copied to
+ * `host` as each leaf-level split finishes, on a second stream, overlapping the copies with the
+ * rest of the traversal (depth-first ranges produce leaves in their final order). When the detect
+ * returns, host[0 .. min(total, cap)) holds the same rows, in the same order, as
+ * hht_result_leaves(ctx, -1, ...); stats.leaves is the total and stats.leaves_streamed the rows
+ * written (fewer than the total only when cap is too small). `host` is borrowed until the sink is
+ * replaced or removed (host = NULL); page-locked memory gives real overlap. */
+hht_status hht_set_leaf_sink(hht_ctx* ctx, hht_leaf* host, int64_t cap);
 
 /* Per-kernel-class timings of the last detect (opts.profile = 1), CUDA events per launch. */
 typedef struct {

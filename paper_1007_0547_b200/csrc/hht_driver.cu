@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include <atomic>
 #include <cmath>
 
 #include "hht.h"
@@ -87,9 +88,22 @@ struct hht_ctx {
     std::vector<int64_t> tree_E;            // global points per tree
 
     Buf stage_in, packed, errflag, beta, stats, tiles, tilectr, totals, rng, bounds, vtmp, dense, gv, leafrows;
+    // leaf sink (hht_set_leaf_sink): double-buffered row staging, copied on its own stream
+    hht_leaf* sink = nullptr;
+    int64_t sink_cap = 0;
+    uint64_t sink_n = 0;
+    cudaStream_t cst = nullptr;
+    Buf sinkrows[2];
+    cudaEvent_t ev_conv[2] = {nullptr, nullptr}, ev_copy[2] = {nullptr, nullptr};
+    bool copy_pending[2] = {false, false};
+    int sink_slot = 0;
+    // pinned host memory that kernels write directly (mapped, UVA): small per-split readbacks
     Totals* totals_h = nullptr;
     RangeInfo* range_h = nullptr;
     uint64_t* misc_h = nullptr;
+    Totals* totals_m = nullptr;      // device-side pointers of the same memory
+    RangeInfo* range_m = nullptr;
+    uint64_t* misc_m = nullptr;
     std::vector<Level> lv;
     Grow rec[64];
     Grow leaves;
@@ -220,6 +234,39 @@ hht_status sync(hht_ctx* x) {
     return HHT_OK;
 }
 
+// Read a value a kernel wrote into mapped pinned host memory (after a stream synchronisation).
+template <class T>
+T read_mapped(const T* p) {
+    std::atomic_thread_fence(std::memory_order_acquire);
+    T t;
+    memcpy(&t, (const void*)p, sizeof t);
+    return t;
+}
+
+// Leaf sink: rows of leaves [first, first + n) -> host, overlapped with the traversal.
+hht_status stream_leaves(hht_ctx* x, uint64_t first, uint64_t n) {
+    if (!x->sink || n == 0 || x->sink_n >= (uint64_t)x->sink_cap) return HHT_OK;
+    const uint64_t k = std::min<uint64_t>(n, (uint64_t)x->sink_cap - x->sink_n);
+    const int s = x->sink_slot;
+    x->sink_slot ^= 1;
+    Buf& b = x->sinkrows[s];
+    if (b.cap < k * sizeof(hht_leaf)) {
+        if (x->copy_pending[s]) CK(cudaEventSynchronize(x->ev_copy[s]));   // before freeing its buffer
+        x->copy_pending[s] = false;
+        TRY(ensure(x, b, k * sizeof(hht_leaf)));
+    }
+    if (x->copy_pending[s]) CK(cudaStreamWaitEvent(x->st, x->ev_copy[s], 0));   // buffer reuse
+    CK(launch_leaf_rows((const LeafRec*)x->leaves.b.p + first, k, (const uint8_t*)x->beta.p, x->H,
+                        (uint32_t*)b.p, x->st));
+    CK(cudaEventRecord(x->ev_conv[s], x->st));
+    CK(cudaStreamWaitEvent(x->cst, x->ev_conv[s], 0));
+    CK(cudaMemcpyAsync(x->sink + x->sink_n, b.p, k * sizeof(hht_leaf), cudaMemcpyDefault, x->cst));
+    CK(cudaEventRecord(x->ev_copy[s], x->cst));
+    x->copy_pending[s] = true;
+    x->sink_n += k;
+    return HHT_OK;
+}
+
 // ---------------------------------------------------------------------------------------------
 // split: threshold the votes of the children of parents P[r0, r0+Fp) into level child_level.
 // ---------------------------------------------------------------------------------------------
@@ -277,19 +324,19 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
     a.tiles = (TileDesc*)x->tiles.p;
     a.tile_counter = (uint32_t*)x->tilectr.p;
     a.stats = (unsigned long long*)x->stats.p;
-    a.totals = (Totals*)x->totals.p;
+    a.totals = x->totals_m;
     a.ntiles = ntiles;
     const uint64_t bytes = (uint64_t)Fp * (16 + (VL != V ? 16 : 0) + 12 + (leaf ? 0 : 16) + (record ? 64 : 0));
     const int id = prof_begin(x, 4, bytes);
     CK(launch_split(a, x->st));
     prof_end(x, id);
-    CK(cudaMemcpyAsync(x->totals_h, x->totals.p, sizeof(Totals), cudaMemcpyDeviceToHost, x->st));
     TRY(sync(x));
-    const Totals t = *x->totals_h;
+    const Totals t = read_mapped(x->totals_h);
     if (record) x->rec[child_level].n += nch;
     if (leaf) {
+        const uint64_t first = x->leaves.n;
         x->leaves.n += t.F;
-        return HHT_OK;
+        return stream_leaves(x, first, t.F);
     }
     C.F = (uint32_t)t.F;
     C.S = t.S;
@@ -346,22 +393,22 @@ hht_status choose_range(hht_ctx* x, int lc, uint32_t q0, uint64_t cap_entries, b
     const int id = prof_begin(x, 6, 0);
     CK(launch_range((const uint64_t*)C.off.p, (const uint32_t*)C.parent.p, C.F, q0, cap_entries,
                     all ? C.F : 0, (const uint64_t*)P.off.p, (const uint64_t*)P.choff.p,
-                    (const uint32_t*)P.len.p, lc == 1, (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->st));
+                    (const uint32_t*)P.len.p, lc == 1, (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->range_m,
+                    x->st));
     prof_end(x, id);
     if (x->comm && !all) {
         // min over ranks of the proposed end, then recompute with the agreed end
         CKN(ncclAllReduce((const char*)x->rng.p + offsetof(RangeInfo, q1), (char*)x->vtmp.p, 1, ncclUint64,
                           ncclMin, x->comm, x->st));
-        CK(cudaMemcpyAsync(x->misc_h, x->vtmp.p, 8, cudaMemcpyDeviceToHost, x->st));
+        CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)x->vtmp.p, 2, x->st));
         TRY(sync(x));
-        const uint64_t q1 = x->misc_h[0];
+        const uint64_t q1 = read_mapped(x->misc_h);
         CK(launch_range((const uint64_t*)C.off.p, (const uint32_t*)C.parent.p, C.F, q0, cap_entries, q1,
                         (const uint64_t*)P.off.p, (const uint64_t*)P.choff.p, (const uint32_t*)P.len.p,
-                        lc == 1, (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->st));
+                        lc == 1, (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->range_m, x->st));
     }
-    CK(cudaMemcpyAsync(x->range_h, x->rng.p, sizeof(RangeInfo), cudaMemcpyDeviceToHost, x->st));
     TRY(sync(x));
-    *out = *x->range_h;
+    *out = read_mapped(x->range_h);
     return HHT_OK;
 }
 
@@ -378,8 +425,7 @@ hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
     TRY(ensure(x, x->dense, (size_t)n * cells * 4));
     CK(cudaMemsetAsync(x->dense.p, 0, (size_t)n * cells * 4, x->st));
     CK(launch_bounds((const uint64_t*)P.off.p, (const uint64_t*)P.choff.p, (const uint32_t*)P.len.p, r0, r1, L == 0,
-                     (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->st));
-    CK(cudaMemcpyAsync(x->range_h, x->rng.p, sizeof(RangeInfo), cudaMemcpyDeviceToHost, x->st));
+                     (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->range_m, x->st));
     PassArgs a = pass_args(x, P, L);
     a.nf_rbase = r0;
     a.votes = (uint32_t*)x->dense.p;
@@ -388,7 +434,7 @@ hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
     else CK(launch_tail(x->int64, a, x->tail_grid[x->int64 ? 1 : 0], x->st));
     prof_end(x, id);
     TRY(sync(x));
-    const uint64_t pairs = x->range_h->pairs;
+    const uint64_t pairs = read_mapped(x->range_h).pairs;
     if (id >= 0) {
         x->pev[id].bytes = pairs * 4 + (uint64_t)n * cells * 4;
         // raster step = 8 instructions per (line, leaf column): advance the height, extract the
@@ -552,6 +598,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     }
     x->leaves.n = 0;
     x->leaves_host_ok = false;
+    x->sink_n = 0;
     if ((int)x->lv.size() < D + 1) x->lv.resize(D + 1);
     for (auto& L : x->lv) {
         L.F = 0;
@@ -615,9 +662,9 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     }
     if (x->comm)
         CKN(ncclAllReduce(x->errflag.p, x->errflag.p, 1, ncclUint32, ncclMax, x->comm, x->st));
-    CK(cudaMemcpyAsync(x->misc_h, x->errflag.p, 4, cudaMemcpyDeviceToHost, x->st));
+    CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)x->errflag.p, 1, x->st));
     TRY(sync(x));
-    if ((uint32_t)(x->misc_h[0] & 0xFFFFFFFFu)) return set_err(x, HHT_ERANGE, "a point lies outside [0, N)^2");
+    if ((uint32_t)read_mapped(x->misc_h)) return set_err(x, HHT_ERANGE, "a point lies outside [0, N)^2");
 
     // stats accumulators
     CK(cudaMemsetAsync(x->stats.p, 0, kStatCount * 8, x->st));
@@ -723,6 +770,12 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, x->ev0, x->ev1));
     x->stat.ms = ms;
+    if (x->sink) {
+        CK(cudaStreamSynchronize(x->cst));
+        x->copy_pending[0] = x->copy_pending[1] = false;
+        x->stat.leaves_streamed = x->sink_n;
+        x->stat.d2h_bytes += x->sink_n * sizeof(hht_leaf);
+    }
     x->launch_log.clear();
     if (x->opts.profile) {
         for (size_t i = 0; i < x->pev_used; ++i) {
@@ -827,6 +880,11 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     if (cudaGetDeviceProperties(&prop, o.device) != cudaSuccess) return fail(HHT_ECUDA);
     x->sms = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&x->st, cudaStreamNonBlocking) != cudaSuccess) return fail(HHT_ECUDA);
+    if (cudaStreamCreateWithFlags(&x->cst, cudaStreamNonBlocking) != cudaSuccess) return fail(HHT_ECUDA);
+    for (int k = 0; k < 2; ++k)
+        if (cudaEventCreateWithFlags(&x->ev_conv[k], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&x->ev_copy[k], cudaEventDisableTiming) != cudaSuccess)
+            return fail(HHT_ECUDA);
     if (cudaEventCreate(&x->ev0) != cudaSuccess || cudaEventCreate(&x->ev1) != cudaSuccess ||
         cudaEventCreate(&x->tb0) != cudaSuccess || cudaEventCreate(&x->tb1) != cudaSuccess)
         return fail(HHT_ECUDA);
@@ -855,6 +913,10 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     if (cudaMallocHost((void**)&x->totals_h, sizeof(Totals)) != cudaSuccess ||
         cudaMallocHost((void**)&x->range_h, sizeof(RangeInfo)) != cudaSuccess ||
         cudaMallocHost((void**)&x->misc_h, 64) != cudaSuccess)
+        return fail(HHT_ECUDA);
+    if (cudaHostGetDevicePointer((void**)&x->totals_m, x->totals_h, 0) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&x->range_m, x->range_h, 0) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&x->misc_m, x->misc_h, 0) != cudaSuccess)
         return fail(HHT_ECUDA);
     if (o.nccl_id) {   // world > 1, or world == 1 with an id: every collective runs (1-rank comm)
         ncclUniqueId id;
@@ -946,6 +1008,16 @@ hht_status hht_result_level(hht_ctx* x, int32_t image, uint32_t half, int32_t le
     return HHT_OK;
 }
 
+hht_status hht_set_leaf_sink(hht_ctx* x, hht_leaf* host, int64_t cap) {
+    if (!x) return HHT_EINVAL;
+    if (host && cap < 0) return set_err(x, HHT_EINVAL, "cap < 0");
+    if (x->cst) cudaStreamSynchronize(x->cst);
+    x->copy_pending[0] = x->copy_pending[1] = false;
+    x->sink = host;
+    x->sink_cap = host ? cap : 0;
+    return HHT_OK;
+}
+
 hht_status hht_result_stats(hht_ctx* x, hht_stats* out) {
     if (!x || !out) return HHT_EINVAL;
     if (!x->have) return set_err(x, HHT_ESTATE, "no successful detect yet");
@@ -991,6 +1063,14 @@ const char* hht_last_error(const hht_ctx* x) { return x ? x->err.c_str() : "null
 void hht_destroy(hht_ctx* x) {
     if (!x) return;
     if (x->st) cudaStreamSynchronize(x->st);
+    if (x->cst) cudaStreamSynchronize(x->cst);
+    for (Buf* b : {&x->sinkrows[0], &x->sinkrows[1]})
+        if (b->p) cudaFree(b->p);
+    for (int k = 0; k < 2; ++k) {
+        if (x->ev_conv[k]) cudaEventDestroy(x->ev_conv[k]);
+        if (x->ev_copy[k]) cudaEventDestroy(x->ev_copy[k]);
+    }
+    if (x->cst) cudaStreamDestroy(x->cst);
     auto fr = [&](Buf& b) {
         if (b.p) cudaFree(b.p);
         b.p = nullptr;

@@ -141,7 +141,8 @@ cudaError_t launch_chunk_map(const uint64_t* choff, const uint64_t* off, const u
 cudaError_t launch_range(const uint64_t* c_off, const uint32_t* c_parent, uint32_t Fc, uint32_t q0,
                          uint64_t cap_entries, uint64_t forced_q1, const uint64_t* p_off,
                          const uint64_t* p_choff, const uint32_t* p_len, int p_is_root, RangeInfo* info,
-                         uint64_t* chunk_bounds, cudaStream_t st);
+                         uint64_t* chunk_bounds, RangeInfo* info_h, cudaStream_t st);
+cudaError_t launch_copy_u32(uint32_t* dst, const uint32_t* src, uint32_t n, cudaStream_t st);
 int pass_blocks_per_sm(int mode, bool int64, bool pref, bool circle);
 int tail_blocks_per_sm(bool int64);
 cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_beta, uint32_t H, uint32_t* out,
@@ -154,6 +155,6 @@ cudaError_t launch_gather(const uint32_t* dense, uint32_t anc_base, const uint32
 int tail16_blocks_per_sm(bool int64, bool pref);
 cudaError_t launch_tail16(bool int64, bool pref, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
-                          int is_root, RangeInfo* info, uint64_t* chunk_bounds, cudaStream_t st);
+                          int is_root, RangeInfo* info, uint64_t* chunk_bounds, RangeInfo* info_h, cudaStream_t st);
 
 }  // namespace hht

@@ -785,7 +785,7 @@ cudaError_t launch_gather(const uint32_t* dense, uint32_t anc_base, const uint32
 
 // Chunk bounds and streamed pairs of a parent range [r0, r1) (one thread).
 __global__ void k_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
-                         int is_root, RangeInfo* info, uint64_t* chunk_bounds) {
+                         int is_root, RangeInfo* info, uint64_t* chunk_bounds, RangeInfo* info_h) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     uint64_t pairs = 0;
     if (is_root) {
@@ -796,11 +796,23 @@ __global__ void k_bounds(const uint64_t* off, const uint64_t* choff, const uint3
     info->pairs = pairs;
     info->chunk_lo = chunk_bounds[0] = choff[r0];
     info->chunk_hi = chunk_bounds[1] = choff[r1];
+    if (info_h) *info_h = *info;      // mapped host copy: read after a stream sync, no copy engine
 }
 
 cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
-                          int is_root, RangeInfo* info, uint64_t* chunk_bounds, cudaStream_t st) {
-    k_bounds<<<1, 32, 0, st>>>(off, choff, len, r0, r1, is_root, info, chunk_bounds);
+                          int is_root, RangeInfo* info, uint64_t* chunk_bounds, RangeInfo* info_h, cudaStream_t st) {
+    k_bounds<<<1, 32, 0, st>>>(off, choff, len, r0, r1, is_root, info, chunk_bounds, info_h);
+    return cudaGetLastError();
+}
+
+// n words device -> mapped host memory (small readbacks that must not queue behind bulk copies on
+// the copy engines, e.g. the leaf-sink transfers).
+__global__ void k_copy_u32(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint32_t n) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+cudaError_t launch_copy_u32(uint32_t* dst, const uint32_t* src, uint32_t n, cudaStream_t st) {
+    k_copy_u32<<<1, 32, 0, st>>>(dst, src, n);
     return cudaGetLastError();
 }
 
@@ -1148,7 +1160,8 @@ cudaError_t launch_chunk_map(const uint64_t* choff, const uint64_t* off, const u
 // ---------------------------------------------------------------------------------------------
 __global__ void k_range(const uint64_t* c_off, const uint32_t* c_parent, uint32_t Fc, uint32_t q0,
                         uint64_t cap, uint64_t forced_q1, const uint64_t* p_off, const uint64_t* p_choff,
-                        const uint32_t* p_len, int p_is_root, RangeInfo* info, uint64_t* chunk_bounds) {
+                        const uint32_t* p_len, int p_is_root, RangeInfo* info, uint64_t* chunk_bounds,
+                        RangeInfo* info_h) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const uint64_t base = c_off[q0];
     uint64_t q1;
@@ -1181,14 +1194,15 @@ __global__ void k_range(const uint64_t* c_off, const uint32_t* c_parent, uint32_
     }
     chunk_bounds[0] = info->chunk_lo;
     chunk_bounds[1] = info->chunk_hi;
+    if (info_h) *info_h = *info;      // mapped host copy: read after a stream sync, no copy engine
 }
 
 cudaError_t launch_range(const uint64_t* c_off, const uint32_t* c_parent, uint32_t Fc, uint32_t q0,
                          uint64_t cap_entries, uint64_t forced_q1, const uint64_t* p_off,
                          const uint64_t* p_choff, const uint32_t* p_len, int p_is_root, RangeInfo* info,
-                         uint64_t* chunk_bounds, cudaStream_t st) {
+                         uint64_t* chunk_bounds, RangeInfo* info_h, cudaStream_t st) {
     k_range<<<1, 32, 0, st>>>(c_off, c_parent, Fc, q0, cap_entries, forced_q1, p_off, p_choff, p_len,
-                              p_is_root, info, chunk_bounds);
+                              p_is_root, info, chunk_bounds, info_h);
     return cudaGetLastError();
 }
 

@@ -28,7 +28,7 @@ STATUS = {0: "HHT_OK", 1: "HHT_EINVAL", 2: "HHT_ERANGE", 3: "HHT_EOVERFLOW", 4: 
 EXPORTS = ["hht_default_opts", "hht_create", "hht_nccl_unique_id", "hht_detect", "hht_detect_batch",
            "hht_result_leaves", "hht_result_level", "hht_result_stats", "hht_result_profile",
            "hht_result_launches", "hht_timer_begin", "hht_timer_end", "hht_last_error", "hht_status_str",
-           "hht_destroy", "hht_version"]
+           "hht_destroy", "hht_version", "hht_set_leaf_sink"]
 
 PROFILE_CLASSES = ["stage", "count", "write", "tail", "split", "gather", "other", "allreduce"]
 
@@ -57,7 +57,8 @@ class Stats(C.Structure):
     _fields_ = [("tests", C.c_uint64), ("votes", C.c_uint64), ("leaves", C.c_uint64), ("pairs", C.c_uint64),
                 ("visited", C.c_uint64 * 64), ("split", C.c_uint64 * 64), ("h2d_bytes", C.c_uint64),
                 ("d2h_bytes", C.c_uint64), ("levels", C.c_uint32), ("int_bits", C.c_uint32),
-                ("ranges", C.c_uint32), ("images", C.c_uint32), ("ms", C.c_double)]
+                ("ranges", C.c_uint32), ("images", C.c_uint32), ("ms", C.c_double),
+                ("leaves_streamed", C.c_uint64)]
 
 
 class Launch(C.Structure):
@@ -90,6 +91,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hht_result_leaves": ([p, i32, p, i64, p], C.c_int),
         "hht_result_level": ([p, i32, u32, i32, p, i64, p], C.c_int),
         "hht_result_stats": ([p, p], C.c_int),
+        "hht_set_leaf_sink": ([p, p, i64], C.c_int),
         "hht_result_profile": ([p, p], C.c_int),
         "hht_result_launches": ([p, p, i64, p], C.c_int),
         "hht_timer_begin": ([p], C.c_int),
@@ -167,6 +169,7 @@ class HHT:
             self._id = C.create_string_buffer(bytes(nccl_id), 128)
             o.nccl_id = C.cast(self._id, C.c_void_p)
         self._ctx = C.c_void_p()
+        self._sink = None
         st = self._lib.hht_create(C.byref(self._ctx), C.byref(o))
         if st:
             raise HHTError(st, "hht_create failed")
@@ -220,6 +223,17 @@ class HHT:
                                                 C.byref(cnt)))
         return cnt.value
 
+    def set_leaf_sink(self, out: Optional[np.ndarray]):
+        """Stream every later detect's leaf rows (image, half, i, j, votes) into `out` (a C-contiguous
+        uint32 [cap, 5] array, ideally pinned) while the detection runs; None removes the sink."""
+        if out is None:
+            self._check(self._lib.hht_set_leaf_sink(self._ctx, None, 0))
+            self._sink = None
+            return
+        assert out.dtype == np.uint32 and out.ndim == 2 and out.shape[1] == 5 and out.flags.c_contiguous
+        self._sink = out
+        self._check(self._lib.hht_set_leaf_sink(self._ctx, C.c_void_p(out.ctypes.data), out.shape[0]))
+
     def leaves(self, image: int = -1) -> np.ndarray:
         """int64 [L, 5]: (image, half, i, j, votes) in image, half, depth-first order."""
         if image == -1:
@@ -257,7 +271,7 @@ class HHT:
         return {"tests": s.tests, "votes": s.votes, "leaves": s.leaves, "pairs": s.pairs,
                 "visited": list(s.visited)[:L], "split": list(s.split)[:L], "h2d_bytes": s.h2d_bytes,
                 "d2h_bytes": s.d2h_bytes, "levels": L, "int_bits": s.int_bits, "ranges": s.ranges,
-                "images": s.images, "ms": s.ms}
+                "images": s.images, "ms": s.ms, "leaves_streamed": s.leaves_streamed}
 
     def profile(self) -> dict:
         p = Profile()

@@ -248,3 +248,31 @@ def test_nccl_collectives_one_rank(torch_dev):
     with pytest.raises(hht.HHTError) as e:
         h.detect(_dev(bad, torch_dev), 64, 6, 5)
     assert e.value.name == "HHT_ERANGE"
+
+
+@pytest.mark.parametrize("budget", [0, 256 << 10])
+def test_leaf_sink_streaming(budget, torch_dev):
+    """hht_set_leaf_sink: rows streamed during the detect equal hht_result_leaves(-1) (same order),
+    also across depth-first ranges; a too-small sink receives the first `cap` rows only."""
+    cfg = synth.CONFIGS[2]
+    pts, _ = synth.config_image(2)
+    h = hht.HHT(halves=cfg.halves, mem_budget=budget)
+    d = _dev(pts, torch_dev)
+    h.detect(d, cfg.N, cfg.D, cfg.T)
+    want = h.leaves(-1)
+    sink = np.zeros((want.shape[0] + 7, 5), dtype=np.uint32)
+    h.set_leaf_sink(sink)
+    h.detect(d, cfg.N, cfg.D, cfg.T)
+    st = h.stats()
+    assert st["leaves_streamed"] == st["leaves"] == want.shape[0]
+    assert np.array_equal(sink[:want.shape[0]].astype(np.int64), want)
+    assert st["d2h_bytes"] >= 20 * want.shape[0]
+    small = np.zeros((100, 5), dtype=np.uint32)
+    h.set_leaf_sink(small)
+    h.detect(pts, cfg.N, cfg.D, cfg.T)            # host input too
+    st = h.stats()
+    assert st["leaves_streamed"] == 100 and st["leaves"] == want.shape[0]
+    assert np.array_equal(small.astype(np.int64), want[:100])
+    h.set_leaf_sink(None)
+    h.detect(d, cfg.N, cfg.D, cfg.T)
+    assert h.stats()["leaves_streamed"] == 0
