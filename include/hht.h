@@ -67,8 +67,11 @@ typedef struct {
     uint32_t record_levels;  /* 1 (default): keep every level's (a, c, votes) records */
     uint32_t force_int64;    /* 1: use the int64 kernels even where int32 is exact (testing) */
     uint32_t profile;        /* 1: time every kernel launch with CUDA events (hht_result_profile) */
-    uint32_t tail_depth;     /* levels counted by the dense leaf-grid tail: 0 = auto (4 when
-                                depth >= 4, else 3), 3 or 4 to force (results are identical) */
+    uint32_t tail_depth;     /* dense leaf-grid tail: 0 = auto (5 when depth >= 5, else 4 when
+                                depth >= 4, else 3); 5 = 16x16 grids of level depth-4 rastered
+                                straight from level depth-5 lists (fused, no level depth-4 lists);
+                                4 = 16x16 grids from level depth-4 lists; 3 = 8x8 grids from level
+                                depth-3 lists. Results are identical. */
     uint32_t prefetch;       /* pass/tail kernels: 0 = auto, 1 = fetch the next chunk's descriptor
                                 only, 2 = also its list entries (more registers); identical results */
     uint32_t variant;        /* membership test: HHT_EXACT (0, default) = the paper's 4-bit corner

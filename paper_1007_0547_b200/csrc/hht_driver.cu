@@ -75,6 +75,7 @@ struct hht_ctx {
     int grid[3][2] = {};
     int tail_grid[2] = {};
     int tail16_grid[2] = {};
+    int fused_grid[2] = {};
     bool pref_pass = true, pref_tail = true;   // opts.prefetch (0 = auto)
     bool circle = false;                       // opts.variant == HHT_FHT_CIRCLE
     int grid_circle[3][2] = {};
@@ -88,6 +89,7 @@ struct hht_ctx {
     std::vector<int64_t> tree_E;            // global points per tree
 
     Buf stage_in, packed, errflag, beta, stats, tiles, tilectr, totals, rng, bounds, vtmp, dense, gv, leafrows;
+    Buf fusedctr;                    // k_fused work counter (u32) + rastered-pair counter (u64)
     // leaf sink (hht_set_leaf_sink): double-buffered row staging, copied on its own stream
     hht_leaf* sink = nullptr;
     int64_t sink_cap = 0;
@@ -121,9 +123,12 @@ struct hht_ctx {
 namespace {
 
 
-// Levels covered by the dense tail: a 16x16 leaf grid under level D-4 when D >= 4, else 8x8.
+// Levels covered by the dense tail: lists exist down to level D - tail_depth. 5 (auto when D >= 5):
+// 16x16 leaf grids of level D-4, rastered straight from level D-5 lists by the fused tail;
+// 4: 16x16 grids from level D-4 lists; 3: 8x8 grids from level D-3 lists.
 int tail_depth(const hht_ctx* x) {
-    const int want = x->opts.tail_depth ? (int)x->opts.tail_depth : 4;
+    const int want = x->opts.tail_depth ? (int)x->opts.tail_depth : 5;
+    if (want >= 5 && x->D >= 5) return 5;
     return (want >= 4 && x->D >= 4) ? 4 : 3;
 }
 
@@ -416,6 +421,8 @@ hht_status choose_range(hht_ctx* x, int lc, uint32_t q0, uint64_t cap_entries, b
 // R_(L+1) (its split children, without lists). One pass counts the 2^TK x 2^TK leaf grid of every
 // R_L region; every deeper level is then split from votes gathered out of the grids (a region's
 // votes = the sum of its diagonal leaves), down to the leaves.
+hht_status gather_levels(hht_ctx* x, int L, int c0, uint32_t anc_base, Level& Own, int TK);
+
 hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
     const int TK = x->D - L;
     const uint32_t cells = 1u << (2 * TK);
@@ -443,8 +450,13 @@ hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
     }
     x->stat.pairs += pairs;
     TRY(allreduce_sum_u32(x, (uint32_t*)x->dense.p, (size_t)n * cells));
-    // levels L+2 .. D: parents R_(c-1), votes gathered from the grids
-    for (int c = L + 2; c <= x->D; ++c) {
+    return gather_levels(x, L, L + 2, r0, P, TK);
+}
+
+// Levels c0 .. D from the leaf grids of the grid owners R_L[anc_base, ...): parents R_(c-1), a
+// child's votes = the sum of its diagonal leaves, then the split of level c.
+hht_status gather_levels(hht_ctx* x, int L, int c0, uint32_t anc_base, Level& Own, int TK) {
+    for (int c = c0; c <= x->D; ++c) {
         Level& Pc = x->lv[c - 1];
         if (Pc.F == 0) return HHT_OK;
         const int hops = c - 1 - L;
@@ -452,7 +464,7 @@ hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
         for (int h = 0; h < hops; ++h) chain.parent[h] = (const uint32_t*)x->lv[c - 1 - h].parent.p;
         TRY(ensure(x, x->gv, 16ull * Pc.F));
         const int g = prof_begin(x, 5, (16ull + 8 + 4ull * hops + 16ull * (1u << (x->D - c))) * Pc.F);
-        CK(launch_gather((const uint32_t*)x->dense.p, r0, (const uint32_t*)P.a.p, (const uint32_t*)P.c.p,
+        CK(launch_gather((const uint32_t*)x->dense.p, anc_base, (const uint32_t*)Own.a.p, (const uint32_t*)Own.c.p,
                          (const uint32_t*)Pc.a.p, (const uint32_t*)Pc.c.p, chain, hops, TK, x->D - c, Pc.F,
                          (uint32_t*)x->gv.p, x->st));
         prof_end(x, g);
@@ -461,12 +473,56 @@ hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
     return HHT_OK;
 }
 
+// Fused tail at parent level l = D-5: lv[l] holds the lists of R_l[r0, r1), lv[l+1] their split
+// children R_(l+1) (no lists). One k_fused pass rasters every child's 16x16 leaf grid straight from
+// the parents' lists; levels l+2 .. D are then split from the grids (the grid owners are R_(l+1)).
+hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
+    const int L = l + 1;
+    Level& P = x->lv[l];
+    Level& C = x->lv[L];
+    const uint32_t n = C.F;
+    if (n == 0 || r1 == r0) return HHT_OK;
+    TRY(ensure(x, x->dense, (size_t)n * kTail16Cells * 4));
+    CK(cudaMemsetAsync(x->dense.p, 0, (size_t)n * kTail16Cells * 4, x->st));
+    TRY(ensure(x, x->fusedctr, 256));
+    CK(cudaMemsetAsync(x->fusedctr.p, 0, 16, x->st));
+    CK(launch_bounds((const uint64_t*)P.off.p, (const uint64_t*)P.choff.p, (const uint32_t*)P.len.p, r0, r1, l == 0,
+                     (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->range_m, x->st));
+    PassArgs a = pass_args(x, P, l);
+    a.nf = (const uint32_t*)C.nf.p;
+    a.nf_rbase = r0;
+    a.q0 = 0;
+    a.q1 = C.F;
+    a.votes = (uint32_t*)x->dense.p;
+    a.p_choff = (const uint64_t*)P.choff.p;
+    a.r_lo = r0;
+    a.r_hi = r1;
+    a.work = (uint32_t*)x->fusedctr.p;
+    a.child_pairs = (unsigned long long*)((char*)x->fusedctr.p + 8);
+    const int id = prof_begin(x, 3, 0);
+    CK(launch_fused(x->int64, a, x->fused_grid[x->int64 ? 1 : 0], x->st));
+    prof_end(x, id);
+    CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)((char*)x->fusedctr.p + 8), 2, x->st));
+    TRY(sync(x));
+    const uint64_t pairs = read_mapped(x->range_h).pairs;
+    const uint64_t child_pairs = read_mapped(x->misc_h);
+    if (id >= 0) {
+        x->pev[id].bytes = pairs * 4 + (uint64_t)n * kTail16Cells * 4;
+        // raster steps: 16 leaf columns x 8 instructions per (line, split child) pair (see tail())
+        x->pev[id].ops = child_pairs * 16 * 8;
+    }
+    x->stat.pairs += pairs;
+    TRY(allreduce_sum_u32(x, (uint32_t*)x->dense.p, (size_t)n * kTail16Cells));
+    return gather_levels(x, L, L + 1, 0, C, 4);
+}
+
 // Preconditions: lv[l] holds the lists of R_l[r0, r1) and lv[l+1] holds R_(l+1) = the split
 // children of R_l[r0, r1) with NF_(l+1). Processes everything below.
 hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
     const int lc = l + 1;
     if (lc >= x->D) return HHT_OK;
-    if (!x->circle && x->D >= 3 && l == x->D - tail_depth(x)) return tail(x, l, r0, r1);
+    if (!x->circle && x->D >= 3 && l == x->D - tail_depth(x))
+        return tail_depth(x) == 5 ? tail_fused(x, l, r0, r1) : tail(x, l, r0, r1);
     Level& P = x->lv[l];
     Level& C = x->lv[lc];
     const uint32_t Fc = C.F;
@@ -867,7 +923,7 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return HHT_EINVAL;
     if (o.world > 1 && !o.nccl_id) return HHT_EINVAL;
     if (o.halves == 0 || (o.halves & ~3u)) return HHT_EINVAL;
-    if (!(o.tail_depth == 0 || o.tail_depth == 3 || o.tail_depth == 4)) return HHT_EINVAL;
+    if (!(o.tail_depth == 0 || (o.tail_depth >= 3 && o.tail_depth <= 5))) return HHT_EINVAL;
     hht_ctx* x = new (std::nothrow) hht_ctx();
     if (!x) return HHT_ENOMEM;
     x->opts = o;
@@ -903,6 +959,7 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
         for (int w = 0; w < 2; ++w) x->grid_circle[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, true, true);
     for (int w = 0; w < 2; ++w) x->tail_grid[w] = x->sms * tail_blocks_per_sm(w == 1);
     for (int w = 0; w < 2; ++w) x->tail16_grid[w] = x->sms * tail16_blocks_per_sm(w == 1, x->pref_tail);
+    for (int w = 0; w < 2; ++w) x->fused_grid[w] = x->sms * fused_blocks_per_sm(w == 1);
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return fail(HHT_ECUDA);
     x->budget = o.mem_budget ? o.mem_budget : (size_t)(0.70 * (double)fr);
@@ -1083,7 +1140,7 @@ void hht_destroy(hht_ctx* x) {
     for (auto& g : x->rec) fr(g.b);
     fr(x->leaves.b);
     for (Buf* b : {&x->stage_in, &x->packed, &x->errflag, &x->beta, &x->stats, &x->tiles, &x->tilectr, &x->totals,
-                   &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv, &x->leafrows})
+                   &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv, &x->leafrows, &x->fusedctr})
         fr(*b);
     if (x->totals_h) cudaFreeHost(x->totals_h);
     if (x->range_h) cudaFreeHost(x->range_h);

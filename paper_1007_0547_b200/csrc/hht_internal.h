@@ -92,6 +92,12 @@ struct PassArgs {
     uint32_t div_m, div_s;         // floor(y / 3N) = umulhi(y, div_m) >> div_s for 0 <= y < 2^31
     uint32_t* votes;               // MODE_COUNT: [4 * nparents] (4*(r - nf_rbase) + q)
                                    // else:       [4 * (q1 - q0)] (4*(nf - q0) + q')
+                                   // tails: 256-cell leaf grids per region
+    // fused tail (k_fused): parents R_l[r_lo, r_hi) are the work units, taken by warps from `work`
+    const uint64_t* p_choff;       // parents' chunk offsets (their chunks are consecutive)
+    uint32_t r_lo, r_hi;
+    uint32_t* work;                // device counter, zero at launch
+    unsigned long long* child_pairs;   // device counter: (line, split child) pairs rastered
 };
 
 struct SplitArgs {
@@ -154,6 +160,8 @@ cudaError_t launch_gather(const uint32_t* dense, uint32_t anc_base, const uint32
                           int j, uint32_t Fp, uint32_t* V, cudaStream_t st);
 int tail16_blocks_per_sm(bool int64, bool pref);
 cudaError_t launch_tail16(bool int64, bool pref, const PassArgs& a, int grid, cudaStream_t st);
+int fused_blocks_per_sm(bool int64);
+cudaError_t launch_fused(bool int64, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
                           int is_root, RangeInfo* info, uint64_t* chunk_bounds, RangeInfo* info_h, cudaStream_t st);
 

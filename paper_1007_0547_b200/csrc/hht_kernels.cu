@@ -615,37 +615,42 @@ __device__ __forceinline__ I floor_div3n_clamp16(I y, I N3, uint32_t div_m, uint
     }
 }
 
-template <typename I, bool PREF>
-__global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) {
-    // table entry e of lane copy c at slot 32e + c: an LDS.64 serves 16 lanes per wavefront and
-    // every lane reads its own bank pair, so lookups never conflict whatever entries lanes need
-    __shared__ uint2 s_tab[kTab16 * 32];
-    for (int t = threadIdx.x; t < kTab16 * 32; t += blockDim.x) s_tab[t] = tab16_entry(t >> 5, t & 31);
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const uint32_t tab_sm = (uint32_t)__cvta_generic_to_shared(s_tab + lane);
-    const uint32_t cdrop = A.tab_stride, ck2n = 0u - 2u * A.tab_stride;   // 256, -512 (runtime)
-    const uint32_t ck2 = 2u * A.tab_stride;
-    const uint32_t ta_zero = tab_sm + 256u * 32u;                          // entry (k = 0, drop 0)
-    const uint32_t ta_base = tab_sm + 256u * 34u;                          // entry (k = 1, drop 0)
-    // cells this lane holds after the reduce-scatter: column 4b + u, u = L1 + 2 L2; rows
-    // 8 L4 + 2 L0 + L3 (+ 4)
-    const uint32_t red_u = ((lane >> 1) & 1) + 2 * ((lane >> 2) & 1);
-    const uint32_t red_row = 8 * ((lane >> 4) & 1) + 2 * (lane & 1) + ((lane >> 3) & 1);
-    const int D = A.D;
-    const int sh = D - A.level;                       // == 4
-    const I N = (I)A.N;
-    const I N3 = (I)3 * N;
-    const uint32_t div_m = A.div_m, div_s = A.div_s;
+// The 16x16 raster of one batch of <= 256 lines (8 per lane) over the leaf grid of one level-(D-4)
+// region (a, c), accumulated into `dst` (256 u32 counters, [16 * column + row]) with one atomic per
+// (lane, cell pair) per column block. Shared by the dense tail (batches = chunks of the region's
+// list) and the fused tail (batches = full shared-memory queues of a child of a level-(D-5) region).
+template <typename I>
+struct Raster16 {
+    uint32_t ta_zero, ta_base, cdrop, ck2n, ck2, red_u, red_row, div_m, div_s;
+    int D;
+    I N, N3;
 
-    chunk_loop<PREF>(A, lane, [&](const ChunkDesc& d, const uint32_t (&p)[kItems]) {
-        const int cnt = (int)d.cnt;
-        const I i0 = (I)d.a << sh;
-        const I j0 = (I)d.c << sh;
+    __device__ __forceinline__ void init(const PassArgs& A, const uint2* s_tab, int lane) {
+        const uint32_t tab_sm = (uint32_t)__cvta_generic_to_shared(s_tab + lane);
+        cdrop = A.tab_stride;                       // 256, -512, 512 (runtime values, see mad_u32)
+        ck2n = 0u - 2u * A.tab_stride;
+        ck2 = 2u * A.tab_stride;
+        ta_zero = tab_sm + 256u * 32u;              // entry (k = 0, drop 0)
+        ta_base = tab_sm + 256u * 34u;              // entry (k = 1, drop 0)
+        // cells this lane holds after the reduce-scatter: column 4b + u, u = L1 + 2 L2; rows
+        // 8 L4 + 2 L0 + L3 (+ 4)
+        red_u = ((lane >> 1) & 1) + 2 * ((lane >> 2) & 1);
+        red_row = 8 * ((lane >> 4) & 1) + 2 * (lane & 1) + ((lane >> 3) & 1);
+        div_m = A.div_m;
+        div_s = A.div_s;
+        D = A.D;
+        N = (I)A.N;
+        N3 = (I)3 * N;
+    }
+
+    __device__ __forceinline__ void run(const uint32_t (&p)[kItems], int cnt, uint32_t ra, uint32_t rc, uint32_t beta,
+                                        uint32_t* dst, int lane) const {
+        const I i0 = (I)ra << 4;
+        const I j0 = (I)rc << 4;
         const I alpha = ((I)1 << D) - 2 * i0;
         const I beta_m1 = (N << D) - N3 * j0 - 1;
         // byte selectors: ex = low half-word of the packed entry for BETA (x <-> y), high for ALPHA
-        const uint32_t sel_ex = d.beta ? 0x4410u : 0x4432u, sel_ey = d.beta ? 0x4432u : 0x4410u;
+        const uint32_t sel_ex = beta ? 0x4410u : 0x4432u, sel_ey = beta ? 0x4432u : 0x4410u;
 
         // per-line raster state carried across the 4 column blocks: z = y - (k-1)*3N (height of the
         // line above its row's floor at the current lattice column; a column drops iff z < 0), the
@@ -663,7 +668,6 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
             z[it] = yy - f * N3;
             ta[it] = (lane + kWarp * it < cnt) ? mad_u32((uint32_t)f, ck2, ta_base) : ta_zero;
         }
-        uint32_t* dst = A.votes + (uint64_t)(d.r - A.nf_rbase) * kTail16Cells;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             uint32_t acc[8];                                  // [2 * column-in-block + row half], nibbles
@@ -715,7 +719,179 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
             if (c0) atomicAdd(dst + 16 * col + red_row, c0);
             if (c1) atomicAdd(dst + 16 * col + red_row + 4, c1);
         }
+    }
+};
+
+template <typename I, bool PREF>
+__global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) {
+    // table entry e of lane copy c at slot 32e + c: an LDS.64 serves 16 lanes per wavefront and
+    // every lane reads its own bank pair, so lookups never conflict whatever entries lanes need
+    __shared__ uint2 s_tab[kTab16 * 32];
+    for (int t = threadIdx.x; t < kTab16 * 32; t += blockDim.x) s_tab[t] = tab16_entry(t >> 5, t & 31);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    Raster16<I> R;
+    R.init(A, s_tab, lane);
+    chunk_loop<PREF>(A, lane, [&](const ChunkDesc& d, const uint32_t (&p)[kItems]) {
+        R.run(p, (int)d.cnt, d.a, d.c, d.beta, A.votes + (uint64_t)(d.r - A.nf_rbase) * kTail16Cells, lane);
     });
+}
+
+// ---------------------------------------------------------------------------------------------
+// Fused tail: the pass over the lists of the split regions R at level l = D-5 and the dense 16x16
+// raster of their split children (level D-4) in one kernel, without materialising level-(D-4)
+// lists. A warp owns one parent R at a time (dynamic, via an atomic counter) and walks its chunks:
+// each chunk's entries are tested against R's 4 children (the exact test of k_pass) and pushed onto
+// per-child stacks in shared memory (4 x 512 entries per warp); whenever a stack holds >= 256
+// entries, its top 256 are rastered over that child's leaf grid exactly as k_tail16 would raster a
+// 256-entry chunk of the child's list (the order of a list is irrelevant to its counts); the last
+// partial stacks are flushed when R is done. Entries never leave the SM between the two steps.
+// ---------------------------------------------------------------------------------------------
+constexpr int kQ = 512;                           // stack capacity per child: < 256 left + <= 256 pushed
+constexpr int kFusedSmem = kTab16 * 32 * 8 + 8 * 4 * kQ * 4;
+
+template <typename I>
+__global__ void __launch_bounds__(256, 2) k_fused(const PassArgs A) {
+    extern __shared__ uint4 s_dyn[];
+    uint2* s_tab = reinterpret_cast<uint2*>(s_dyn);
+    uint32_t* s_q = reinterpret_cast<uint32_t*>(s_tab + kTab16 * 32);
+    for (int t = threadIdx.x; t < kTab16 * 32; t += blockDim.x) s_tab[t] = tab16_entry(t >> 5, t & 31);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    uint32_t* Q = s_q + (threadIdx.x >> 5) * (4 * kQ);
+    const uint32_t q_sa = (uint32_t)__cvta_generic_to_shared(Q);
+    Raster16<I> R;
+    R.init(A, s_tab, lane);
+    const int D = A.D;
+    const int sh = D - A.level;                       // == 5: parent side 32 lattice steps
+    const I N = (I)A.N;
+    const I Qc = ((I)3 * N) << (sh - 1);              // child b-step 3N * s/2
+
+    while (true) {
+        uint32_t r = 0;
+        if (lane == 0) r = atomicAdd(A.work, 1u);
+        r = __shfl_sync(kFull, r, 0) + A.r_lo;
+        if (r >= A.r_hi) break;
+        const uint64_t c_lo = __ldg(A.p_choff + r), c_hi = __ldg(A.p_choff + r + 1);
+        if (c_lo == c_hi) continue;
+        // lanes 0..3: grid (next-frontier) index of split child `lane`, kNone otherwise
+        uint32_t my_nf = kNone;
+        if (lane < 4) {
+            my_nf = __ldg(A.nf + 4 * (uint64_t)(r - A.nf_rbase) + lane);
+            if (my_nf != kNone && (my_nf < A.q0 || my_nf >= A.q1)) my_nf = kNone;
+        }
+        uint32_t nfq[4], splitm = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            nfq[q] = __shfl_sync(kFull, my_nf, q);
+            splitm |= (nfq[q] != kNone ? 1u : 0u) << q;
+        }
+        if (splitm == 0) continue;
+        ChunkDesc d = load_desc(A.chunks, c_lo, c_hi);
+        const uint32_t pa = d.a, pc = d.c, beta = d.beta;
+        const I i0 = (I)pa << sh;
+        const I j0 = (I)pc << sh;
+        const I alpha = ((I)1 << D) - 2 * i0;
+        const I beta_m1 = (N << D) - (I)3 * N * j0 - 1;
+        uint32_t top0 = 0, top1 = 0, top2 = 0, top3 = 0;   // stack heights (warp-uniform)
+        uint32_t p[kItems];
+        load_items(p, A.list, A.list_base, d, lane);
+        uint64_t ch = c_lo;
+        // One loop whose every iteration either rasters one stack (a full one, or once the parent's
+        // chunks are exhausted any non-empty one) or pushes one chunk: the raster code is
+        // instantiated once (four inlined copies measured 2x slower: instruction-cache misses).
+        while (true) {
+            const uint32_t full = (top0 >= (uint32_t)kChunk ? 1u : 0u) | (top1 >= (uint32_t)kChunk ? 2u : 0u) |
+                                  (top2 >= (uint32_t)kChunk ? 4u : 0u) | (top3 >= (uint32_t)kChunk ? 8u : 0u);
+            const uint32_t nonempty = (top0 ? 1u : 0u) | (top1 ? 2u : 0u) | (top2 ? 4u : 0u) | (top3 ? 8u : 0u);
+            const uint32_t job = full ? full : (ch >= c_hi ? nonempty : 0u);
+            if (job) {
+                const int q = __ffs(job) - 1;
+                const uint32_t t = q == 0 ? top0 : q == 1 ? top1 : q == 2 ? top2 : top3;
+                const uint32_t n = min(t, (uint32_t)kChunk);
+                const uint32_t base = t - n;               // raster the top n entries of stack q
+                uint32_t pq[kItems];
+#pragma unroll
+                for (int it = 0; it < kItems; ++it)
+                    pq[it] = (lane + kWarp * it < (int)n) ? Q[q * kQ + base + lane + kWarp * it] : 0u;
+                const uint32_t nf_q = __shfl_sync(kFull, my_nf, q);
+                R.run(pq, (int)n, 2 * pa + quad_da(q), 2 * pc + quad_dc(q), beta,
+                      A.votes + (uint64_t)(nf_q - A.q0) * kTail16Cells, lane);
+                if (lane == 0) atomicAdd(A.child_pairs, (unsigned long long)n);
+                if (q == 0) top0 = base; else if (q == 1) top1 = base; else if (q == 2) top2 = base; else top3 = base;
+                __syncwarp();
+                continue;
+            }
+            if (ch >= c_hi) break;
+            // push chunk ch: child bits of its entries (split children only)
+            const int cnt = (int)d.cnt;
+            uint32_t cm = 0;
+#pragma unroll
+            for (int it = 0; it < kItems; ++it) {
+                const uint32_t w = p[it];
+                const I ex = (I)__byte_perm(w, 0, beta ? 0x4410u : 0x4432u);
+                const I ey = (I)__byte_perm(w, 0, beta ? 0x4432u : 0x4410u);
+                I gm1 = ex * alpha + (ey << D) + beta_m1;  // G(SW corner of R) - 1
+                if (lane + kWarp * it >= cnt) gm1 = (I)-1;
+                const I Pc = ex << sh;
+                const I Uc = Pc + Qc;
+                const uint32_t b = crosses<I>(gm1 - Pc - Qc, Uc) | (crosses<I>(gm1 - Qc, Uc) << 1) |
+                                   (crosses<I>(gm1, Uc) << 2) | (crosses<I>(gm1 - Pc, Uc) << 3);
+                cm |= b << (4 * it);
+            }
+            cm &= splitm * 0x11111111u;
+            // push onto the stacks: byte-field warp scan of the 4 per-lane counts (as in k_pass)
+            const uint32_t c0 = __popc(cm & 0x11111111u), c1 = __popc(cm & 0x22222222u);
+            const uint32_t c2 = __popc(cm & 0x44444444u), c3 = __popc(cm & 0x88888888u);
+            const uint32_t own = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+            uint32_t inc = own;
+#pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                uint32_t t;
+                asm volatile("{\n\t.reg .pred p;\n\tshfl.sync.up.b32 %0|p, %1, %2, 0, 0xffffffff;\n\t@!p mov.b32 %0, 0;\n\t}"
+                             : "=r"(t) : "r"(inc), "r"(dd));
+                inc += t;
+            }
+            const uint32_t exc = inc - own;
+            const uint32_t t02 = __reduce_add_sync(kFull, c0 | (c2 << 16));
+            const uint32_t t13 = __reduce_add_sync(kFull, c1 | (c3 << 16));
+            uint32_t sa[4] = {q_sa + 4 * (top0 + (exc & 0xFFu)), q_sa + 4 * (kQ + top1 + ((exc >> 8) & 0xFFu)),
+                              q_sa + 4 * (2 * kQ + top2 + ((exc >> 16) & 0xFFu)),
+                              q_sa + 4 * (3 * kQ + top3 + (exc >> 24))};
+#pragma unroll
+            for (int it = 0; it < kItems; ++it) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) sts_if(cm & (1u << (4 * it + q)), sa[q], p[it]);
+            }
+            top0 += t02 & 0xFFFFu;
+            top1 += t13 & 0xFFFFu;
+            top2 += t02 >> 16;
+            top3 += t13 >> 16;
+            __syncwarp();
+            // the next chunk's entries are in flight while the full stacks are rastered
+            ++ch;
+            d = load_desc(A.chunks, ch, c_hi);
+            load_items(p, A.list, A.list_base, d, lane);
+        }
+    }
+}
+
+int fused_blocks_per_sm(bool int64) {
+    int n = 0;
+    if (int64) {
+        cudaFuncSetAttribute(k_fused<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fused<int64_t>, 256, kFusedSmem);
+    } else {
+        cudaFuncSetAttribute(k_fused<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fused<int32_t>, 256, kFusedSmem);
+    }
+    return n > 0 ? n : 1;
+}
+
+cudaError_t launch_fused(bool int64, const PassArgs& a, int grid, cudaStream_t st) {
+    if (int64) k_fused<int64_t><<<grid, 256, kFusedSmem, st>>>(a);
+    else k_fused<int32_t><<<grid, 256, kFusedSmem, st>>>(a);
+    return cudaGetLastError();
 }
 
 using PassKernel = void (*)(const PassArgs);

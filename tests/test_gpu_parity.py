@@ -212,10 +212,10 @@ def test_c2_structure_and_profile(torch_dev):
     assert prof["write"]["launches"] > 0 and prof["split"]["launches"] >= cfg.D
 
 
-@pytest.mark.parametrize("tail_depth", [3, 4])
+@pytest.mark.parametrize("tail_depth", [3, 4, 5])
 @pytest.mark.parametrize("seed", range(8))
 def test_tail_depth_variants(seed, tail_depth, torch_dev):
-    """The 8x8 (D-3) and 16x16 (D-4) leaf-grid tails give identical records and leaves."""
+    """The 8x8 (D-3), 16x16 (D-4) and fused 16x16-from-(D-5) tails give identical records and leaves."""
     rng = np.random.default_rng(100 + seed)
     N = int(rng.choice([16, 33, 64, 200]))
     D = int(rng.integers(3, 9))
