@@ -17,7 +17,7 @@ t=open('gpurun_out/plain_c5.log').read()
 b=ast.literal_eval(re.search(r'^write launches \d+ first bytes \d+ bytes\[:16\] (\[.*\])$', t, re.M).group(1))
 print(1 + max(range(len(b)), key=lambda i: b[i]))")
 echo "write capture index $WSKIP" > gpurun_out/write_skip.txt
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_tail -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_tail|k_fused" -c 1 \
     -o gpurun_out/c5_tail python scripts/run_once.py --config 5 > gpurun_out/ncu_tail.log 2>&1
 echo "tail capture rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pass -s $WSKIP -c 1 \
