@@ -58,6 +58,7 @@ typedef enum {
 #define HHT_FHT_CIRCLE 1u  /* opts.variant: FHT circumcircle test (comparison) */
 
 typedef struct hht_ctx hht_ctx;   /* opaque */
+typedef struct hht_group hht_group;   /* opaque: in-process collective group (hht_group_create) */
 
 typedef struct {
     int32_t device;          /* CUDA ordinal */
@@ -83,6 +84,11 @@ typedef struct {
     const void* nccl_id;     /* world > 1: 128-byte ncclUniqueId from hht_nccl_unique_id on rank 0,
                                 identical on every rank. NULL when world == 1; a non-NULL id with
                                 world == 1 runs every collective on a 1-rank communicator (tests) */
+    hht_group* group;        /* instead of nccl_id: the ranks are `world` contexts of this process,
+                                each driven by its own host thread, and every collective the
+                                multi-rank path makes (the same calls, in the same order, as with
+                                NCCL) is a host-staged allreduce among them. For testing the
+                                multi-rank logic on one GPU; the contexts may share a device. */
 } hht_opts;
 
 /* One detected line: leaf (i, j) of tree (image, half) with votes > threshold. */
@@ -130,6 +136,11 @@ typedef struct {
     uint64_t ops[8];         /* algorithmic integer instructions (thread-level) of that class where
                                 it is issue-bound: the dense tail's raster steps; 0 else */
 } hht_profile;
+
+/* In-process collective group of `world` ranks (see hht_opts.group). Destroy after every context
+ * that uses it. */
+hht_status hht_group_create(hht_group** out, int32_t world);
+void hht_group_destroy(hht_group* group);
 
 /* Fill opts with defaults (device 0, rank 0 of 1, both halves, records on). */
 hht_status hht_default_opts(hht_opts* opts);

@@ -19,6 +19,8 @@
 #include <vector>
 
 #include <atomic>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 
 #include "hht.h"
@@ -64,12 +66,37 @@ struct ProfEv {
 
 }  // namespace
 
+// In-process collective group: `world` contexts, one host thread each. An allreduce stages every
+// rank's buffer in host memory, waits for all ranks, reduces in rank order and copies the result
+// back (deterministic; a test transport, not a fast one).
+struct hht_group {
+    int world = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t generation = 0;
+    std::vector<std::vector<uint8_t>> slot;
+
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const uint64_t gen = generation;
+        if (++arrived == world) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen; });
+        }
+    }
+};
+
 struct hht_ctx {
     hht_opts opts{};
     int sms = 148;
     cudaStream_t st = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, tb0 = nullptr, tb1 = nullptr;
     ncclComm_t comm = nullptr;
+    hht_group* group = nullptr;        // borrowed (opts.group)
     std::string err;
     size_t budget = 0;
     int grid[3][2] = {};
@@ -226,10 +253,51 @@ void prof_end(hht_ctx* x, int id) {
     if (id >= 0) cudaEventRecord(x->pev[id].b, x->st);
 }
 
+bool multi(const hht_ctx* x) { return x->comm != nullptr || x->group != nullptr; }
+
+enum CollType { C_U32, C_U64, C_I64 };
+enum CollOp { C_SUM, C_MIN, C_MAX };
+
+template <class T>
+void host_reduce(T* acc, const T* v, size_t n, CollOp op) {
+    for (size_t i = 0; i < n; ++i)
+        acc[i] = op == C_SUM ? (T)(acc[i] + v[i]) : op == C_MIN ? std::min(acc[i], v[i]) : std::max(acc[i], v[i]);
+}
+
+// Allreduce of `count` elements from device `send` into device `recv` (may alias), over NCCL or the
+// in-process group. Asynchronous on the ctx stream for NCCL; synchronous for the group.
+hht_status coll_allreduce(hht_ctx* x, const void* send, void* recv, size_t count, CollType t, CollOp op) {
+    if (!multi(x) || count == 0) return HHT_OK;
+    if (x->comm) {
+        const ncclDataType_t dt = t == C_U32 ? ncclUint32 : t == C_U64 ? ncclUint64 : ncclInt64;
+        const ncclRedOp_t ro = op == C_SUM ? ncclSum : op == C_MIN ? ncclMin : ncclMax;
+        CKN(ncclAllReduce(send, recv, count, dt, ro, x->comm, x->st));
+        return HHT_OK;
+    }
+    hht_group* g = x->group;
+    const size_t es = t == C_U32 ? 4 : 8, bytes = count * es;
+    const int r = x->opts.rank;
+    g->slot[r].resize(bytes);
+    CK(cudaMemcpyAsync(g->slot[r].data(), send, bytes, cudaMemcpyDeviceToHost, x->st));
+    CK(cudaStreamSynchronize(x->st));
+    g->barrier();                                  // every rank's contribution is staged
+    std::vector<uint8_t> acc(g->slot[0]);
+    for (int k = 1; k < g->world; ++k) {
+        if (g->slot[k].size() != bytes) return set_err(x, HHT_EMISMATCH, "group allreduce sizes differ");
+        if (t == C_U32) host_reduce((uint32_t*)acc.data(), (const uint32_t*)g->slot[k].data(), count, op);
+        else if (t == C_U64) host_reduce((uint64_t*)acc.data(), (const uint64_t*)g->slot[k].data(), count, op);
+        else host_reduce((int64_t*)acc.data(), (const int64_t*)g->slot[k].data(), count, op);
+    }
+    g->barrier();                                  // every rank has read every slot
+    CK(cudaMemcpyAsync(recv, acc.data(), bytes, cudaMemcpyHostToDevice, x->st));
+    CK(cudaStreamSynchronize(x->st));
+    return HHT_OK;
+}
+
 hht_status allreduce_sum_u32(hht_ctx* x, uint32_t* buf, size_t count) {
-    if (!x->comm || count == 0) return HHT_OK;
+    if (!multi(x) || count == 0) return HHT_OK;
     const int id = prof_begin(x, 7, count * 4);
-    CKN(ncclAllReduce(buf, buf, count, ncclUint32, ncclSum, x->comm, x->st));
+    TRY(coll_allreduce(x, buf, buf, count, C_U32, C_SUM));
     prof_end(x, id);
     return HHT_OK;
 }
@@ -401,10 +469,9 @@ hht_status choose_range(hht_ctx* x, int lc, uint32_t q0, uint64_t cap_entries, b
                     (const uint32_t*)P.len.p, lc == 1, (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->range_m,
                     x->st));
     prof_end(x, id);
-    if (x->comm && !all) {
+    if (multi(x) && !all) {
         // min over ranks of the proposed end, then recompute with the agreed end
-        CKN(ncclAllReduce((const char*)x->rng.p + offsetof(RangeInfo, q1), (char*)x->vtmp.p, 1, ncclUint64,
-                          ncclMin, x->comm, x->st));
+        TRY(coll_allreduce(x, (const char*)x->rng.p + offsetof(RangeInfo, q1), x->vtmp.p, 1, C_U64, C_MIN));
         CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)x->vtmp.p, 2, x->st));
         TRY(sync(x));
         const uint64_t q1 = read_mapped(x->misc_h);
@@ -589,7 +656,7 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         TRY(run_pass(x, MODE_WRITE, a, ri.pairs, entries));
         x->stat.ranges += 1;
         const uint32_t* VL = (const uint32_t*)C.votes.p;
-        if (x->comm) {
+        if (multi(x)) {
             TRY(ensure(x, C.votes_local, 16ull * nq));
             CK(cudaMemcpyAsync(C.votes_local.p, C.votes.p, 16ull * nq, cudaMemcpyDeviceToDevice, x->st));
             VL = (const uint32_t*)C.votes_local.p;
@@ -676,21 +743,21 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
                 if (x->opts.halves & h) x->tree_half[t++] = (uint8_t)h;
     }
     std::vector<int64_t> global_n = local_n;
-    if (x->comm) {
+    if (multi(x)) {
         // argument agreement: min and max of (N, D, T, halves, B) must coincide
         int64_t prm[5] = {N, D, T, (int64_t)x->opts.halves, B};
         TRY(ensure(x, x->vtmp, std::max<size_t>(8 * 10, 8 * (size_t)B)));
         CK(cudaMemcpyAsync(x->vtmp.p, prm, sizeof prm, cudaMemcpyHostToDevice, x->st));
         CK(cudaMemcpyAsync((char*)x->vtmp.p + 40, prm, sizeof prm, cudaMemcpyHostToDevice, x->st));
-        CKN(ncclAllReduce(x->vtmp.p, x->vtmp.p, 5, ncclInt64, ncclMin, x->comm, x->st));
-        CKN(ncclAllReduce((char*)x->vtmp.p + 40, (char*)x->vtmp.p + 40, 5, ncclInt64, ncclMax, x->comm, x->st));
+        TRY(coll_allreduce(x, x->vtmp.p, x->vtmp.p, 5, C_I64, C_MIN));
+        TRY(coll_allreduce(x, (char*)x->vtmp.p + 40, (char*)x->vtmp.p + 40, 5, C_I64, C_MAX));
         int64_t got[10];
         CK(cudaMemcpyAsync(got, x->vtmp.p, sizeof got, cudaMemcpyDeviceToHost, x->st));
         TRY(sync(x));
         for (int i = 0; i < 5; ++i)
             if (got[i] != got[5 + i]) return set_err(x, HHT_EMISMATCH, "ranks disagree on (N, depth, threshold, halves, images)");
         CK(cudaMemcpyAsync(x->vtmp.p, local_n.data(), 8 * (size_t)B, cudaMemcpyHostToDevice, x->st));
-        CKN(ncclAllReduce(x->vtmp.p, x->vtmp.p, B, ncclInt64, ncclSum, x->comm, x->st));
+        TRY(coll_allreduce(x, x->vtmp.p, x->vtmp.p, B, C_I64, C_SUM));
         CK(cudaMemcpyAsync(global_n.data(), x->vtmp.p, 8 * (size_t)B, cudaMemcpyDeviceToHost, x->st));
         TRY(sync(x));
     }
@@ -716,8 +783,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         CK(launch_stage(dev_pts, (uint64_t)n, N, (uint32_t*)x->packed.p, (uint32_t*)x->errflag.p, x->st));
         prof_end(x, id);
     }
-    if (x->comm)
-        CKN(ncclAllReduce(x->errflag.p, x->errflag.p, 1, ncclUint32, ncclMax, x->comm, x->st));
+    TRY(coll_allreduce(x, x->errflag.p, x->errflag.p, 1, C_U32, C_MAX));
     CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)x->errflag.p, 1, x->st));
     TRY(sync(x));
     if ((uint32_t)read_mapped(x->misc_h)) return set_err(x, HHT_ERANGE, "a point lies outside [0, N)^2");
@@ -801,7 +867,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         a.nf_rbase = 0;
         TRY(run_pass(x, MODE_COUNT, a, pairs0, 0));
         const uint32_t* VL = (const uint32_t*)L0.votes.p;
-        if (x->comm) {
+        if (multi(x)) {
             TRY(ensure(x, L0.votes_local, 16ull * F0));
             CK(cudaMemcpyAsync(L0.votes_local.p, L0.votes.p, 16ull * F0, cudaMemcpyDeviceToDevice, x->st));
             VL = (const uint32_t*)L0.votes_local.p;
@@ -907,6 +973,18 @@ hht_status hht_default_opts(hht_opts* o) {
     return HHT_OK;
 }
 
+hht_status hht_group_create(hht_group** out, int32_t world) {
+    if (!out || world < 1) return HHT_EINVAL;
+    hht_group* g = new (std::nothrow) hht_group();
+    if (!g) return HHT_ENOMEM;
+    g->world = world;
+    g->slot.resize(world);
+    *out = g;
+    return HHT_OK;
+}
+
+void hht_group_destroy(hht_group* g) { delete g; }
+
 hht_status hht_nccl_unique_id(void* out, size_t cap) {
     if (!out || cap < sizeof(ncclUniqueId)) return HHT_EINVAL;
     ncclUniqueId id;
@@ -921,7 +999,8 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     hht_opts o;
     if (opts) o = *opts; else hht_default_opts(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return HHT_EINVAL;
-    if (o.world > 1 && !o.nccl_id) return HHT_EINVAL;
+    if (o.world > 1 && !o.nccl_id && !o.group) return HHT_EINVAL;
+    if (o.group && (o.nccl_id || o.group->world != o.world)) return HHT_EINVAL;
     if (o.halves == 0 || (o.halves & ~3u)) return HHT_EINVAL;
     if (!(o.tail_depth == 0 || (o.tail_depth >= 3 && o.tail_depth <= 5))) return HHT_EINVAL;
     hht_ctx* x = new (std::nothrow) hht_ctx();
@@ -975,6 +1054,7 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
         cudaHostGetDevicePointer((void**)&x->range_m, x->range_h, 0) != cudaSuccess ||
         cudaHostGetDevicePointer((void**)&x->misc_m, x->misc_h, 0) != cudaSuccess)
         return fail(HHT_ECUDA);
+    x->group = o.group;
     if (o.nccl_id) {   // world > 1, or world == 1 with an id: every collective runs (1-rank comm)
         ncclUniqueId id;
         memcpy(&id, o.nccl_id, sizeof id);

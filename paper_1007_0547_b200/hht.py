@@ -28,7 +28,7 @@ STATUS = {0: "HHT_OK", 1: "HHT_EINVAL", 2: "HHT_ERANGE", 3: "HHT_EOVERFLOW", 4: 
 EXPORTS = ["hht_default_opts", "hht_create", "hht_nccl_unique_id", "hht_detect", "hht_detect_batch",
            "hht_result_leaves", "hht_result_level", "hht_result_stats", "hht_result_profile",
            "hht_result_launches", "hht_timer_begin", "hht_timer_end", "hht_last_error", "hht_status_str",
-           "hht_destroy", "hht_version", "hht_set_leaf_sink"]
+           "hht_destroy", "hht_version", "hht_set_leaf_sink", "hht_group_create", "hht_group_destroy"]
 
 PROFILE_CLASSES = ["stage", "count", "write", "tail", "split", "gather", "other", "allreduce"]
 
@@ -45,7 +45,7 @@ class Opts(C.Structure):
                 ("record_levels", C.c_uint32), ("force_int64", C.c_uint32), ("profile", C.c_uint32),
                 ("tail_depth", C.c_uint32), ("prefetch", C.c_uint32), ("variant", C.c_uint32),
                 ("mem_budget", C.c_size_t),
-                ("nccl_id", C.c_void_p)]
+                ("nccl_id", C.c_void_p), ("group", C.c_void_p)]
 
 
 class Leaf(C.Structure):
@@ -92,6 +92,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hht_result_level": ([p, i32, u32, i32, p, i64, p], C.c_int),
         "hht_result_stats": ([p, p], C.c_int),
         "hht_set_leaf_sink": ([p, p, i64], C.c_int),
+        "hht_group_create": ([p, i32], C.c_int),
+        "hht_group_destroy": ([p], None),
         "hht_result_profile": ([p, p], C.c_int),
         "hht_result_launches": ([p, p, i64, p], C.c_int),
         "hht_timer_begin": ([p], C.c_int),
@@ -148,13 +150,31 @@ def _as_points(points):
     return a.ctypes.data, a.shape[0], a, False
 
 
+class Group:
+    """In-process collective group of `world` ranks (include/hht.h hht_group_create): W contexts
+    driven from W host threads run the multi-rank path with host-staged allreduces (tests)."""
+
+    def __init__(self, world: int):
+        self._lib = load()
+        self._g = C.c_void_p()
+        st = self._lib.hht_group_create(C.byref(self._g), world)
+        if st:
+            raise HHTError(st, "hht_group_create failed")
+        self.world = world
+
+    def close(self):
+        if self._g:
+            self._lib.hht_group_destroy(self._g)
+            self._g = None
+
+
 class HHT:
     """One libhht context (one device, one rank)."""
 
     def __init__(self, device: int = 0, halves: int = ALPHA | BETA, record_levels: bool = True,
                  force_int64: bool = False, profile: bool = False, mem_budget: int = 0,
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, tail_depth: int = 0,
-                 prefetch: int = 0, variant: int = 0):
+                 prefetch: int = 0, variant: int = 0, group: Optional["Group"] = None):
         self._lib = load()
         o = Opts()
         self._lib.hht_default_opts(C.byref(o))
@@ -165,6 +185,8 @@ class HHT:
         o.prefetch = prefetch
         o.variant = variant
         self._id = None
+        if group is not None:
+            o.group = group._g
         if nccl_id is not None:
             self._id = C.create_string_buffer(bytes(nccl_id), 128)
             o.nccl_id = C.cast(self._id, C.c_void_p)

@@ -1,0 +1,91 @@
+"""The multi-rank path on one GPU: W contexts in one process, one host thread each, joined by an
+in-process collective group (include/hht.h hht_group_create). Every collective the NCCL path makes
+(argument agreement, per-image point counts, error flag, range agreement, per-level vote
+allreduce, tail-grid allreduce) runs in the same order through a host-staged allreduce, so the
+logic that differs between ranks — local candidate lists and list lengths against global votes,
+agreed depth-first ranges — is checked bit-exactly against the oracle on the whole image. Points
+are sharded contiguously as bench.py shards them (paper_1007_0547_b200/dist.py)."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1007_0547_b200 import hht, synth
+from tests.hht_compare import compare_all
+
+pytestmark = pytest.mark.gpu
+
+AB = hht.ALPHA | hht.BETA
+
+
+def _run_ranks(pts, N, D, T, halves, world, dev, **kw):
+    import torch
+    g = hht.Group(world)
+    hs = [hht.HHT(halves=halves, rank=r, world=world, group=g, **kw) for r in range(world)]
+    errs = [None] * world
+    bounds = [synth.shard(pts.shape[0], r, world) for r in range(world)]
+    shards = [torch.from_numpy(np.ascontiguousarray(pts[lo:hi])).to(dev) for lo, hi in bounds]
+
+    def work(r):
+        try:
+            hs[r].detect(shards[r], N, D, T)
+        except Exception as e:  # noqa: BLE001
+            errs[r] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    return hs, g, errs
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("kw", [{}, {"tail_depth": 4}, {"tail_depth": 3}, {"mem_budget": 256 << 10},
+                                {"variant": 1}])
+def test_multirank_c2(world, kw, cuda_device):
+    cfg = synth.CONFIGS[2]
+    pts, _ = synth.config_image(2)
+    ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves, variant=kw.get("variant", 0))
+    hs, g, errs = _run_ranks(pts, cfg.N, cfg.D, cfg.T, cfg.halves, world, cuda_device, **kw)
+    assert errs == [None] * world, errs
+    pairs = 0
+    for h in hs:   # every rank holds the global result
+        compare_all(h, ref, cfg.halves, cfg.D)
+        st = h.stats()
+        assert (st["tests"], st["votes"], st["leaves"]) == (ref.tests, ref.votes, ref.leaves.shape[0])
+        pairs += st["pairs"]
+    if "mem_budget" in kw:
+        assert min(h.stats()["ranges"] for h in hs) > 4 * cfg.D
+    for h in hs:
+        h.close()
+    g.close()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_multirank_random(seed, cuda_device):
+    rng = np.random.default_rng(900 + seed)
+    N = int(rng.choice([16, 64, 128, 200]))
+    D = int(rng.integers(2, 9))
+    T = int(rng.choice([2, 5, 12]))
+    world = int(rng.integers(2, 5))
+    pts = synth.random_scene(4000 + seed, N, max_lines=4, max_noise=int(rng.choice([100, 1500])))
+    ref = oracle.detect(pts, N, D, T, AB)
+    hs, g, errs = _run_ranks(pts, N, D, T, AB, world, cuda_device)
+    assert errs == [None] * world, errs
+    for h in hs:
+        compare_all(h, ref, AB, D)
+        h.close()
+    g.close()
+
+
+def test_multirank_error_flag_is_collective(cuda_device):
+    """One rank holds an out-of-range point: every rank fails with HHT_ERANGE."""
+    pts = synth.random_scene(7, 64, max_noise=200).copy()
+    pts[-1] = (64, 3)                    # lands on the last rank
+    hs, g, errs = _run_ranks(pts, 64, 6, 5, AB, 2, cuda_device)
+    assert all(isinstance(e, hht.HHTError) and e.name == "HHT_ERANGE" for e in errs), errs
+    for h in hs:
+        h.close()
+    g.close()
