@@ -167,6 +167,28 @@ hht_status hht_detect_batch(hht_ctx* ctx, const int32_t* points, const int64_t* 
 
 /* Detected lines of `image` (ALPHA tree first, each in the paper's depth-first NE,NW,SW,SE order);
  * image = -1 returns every image's lines in image order. */
+/* Per-tree point sets (each point in ONE tree, e.g. the edge front end's ALPHA/BETA partition,
+ * PAPER.md:67): tree t = image t / H + half index t % H (H = number of halves in opts.halves,
+ * ALPHA first) gets the int2 (x, y) points [tree_offsets[t], tree_offsets[t+1]) of `points`
+ * (device or host, same conventions as hht_detect_batch); tree_offsets is host int64 [B*H + 1].
+ * Results are read with the same getters. Multi-rank: each rank passes its local points per tree. */
+hht_status hht_detect_trees(hht_ctx* ctx, const int32_t* points, const int64_t* tree_offsets, int32_t B,
+                            int32_t N, int32_t depth, int64_t threshold);
+
+/* Edge front end + detection of one square grayscale image (readings
+ * DESIGN.md R18-R21 after SPEC.md:104-131): img is uint8 [N][N] row-major, row 0 = top (device or
+ * host). Interior pixels get the 3x3 Sobel gradient in geometric coordinates (x = column,
+ * y = N-1-row); a pixel is an edge point iff |gx| + |gy| >= mag_threshold > 0; it goes to ALPHA iff
+ * |gx| <= |gy|, else to BETA; then the ALPHA tree is run on the ALPHA points and the BETA tree on
+ * the BETA points (hht_detect_trees). 3 <= N <= 46340; one rank only. */
+hht_status hht_detect_image(hht_ctx* ctx, const uint8_t* img, int32_t N, int32_t mag_threshold, int32_t depth,
+                            int64_t threshold);
+
+/* The edge points of the last hht_detect_image as host int2 (x, y): the ALPHA set then the BETA set
+ * (only the halves in opts.halves), each in raster order. out = NULL: counts only. Invalidated by
+ * the next detect call. HHT_EINVAL if cap < n_alpha + n_beta; HHT_ESTATE without such a result. */
+hht_status hht_result_edges(hht_ctx* ctx, int32_t* out, int64_t cap, int64_t* n_alpha, int64_t* n_beta);
+
 hht_status hht_result_leaves(hht_ctx* ctx, int32_t image, hht_leaf* out, int64_t cap, int64_t* count);
 
 /* Visited regions of tree (image, half) at `level` in depth-first quad order, as uint32 triplets

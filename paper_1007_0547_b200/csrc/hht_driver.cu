@@ -94,7 +94,7 @@ struct hht_ctx {
     hht_opts opts{};
     int sms = 148;
     cudaStream_t st = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr, tb0 = nullptr, tb1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, tb0 = nullptr, tb1 = nullptr, ee0 = nullptr, ee1 = nullptr;
     ncclComm_t comm = nullptr;
     hht_group* group = nullptr;        // borrowed (opts.group)
     std::string err;
@@ -117,6 +117,9 @@ struct hht_ctx {
 
     Buf stage_in, packed, errflag, beta, stats, tiles, tilectr, totals, rng, bounds, vtmp, dense, gv, leafrows;
     Buf fusedctr;                    // k_fused work counter (u32) + rastered-pair counter (u64)
+    Buf img, edgeB, edgetiles;       // edge front end: staged image, BETA points, look-back words
+    bool edges_valid = false;        // x->packed holds the last hht_detect_image's edge points
+    int64_t edge_na = 0, edge_nb = 0;
     // leaf sink (hht_set_leaf_sink): double-buffered row staging, copied on its own stream
     hht_leaf* sink = nullptr;
     int64_t sink_cap = 0;
@@ -690,15 +693,20 @@ hht_status check_args(hht_ctx* x, const int32_t* points, int64_t n_total, int32_
 }
 
 hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets, int32_t B, int32_t N,
-                       int32_t D, int64_t T) {
+                       int32_t D, int64_t T, const int64_t* tree_offsets = nullptr, bool prepacked = false) {
+    // offsets: per image [B+1] (every point enters each of the image's trees); tree_offsets: per
+    // tree [B*H+1] (tree t = image t/H, halves in ALPHA, BETA order; each point in one tree)
     if (!x) return HHT_EINVAL;
     x->err.clear();
     x->have = false;
-    if (B < 1 || !offsets) return set_err(x, HHT_EINVAL, "need B >= 1 images and host offsets");
-    if (offsets[0] != 0) return set_err(x, HHT_EINVAL, "offsets[0] must be 0");
-    for (int b = 0; b < B; ++b)
-        if (offsets[b + 1] < offsets[b]) return set_err(x, HHT_EINVAL, "offsets must be non-decreasing");
-    const int64_t n = offsets[B];
+    const int Hh = (x->opts.halves & HHT_ALPHA ? 1 : 0) + (x->opts.halves & HHT_BETA ? 1 : 0);
+    const int64_t* segs = tree_offsets ? tree_offsets : offsets;
+    const int nseg = tree_offsets ? B * Hh : B;
+    if (B < 1 || !segs) return set_err(x, HHT_EINVAL, "need B >= 1 images and host offsets");
+    if (segs[0] != 0) return set_err(x, HHT_EINVAL, "offsets[0] must be 0");
+    for (int b = 0; b < nseg; ++b)
+        if (segs[b + 1] < segs[b]) return set_err(x, HHT_EINVAL, "offsets must be non-decreasing");
+    const int64_t n = segs[nseg];
     TRY(check_args(x, points, n, N, D, T));
 
     x->N = N;
@@ -734,8 +742,8 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
 
     // trees and per-tree point counts (global over ranks)
     x->tree_half.assign(x->ntrees, 0);
-    std::vector<int64_t> local_n(B);
-    for (int b = 0; b < B; ++b) local_n[b] = offsets[b + 1] - offsets[b];
+    std::vector<int64_t> local_n(nseg);
+    for (int b = 0; b < nseg; ++b) local_n[b] = segs[b + 1] - segs[b];
     {
         int t = 0;
         for (int b = 0; b < B; ++b)
@@ -744,30 +752,35 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     }
     std::vector<int64_t> global_n = local_n;
     if (multi(x)) {
-        // argument agreement: min and max of (N, D, T, halves, B) must coincide
-        int64_t prm[5] = {N, D, T, (int64_t)x->opts.halves, B};
-        TRY(ensure(x, x->vtmp, std::max<size_t>(8 * 10, 8 * (size_t)B)));
+        // argument agreement: min and max of (N, D, T, halves, B, per-tree mode) must coincide
+        int64_t prm[6] = {N, D, T, (int64_t)x->opts.halves, B, tree_offsets ? 1 : 0};
+        TRY(ensure(x, x->vtmp, std::max<size_t>(8 * 12, 8 * (size_t)nseg)));
         CK(cudaMemcpyAsync(x->vtmp.p, prm, sizeof prm, cudaMemcpyHostToDevice, x->st));
-        CK(cudaMemcpyAsync((char*)x->vtmp.p + 40, prm, sizeof prm, cudaMemcpyHostToDevice, x->st));
-        TRY(coll_allreduce(x, x->vtmp.p, x->vtmp.p, 5, C_I64, C_MIN));
-        TRY(coll_allreduce(x, (char*)x->vtmp.p + 40, (char*)x->vtmp.p + 40, 5, C_I64, C_MAX));
-        int64_t got[10];
+        CK(cudaMemcpyAsync((char*)x->vtmp.p + 48, prm, sizeof prm, cudaMemcpyHostToDevice, x->st));
+        TRY(coll_allreduce(x, x->vtmp.p, x->vtmp.p, 6, C_I64, C_MIN));
+        TRY(coll_allreduce(x, (char*)x->vtmp.p + 48, (char*)x->vtmp.p + 48, 6, C_I64, C_MAX));
+        int64_t got[12];
         CK(cudaMemcpyAsync(got, x->vtmp.p, sizeof got, cudaMemcpyDeviceToHost, x->st));
         TRY(sync(x));
-        for (int i = 0; i < 5; ++i)
-            if (got[i] != got[5 + i]) return set_err(x, HHT_EMISMATCH, "ranks disagree on (N, depth, threshold, halves, images)");
-        CK(cudaMemcpyAsync(x->vtmp.p, local_n.data(), 8 * (size_t)B, cudaMemcpyHostToDevice, x->st));
-        TRY(coll_allreduce(x, x->vtmp.p, x->vtmp.p, B, C_I64, C_SUM));
-        CK(cudaMemcpyAsync(global_n.data(), x->vtmp.p, 8 * (size_t)B, cudaMemcpyDeviceToHost, x->st));
+        for (int i = 0; i < 6; ++i)
+            if (got[i] != got[6 + i]) return set_err(x, HHT_EMISMATCH, "ranks disagree on (N, depth, threshold, halves, images)");
+        CK(cudaMemcpyAsync(x->vtmp.p, local_n.data(), 8 * (size_t)nseg, cudaMemcpyHostToDevice, x->st));
+        TRY(coll_allreduce(x, x->vtmp.p, x->vtmp.p, nseg, C_I64, C_SUM));
+        CK(cudaMemcpyAsync(global_n.data(), x->vtmp.p, 8 * (size_t)nseg, cudaMemcpyDeviceToHost, x->st));
         TRY(sync(x));
     }
     x->tree_E.assign(x->ntrees, 0);
-    for (int t = 0; t < x->ntrees; ++t) x->tree_E[t] = global_n[t / x->H];
+    for (int t = 0; t < x->ntrees; ++t) x->tree_E[t] = global_n[tree_offsets ? t : t / x->H];
 
     // K0: stage + validate (reject before any traversal; collective over ranks)
-    TRY(ensure(x, x->packed, std::max<int64_t>(n, 1) * 4));
+    if (!prepacked) x->edges_valid = false;
+    if (prepacked) {
+        if (x->packed.cap < (size_t)n * 4) return set_err(x, HHT_EINVAL, "internal: prepacked points exceed the buffer");
+    } else {
+        TRY(ensure(x, x->packed, std::max<int64_t>(n, 1) * 4));
+    }
     CK(cudaMemsetAsync(x->errflag.p, 0, 4, x->st));
-    if (n > 0) {
+    if (n > 0 && !prepacked) {   // prepacked: x->packed already holds in-range points (edge front end)
         const int32_t* dev_pts = points;
         cudaPointerAttributes pa{};
         cudaError_t e = cudaPointerGetAttributes(&pa, points);
@@ -812,10 +825,10 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
             root_tests += 4 * E;
             h_tree.push_back(t);
             h_zero.push_back(0);
-            const uint64_t ln = (uint64_t)local_n[b];
+            const uint64_t ln = (uint64_t)local_n[tree_offsets ? t : b];
             h_len.push_back((uint32_t)ln);
             h_votes.push_back((uint32_t)E);
-            h_off.push_back((uint64_t)offsets[b]);
+            h_off.push_back((uint64_t)segs[tree_offsets ? t : b]);
             h_choff.push_back(chunks);
             chunks += (ln + kChunk - 1) / kChunk;
             pairs0 += ln;
@@ -1021,7 +1034,8 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
             cudaEventCreateWithFlags(&x->ev_copy[k], cudaEventDisableTiming) != cudaSuccess)
             return fail(HHT_ECUDA);
     if (cudaEventCreate(&x->ev0) != cudaSuccess || cudaEventCreate(&x->ev1) != cudaSuccess ||
-        cudaEventCreate(&x->tb0) != cudaSuccess || cudaEventCreate(&x->tb1) != cudaSuccess)
+        cudaEventCreate(&x->tb0) != cudaSuccess || cudaEventCreate(&x->tb1) != cudaSuccess ||
+        cudaEventCreate(&x->ee0) != cudaSuccess || cudaEventCreate(&x->ee1) != cudaSuccess)
         return fail(HHT_ECUDA);
     // keep freed pool memory cached across calls
     cudaMemPool_t pool;
@@ -1076,6 +1090,96 @@ hht_status hht_detect_batch(hht_ctx* ctx, const int32_t* points, const int64_t* 
                             int32_t depth, int64_t threshold) {
     if (!ctx) return HHT_EINVAL;
     return detect_impl(ctx, points, offsets, B, N, depth, threshold);
+}
+
+hht_status hht_detect_trees(hht_ctx* ctx, const int32_t* points, const int64_t* tree_offsets, int32_t B, int32_t N,
+                            int32_t depth, int64_t threshold) {
+    if (!ctx) return HHT_EINVAL;
+    if (!tree_offsets) return set_err(ctx, HHT_EINVAL, "tree_offsets is NULL");
+    return detect_impl(ctx, points, nullptr, B, N, depth, threshold, tree_offsets);
+}
+
+hht_status hht_detect_image(hht_ctx* x, const uint8_t* img, int32_t N, int32_t mag_threshold, int32_t depth,
+                            int64_t threshold) {
+    if (!x) return HHT_EINVAL;
+    x->err.clear();
+    x->have = false;
+    x->edges_valid = false;
+    if (!img) return set_err(x, HHT_EINVAL, "img is NULL");
+    if (N < 3 || N > 46340) return set_err(x, HHT_EINVAL, "image side must be in [3, 46340]");
+    if (mag_threshold < 0) return set_err(x, HHT_EINVAL, "mag_threshold < 0");
+    if (multi(x)) return set_err(x, HHT_EINVAL, "hht_detect_image runs on one rank (shard with hht_detect_trees)");
+    CK(cudaSetDevice(x->opts.device));
+    const uint64_t npix = (uint64_t)N * N;
+    const uint8_t* dimg = img;
+    cudaPointerAttributes pa{};
+    cudaError_t e = cudaPointerGetAttributes(&pa, img);
+    if (e != cudaSuccess) cudaGetLastError();
+    if (!(e == cudaSuccess && (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged))) {
+        TRY(ensure(x, x->img, npix));
+        CK(cudaMemcpyAsync(x->img.p, img, npix, cudaMemcpyHostToDevice, x->st));
+        dimg = (const uint8_t*)x->img.p;
+    }
+    const uint32_t ntiles = (uint32_t)((npix + kEdgeTile - 1) / kEdgeTile);
+    TRY(ensure(x, x->packed, npix * 4));
+    TRY(ensure(x, x->edgeB, npix * 4));
+    TRY(ensure(x, x->edgetiles, (size_t)ntiles * 8 + 256));
+    CK(cudaMemsetAsync(x->edgetiles.p, 0, (size_t)ntiles * 8 + 256, x->st));
+    EdgeArgs a{};
+    a.img = dimg;
+    a.W = a.H = N;
+    a.thr = mag_threshold;
+    a.outA = (uint32_t*)x->packed.p;
+    a.outB = (uint32_t*)x->edgeB.p;
+    a.tiles = (unsigned long long*)((char*)x->edgetiles.p + 256);
+    a.tile_ctr = (uint32_t*)x->edgetiles.p;
+    a.ntiles = ntiles;
+    a.totals = x->misc_m;
+    CK(cudaEventRecord(x->ee0, x->st));
+    CK(launch_edges(a, x->st));
+    CK(cudaEventRecord(x->ee1, x->st));
+    TRY(sync(x));
+    float edge_ms = 0;
+    CK(cudaEventElapsedTime(&edge_ms, x->ee0, x->ee1));
+    const int64_t na = (int64_t)x->misc_h[0], nb = (int64_t)x->misc_h[1];
+    // the trees' point sets, contiguous in x->packed: ALPHA points, then BETA points
+    const bool wa = x->opts.halves & HHT_ALPHA, wb = x->opts.halves & HHT_BETA;
+    int64_t toff[3] = {0, 0, 0};
+    int k = 0;
+    if (wa) toff[++k] = na;
+    if (wb) {
+        CK(cudaMemcpyAsync((uint32_t*)x->packed.p + (wa ? na : 0), x->edgeB.p, (size_t)nb * 4,
+                           cudaMemcpyDeviceToDevice, x->st));
+        toff[k + 1] = toff[k] + nb;
+    }
+    TRY(detect_impl(x, (const int32_t*)x->packed.p, nullptr, 1, N, depth, threshold, toff, true));
+    x->edge_na = wa ? na : 0;
+    x->edge_nb = wb ? nb : 0;
+    x->edges_valid = true;
+    if (x->opts.profile) {            // the detection reset the profile: add the edge kernel (class 0)
+        x->prof.launches[0] += 1;
+        x->prof.ms[0] += edge_ms;
+        x->prof.bytes[0] += npix + 4ull * (uint64_t)(na + nb);
+    }
+    return HHT_OK;
+}
+
+hht_status hht_result_edges(hht_ctx* x, int32_t* out, int64_t cap, int64_t* n_alpha, int64_t* n_beta) {
+    if (!x || !n_alpha || !n_beta) return HHT_EINVAL;
+    if (!x->edges_valid) return set_err(x, HHT_ESTATE, "no hht_detect_image result");
+    *n_alpha = x->edge_na;
+    *n_beta = x->edge_nb;
+    const int64_t n = x->edge_na + x->edge_nb;
+    if (!out) return HHT_OK;
+    if (cap < n) return set_err(x, HHT_EINVAL, "cap < %lld edge points", (long long)n);
+    std::vector<uint32_t> h((size_t)n);
+    if (n) CK(cudaMemcpyAsync(h.data(), x->packed.p, (size_t)n * 4, cudaMemcpyDeviceToHost, x->st));
+    TRY(sync(x));
+    for (int64_t i = 0; i < n; ++i) {
+        out[2 * i] = (int32_t)(h[i] >> 16);
+        out[2 * i + 1] = (int32_t)(h[i] & 0xFFFFu);
+    }
+    return HHT_OK;
 }
 
 hht_status hht_result_leaves(hht_ctx* x, int32_t image, hht_leaf* out, int64_t cap, int64_t* count) {
@@ -1220,7 +1324,8 @@ void hht_destroy(hht_ctx* x) {
     for (auto& g : x->rec) fr(g.b);
     fr(x->leaves.b);
     for (Buf* b : {&x->stage_in, &x->packed, &x->errflag, &x->beta, &x->stats, &x->tiles, &x->tilectr, &x->totals,
-                   &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv, &x->leafrows, &x->fusedctr})
+                   &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv, &x->leafrows, &x->fusedctr, &x->img,
+                   &x->edgeB, &x->edgetiles})
         fr(*b);
     if (x->totals_h) cudaFreeHost(x->totals_h);
     if (x->range_h) cudaFreeHost(x->range_h);
@@ -1229,7 +1334,7 @@ void hht_destroy(hht_ctx* x) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
     }
-    for (cudaEvent_t e : {x->ev0, x->ev1, x->tb0, x->tb1})
+    for (cudaEvent_t e : {x->ev0, x->ev1, x->tb0, x->tb1, x->ee0, x->ee1})
         if (e) cudaEventDestroy(e);
     if (x->comm) ncclCommDestroy(x->comm);
     if (x->st) cudaStreamDestroy(x->st);

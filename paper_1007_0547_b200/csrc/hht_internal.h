@@ -161,6 +161,19 @@ cudaError_t launch_gather(const uint32_t* dense, uint32_t anc_base, const uint32
 int tail16_blocks_per_sm(bool int64, bool pref);
 cudaError_t launch_tail16(bool int64, bool pref, const PassArgs& a, int grid, cudaStream_t st);
 int fused_blocks_per_sm(bool int64);
+// Edge front end (k_edges): Sobel + L1 threshold + ALPHA/BETA partition, raster-order compaction.
+struct EdgeArgs {
+    const uint8_t* img;            // [H][W], row 0 = top
+    int W, H, thr;
+    uint32_t* outA;                // packed (x << 16 | y) ALPHA points, raster order
+    uint32_t* outB;                // BETA points
+    unsigned long long* tiles;     // [ntiles] look-back words (zeroed)
+    uint32_t* tile_ctr;            // zeroed
+    uint32_t ntiles;
+    uint64_t* totals;              // [2] (mapped host): ALPHA count, BETA count (written by the last tile)
+};
+constexpr int kEdgeTile = 4096;    // pixels per 256-thread tile (16 per lane, lane-interleaved)
+cudaError_t launch_edges(const EdgeArgs& a, cudaStream_t st);
 cudaError_t launch_fused(bool int64, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
                           int is_root, RangeInfo* info, uint64_t* chunk_bounds, RangeInfo* info_h, cudaStream_t st);

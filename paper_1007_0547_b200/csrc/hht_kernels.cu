@@ -894,6 +894,251 @@ cudaError_t launch_fused(bool int64, const PassArgs& a, int grid, cudaStream_t s
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Edge front end (§3 "Sobel's gradient operator is being
+// applied", readings DESIGN.md R18-R21 after SPEC.md:104-131): per interior pixel
+//   gx = sum_dy w(dy) (I(x+1, y+dy) - I(x-1, y+dy)),  gy = sum_dx w(dx) (I(x+dx, y+1) - I(x+dx, y-1))
+// (w = 1, 2, 1; geometric y = H-1-row), edge iff |gx| + |gy| >= thr > 0, ALPHA iff |gx| <= |gy|,
+// each set compacted in raster order. A tile of 256 threads covers 4096 consecutive pixels, lane l
+// of warp w taking pixels 512w + 32k + l (coalesced byte loads); ballots give in-order positions
+// within the warp, a block scan orders the warps, and a single-pass look-back over packed 64-bit
+// (status | ALPHA count | BETA count) words orders the tiles, so no second pass over the image.
+// ---------------------------------------------------------------------------------------------
+namespace {
+constexpr unsigned long long kEdgeAgg = 1ull << 62, kEdgeInc = 2ull << 62, kEdgeMask = (1ull << 31) - 1;
+__device__ __forceinline__ unsigned long long edge_word(unsigned long long st, uint32_t a, uint32_t b) {
+    return st | ((unsigned long long)a << 31) | (unsigned long long)b;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256) k_edges(const EdgeArgs A) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_wa[8], s_wb[8];
+    __shared__ uint32_t s_pa, s_pb;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(A.tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t npix = (uint64_t)A.W * A.H;
+    const uint64_t p0 = (uint64_t)tile * kEdgeTile + 512 * wid + lane;
+    // pixel k of this lane: p0 + 32k -> (r, c), stepped without divisions
+    uint32_t r = (uint32_t)(p0 / (uint64_t)A.W), c = (uint32_t)(p0 - (uint64_t)r * A.W);
+    uint32_t em = 0, am = 0;
+#pragma unroll 4
+    for (int k = 0; k < 16; ++k) {
+        const uint64_t p = p0 + 32 * k;
+        if (p < npix && A.thr > 0 && r >= 1 && r + 1 < (uint32_t)A.H && c >= 1 && c + 1 < (uint32_t)A.W) {
+            const uint8_t* m = A.img + (uint64_t)r * A.W + c;
+            const uint8_t* u = m - A.W;
+            const uint8_t* d = m + A.W;
+            const int ul = __ldg(u - 1), uc = __ldg(u), ur = __ldg(u + 1);
+            const int ml = __ldg(m - 1), mr = __ldg(m + 1);
+            const int dl = __ldg(d - 1), dc = __ldg(d), dr = __ldg(d + 1);
+            const int gx = (ur - ul) + 2 * (mr - ml) + (dr - dl);
+            const int gy = (ul + 2 * uc + ur) - (dl + 2 * dc + dr);   // row above = geometric y+1
+            const int ax = abs(gx), ay = abs(gy);
+            if (ax + ay >= A.thr) {
+                em |= 1u << k;
+                if (ax <= ay) am |= 1u << k;
+            }
+        }
+        c += 32;
+        while (c >= (uint32_t)A.W) { c -= A.W; ++r; }
+    }
+    // tile order: warp counts -> block scan -> look-back over tiles
+    const uint32_t wa = __reduce_add_sync(kFull, __popc(em & am)), wb = __reduce_add_sync(kFull, __popc(em & ~am));
+    if (lane == 0) { s_wa[wid] = wa; s_wb[wid] = wb; }
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t va = lane < 8 ? s_wa[lane] : 0, vb = lane < 8 ? s_wb[lane] : 0;
+        uint32_t ia = va, ib = vb;
+#pragma unroll
+        for (int dd = 1; dd < 8; dd <<= 1) {
+            const uint32_t ta = __shfl_up_sync(kFull, ia, dd), tb = __shfl_up_sync(kFull, ib, dd);
+            if (lane >= dd) { ia += ta; ib += tb; }
+        }
+        if (lane < 8) { s_wa[lane] = ia - va; s_wb[lane] = ib - vb; }
+        const uint32_t ta = __shfl_sync(kFull, ia, 7), tb = __shfl_sync(kFull, ib, 7);
+        using dev_u64w = cuda::atomic_ref<unsigned long long, cuda::thread_scope_device>;
+        uint32_t ea = 0, eb = 0;
+        if (tile == 0) {
+            if (lane == 0) dev_u64w(A.tiles[0]).store(edge_word(kEdgeInc, ta, tb), cuda::memory_order_relaxed);
+        } else {
+            if (lane == 0) dev_u64w(A.tiles[tile]).store(edge_word(kEdgeAgg, ta, tb), cuda::memory_order_relaxed);
+            int64_t pred = (int64_t)tile - 1;
+            while (true) {
+                const int64_t t = pred - lane;
+                unsigned long long wv = kEdgeInc;                 // before tile 0: inclusive zero
+                if (t >= 0) {
+                    do { wv = dev_u64w(A.tiles[t]).load(cuda::memory_order_relaxed); } while ((wv >> 62) == 0);
+                }
+                const uint32_t pm = __ballot_sync(kFull, (wv >> 62) == 2);
+                const int stop = pm ? __ffs(pm) - 1 : 31;
+                uint32_t xa = (uint32_t)((wv >> 31) & kEdgeMask), xb = (uint32_t)(wv & kEdgeMask);
+                if (lane > stop || t < 0) { xa = 0; xb = 0; }
+                ea += __reduce_add_sync(kFull, xa);
+                eb += __reduce_add_sync(kFull, xb);
+                if (pm) break;
+                pred -= 32;
+            }
+            if (lane == 0) dev_u64w(A.tiles[tile]).store(edge_word(kEdgeInc, ea + ta, eb + tb), cuda::memory_order_relaxed);
+        }
+        if (lane == 0) {
+            s_pa = ea;
+            s_pb = eb;
+            if (tile == A.ntiles - 1) { A.totals[0] = ea + ta; A.totals[1] = eb + tb; }
+        }
+    }
+    __syncthreads();
+    // in-order writes: ballot per k gives each edge pixel its rank within the warp's 32 pixels
+    const uint32_t lt = (1u << lane) - 1;
+    uint32_t pa = s_pa + s_wa[wid], pb = s_pb + s_wb[wid];
+    r = (uint32_t)(p0 / (uint64_t)A.W);
+    c = (uint32_t)(p0 - (uint64_t)r * A.W);
+#pragma unroll 4
+    for (int k = 0; k < 16; ++k) {
+        const bool e = (em >> k) & 1u, isa = e && ((am >> k) & 1u), isb = e && !((am >> k) & 1u);
+        const uint32_t ba = __ballot_sync(kFull, isa), bb = __ballot_sync(kFull, isb);
+        const uint32_t pt = (c << 16) | (uint32_t)(A.H - 1 - (int)r);
+        if (isa) A.outA[pa + __popc(ba & lt)] = pt;
+        if (isb) A.outB[pb + __popc(bb & lt)] = pt;
+        pa += __popc(ba);
+        pb += __popc(bb);
+        c += 32;
+        while (c >= (uint32_t)A.W) { c -= A.W; ++r; }
+    }
+}
+
+// Rows whose width is a multiple of 16 (every power-of-two image): thread t of tile g owns the 16
+// consecutive pixels 4096 g + 16 t of one row, read as one 16-byte vector per row (rows r-1, r, r+1)
+// plus two halo bytes, so raster order is thread order.
+__device__ __forceinline__ int byte_of(const uint4& v, int k) {
+    const uint32_t w = k < 4 ? v.x : k < 8 ? v.y : k < 12 ? v.z : v.w;
+    return (int)((w >> (8 * (k & 3))) & 0xFFu);
+}
+
+// Edge (em) and ALPHA (am) bit masks of the 16 pixels starting at raster index p; r, c0 set.
+__device__ __forceinline__ void edge_masks16(const EdgeArgs& A, uint64_t p, uint32_t& r, uint32_t& c0,
+                                             uint32_t& em, uint32_t& am) {
+    em = am = 0;
+    r = (uint32_t)(p / (uint64_t)A.W);
+    c0 = (uint32_t)(p - (uint64_t)r * A.W);
+    if (p >= (uint64_t)A.W * A.H || A.thr <= 0 || r < 1 || r + 1 >= (uint32_t)A.H) return;
+    const uint8_t* m = A.img + (uint64_t)r * A.W + c0;
+    uint4 rows[3];
+    int hl[3], hr[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {                 // j = 0: row above (geometric y+1), 1: this row, 2: below
+        const uint8_t* q = m + (j - 1) * (int64_t)A.W;
+        rows[j] = __ldg(reinterpret_cast<const uint4*>(q));
+        hl[j] = c0 > 0 ? __ldg(q - 1) : 0;
+        hr[j] = c0 + 16 < (uint32_t)A.W ? __ldg(q + 16) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint32_t c = c0 + k;
+        if (c >= 1 && c + 1 < (uint32_t)A.W) {
+            int v[3][3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                v[j][0] = k == 0 ? hl[j] : byte_of(rows[j], k - 1);
+                v[j][1] = byte_of(rows[j], k);
+                v[j][2] = k == 15 ? hr[j] : byte_of(rows[j], k + 1);
+            }
+            const int gx = (v[0][2] - v[0][0]) + 2 * (v[1][2] - v[1][0]) + (v[2][2] - v[2][0]);
+            const int gy = (v[0][0] + 2 * v[0][1] + v[0][2]) - (v[2][0] + 2 * v[2][1] + v[2][2]);
+            const int ax = abs(gx), ay = abs(gy);
+            if (ax + ay >= A.thr) {
+                em |= 1u << k;
+                if (ax <= ay) am |= 1u << k;
+            }
+        }
+    }
+}
+
+// Single pass: masks, block scan in thread (= raster) order, look-back over the tiles (as k_edges),
+// direct writes of each thread's points. Measured faster than both a smem-staged copy-out and a
+// reduce-then-scan pair of passes (the per-pixel arithmetic, not the compaction, is the cost).
+__global__ void __launch_bounds__(256) k_edges16(const EdgeArgs A) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_w[8];
+    __shared__ uint32_t s_pa, s_pb;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(A.tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    uint32_t r, c0, em, am;
+    edge_masks16(A, (uint64_t)tile * kEdgeTile + 16ull * tid, r, c0, em, am);
+    const uint32_t own = __popc(em & am) | (__popc(em & ~am) << 16);
+    uint32_t inc = own;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, inc, dd);
+        if (lane >= dd) inc += t;
+    }
+    if (lane == 31) s_w[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t vw = lane < 8 ? s_w[lane] : 0;
+        uint32_t iw = vw;
+#pragma unroll
+        for (int dd = 1; dd < 8; dd <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, iw, dd);
+            if (lane >= dd) iw += t;
+        }
+        if (lane < 8) s_w[lane] = iw - vw;
+        const uint32_t tot = __shfl_sync(kFull, iw, 7);
+        const uint32_t ta = tot & 0xFFFFu, tb = tot >> 16;
+        using dev_u64w = cuda::atomic_ref<unsigned long long, cuda::thread_scope_device>;
+        uint32_t ea = 0, eb = 0;
+        if (tile == 0) {
+            if (lane == 0) dev_u64w(A.tiles[0]).store(edge_word(kEdgeInc, ta, tb), cuda::memory_order_relaxed);
+        } else {
+            if (lane == 0) dev_u64w(A.tiles[tile]).store(edge_word(kEdgeAgg, ta, tb), cuda::memory_order_relaxed);
+            int64_t pred = (int64_t)tile - 1;
+            while (true) {
+                const int64_t t = pred - lane;
+                unsigned long long wv = kEdgeInc;
+                if (t >= 0) {
+                    do { wv = dev_u64w(A.tiles[t]).load(cuda::memory_order_relaxed); } while ((wv >> 62) == 0);
+                }
+                const uint32_t pm = __ballot_sync(kFull, (wv >> 62) == 2);
+                const int stop = pm ? __ffs(pm) - 1 : 31;
+                uint32_t xa = (uint32_t)((wv >> 31) & kEdgeMask), xb = (uint32_t)(wv & kEdgeMask);
+                if (lane > stop || t < 0) { xa = 0; xb = 0; }
+                ea += __reduce_add_sync(kFull, xa);
+                eb += __reduce_add_sync(kFull, xb);
+                if (pm) break;
+                pred -= 32;
+            }
+            if (lane == 0) dev_u64w(A.tiles[tile]).store(edge_word(kEdgeInc, ea + ta, eb + tb), cuda::memory_order_relaxed);
+        }
+        if (lane == 0) {
+            s_pa = ea;
+            s_pb = eb;
+            if (tile == A.ntiles - 1) { A.totals[0] = ea + ta; A.totals[1] = eb + tb; }
+        }
+    }
+    __syncthreads();
+    const uint32_t excl = inc - own + s_w[wid];
+    uint32_t pa = s_pa + (excl & 0xFFFFu), pb = s_pb + (excl >> 16);
+    const uint32_t y = (uint32_t)(A.H - 1) - r;
+    while (em) {
+        const int k = __ffs(em) - 1;
+        em &= em - 1;
+        const uint32_t pt = ((c0 + k) << 16) | y;
+        if ((am >> k) & 1u) A.outA[pa++] = pt;
+        else A.outB[pb++] = pt;
+    }
+}
+
+cudaError_t launch_edges(const EdgeArgs& a, cudaStream_t st) {
+    if (a.ntiles == 0) return cudaSuccess;
+    if (a.W % 16 == 0) k_edges16<<<a.ntiles, 256, 0, st>>>(a);
+    else k_edges<<<a.ntiles, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
 using PassKernel = void (*)(const PassArgs);
 
 static PassKernel tail16_kernel(bool int64, bool pref) {

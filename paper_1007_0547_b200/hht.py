@@ -28,7 +28,8 @@ STATUS = {0: "HHT_OK", 1: "HHT_EINVAL", 2: "HHT_ERANGE", 3: "HHT_EOVERFLOW", 4: 
 EXPORTS = ["hht_default_opts", "hht_create", "hht_nccl_unique_id", "hht_detect", "hht_detect_batch",
            "hht_result_leaves", "hht_result_level", "hht_result_stats", "hht_result_profile",
            "hht_result_launches", "hht_timer_begin", "hht_timer_end", "hht_last_error", "hht_status_str",
-           "hht_destroy", "hht_version", "hht_set_leaf_sink", "hht_group_create", "hht_group_destroy"]
+           "hht_destroy", "hht_version", "hht_set_leaf_sink", "hht_group_create", "hht_group_destroy",
+           "hht_detect_trees", "hht_detect_image", "hht_result_edges"]
 
 PROFILE_CLASSES = ["stage", "count", "write", "tail", "split", "gather", "other", "allreduce"]
 
@@ -93,6 +94,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hht_result_stats": ([p, p], C.c_int),
         "hht_set_leaf_sink": ([p, p, i64], C.c_int),
         "hht_group_create": ([p, i32], C.c_int),
+        "hht_detect_trees": ([p, p, p, i32, i32, i32, i64], C.c_int),
+        "hht_detect_image": ([p, p, i32, i32, i32, i64], C.c_int),
+        "hht_result_edges": ([p, p, i64, p, p], C.c_int),
         "hht_group_destroy": ([p], None),
         "hht_result_profile": ([p, p], C.c_int),
         "hht_result_launches": ([p, p, i64, p], C.c_int),
@@ -244,6 +248,41 @@ class HHT:
         self._check(self._lib.hht_result_leaves(self._ctx, -1, C.c_void_p(out.ctypes.data), out.shape[0],
                                                 C.byref(cnt)))
         return cnt.value
+
+    def detect_trees(self, points, tree_offsets, N: int, depth: int, threshold: int):
+        """Per-tree point sets: tree t (image t // H, half t % H in ALPHA, BETA order) gets
+        points[tree_offsets[t]:tree_offsets[t+1]]."""
+        ptr, n, keep, _ = _as_points(points)
+        to = np.ascontiguousarray(np.asarray(tree_offsets, dtype=np.int64))
+        H = bin(self.halves).count("1")
+        assert to.ndim == 1 and (to.shape[0] - 1) % H == 0 and to[-1] == n
+        B = (to.shape[0] - 1) // H
+        self._check(self._lib.hht_detect_trees(self._ctx, C.c_void_p(ptr), to.ctypes.data, B, N, depth, threshold))
+        del keep
+        return self
+
+    def detect_image(self, img, mag_threshold: int, depth: int, threshold: int):
+        """Sobel edge front end + detection of one square uint8 image [N, N] (row 0 = top), numpy or a
+        CUDA tensor."""
+        if hasattr(img, "data_ptr"):
+            assert img.dtype.itemsize == 1 and img.is_contiguous() and img.dim() == 2
+            N, ptr, keep = int(img.shape[0]), img.data_ptr(), img
+            assert img.shape[1] == N
+        else:
+            keep = np.ascontiguousarray(img, dtype=np.uint8)
+            assert keep.ndim == 2 and keep.shape[0] == keep.shape[1]
+            N, ptr = keep.shape[0], keep.ctypes.data
+        self._check(self._lib.hht_detect_image(self._ctx, C.c_void_p(ptr), N, mag_threshold, depth, threshold))
+        del keep
+
+    def edges(self):
+        """(alpha, beta) int32 [k, 2] (x, y) edge points of the last detect_image, raster order."""
+        na, nb = C.c_int64(0), C.c_int64(0)
+        self._check(self._lib.hht_result_edges(self._ctx, None, 0, C.byref(na), C.byref(nb)))
+        out = np.empty((max(na.value + nb.value, 1), 2), dtype=np.int32)
+        self._check(self._lib.hht_result_edges(self._ctx, out.ctypes.data, out.shape[0], C.byref(na),
+                                               C.byref(nb)))
+        return out[:na.value].copy(), out[na.value:na.value + nb.value].copy()
 
     def set_leaf_sink(self, out: Optional[np.ndarray]):
         """Stream every later detect's leaf rows (image, half, i, j, votes) into `out` (a C-contiguous
