@@ -99,7 +99,7 @@ struct hht_ctx {
     hht_group* group = nullptr;        // borrowed (opts.group)
     std::string err;
     size_t budget = 0;
-    int grid[3][2] = {};
+    int grid[4][2] = {};
     int tail_grid[2] = {};
     int tail16_grid[2] = {};
     int fused_grid[2] = {};
@@ -161,6 +161,10 @@ int tail_depth(const hht_ctx* x) {
     if (want >= 5 && x->D >= 5) return 5;
     return (want >= 4 && x->D >= 4) ? 4 : 3;
 }
+
+// With the fused tail and D >= 6, the last list pass (parent level D-6) skips the count-ahead: the
+// fused tail rasters all children of the level-(D-5) regions and takes their votes from the grids.
+bool no_count_ahead(const hht_ctx* x) { return !x->circle && tail_depth(x) == 5 && x->D >= 6; }
 
 hht_status set_err(hht_ctx* x, hht_status s, const char* fmt, ...) {
     char buf[512];
@@ -453,7 +457,7 @@ PassArgs pass_args(hht_ctx* x, Level& P, int level) {
 }
 
 hht_status run_pass(hht_ctx* x, int mode, const PassArgs& a, uint64_t pairs, uint64_t written) {
-    const int cls = mode == MODE_COUNT ? 1 : (mode == MODE_WRITE ? 2 : 3);
+    const int cls = mode == MODE_COUNT ? 1 : ((mode == MODE_WRITE || mode == MODE_WRITE_NC) ? 2 : 3);
     const int id = prof_begin(x, cls, pairs * 4 + written * 4);
     const int grid = x->circle ? x->grid_circle[mode][x->int64 ? 1 : 0] : x->grid[mode][x->int64 ? 1 : 0];
     CK(launch_pass(mode, x->int64, x->pref_pass || x->circle, x->circle, a, grid, x->st));
@@ -491,7 +495,8 @@ hht_status choose_range(hht_ctx* x, int lc, uint32_t q0, uint64_t cap_entries, b
 // R_(L+1) (its split children, without lists). One pass counts the 2^TK x 2^TK leaf grid of every
 // R_L region; every deeper level is then split from votes gathered out of the grids (a region's
 // votes = the sum of its diagonal leaves), down to the leaves.
-hht_status gather_levels(hht_ctx* x, int L, int c0, uint32_t anc_base, Level& Own, int TK);
+hht_status gather_levels(hht_ctx* x, int L, int c0, uint32_t anc_base, Level& Own, int TK,
+                         const uint32_t* owner_parent = nullptr);
 
 hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
     const int TK = x->D - L;
@@ -525,7 +530,8 @@ hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
 
 // Levels c0 .. D from the leaf grids of the grid owners R_L[anc_base, ...): parents R_(c-1), a
 // child's votes = the sum of its diagonal leaves, then the split of level c.
-hht_status gather_levels(hht_ctx* x, int L, int c0, uint32_t anc_base, Level& Own, int TK) {
+hht_status gather_levels(hht_ctx* x, int L, int c0, uint32_t anc_base, Level& Own, int TK,
+                         const uint32_t* owner_parent) {
     for (int c = c0; c <= x->D; ++c) {
         Level& Pc = x->lv[c - 1];
         if (Pc.F == 0) return HHT_OK;
@@ -536,22 +542,25 @@ hht_status gather_levels(hht_ctx* x, int L, int c0, uint32_t anc_base, Level& Ow
         const int g = prof_begin(x, 5, (16ull + 8 + 4ull * hops + 16ull * (1u << (x->D - c))) * Pc.F);
         CK(launch_gather((const uint32_t*)x->dense.p, anc_base, (const uint32_t*)Own.a.p, (const uint32_t*)Own.c.p,
                          (const uint32_t*)Pc.a.p, (const uint32_t*)Pc.c.p, chain, hops, TK, x->D - c, Pc.F,
-                         (uint32_t*)x->gv.p, x->st));
+                         (uint32_t*)x->gv.p, owner_parent, x->st));
         prof_end(x, g);
         TRY(do_split(x, c, Pc, 0, Pc.F, (const uint32_t*)x->gv.p, (const uint32_t*)x->gv.p));
     }
     return HHT_OK;
 }
 
-// Fused tail at parent level l = D-5: lv[l] holds the lists of R_l[r0, r1), lv[l+1] their split
-// children R_(l+1) (no lists). One k_fused pass rasters every child's 16x16 leaf grid straight from
-// the parents' lists; levels l+2 .. D are then split from the grids (the grid owners are R_(l+1)).
-hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
+// Fused tail at parent level l = D-5: lv[l] holds the lists of R_l[r0, r1). One k_fused pass rasters
+// 16x16 leaf grids straight from those lists: of the split children R_(l+1) (their votes came from
+// the previous pass's count-ahead), or, when `all_children` (that pass ran without count-ahead),
+// of all 4 children of each parent, whose votes are then the grids' diagonal sums and whose split
+// happens here. Levels l+2 .. D are split from the grids.
+hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_children) {
     const int L = l + 1;
     Level& P = x->lv[l];
     Level& C = x->lv[L];
-    const uint32_t n = C.F;
-    if (n == 0 || r1 == r0) return HHT_OK;
+    if (r1 == r0) return HHT_OK;
+    const uint32_t n = all_children ? 4 * (r1 - r0) : C.F;
+    if (n == 0) return HHT_OK;
     TRY(ensure(x, x->dense, (size_t)n * kTail16Cells * 4));
     CK(cudaMemsetAsync(x->dense.p, 0, (size_t)n * kTail16Cells * 4, x->st));
     TRY(ensure(x, x->fusedctr, 256));
@@ -559,16 +568,17 @@ hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
     CK(launch_bounds((const uint64_t*)P.off.p, (const uint64_t*)P.choff.p, (const uint32_t*)P.len.p, r0, r1, l == 0,
                      (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->range_m, x->st));
     PassArgs a = pass_args(x, P, l);
-    a.nf = (const uint32_t*)C.nf.p;
+    a.nf = all_children ? nullptr : (const uint32_t*)C.nf.p;
     a.nf_rbase = r0;
     a.q0 = 0;
-    a.q1 = C.F;
+    a.q1 = all_children ? n : C.F;
     a.votes = (uint32_t*)x->dense.p;
     a.p_choff = (const uint64_t*)P.choff.p;
     a.r_lo = r0;
     a.r_hi = r1;
     a.work = (uint32_t*)x->fusedctr.p;
     a.child_pairs = (unsigned long long*)((char*)x->fusedctr.p + 8);
+    a.all_children = all_children ? 1u : 0u;
     const int id = prof_begin(x, 3, 0);
     CK(launch_fused(x->int64, a, x->fused_grid[x->int64 ? 1 : 0], x->st));
     prof_end(x, id);
@@ -578,12 +588,20 @@ hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
     const uint64_t child_pairs = read_mapped(x->misc_h);
     if (id >= 0) {
         x->pev[id].bytes = pairs * 4 + (uint64_t)n * kTail16Cells * 4;
-        // raster steps: 16 leaf columns x 8 instructions per (line, split child) pair (see tail())
-        x->pev[id].ops = child_pairs * 16 * 8;
+        // raster steps: 16 leaf columns x 8 instructions per (line, child) pair (see tail()), plus the
+        // 4 exact child tests (subtract + compare) per parent entry
+        x->pev[id].ops = child_pairs * 16 * 8 + pairs * 4 * 2;
     }
     x->stat.pairs += pairs;
     TRY(allreduce_sum_u32(x, (uint32_t*)x->dense.p, (size_t)n * kTail16Cells));
-    return gather_levels(x, L, L + 1, 0, C, 4);
+    if (!all_children) return gather_levels(x, L, L + 1, 0, C, 4);
+    // votes of the level-L children from their grids, then their split (creates lv[L])
+    TRY(ensure(x, x->gv, 16ull * (r1 - r0)));
+    const int g = prof_begin(x, 5, (uint64_t)n * 64 + 16ull * (r1 - r0));
+    CK(launch_grid_diag((const uint32_t*)x->dense.p, r1 - r0, (uint32_t*)x->gv.p, x->st));
+    prof_end(x, g);
+    TRY(do_split(x, L, P, r0, r1 - r0, (const uint32_t*)x->gv.p, (const uint32_t*)x->gv.p));
+    return gather_levels(x, L, L + 1, r0, x->lv[L], 4, (const uint32_t*)x->lv[L].parent.p);
 }
 
 // Preconditions: lv[l] holds the lists of R_l[r0, r1) and lv[l+1] holds R_(l+1) = the split
@@ -592,7 +610,7 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
     const int lc = l + 1;
     if (lc >= x->D) return HHT_OK;
     if (!x->circle && x->D >= 3 && l == x->D - tail_depth(x))
-        return tail_depth(x) == 5 ? tail_fused(x, l, r0, r1) : tail(x, l, r0, r1);
+        return tail_depth(x) == 5 ? tail_fused(x, l, r0, r1, no_count_ahead(x)) : tail(x, l, r0, r1);
     Level& P = x->lv[l];
     Level& C = x->lv[lc];
     const uint32_t Fc = C.F;
@@ -656,8 +674,14 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         a.c_cursor = (uint32_t*)C.cursor.p;
         a.c_list = (uint32_t*)C.list_own.p;
         a.votes = (uint32_t*)C.votes.p;
-        TRY(run_pass(x, MODE_WRITE, a, ri.pairs, entries));
+        const bool nc = no_count_ahead(x) && lc == x->D - 5;
+        TRY(run_pass(x, nc ? MODE_WRITE_NC : MODE_WRITE, a, ri.pairs, entries));
         x->stat.ranges += 1;
+        if (nc) {                     // level lc+1 votes come from the fused tail's grids
+            TRY(descend(x, lc, q0, q1));
+            q0 = q1;
+            continue;
+        }
         const uint32_t* VL = (const uint32_t*)C.votes.p;
         if (multi(x)) {
             TRY(ensure(x, C.votes_local, 16ull * nq));
@@ -1045,7 +1069,7 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     }
     if (o.prefetch == 1) x->pref_pass = x->pref_tail = false;
     if (o.prefetch == 2) x->pref_pass = x->pref_tail = true;
-    for (int m = 0; m < 3; ++m)
+    for (int m = 0; m < 4; ++m)
         for (int w = 0; w < 2; ++w) x->grid[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, x->pref_pass, false);
     x->circle = o.variant == HHT_FHT_CIRCLE;
     for (int m = 0; m < 3; ++m)

@@ -64,7 +64,7 @@ struct Totals {          // written by the last split tile
 enum { kStatTests = 0, kStatVotes = 1, kStatLeaves = 2, kStatSplit0 = 8, kStatVisited0 = 8 + 64,
        kStatCount = 8 + 128 };
 
-enum PassMode { MODE_COUNT = 0, MODE_WRITE = 1, MODE_COUNT2 = 2 };
+enum PassMode { MODE_COUNT = 0, MODE_WRITE = 1, MODE_COUNT2 = 2, MODE_WRITE_NC = 3 };   // NC: no count-ahead
 
 // Geometry of one pass over the lists of split regions at parent level l:
 //   g(p) = G(i0, j0) = ex*alpha + (ey << D) + beta,  alpha = 2^D - 2*i0,  beta = N*2^D - 3N*j0,
@@ -98,6 +98,7 @@ struct PassArgs {
     uint32_t r_lo, r_hi;
     uint32_t* work;                // device counter, zero at launch
     unsigned long long* child_pairs;   // device counter: (line, split child) pairs rastered
+    uint32_t all_children;         // k_fused: raster all 4 children of every parent, grid 4 (r - r_lo) + q
 };
 
 struct SplitArgs {
@@ -157,7 +158,8 @@ cudaError_t launch_tail(bool int64, const PassArgs& a, int grid, cudaStream_t st
 struct GatherChain { const uint32_t* parent[3]; };   // parent-index arrays, nearest level first
 cudaError_t launch_gather(const uint32_t* dense, uint32_t anc_base, const uint32_t* anc_a, const uint32_t* anc_c,
                           const uint32_t* p_a, const uint32_t* p_c, const GatherChain& chain, int hops, int tk,
-                          int j, uint32_t Fp, uint32_t* V, cudaStream_t st);
+                          int j, uint32_t Fp, uint32_t* V, const uint32_t* owner_parent, cudaStream_t st);
+cudaError_t launch_grid_diag(const uint32_t* dense, uint32_t nparents, uint32_t* V, cudaStream_t st);
 int tail16_blocks_per_sm(bool int64, bool pref);
 cudaError_t launch_tail16(bool int64, bool pref, const PassArgs& a, int grid, cudaStream_t st);
 int fused_blocks_per_sm(bool int64);

@@ -160,7 +160,7 @@ __device__ __forceinline__ void chunk_math(const uint32_t (&p)[kItems], int cnt,
                 cm |= (bNE | (bNW << 1) | (bSW << 2) | (bSE << 3)) << (4 * it);
             }
         }
-        if (MODE != MODE_COUNT) {
+        if (MODE == MODE_WRITE || MODE == MODE_COUNT2) {
             // 12 of the 16 cells: the NE grandchild of each child is derived later from
             // votes(child) = votes(SW grandchild) + votes(NE grandchild).
             const I Pg = Pc >> 1;
@@ -314,7 +314,8 @@ __device__ __forceinline__ void chunk_math_circle(const uint32_t (&p)[kItems], i
 
 template <typename I, int MODE, bool PREF, bool CIRCLE>
 __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
-    __shared__ uint32_t s_stage[MODE == MODE_WRITE ? 8 * 4 * kChunk : 1];   // 4 KB per warp
+    constexpr bool kWrites = MODE == MODE_WRITE || MODE == MODE_WRITE_NC;
+    __shared__ uint32_t s_stage[kWrites ? 8 * 4 * kChunk : 1];   // 4 KB per warp
     const int lane = threadIdx.x & 31;
     const int D = A.D;
     const int sh = D - A.level;                       // log2 of the parent side s (>= 1)
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
         if (MODE != MODE_COUNT && lane < 4) {
             const uint64_t k = 4 * (uint64_t)(d.r - A.nf_rbase) + lane;
             my_nf = __ldg(A.nf + k);
-            if (MODE == MODE_WRITE) my_off = __ldg(A.nfoff + k);
+            if (kWrites) my_off = __ldg(A.nfoff + k);
         }
 
         uint32_t cm = 0;
@@ -363,7 +364,9 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
 
         if (my_nf != kNone && (my_nf < A.q0 || my_nf >= A.q1)) my_nf = kNone;
 
-        if (CIRCLE) {
+        if (MODE == MODE_WRITE_NC) {
+            // no count-ahead: the next level's votes come from the fused tail's leaf grids
+        } else if (CIRCLE) {
             // all 16 grandchild cells (no derivation for circles): cell L = 4q + qq at field L & 1
             // of word L >> 1, one warp sum per word; lane L < 16 adds cell L
             uint32_t sw = 0;
@@ -398,7 +401,7 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
             if (lane < 12 && nf_l != kNone && v) atomicAdd(A.votes + 4 * (uint64_t)(nf_l - A.q0) + cell_qq, v);
         }
 
-        if (MODE == MODE_WRITE) {
+        if (kWrites) {
             // Child list compaction (warp-private, order within a child list is irrelevant to the
             // counts): per-lane per-child counts -> one packed warp scan -> predicated stores into a
             // per-child shared-memory staging area -> one atomic per (chunk, split child) reserves a
@@ -774,11 +777,16 @@ __global__ void __launch_bounds__(256, 2) k_fused(const PassArgs A) {
         if (r >= A.r_hi) break;
         const uint64_t c_lo = __ldg(A.p_choff + r), c_hi = __ldg(A.p_choff + r + 1);
         if (c_lo == c_hi) continue;
-        // lanes 0..3: grid (next-frontier) index of split child `lane`, kNone otherwise
+        // lanes 0..3: grid index of child `lane` (+ q0): its next-frontier index when only split
+        // children are rastered, 4 (r - r_lo) + lane when all are; kNone for skipped children
         uint32_t my_nf = kNone;
         if (lane < 4) {
-            my_nf = __ldg(A.nf + 4 * (uint64_t)(r - A.nf_rbase) + lane);
-            if (my_nf != kNone && (my_nf < A.q0 || my_nf >= A.q1)) my_nf = kNone;
+            if (A.all_children) {
+                my_nf = 4 * (r - A.r_lo) + lane;
+            } else {
+                my_nf = __ldg(A.nf + 4 * (uint64_t)(r - A.nf_rbase) + lane);
+                if (my_nf != kNone && (my_nf < A.q0 || my_nf >= A.q1)) my_nf = kNone;
+            }
         }
         uint32_t nfq[4], splitm = 0;
 #pragma unroll
@@ -1177,14 +1185,17 @@ __global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ den
                                                 const uint32_t* __restrict__ anc_a, const uint32_t* __restrict__ anc_c,
                                                 const uint32_t* __restrict__ p_a, const uint32_t* __restrict__ p_c,
                                                 GatherChain chain, int hops, int tk, int j, uint32_t Fp,
-                                                uint32_t* __restrict__ V) {
+                                                uint32_t* __restrict__ V, const uint32_t* __restrict__ owner_parent) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= Fp) return;
     uint32_t A = p;
     for (int h = 0; h < hops; ++h) A = chain.parent[h][A];
     const uint32_t la = p_a[p] - (anc_a[A] << hops), lc = p_c[p] - (anc_c[A] << hops);
     const uint32_t G = 1u << tk, S = 1u << j;
-    const uint32_t* g = dense + (uint64_t)(A - anc_base) * (G * G);   // leaf grid, [G*u + v]
+    // grid of owner A: A - anc_base, or (all-children fused tail) 4 (parent(A) - anc_base) + quad(A)
+    const uint32_t gi = owner_parent ? 4 * (owner_parent[A] - anc_base) + quad_of(anc_a[A] & 1, anc_c[A] & 1)
+                                     : A - anc_base;
+    const uint32_t* g = dense + (uint64_t)gi * (G * G);   // leaf grid, [G*u + v]
     uint32_t v[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -1198,9 +1209,29 @@ __global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ den
 
 cudaError_t launch_gather(const uint32_t* dense, uint32_t anc_base, const uint32_t* anc_a, const uint32_t* anc_c,
                           const uint32_t* p_a, const uint32_t* p_c, const GatherChain& chain, int hops, int tk,
-                          int j, uint32_t Fp, uint32_t* V, cudaStream_t st) {
+                          int j, uint32_t Fp, uint32_t* V, const uint32_t* owner_parent, cudaStream_t st) {
     if (Fp == 0) return cudaSuccess;
-    k_gather<<<(Fp + 255) / 256, 256, 0, st>>>(dense, anc_base, anc_a, anc_c, p_a, p_c, chain, hops, tk, j, Fp, V);
+    k_gather<<<(Fp + 255) / 256, 256, 0, st>>>(dense, anc_base, anc_a, anc_c, p_a, p_c, chain, hops, tk, j, Fp, V,
+                                               owner_parent);
+    return cudaGetLastError();
+}
+
+// Votes of the 4 children of each of nparents parents from their own 16x16 leaf grids (grid 4p + q):
+// a region's votes are the sum of its diagonal leaves (identity 2 applied recursively).
+__global__ void __launch_bounds__(256) k_grid_diag(const uint32_t* __restrict__ dense, uint32_t nparents,
+                                                   uint32_t* __restrict__ V) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= 4 * nparents) return;
+    const uint32_t* d = dense + (uint64_t)g * kTail16Cells;
+    uint32_t s = 0;
+#pragma unroll
+    for (int t = 0; t < 16; ++t) s += d[17 * t];
+    V[g] = s;
+}
+
+cudaError_t launch_grid_diag(const uint32_t* dense, uint32_t nparents, uint32_t* V, cudaStream_t st) {
+    if (nparents == 0) return cudaSuccess;
+    k_grid_diag<<<(4 * nparents + 255) / 256, 256, 0, st>>>(dense, nparents, V);
     return cudaGetLastError();
 }
 
@@ -1266,6 +1297,7 @@ template <typename I, bool P, bool C>
 static PassKernel pass_kernel_t(int mode) {
     if (mode == MODE_COUNT) return k_pass<I, MODE_COUNT, P, C>;
     if (mode == MODE_WRITE) return k_pass<I, MODE_WRITE, P, C>;
+    if (mode == MODE_WRITE_NC && !C) return k_pass<I, MODE_WRITE_NC, P, false>;
     return k_pass<I, MODE_COUNT2, P, C>;
 }
 
