@@ -646,7 +646,11 @@ struct Raster16 {
         N3 = (I)3 * N;
     }
 
-    __device__ __forceinline__ void run(const uint32_t (&p)[kItems], int cnt, uint32_t ra, uint32_t rc, uint32_t beta,
+    // ITEMS lines per lane (a batch of <= 32 ITEMS). ITEMS <= 7 keeps every per-lane cell count
+    // <= 7, so the first reduce-scatter level can add the 4-bit counters of two lanes before they
+    // are widened to bytes (sums <= 14): half the widening work and shuffles of that level.
+    template <int ITEMS>
+    __device__ __forceinline__ void run(const uint32_t (&p)[ITEMS], int cnt, uint32_t ra, uint32_t rc, uint32_t beta,
                                         uint32_t* dst, int lane) const {
         const I i0 = (I)ra << 4;
         const I j0 = (I)rc << 4;
@@ -658,10 +662,10 @@ struct Raster16 {
         // per-line raster state carried across the 4 column blocks: z = y - (k-1)*3N (height of the
         // line above its row's floor at the current lattice column; a column drops iff z < 0), the
         // shared-memory address of table entry (k, 0) in this lane's copy, and the column step 2ex
-        I z[kItems], P8[kItems];
-        uint32_t ta[kItems];
+        I z[ITEMS], P8[ITEMS];
+        uint32_t ta[ITEMS];
 #pragma unroll
-        for (int it = 0; it < kItems; ++it) {
+        for (int it = 0; it < ITEMS; ++it) {
             const uint32_t w = p[it];
             const I ex = (I)__byte_perm(w, 0, sel_ex);
             const I ey = (I)__byte_perm(w, 0, sel_ey);
@@ -677,7 +681,7 @@ struct Raster16 {
 #pragma unroll
             for (int i = 0; i < 8; ++i) acc[i] = 0;
 #pragma unroll
-            for (int it = 0; it < kItems; ++it) {
+            for (int it = 0; it < ITEMS; ++it) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const I zz = z[it] - P8[it];
@@ -691,18 +695,26 @@ struct Raster16 {
                     z[it] = mad_i(dr, N3, zz);                          // threshold -= drop * 3N
                 }
             }
-            // widen nibbles to bytes (physical nibble 0 / 1 of each byte), then a butterfly
-            // reduce-scatter over the lanes: xor 16 pairs the two physical words of a column, xor 8
-            // the two nibble parities, xor 4 and xor 2 the columns (selects), xor 1 the byte pairs
-            // (0,2) / (1,3) split into 16-bit fields (sums <= 256). The per-lane table layout makes
-            // "keep the first, send the second" correct for the select-free levels.
+            // butterfly reduce-scatter over the lanes: xor 16 pairs the two physical words of a
+            // column, xor 8 the two nibble parities, xor 4 and xor 2 the columns (selects), xor 1 the
+            // byte pairs (0,2) / (1,3) split into 16-bit fields (sums <= 256). The per-lane table
+            // layout makes "keep the first, send the second" correct for the select-free levels.
             uint32_t e1[4], o1[4];
+            if (ITEMS <= 7) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t e0 = acc[2 * u] & 0x0F0F0F0Fu, eh = acc[2 * u + 1] & 0x0F0F0F0Fu;
-                const uint32_t q0 = (acc[2 * u] >> 4) & 0x0F0F0F0Fu, qh = (acc[2 * u + 1] >> 4) & 0x0F0F0F0Fu;
-                e1[u] = e0 + __shfl_xor_sync(kFull, eh, 16);
-                o1[u] = q0 + __shfl_xor_sync(kFull, qh, 16);
+                for (int u = 0; u < 4; ++u) {                 // xor 16 on 4-bit counters, then widen
+                    const uint32_t n = acc[2 * u] + __shfl_xor_sync(kFull, acc[2 * u + 1], 16);
+                    e1[u] = n & 0x0F0F0F0Fu;
+                    o1[u] = (n >> 4) & 0x0F0F0F0Fu;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {                 // widen, then xor 16 on bytes
+                    const uint32_t e0 = acc[2 * u] & 0x0F0F0F0Fu, eh = acc[2 * u + 1] & 0x0F0F0F0Fu;
+                    const uint32_t q0 = (acc[2 * u] >> 4) & 0x0F0F0F0Fu, qh = (acc[2 * u + 1] >> 4) & 0x0F0F0F0Fu;
+                    e1[u] = e0 + __shfl_xor_sync(kFull, eh, 16);
+                    o1[u] = q0 + __shfl_xor_sync(kFull, qh, 16);
+                }
             }
             uint32_t w4[4];
 #pragma unroll
@@ -736,7 +748,7 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
     Raster16<I> R;
     R.init(A, s_tab, lane);
     chunk_loop<PREF>(A, lane, [&](const ChunkDesc& d, const uint32_t (&p)[kItems]) {
-        R.run(p, (int)d.cnt, d.a, d.c, d.beta, A.votes + (uint64_t)(d.r - A.nf_rbase) * kTail16Cells, lane);
+        R.template run<kItems>(p, (int)d.cnt, d.a, d.c, d.beta, A.votes + (uint64_t)(d.r - A.nf_rbase) * kTail16Cells, lane);
     });
 }
 
@@ -750,7 +762,9 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
 // 256-entry chunk of the child's list (the order of a list is irrelevant to its counts); the last
 // partial stacks are flushed when R is done. Entries never leave the SM between the two steps.
 // ---------------------------------------------------------------------------------------------
-constexpr int kQ = 512;                           // stack capacity per child: < 256 left + <= 256 pushed
+constexpr int kQ = 512;                           // stack capacity per child: < 224 left + <= 256 pushed
+constexpr int kFusedItems = 7;                    // raster batches of 7 lines per lane (224 entries)
+constexpr uint32_t kFusedBatch = kWarp * kFusedItems;
 constexpr int kFusedSmem = kTab16 * 32 * 8 + 8 * 4 * kQ * 4;
 
 template <typename I>
@@ -809,22 +823,22 @@ __global__ void __launch_bounds__(256, 2) k_fused(const PassArgs A) {
         // chunks are exhausted any non-empty one) or pushes one chunk: the raster code is
         // instantiated once (four inlined copies measured 2x slower: instruction-cache misses).
         while (true) {
-            const uint32_t full = (top0 >= (uint32_t)kChunk ? 1u : 0u) | (top1 >= (uint32_t)kChunk ? 2u : 0u) |
-                                  (top2 >= (uint32_t)kChunk ? 4u : 0u) | (top3 >= (uint32_t)kChunk ? 8u : 0u);
+            const uint32_t full = (top0 >= kFusedBatch ? 1u : 0u) | (top1 >= kFusedBatch ? 2u : 0u) |
+                                  (top2 >= kFusedBatch ? 4u : 0u) | (top3 >= kFusedBatch ? 8u : 0u);
             const uint32_t nonempty = (top0 ? 1u : 0u) | (top1 ? 2u : 0u) | (top2 ? 4u : 0u) | (top3 ? 8u : 0u);
             const uint32_t job = full ? full : (ch >= c_hi ? nonempty : 0u);
             if (job) {
                 const int q = __ffs(job) - 1;
                 const uint32_t t = q == 0 ? top0 : q == 1 ? top1 : q == 2 ? top2 : top3;
-                const uint32_t n = min(t, (uint32_t)kChunk);
+                const uint32_t n = min(t, kFusedBatch);
                 const uint32_t base = t - n;               // raster the top n entries of stack q
-                uint32_t pq[kItems];
+                uint32_t pq[kFusedItems];
 #pragma unroll
-                for (int it = 0; it < kItems; ++it)
+                for (int it = 0; it < kFusedItems; ++it)
                     pq[it] = (lane + kWarp * it < (int)n) ? Q[q * kQ + base + lane + kWarp * it] : 0u;
                 const uint32_t nf_q = __shfl_sync(kFull, my_nf, q);
-                R.run(pq, (int)n, 2 * pa + quad_da(q), 2 * pc + quad_dc(q), beta,
-                      A.votes + (uint64_t)(nf_q - A.q0) * kTail16Cells, lane);
+                R.template run<kFusedItems>(pq, (int)n, 2 * pa + quad_da(q), 2 * pc + quad_dc(q), beta,
+                                            A.votes + (uint64_t)(nf_q - A.q0) * kTail16Cells, lane);
                 if (lane == 0) atomicAdd(A.child_pairs, (unsigned long long)n);
                 if (q == 0) top0 = base; else if (q == 1) top1 = base; else if (q == 2) top2 = base; else top3 = base;
                 __syncwarp();
