@@ -50,11 +50,21 @@ def broadcast_bytes(data: Optional[bytes], src: int = 0) -> bytes:
     return obj[0]
 
 
+def _coll_device():
+    """Device for collective tensors: the current CUDA device under NCCL (which rejects CPU tensors),
+    the CPU under gloo."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def check_consistent(N: int, depth: int, threshold: int, halves: int, images: int) -> None:
     """Raise if ranks disagree on the call arguments (libhht re-checks with NCCL: HHT_EMISMATCH)."""
     import torch
     import torch.distributed as dist
-    v = torch.tensor([N, depth, threshold, halves, images], dtype=torch.int64)
+    v = torch.tensor([N, depth, threshold, halves, images], dtype=torch.int64, device=_coll_device())
     lo, hi = v.clone(), v.clone()
     dist.all_reduce(lo, op=dist.ReduceOp.MIN)
     dist.all_reduce(hi, op=dist.ReduceOp.MAX)
@@ -65,7 +75,7 @@ def check_consistent(N: int, depth: int, threshold: int, halves: int, images: in
 def max_over_ranks(x: float, device=None) -> float:
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    t = torch.tensor([x], dtype=torch.float64, device=device if device is not None else _coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -73,7 +83,7 @@ def max_over_ranks(x: float, device=None) -> float:
 def sum_over_ranks(x: float, device=None) -> float:
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    t = torch.tensor([x], dtype=torch.float64, device=device if device is not None else _coll_device())
     dist.all_reduce(t)
     return float(t.item())
 
