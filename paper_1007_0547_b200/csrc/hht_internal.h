@@ -127,6 +127,8 @@ struct SplitArgs {
     unsigned long long* stats;
     Totals* totals;
     uint32_t ntiles;
+    int pass;                      // 0: single pass with look-back; 1: tile aggregates only;
+                                   // 2: outputs, tiles[t].inc* = exclusive tile prefix (k_split_scan)
 };
 
 // Range selection over a next frontier (one thread).
@@ -142,6 +144,7 @@ cudaError_t launch_stage(const int32_t* pts, uint64_t n, int N, uint32_t* packed
                          cudaStream_t st);
 cudaError_t launch_pass(int mode, bool int64, bool pref, bool circle, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_split(const SplitArgs& a, cudaStream_t st);
+constexpr uint32_t kSplitPrescanTiles = 1024;   // reduce-then-scan split from this many tiles on
 cudaError_t launch_chunk_map(const uint64_t* choff, const uint64_t* off, const uint32_t* len, const uint32_t* a,
                              const uint32_t* c, const uint32_t* tree, const uint8_t* tree_beta, uint32_t F,
                              ChunkDesc* chunks, cudaStream_t st);

@@ -1404,7 +1404,8 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
     __shared__ uint4 s_rec[kSplitThreads / 32][128];   // per-warp record staging (4 per parent)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) {
-        s_tile = atomicAdd(A.tile_counter, 1u);   // dynamic tile order: predecessors are running
+        // dynamic tile order for the look-back (predecessors are running); static for the 2 passes
+        s_tile = A.pass == 0 ? atomicAdd(A.tile_counter, 1u) : blockIdx.x;
         s_stat[0] = s_stat[1] = s_stat[2] = 0;
     }
     __syncthreads();
@@ -1451,9 +1452,17 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
         const Agg wi = warp_inclusive(w, lane);
         if (lane < kSplitThreads / 32) s_warp[lane] = {wi.F - w.F, wi.C - w.C, wi.S - w.S};  // exclusive
         const Agg block_total = {__shfl_sync(kFull, wi.F, 31), __shfl_sync(kFull, wi.C, 31), shfl_u64(wi.S, 31)};
-        // decoupled look-back (warp-wide window of 32 predecessors)
         Agg excl = {0, 0, 0};
-        if (tile == 0) {
+        if (A.pass == 1) {                            // aggregates only (k_split_scan orders the tiles)
+            if (lane == 0) {
+                A.tiles[tile].aggF = block_total.F;
+                A.tiles[tile].aggC = block_total.C;
+                A.tiles[tile].aggS = block_total.S;
+            }
+        } else if (A.pass == 2) {                     // the exclusive tile prefix is precomputed
+            excl = {A.tiles[tile].incF, A.tiles[tile].incC, A.tiles[tile].incS};
+        } else if (tile == 0) {
+            // decoupled look-back (warp-wide window of 32 predecessors)
             if (lane == 0) publish(A.tiles + 0, block_total, 2);
         } else {
             if (lane == 0) publish(A.tiles + tile, block_total, 1);
@@ -1489,7 +1498,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
         }
         if (lane == 0) {
             s_prefix = excl;
-            if (tile == A.ntiles - 1) {
+            if (A.pass == 0 && tile == A.ntiles - 1) {
                 const Agg tot = agg_add(excl, block_total);
                 A.totals->F = tot.F;
                 A.totals->S = tot.S;
@@ -1502,6 +1511,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
         }
     }
     __syncthreads();
+    if (A.pass == 1) return;
     const Agg base = agg_add(agg_add(s_prefix, s_warp[wid]), Agg{incl.F - mine.F, incl.C - mine.C, incl.S - mine.S});
 
     if (valid) {
@@ -1583,9 +1593,57 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
     }
 }
 
+// One block: exclusive scan of the tile aggregates of pass 1 into tiles[t].inc*, totals, sentinels.
+__global__ void __launch_bounds__(1024) k_split_scan(const SplitArgs A) {
+    __shared__ Agg s_w[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t per = (A.ntiles + 1023) / 1024, t0 = tid * per, t1 = min(A.ntiles, t0 + per);
+    Agg mine = {0, 0, 0};
+    for (uint32_t t = t0; t < t1; ++t) mine = agg_add(mine, Agg{A.tiles[t].aggF, A.tiles[t].aggC, A.tiles[t].aggS});
+    const Agg incl = warp_inclusive(mine, lane);
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const Agg w = s_w[lane];
+        const Agg wi = warp_inclusive(w, lane);
+        s_w[lane] = {wi.F - w.F, wi.C - w.C, wi.S - w.S};
+        if (lane == 31) {
+            A.totals->F = wi.F;
+            A.totals->S = wi.S;
+            A.totals->C = wi.C;
+            if (!A.leaf_level) {
+                A.out.off[wi.F] = wi.S;
+                A.out.choff[wi.F] = wi.C;
+            }
+        }
+    }
+    __syncthreads();
+    Agg run = agg_add(s_w[wid], Agg{incl.F - mine.F, incl.C - mine.C, incl.S - mine.S});
+    for (uint32_t t = t0; t < t1; ++t) {
+        const Agg a = {A.tiles[t].aggF, A.tiles[t].aggC, A.tiles[t].aggS};
+        A.tiles[t].incF = run.F;
+        A.tiles[t].incC = run.C;
+        A.tiles[t].incS = run.S;
+        run = agg_add(run, a);
+    }
+}
+
 cudaError_t launch_split(const SplitArgs& a, cudaStream_t st) {
     if (a.ntiles == 0) return cudaSuccess;
-    k_split<<<a.ntiles, kSplitThreads, 0, st>>>(a);
+    if (a.ntiles < kSplitPrescanTiles) {
+        SplitArgs b = a;
+        b.pass = 0;
+        k_split<<<a.ntiles, kSplitThreads, 0, st>>>(b);
+        return cudaGetLastError();
+    }
+    // reduce-then-scan: with many tiles the look-back's first wave walks back over ~1000 running
+    // tiles and holds their warps at the barrier; two passes over V cost 16 B per parent more
+    SplitArgs b = a;
+    b.pass = 1;
+    k_split<<<a.ntiles, kSplitThreads, 0, st>>>(b);
+    k_split_scan<<<1, 1024, 0, st>>>(b);
+    b.pass = 2;
+    k_split<<<a.ntiles, kSplitThreads, 0, st>>>(b);
     return cudaGetLastError();
 }
 
