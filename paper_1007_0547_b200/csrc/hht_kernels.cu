@@ -1402,6 +1402,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
     __shared__ uint32_t s_tile;
     __shared__ unsigned long long s_stat[3];    // votes, split-or-leaf count, 4 * split votes
     __shared__ uint4 s_rec[kSplitThreads / 32][128];   // per-warp record staging (4 per parent)
+    __shared__ uint4 s_leaf[kSplitThreads / 32][128];  // per-warp leaf staging (leaf level)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) {
         // dynamic tile order for the look-back (predecessors are running); static for the 2 passes
@@ -1514,6 +1515,8 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
     if (A.pass == 1) return;
     const Agg base = agg_add(agg_add(s_prefix, s_warp[wid]), Agg{incl.F - mine.F, incl.C - mine.C, incl.S - mine.S});
 
+    // the warp's leaves are the contiguous range [f_w, f_w + n_w): staged, then stored coalesced
+    const uint32_t f_w = __shfl_sync(kFull, base.F, 0);
     if (valid) {
         uint32_t f = base.F, cc = base.C;
         uint64_t s = base.S;
@@ -1526,7 +1529,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
             so[q] = s;
             if (flag[q]) {
                 if (A.leaf_level) {
-                    A.leaves[f] = {tree, ca, cb, v[q]};
+                    s_leaf[wid][f - f_w] = make_uint4(tree, ca, cb, v[q]);
                 } else {
                     nf4[q] = f;
                     A.out.tree[f] = tree;
@@ -1564,6 +1567,12 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
             const uint32_t k = lane + 32 * i;
             if (k < nrec) dst[k] = s_rec[wid][k];
         }
+    }
+    if (A.leaf_level) {
+        __syncwarp();
+        const uint32_t n_w = __shfl_sync(kFull, base.F + mine.F, 31) - f_w;
+        uint4* dst = reinterpret_cast<uint4*>(A.leaves) + f_w;
+        for (uint32_t k = lane; k < n_w; k += 32) dst[k] = s_leaf[wid][k];
     }
 
     // stats
