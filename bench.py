@@ -301,6 +301,7 @@ def main():
         nleaf = h2.stats()["leaves"]
         lbuf = torch.empty((max(int(nleaf * 1.1) + 1024, 1024), 5), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
         h2.set_leaf_sink(lbuf)          # detected lines stream to the pinned buffer during detection
+        h2.detect_batch(hnp, my_offs, cfg.N, cfg.D, cfg.T)   # untimed warm-up of the streaming path
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()

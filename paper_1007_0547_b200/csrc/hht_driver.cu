@@ -754,6 +754,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     x->leaves.n = 0;
     x->leaves_host_ok = false;
     x->sink_n = 0;
+    x->sink_slot = 0;        // same staging-slot sequence every call: buffers sized once, then reused
     if ((int)x->lv.size() < D + 1) x->lv.resize(D + 1);
     for (auto& L : x->lv) {
         L.F = 0;

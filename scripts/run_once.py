@@ -42,3 +42,5 @@ for cls in ("count", "write", "tail"):
     xs = by.get(cls, [])
     if xs:
         print(cls, "launches", len(xs), "first bytes", xs[0][0], "bytes[:16]", [b for b, _ in xs[:16]])
+        print(cls, "ms[:16]", [round(m, 3) for _, m in xs[:16]],
+              "GB/s[:16]", [round(b / m / 1e6) if m > 0 else 0 for b, m in xs[:16]])
