@@ -177,6 +177,8 @@ typedef struct oracle_result {
     int64_t tests, votes, max_tests;
     int64_t visited[2][ORACLE_MAXLEV], split[2][ORACLE_MAXLEV];
     int truncated, oom;
+    uint8_t *removed;                 /* removal on: per point of the current half, 1 = removed */
+    vec_u32 support;                  /* removal on: (emitted leaf index, point index) pairs */
 } oracle_result;
 
 typedef struct {
@@ -197,6 +199,7 @@ static void visit(dfs_ctx *k, int32_t l, int64_t a, int64_t c, const int64_t *ca
     int64_t nv = 0;
     for (int64_t q = 0; q < ncand; ++q) {                  /* steps 2-5 / 12.a-b */
         const int64_t p = cand[q];
+        if (r->removed && r->removed[p]) continue;         /* solution(): its codes were set to 0000 */
         if (member(r->variant, k->pts[2 * p], k->pts[2 * p + 1], k->half, r->N, r->D, l, a, c))
             voters[nv++] = p;                              /* level.vote <- level.vote + 1 */
     }
@@ -206,9 +209,18 @@ static void visit(dfs_ctx *k, int32_t l, int64_t a, int64_t c, const int64_t *ca
     vec_u32 *rec = &r->level[hi][l];
     if (vec_push(rec, (uint32_t)a) || vec_push(rec, (uint32_t)c) || vec_push(rec, (uint32_t)nv)) r->oom = 1;
     if (nv > r->T) {                                       /* step 13: level.vote > THRESHOLD */
-        if (l == r->D) {                                   /* leaf: solution() without removal */
+        if (l == r->D) {                                   /* leaf: solution() */
+            const uint32_t li = (uint32_t)(r->leaves.n / 4);
             if (vec_push(&r->leaves, (uint32_t)k->half) || vec_push(&r->leaves, (uint32_t)a) ||
                 vec_push(&r->leaves, (uint32_t)c) || vec_push(&r->leaves, (uint32_t)nv)) r->oom = 1;
+            if (r->removed) {
+                /* plot every edge point whose leaf code is mixed, then set its
+                 * codes at all levels to 0000 ("exclude the edge point from further calculations") */
+                for (int64_t q = 0; q < nv; ++q) {
+                    r->removed[voters[q]] = 1;
+                    if (vec_push(&r->support, li) || vec_push(&r->support, (uint32_t)voters[q])) r->oom = 1;
+                }
+            }
         } else {
             r->split[hi][l] += 1;
             /* quad1..quad4 = NE, NW, SW, SE: (da,dc) = (1,1),(0,1),(0,0),(1,0) */
@@ -237,6 +249,35 @@ oracle_result *oracle_detect(const int32_t *pts, int64_t n, int32_t N, int32_t D
     }
     free(all);
     return r;
+}
+
+/* The same depth-first detector with solution()'s point removal ON (SPEC.md:307,
+ * 341, 348, 350): a leaf whose live votes exceed THRESHOLD emits its voters, which then vote nowhere
+ * else; votes are counted on live points at visit time, so later siblings see reduced votes. Each
+ * tree (half) removes from its own copy of the points (reading R13: every point enters both trees). */
+oracle_result *oracle_detect_removal(const int32_t *pts, int64_t n, int32_t N, int32_t D, int64_t T,
+                                     int32_t halves) {
+    if (D < 0 || D >= ORACLE_MAXLEV - 1 || N < 1 || n < 0) return NULL;
+    oracle_result *r = (oracle_result *)calloc(1, sizeof(oracle_result));
+    if (!r) return NULL;
+    r->N = N; r->D = D; r->T = T; r->halves = halves; r->variant = 0;
+    int64_t *all = (int64_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+    r->removed = (uint8_t *)malloc((size_t)(n > 0 ? n : 1));
+    if (!all || !r->removed) { free(all); free(r->removed); free(r); return NULL; }
+    for (int64_t p = 0; p < n; ++p) all[p] = p;
+    for (int32_t h = ORACLE_ALPHA; h <= ORACLE_BETA; ++h) {
+        if (!(halves & h)) continue;
+        memset(r->removed, 0, (size_t)(n > 0 ? n : 1));
+        dfs_ctx k = {pts, h, r};
+        visit(&k, 0, 0, 0, all, n);
+    }
+    free(all);
+    return r;
+}
+
+int64_t oracle_result_support_count(const oracle_result *r) { return r->support.n / 2; }
+void oracle_result_support(const oracle_result *r, uint32_t *out) {
+    if (r->support.n) memcpy(out, r->support.v, (size_t)r->support.n * sizeof(uint32_t));
 }
 
 /* Run the same visit() from region (level, a, c) with ALL points as candidates. By containment
@@ -283,5 +324,7 @@ void oracle_result_free(oracle_result *r) {
     for (int h = 0; h < 2; ++h)
         for (int l = 0; l < ORACLE_MAXLEV; ++l) free(r->level[h][l].v);
     free(r->leaves.v);
+    free(r->support.v);
+    free(r->removed);
     free(r);
 }

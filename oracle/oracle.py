@@ -54,6 +54,12 @@ def _load():
             lib.oracle_dense_votes.restype = None
             lib.oracle_detect.argtypes = [p, i64, i32, i32, i64, i32, i32, i64]
             lib.oracle_detect.restype = p
+            lib.oracle_detect_removal.argtypes = [p, i64, i32, i32, i64, i32]
+            lib.oracle_detect_removal.restype = p
+            lib.oracle_result_support_count.argtypes = [p]
+            lib.oracle_result_support_count.restype = i64
+            lib.oracle_result_support.argtypes = [p, p]
+            lib.oracle_result_support.restype = None
             lib.oracle_detect_subtree.argtypes = [p, i64, i32, i32, i64, i32, i32, i64, i64]
             lib.oracle_detect_subtree.restype = p
             lib.oracle_result_level_count.argtypes = [p, i32, i32]
@@ -162,6 +168,29 @@ def detect(points, N: int, D: int, T: int, halves: int = ALPHA | BETA, variant: 
     if not h:
         raise ValueError("oracle_detect rejected its arguments")
     return _collect(lib, h, N, D, T, halves)
+
+
+def detect_removal(points, N: int, D: int, T: int, halves: int = ALPHA | BETA):
+    """The detector with solution()'s point removal ON: returns (lines, support)
+    where lines is uint32 [k, 4] (half, i, j, live votes) in emission (depth-first) order and support
+    is uint32 [m, 2] (line index, point index): the points each line emitted and removed."""
+    p = _pts(points)
+    lib = _load()
+    h = lib.oracle_detect_removal(p.ctypes.data, p.shape[0], N, D, T, halves)
+    if not h:
+        raise ValueError("oracle_detect_removal rejected its arguments")
+    try:
+        nl = lib.oracle_result_leaf_count(h)
+        lines = np.zeros((nl, 4), dtype=np.uint32)
+        if nl:
+            lib.oracle_result_leaves(h, lines.ctypes.data)
+        ns = lib.oracle_result_support_count(h)
+        sup = np.zeros((ns, 2), dtype=np.uint32)
+        if ns:
+            lib.oracle_result_support(h, sup.ctypes.data)
+        return lines, sup
+    finally:
+        lib.oracle_result_free(h)
 
 
 def detect_subtree(points, N: int, D: int, T: int, half: int, level: int, a: int, c: int) -> OracleResult:
