@@ -167,6 +167,18 @@ hht_status hht_detect_batch(hht_ctx* ctx, const int32_t* points, const int64_t* 
 
 /* Detected lines of `image` (ALPHA tree first, each in the paper's depth-first NE,NW,SW,SE order);
  * image = -1 returns every image's lines in image order. */
+/* solution() with point removal for the last detect: the
+ * candidate leaves (hht_result_leaves) are taken in depth-first order within each tree and a leaf is
+ * emitted iff more than `threshold` of its voters have not been removed by an earlier emitted leaf of
+ * the same tree; its live voters are then removed (the paper's "exclude the edge point from further
+ * calculations"). Rows (image, half, i, j, live votes), image -1 = all, same cap/count protocol as
+ * hht_result_leaves. This equals the paper's depth-first detector with removal on (the oracle's
+ * oracle_detect_removal). Computed on the GPU on first request and cached until the next detect:
+ * support bitsets of candidates x points / 8 bytes (HHT_ENOMEM beyond the memory budget), then one
+ * block per tree walks its candidates sequentially — meant for images with sparse detections (the
+ * paper's regime), not for saturated configs with 1e7+ candidates. Single rank, exact test only. */
+hht_status hht_result_lines(hht_ctx* ctx, int32_t image, hht_leaf* out, int64_t cap, int64_t* count);
+
 /* Per-tree point sets (each point in ONE tree, e.g. the edge front end's ALPHA/BETA partition,
  * PAPER.md:67): tree t = image t / H + half index t % H (H = number of halves in opts.halves,
  * ALPHA first) gets the int2 (x, y) points [tree_offsets[t], tree_offsets[t+1]) of `points`

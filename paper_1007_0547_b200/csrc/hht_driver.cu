@@ -119,6 +119,11 @@ struct hht_ctx {
     Buf fusedctr;                    // k_fused work counter (u32) + rastered-pair counter (u64)
     Buf img, edgeB, edgetiles;       // edge front end: staged image, BETA points, look-back words
     bool edges_valid = false;        // x->packed holds the last hht_detect_image's edge points
+    std::vector<uint64_t> tree_pt_off;   // last detect: tree t's points in x->packed (local)
+    std::vector<uint32_t> tree_pt_n;
+    bool lines_ok = false;               // removal post-pass cached for the last detect
+    std::vector<hht_leaf> lines_host;
+    std::vector<int64_t> lines_img;      // [B+1] row offsets per image
     int64_t edge_na = 0, edge_nb = 0;
     // leaf sink (hht_set_leaf_sink): double-buffered row staging, copied on its own stream
     hht_leaf* sink = nullptr;
@@ -796,6 +801,14 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     }
     x->tree_E.assign(x->ntrees, 0);
     for (int t = 0; t < x->ntrees; ++t) x->tree_E[t] = global_n[tree_offsets ? t : t / x->H];
+    x->tree_pt_off.assign(x->ntrees, 0);
+    x->tree_pt_n.assign(x->ntrees, 0);
+    for (int t = 0; t < x->ntrees; ++t) {
+        const int sgi = tree_offsets ? t : t / x->H;
+        x->tree_pt_off[t] = (uint64_t)segs[sgi];
+        x->tree_pt_n[t] = (uint32_t)local_n[sgi];
+    }
+    x->lines_ok = false;
 
     // K0: stage + validate (reject before any traversal; collective over ranks)
     if (!prepacked) x->edges_valid = false;
@@ -1204,6 +1217,104 @@ hht_status hht_result_edges(hht_ctx* x, int32_t* out, int64_t cap, int64_t* n_al
         out[2 * i] = (int32_t)(h[i] >> 16);
         out[2 * i + 1] = (int32_t)(h[i] & 0xFFFFu);
     }
+    return HHT_OK;
+}
+
+// solution() with removal (NEXT-1) over the last detect's candidate leaves; cached until the next detect.
+hht_status compute_lines(hht_ctx* x) {
+    if (x->lines_ok) return HHT_OK;
+    if (multi(x)) return set_err(x, HHT_EINVAL, "removal needs every point of a tree: single rank only");
+    if (x->circle) return set_err(x, HHT_EINVAL, "removal is defined for the exact test");
+    TRY(host_leaves(x));
+    const std::vector<LeafRec>& L = x->leaves_host;
+    const uint32_t nt = (uint32_t)x->ntrees;
+    std::vector<uint64_t> cand_lo(nt + 1, 0), bits_off(nt + 1, 0);
+    {
+        uint64_t k = 0;
+        for (uint32_t t = 0; t < nt; ++t) {
+            cand_lo[t] = k;
+            while (k < L.size() && L[k].tree == t) ++k;
+        }
+        cand_lo[nt] = k;
+    }
+    uint32_t maxW = 1;
+    for (uint32_t t = 0; t < nt; ++t) {
+        const uint64_t W = (x->tree_pt_n[t] + 31) / 32;
+        maxW = std::max<uint32_t>(maxW, (uint32_t)W);
+        bits_off[t + 1] = bits_off[t] + (cand_lo[t + 1] - cand_lo[t]) * W;
+    }
+    const uint64_t words = bits_off[nt];
+    if (words * 4 > x->budget)
+        return set_err(x, HHT_ENOMEM, "removal post-pass needs %llu B of support bitsets (candidates x points / 8)",
+                       (unsigned long long)(words * 4));
+    if ((size_t)maxW * 4 > 200 * 1024)
+        return set_err(x, HHT_ENOMEM, "removal post-pass: a tree of more than 1.6M points");
+    Buf bits, meta, outb;
+    auto cleanup = [&]() { for (Buf* b : {&bits, &meta, &outb}) if (b->p) cudaFreeAsync(b->p, x->st); };
+    const uint64_t nl = L.size();
+    hht_status st = ensure(x, bits, std::max<uint64_t>(words, 1) * 4);
+    if (st == HHT_OK) st = ensure(x, meta, (size_t)(nt + 1) * 8 * 3 + (size_t)nt * 4 + 64);
+    if (st == HHT_OK) st = ensure(x, outb, (size_t)std::max<uint64_t>(nl, 1) * 8 + (size_t)nt * 4);
+    if (st != HHT_OK) { cleanup(); return st; }
+    uint64_t* d_cand = (uint64_t*)meta.p;
+    uint64_t* d_off = d_cand + (nt + 1);
+    uint64_t* d_bits = d_off + (nt + 1);
+    uint32_t* d_n = (uint32_t*)(d_bits + (nt + 1));
+    CK(cudaMemcpyAsync(d_cand, cand_lo.data(), (nt + 1) * 8, cudaMemcpyHostToDevice, x->st));
+    CK(cudaMemcpyAsync(d_off, x->tree_pt_off.data(), nt * 8, cudaMemcpyHostToDevice, x->st));
+    CK(cudaMemcpyAsync(d_bits, bits_off.data(), (nt + 1) * 8, cudaMemcpyHostToDevice, x->st));
+    CK(cudaMemcpyAsync(d_n, x->tree_pt_n.data(), nt * 4, cudaMemcpyHostToDevice, x->st));
+    RemovalArgs a{};
+    a.leaves = (const LeafRec*)x->leaves.b.p;
+    a.packed = (const uint32_t*)x->packed.p;
+    a.cand_lo = d_cand;
+    a.pt_off = d_off;
+    a.pt_n = d_n;
+    a.bits_off = d_bits;
+    a.tree_beta = (const uint8_t*)x->beta.p;
+    a.bits = (uint32_t*)bits.p;
+    a.out = (uint32_t*)outb.p;
+    a.out_live = (uint32_t*)outb.p + std::max<uint64_t>(nl, 1);
+    a.out_n = a.out_live + std::max<uint64_t>(nl, 1);
+    a.N = x->N;
+    a.D = x->D;
+    a.T = x->T;
+    a.ntrees = nt;
+    a.total_words = words;
+    CK(launch_removal(a, x->int64, maxW, x->st));
+    std::vector<uint32_t> h_out(nl), h_live(nl), h_n(nt);
+    if (nl) {
+        CK(cudaMemcpyAsync(h_out.data(), a.out, nl * 4, cudaMemcpyDeviceToHost, x->st));
+        CK(cudaMemcpyAsync(h_live.data(), a.out_live, nl * 4, cudaMemcpyDeviceToHost, x->st));
+    }
+    CK(cudaMemcpyAsync(h_n.data(), a.out_n, nt * 4, cudaMemcpyDeviceToHost, x->st));
+    TRY(sync(x));
+    cleanup();
+    x->lines_host.clear();
+    x->lines_img.assign(x->B + 1, 0);
+    for (uint32_t t = 0; t < nt; ++t) {
+        for (uint32_t e = 0; e < h_n[t]; ++e) {
+            const LeafRec& r = L[cand_lo[t] + h_out[cand_lo[t] + e]];
+            x->lines_host.push_back({(int32_t)(t / x->H), (uint32_t)x->tree_half[t], r.i, r.j, h_live[cand_lo[t] + e]});
+        }
+        x->lines_img[t / x->H + 1] = (int64_t)x->lines_host.size();
+    }
+    for (int b = 1; b <= x->B; ++b) x->lines_img[b] = std::max(x->lines_img[b], x->lines_img[b - 1]);
+    x->lines_ok = true;
+    return HHT_OK;
+}
+
+hht_status hht_result_lines(hht_ctx* x, int32_t image, hht_leaf* out, int64_t cap, int64_t* count) {
+    if (!x || !count) return HHT_EINVAL;
+    if (!x->have) return set_err(x, HHT_ESTATE, "no successful detect yet");
+    if (image < -1 || image >= x->B) return set_err(x, HHT_EINVAL, "image out of range");
+    TRY(compute_lines(x));
+    const int64_t b = image < 0 ? 0 : x->lines_img[image], e = image < 0 ? (int64_t)x->lines_host.size()
+                                                                        : x->lines_img[image + 1];
+    *count = e - b;
+    if (!out) return HHT_OK;
+    if (cap < e - b) return set_err(x, HHT_EINVAL, "cap < %lld lines", (long long)(e - b));
+    if (e > b) memcpy(out, x->lines_host.data() + b, (size_t)(e - b) * sizeof(hht_leaf));
     return HHT_OK;
 }
 

@@ -179,6 +179,26 @@ struct EdgeArgs {
 };
 constexpr int kEdgeTile = 4096;    // pixels per 256-thread tile (16 per lane, lane-interleaved)
 cudaError_t launch_edges(const EdgeArgs& a, cudaStream_t st);
+// solution() with point removal as a post-pass: per tree t, candidate leaves
+// leaves[cand_lo[t] .. cand_lo[t+1]) and points packed[pt_off[t] .. pt_off[t] + pt_n[t]).
+struct RemovalArgs {
+    const LeafRec* leaves;
+    const uint32_t* packed;
+    const uint64_t* cand_lo;       // [ntrees + 1]
+    const uint64_t* pt_off;        // [ntrees]
+    const uint32_t* pt_n;          // [ntrees]
+    const uint64_t* bits_off;      // [ntrees] word offset of tree t's support bitsets
+    const uint8_t* tree_beta;
+    uint32_t* bits;                // supports: tree t, candidate k: W_t words
+    uint32_t* out;                 // [total candidates] emitted candidate indices, per tree at cand_lo[t]
+    uint32_t* out_live;            // live votes of the emitted lines
+    uint32_t* out_n;               // [ntrees] emitted per tree
+    int N, D;
+    uint64_t T;
+    uint32_t ntrees;
+    uint64_t total_words;
+};
+cudaError_t launch_removal(const RemovalArgs& a, bool int64, size_t smem_words, cudaStream_t st);
 cudaError_t launch_fused(bool int64, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
                           int is_root, RangeInfo* info, uint64_t* chunk_bounds, RangeInfo* info_h, cudaStream_t st);

@@ -14,6 +14,7 @@
 // that is the single compare (G_SW - 1) <u s*(2ex + 3N). The children of a region with SW value g
 // have SW values g - {0, Pc} - {0, Qc} (Pc = ex*s, Qc = 3N*s/2): the 9 lattice points of the
 // region (corners, edge midpoints, centre) decide the parent code and all four child codes.
+#include <algorithm>
 #include <cuda/atomic>
 
 #include "hht_internal.h"
@@ -1158,6 +1159,100 @@ cudaError_t launch_edges(const EdgeArgs& a, cudaStream_t st) {
     if (a.ntiles == 0) return cudaSuccess;
     if (a.W % 16 == 0) k_edges16<<<a.ntiles, 256, 0, st>>>(a);
     else k_edges<<<a.ntiles, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// solution() with point removal: the removal-on result
+// equals a greedy pass over the removal-off candidate leaves in depth-first order that emits a leaf
+// iff its voters not yet removed exceed THRESHOLD and then removes them (live votes only shrink, so a
+// leaf live at its turn had live ancestors at theirs; pinned in tests/test_oracle_removal.py).
+// k_support: support bitset of every candidate leaf (bit p = point p crosses the leaf cell, the exact
+// test at level D: 0 < G_SW <= 2ex + 3N); k_greedy: one block per tree walks its candidates in order
+// with the removed-point bitset in shared memory.
+// ---------------------------------------------------------------------------------------------
+template <typename I>
+__global__ void __launch_bounds__(256) k_support(const RemovalArgs A) {
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;    // global support word
+    if (g >= A.total_words) return;
+    uint32_t lo = 0, hi = A.ntrees - 1;                                    // tree of word g
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) / 2;
+        if (A.bits_off[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    const uint32_t t = lo;
+    const uint32_t n = A.pt_n[t], W = (n + 31) / 32;
+    const uint64_t rel = g - A.bits_off[t];
+    const uint64_t k = A.cand_lo[t] + rel / W;                              // candidate leaf
+    const uint32_t w = (uint32_t)(rel % W);
+    const LeafRec L = A.leaves[k];
+    const bool beta = A.tree_beta[t] != 0;
+    const I N = (I)A.N;
+    const I base = ((I)N << A.D) - (I)3 * N * (I)L.j;                      // + 2^D (ex + ey) - 2 i ex below
+    uint32_t word = 0;
+    for (int b = 0; b < 32; ++b) {
+        const uint32_t p = 32 * w + b;
+        if (p >= n) break;
+        const uint32_t pk = A.packed[A.pt_off[t] + p];
+        const I ex = (I)(beta ? (pk & 0xFFFFu) : (pk >> 16)), ey = (I)(beta ? (pk >> 16) : (pk & 0xFFFFu));
+        const I g_sw = base + ((ex + ey) << A.D) - (I)2 * (I)L.i * ex;      // G(i, j) of the leaf's SW corner
+        if (g_sw > 0 && g_sw <= (I)2 * ex + (I)3 * N) word |= 1u << b;
+    }
+    A.bits[g] = word;
+}
+
+__global__ void __launch_bounds__(1024) k_greedy(const RemovalArgs A, uint32_t smem_words) {
+    extern __shared__ uint32_t s_removed[];
+    __shared__ uint32_t s_part[32];
+    __shared__ uint32_t s_emit;
+    const uint32_t t = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t n = A.pt_n[t], W = (n + 31) / 32;
+    // removed-point bitset: shared memory when it fits, else this tree's slice of `out` is not
+    // usable, so the caller guarantees W <= smem_words
+    for (uint32_t w = tid; w < W; w += blockDim.x) s_removed[w] = 0;
+    if (tid == 0) s_emit = 0;
+    __syncthreads();
+    const uint64_t c0 = A.cand_lo[t], c1 = A.cand_lo[t + 1];
+    const uint32_t* bits = A.bits + A.bits_off[t];
+    uint32_t emitted = 0;
+    for (uint64_t k = c0; k < c1; ++k) {
+        const uint32_t* sk = bits + (k - c0) * W;
+        uint32_t live = 0;
+        for (uint32_t w = tid; w < W; w += blockDim.x) live += __popc(sk[w] & ~s_removed[w]);
+        live = __reduce_add_sync(0xFFFFFFFFu, live);
+        if (lane == 0) s_part[wid] = live;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t v = lane < (int)(blockDim.x >> 5) ? s_part[lane] : 0u;
+            v = __reduce_add_sync(0xFFFFFFFFu, v);
+            if (lane == 0) s_emit = (uint64_t)v > A.T ? v : 0u;
+        }
+        __syncthreads();
+        const uint32_t e = s_emit;
+        if (e) {                                       // emit, then remove its live voters
+            for (uint32_t w = tid; w < W; w += blockDim.x) s_removed[w] |= sk[w];
+            if (tid == 0) {
+                A.out[c0 + emitted] = (uint32_t)(k - c0);
+                A.out_live[c0 + emitted] = e;
+            }
+            ++emitted;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) A.out_n[t] = emitted;
+    (void)smem_words;
+}
+
+cudaError_t launch_removal(const RemovalArgs& a, bool int64, size_t smem_words, cudaStream_t st) {
+    if (a.total_words) {
+        const uint64_t blocks = (a.total_words + 255) / 256;
+        if (int64) k_support<int64_t><<<(unsigned)blocks, 256, 0, st>>>(a);
+        else k_support<int32_t><<<(unsigned)blocks, 256, 0, st>>>(a);
+    }
+    const size_t smem = std::max<size_t>(smem_words, 1) * 4;
+    cudaFuncSetAttribute(k_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_greedy<<<a.ntrees, 1024, smem, st>>>(a, (uint32_t)smem_words);
     return cudaGetLastError();
 }
 

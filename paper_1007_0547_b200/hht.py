@@ -29,7 +29,7 @@ EXPORTS = ["hht_default_opts", "hht_create", "hht_nccl_unique_id", "hht_detect",
            "hht_result_leaves", "hht_result_level", "hht_result_stats", "hht_result_profile",
            "hht_result_launches", "hht_timer_begin", "hht_timer_end", "hht_last_error", "hht_status_str",
            "hht_destroy", "hht_version", "hht_set_leaf_sink", "hht_group_create", "hht_group_destroy",
-           "hht_detect_trees", "hht_detect_image", "hht_result_edges"]
+           "hht_detect_trees", "hht_detect_image", "hht_result_edges", "hht_result_lines"]
 
 PROFILE_CLASSES = ["stage", "count", "write", "tail", "split", "gather", "other", "allreduce"]
 
@@ -97,6 +97,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hht_detect_trees": ([p, p, p, i32, i32, i32, i64], C.c_int),
         "hht_detect_image": ([p, p, i32, i32, i32, i64], C.c_int),
         "hht_result_edges": ([p, p, i64, p, p], C.c_int),
+        "hht_result_lines": ([p, i32, p, i64, p], C.c_int),
         "hht_group_destroy": ([p], None),
         "hht_result_profile": ([p, p], C.c_int),
         "hht_result_launches": ([p, p, i64, p], C.c_int),
@@ -274,6 +275,15 @@ class HHT:
             N, ptr = keep.shape[0], keep.ctypes.data
         self._check(self._lib.hht_detect_image(self._ctx, C.c_void_p(ptr), N, mag_threshold, depth, threshold))
         del keep
+
+    def lines(self, image: int = -1) -> np.ndarray:
+        """int64 [k, 5] (image, half, i, j, live votes): solution() with point removal
+        over the last detect's candidate leaves, depth-first order per tree."""
+        cnt = C.c_int64(0)
+        self._check(self._lib.hht_result_lines(self._ctx, image, None, 0, C.byref(cnt)))
+        out = (Leaf * max(cnt.value, 1))()
+        self._check(self._lib.hht_result_lines(self._ctx, image, out, cnt.value, C.byref(cnt)))
+        return np.frombuffer(out, dtype=np.uint32, count=5 * cnt.value).reshape(-1, 5).astype(np.int64)
 
     def edges(self):
         """(alpha, beta) int32 [k, 2] (x, y) edge points of the last detect_image, raster order."""
