@@ -75,6 +75,10 @@ typedef struct {
                                 depth-3 lists. Results are identical. */
     uint32_t prefetch;       /* pass/tail kernels: 0 = auto, 1 = fetch the next chunk's descriptor
                                 only, 2 = also its list entries (more registers); identical results */
+    uint32_t latency_path;   /* 0 = auto: a detection whose every per-level array fits one block's
+                                shared memory (about sum over trees of points x 2^depth <= 26k;
+                                one rank, exact test) runs as ONE kernel launch (k_small);
+                                1 = same; 2 = never (always the multi-kernel path) */
     uint32_t variant;        /* membership test: HHT_EXACT (0, default) = the paper's 4-bit corner
                                 code; HHT_FHT_CIRCLE (1) = the FHT comparison: the line meets the
                                 region's circumscribing circle (exact integers, see
@@ -114,6 +118,8 @@ typedef struct {
     uint32_t images;
     double ms;               /* device time of the call (CUDA events on the ctx stream) */
     uint64_t leaves_streamed;   /* leaf rows written to the leaf sink (hht_set_leaf_sink) */
+    uint32_t latency_path;      /* 1 if the detection ran on the one-launch latency path */
+    uint32_t reserved;
 } hht_stats;
 
 /* Leaf sink: while a detect runs, the detected lines are converted to hht_leaf rows and copied to

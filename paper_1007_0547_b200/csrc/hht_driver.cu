@@ -118,6 +118,7 @@ struct hht_ctx {
     Buf stage_in, packed, errflag, beta, stats, tiles, tilectr, totals, rng, bounds, vtmp, dense, gv, leafrows;
     Buf fusedctr;                    // k_fused work counter (u32) + rastered-pair counter (u64)
     Buf img, edgeB, edgetiles;       // edge front end: staged image, BETA points, look-back words
+    Buf small;                       // latency path scratch (k_small)
     bool edges_valid = false;        // x->packed holds the last hht_detect_image's edge points
     std::vector<uint64_t> tree_pt_off;   // last detect: tree t's points in x->packed (local)
     std::vector<uint32_t> tree_pt_n;
@@ -721,6 +722,115 @@ hht_status check_args(hht_ctx* x, const int32_t* points, int64_t n_total, int32_
     return HHT_OK;
 }
 
+// Latency path: eligible when every per-level array of the traversal fits one block's shared memory
+// (lists: a line crosses at most 2^(l+1) - 1 regions of level l, so a level-l list holds at most
+// sum_t n_t (2^(l+1) - 1) entries; frontier: a split region holds > T entries), one rank, the exact
+// test, and opts.latency_path != 2. One k_small launch does every level; one synchronisation reads
+// the per-level record counts, the leaf count and the statistics.
+void small_bounds(const hht_ctx* x, uint64_t& S, uint64_t& F) {
+    uint64_t n = 0;
+    for (int t = 0; t < x->ntrees; ++t) n += x->tree_pt_n[t];
+    S = std::max<uint64_t>(n * ((1ull << x->D) - 1), 1);   // list levels 0 .. D-1
+    F = S / (x->T + 1) + x->ntrees + 1;
+}
+
+bool small_eligible(const hht_ctx* x) {
+    if (x->opts.latency_path == 2 || multi(x) || x->circle || x->D > 24 || x->ntrees > 4096) return false;
+    uint64_t S, F;
+    small_bounds(x, S, F);
+    return S < (1ull << 32) && small_smem_bytes((uint32_t)S, (uint32_t)std::min<uint64_t>(F, S + 1)) <= kSmallSmemMax;
+}
+
+hht_status detect_small(hht_ctx* x) {
+    const int D = x->D;
+    const uint32_t nt = (uint32_t)x->ntrees;
+    uint64_t n = 0;
+    for (uint32_t t = 0; t < nt; ++t) n += x->tree_pt_n[t];
+    uint64_t Smax, Fmax;
+    small_bounds(x, Smax, Fmax);
+    Fmax = std::min<uint64_t>(Fmax, Smax + 1);
+    // global scratch: tree offsets and counts, per-level counts, record pointers
+    const uint64_t words = 3ull * nt + (D + 2) + 2ull * (D + 1) + 16;
+    TRY(ensure(x, x->small, words * 4));
+    uint32_t* w = (uint32_t*)x->small.p;
+    SmallArgs a{};
+    a.smem_S = (uint32_t)Smax;
+    a.smem_F = (uint32_t)Fmax;
+    uint64_t* d_off = (uint64_t*)w; w += 2ull * nt;
+    uint32_t* d_n = w; w += nt;
+    a.counts = w; w += D + 2;
+    w = (uint32_t*)(((uintptr_t)w + 7) & ~(uintptr_t)7);
+    Record** d_rec = (Record**)w;
+    std::vector<Record*> h_rec(D + 1);
+    for (int l = 0; l <= D; ++l) {
+        const uint64_t cap = l == 0 ? nt : 4 * Fmax;
+        TRY(grow(x, x->rec[l], sizeof(Record), cap));
+        h_rec[l] = (Record*)x->rec[l].b.p;
+    }
+    TRY(grow(x, x->leaves, sizeof(LeafRec), 4 * Fmax));
+    {   // one host-to-device copy of everything the launch needs (offsets, counts, zeroed counters,
+        // record pointers), laid out exactly as in `x->small`
+        std::vector<uint32_t> h(words, 0);
+        memcpy(h.data(), x->tree_pt_off.data(), 8ull * nt);
+        memcpy(h.data() + 2ull * nt, x->tree_pt_n.data(), 4ull * nt);
+        memcpy((char*)h.data() + ((char*)d_rec - (char*)x->small.p), h_rec.data(), sizeof(Record*) * (D + 1));
+        CK(cudaMemcpyAsync(x->small.p, h.data(), words * 4, cudaMemcpyHostToDevice, x->st));
+    }
+    a.packed = (const uint32_t*)x->packed.p;
+    a.tree_off = d_off;
+    a.tree_n = d_n;
+    a.tree_beta = (const uint8_t*)x->beta.p;
+    a.ntrees = nt;
+    a.N = x->N;
+    a.D = D;
+    a.T = x->T;
+    a.rec = d_rec;
+    a.leaves = (LeafRec*)x->leaves.b.p;
+    a.stats = (unsigned long long*)x->stats.p;
+    const int id = prof_begin(x, 1, n * 4 * (uint64_t)(D + 1));
+    CK(launch_small(a, x->int64, x->st));
+    prof_end(x, id);
+    std::vector<uint32_t> counts(D + 2);
+    uint64_t st[kStatCount];
+    CK(cudaMemcpyAsync(counts.data(), a.counts, 4ull * (D + 2), cudaMemcpyDeviceToHost, x->st));
+    CK(cudaMemcpyAsync(st, x->stats.p, sizeof st, cudaMemcpyDeviceToHost, x->st));
+    CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)x->errflag.p, 1, x->st));
+    CK(cudaEventRecord(x->ev1, x->st));
+    TRY(sync(x));
+    if ((uint32_t)read_mapped(x->misc_h)) return set_err(x, HHT_ERANGE, "a point lies outside [0, N)^2");
+    for (int l = 0; l <= D; ++l) x->rec[l].n = x->opts.record_levels ? counts[l] : 0;
+    x->leaves.n = counts[D + 1];
+    x->stat.tests = st[kStatTests];
+    x->stat.votes = st[kStatVotes];
+    x->stat.leaves = st[kStatLeaves];
+    for (int l = 0; l <= D && l < 64; ++l) {
+        x->stat.visited[l] = st[kStatVisited0 + l];
+        x->stat.split[l] = st[kStatSplit0 + l];
+    }
+    x->stat.latency_path = 1;
+    TRY(stream_leaves(x, 0, x->leaves.n));
+    if (x->sink) {
+        CK(cudaStreamSynchronize(x->cst));
+        x->stat.leaves_streamed = x->sink_n;
+        x->stat.d2h_bytes += x->sink_n * sizeof(hht_leaf);
+    }
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, x->ev0, x->ev1));
+    x->stat.ms = ms;
+    x->launch_log.clear();
+    if (x->opts.profile && id >= 0) {
+        float m = 0;
+        if (cudaEventElapsedTime(&m, x->pev[id].a, x->pev[id].b) == cudaSuccess) {
+            x->prof.ms[1] += m;
+            x->prof.launches[1] += 1;
+            x->prof.bytes[1] += x->pev[id].bytes;
+            x->launch_log.push_back({1u, 0, x->pev[id].bytes, (double)m});
+        }
+    }
+    x->have = true;
+    return HHT_OK;
+}
+
 hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets, int32_t B, int32_t N,
                        int32_t D, int64_t T, const int64_t* tree_offsets = nullptr, bool prepacked = false) {
     // offsets: per image [B+1] (every point enters each of the image's trees); tree_offsets: per
@@ -833,6 +943,16 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         const int id = prof_begin(x, 0, (uint64_t)n * 12);
         CK(launch_stage(dev_pts, (uint64_t)n, N, (uint32_t*)x->packed.p, (uint32_t*)x->errflag.p, x->st));
         prof_end(x, id);
+    }
+    if (small_eligible(x)) {
+        // latency path: no synchronisation before the traversal; the range check is read with the
+        // results (an out-of-range point still fails the call with HHT_ERANGE, nothing is returned)
+        CK(cudaMemsetAsync(x->stats.p, 0, kStatCount * 8, x->st));
+        std::vector<uint8_t> beta(x->ntrees);
+        for (int t = 0; t < x->ntrees; ++t) beta[t] = x->tree_half[t] == HHT_BETA;
+        TRY(ensure(x, x->beta, x->ntrees));
+        CK(cudaMemcpyAsync(x->beta.p, beta.data(), x->ntrees, cudaMemcpyHostToDevice, x->st));
+        return detect_small(x);
     }
     TRY(coll_allreduce(x, x->errflag.p, x->errflag.p, 1, C_U32, C_MAX));
     CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)x->errflag.p, 1, x->st));
@@ -1461,7 +1581,7 @@ void hht_destroy(hht_ctx* x) {
     fr(x->leaves.b);
     for (Buf* b : {&x->stage_in, &x->packed, &x->errflag, &x->beta, &x->stats, &x->tiles, &x->tilectr, &x->totals,
                    &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv, &x->leafrows, &x->fusedctr, &x->img,
-                   &x->edgeB, &x->edgetiles})
+                   &x->edgeB, &x->edgetiles, &x->small})
         fr(*b);
     if (x->totals_h) cudaFreeHost(x->totals_h);
     if (x->range_h) cudaFreeHost(x->range_h);

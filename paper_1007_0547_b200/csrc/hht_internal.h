@@ -199,6 +199,33 @@ struct RemovalArgs {
     uint64_t total_words;
 };
 cudaError_t launch_removal(const RemovalArgs& a, bool int64, size_t smem_words, cudaStream_t st);
+// Latency path (k_small): the whole level-synchronous traversal of a tiny detection in ONE block.
+struct SmallArgs {
+    const uint32_t* packed;        // staged points
+    const uint64_t* tree_off;      // [ntrees] first point of each tree in `packed`
+    const uint32_t* tree_n;        // [ntrees] points of each tree
+    const uint8_t* tree_beta;
+    uint32_t ntrees;
+    int N, D;
+    uint64_t T;
+    // scratch (capacities from the host's bounds)
+    uint32_t* list[2];             // candidate lists of the current / next frontier
+    uint32_t* f_tree[2];           // frontier (regions split at the current level) and next
+    uint32_t* f_a[2];
+    uint32_t* f_c[2];
+    uint32_t* f_off[2];            // [F + 1] list offsets
+    uint32_t* cv;                  // [4 F] child votes, then split flags / scan
+    uint32_t* cursor;              // [4 F] append cursors of the next lists
+    // outputs
+    Record* const* rec;            // [D + 1] per-level record arrays
+    LeafRec* leaves;
+    unsigned long long* stats;     // kStat* layout (tests, votes, leaves, split[l], visited[l])
+    uint32_t* counts;              // [D + 2] records per level, then leaves (read by the host)
+    uint32_t smem_S, smem_F;       // shared-memory capacities: list entries, frontier regions
+};
+uint64_t small_smem_bytes(uint32_t S, uint32_t F);
+constexpr uint64_t kSmallSmemMax = 220 * 1024;
+cudaError_t launch_small(const SmallArgs& a, bool int64, cudaStream_t st);
 cudaError_t launch_fused(bool int64, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
                           int is_root, RangeInfo* info, uint64_t* chunk_bounds, RangeInfo* info_h, cudaStream_t st);

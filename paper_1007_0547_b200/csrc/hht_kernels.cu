@@ -1256,6 +1256,249 @@ cudaError_t launch_removal(const RemovalArgs& a, bool int64, size_t smem_words, 
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Latency path: a detection whose lists are tiny (the paper's own image sizes) runs as ONE launch of
+// one 1024-thread block that walks every level itself, so a single image costs one kernel instead of
+// ~30 launches and ~10 host synchronisations. Same method and outputs as the multi-kernel path: at
+// each level, one pass over the (region, candidate) pairs counts the 4 child votes with the exact
+// test (0 < G_SW <= s (2ex + 3N), PAPER.md:85 / DESIGN.md §4), a block scan over the children writes
+// their records and the next frontier (strict votes > T) or the leaves at level D, and a
+// second pass appends each candidate to the lists of the split children it crosses.
+// ---------------------------------------------------------------------------------------------
+namespace {
+// exclusive block scan of n values in place (one block of blockDim.x threads), returns the total
+__device__ uint32_t block_scan(uint32_t* v, uint32_t n, uint32_t* s_warp) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < n; base += blockDim.x) {
+        const uint32_t i = base + tid;
+        const uint32_t x = i < n ? v[i] : 0u;
+        uint32_t inc = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+            if (lane >= d) inc += t;
+        }
+        if (lane == 31) s_warp[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            const uint32_t w = lane < nw ? s_warp[lane] : 0u;
+            uint32_t wi = w;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, wi, d);
+                if (lane >= d) wi += t;
+            }
+            if (lane < nw) s_warp[lane] = wi - w;
+            if (lane == 31) s_warp[32] = wi;            // chunk total
+        }
+        __syncthreads();
+        if (i < n) v[i] = carry + s_warp[wid] + inc - x;
+        carry += s_warp[32];
+        __syncthreads();
+    }
+    return carry;
+}
+}  // namespace
+
+template <typename I>
+__global__ void __launch_bounds__(1024) k_small(SmallArgs A) {
+    __shared__ uint32_t s_warp[33];
+    __shared__ uint32_t s_F, s_S;
+    __shared__ unsigned long long s_v[32], s_sv[32];
+    // every per-level array lives in shared memory (the host admits only problems that fit), so the
+    // ~12 dependent phases of a level cost shared-memory, not L2, round trips
+    extern __shared__ uint4 s_small_dyn[];
+    {
+        uint32_t* w = reinterpret_cast<uint32_t*>(s_small_dyn);
+        const uint32_t Sm = A.smem_S, Fm = A.smem_F;
+        A.list[0] = w; w += Sm;
+        A.list[1] = w; w += Sm;
+        for (int b = 0; b < 2; ++b) {
+            A.f_tree[b] = w; w += Fm + 1;
+            A.f_a[b] = w; w += Fm + 1;
+            A.f_c[b] = w; w += Fm + 1;
+            A.f_off[b] = w; w += Fm + 1;
+        }
+        A.cv = w; w += 4 * Fm;
+        A.cursor = w;
+    }
+    const int tid = threadIdx.x;
+    const I N = (I)A.N;
+    const int D = A.D;
+    unsigned long long tests = 0, votes = 0;          // thread 0 accumulates
+    // level 0: roots (every line crosses the root); split iff E > T (reading R6)
+    if (tid == 0) {
+        uint32_t F = 0, S = 0;
+        for (uint32_t t = 0; t < A.ntrees; ++t) {
+            const uint32_t E = A.tree_n[t];
+            A.rec[0][t] = {t, 0, 0, E};
+            tests += E;
+            votes += E;
+            if ((uint64_t)E > A.T) {
+                A.f_tree[0][F] = t; A.f_a[0][F] = 0; A.f_c[0][F] = 0; A.f_off[0][F] = S;
+                S += E;
+                ++F;
+                tests += 4ull * E;                        // the root's 4 child tests per point
+                A.stats[kStatSplit0] += 1;
+            }
+        }
+        A.f_off[0][F] = S;
+        A.counts[0] = A.ntrees;
+        A.stats[kStatVisited0] = A.ntrees;
+        s_F = F;
+        s_S = S;
+    }
+    __syncthreads();
+    // root lists: the trees' points, in frontier order
+    {
+        const uint32_t F = s_F;
+        for (uint32_t r = 0; r < F; ++r) {
+            const uint32_t t = A.f_tree[0][r], o = A.f_off[0][r], n = A.tree_n[t];
+            for (uint32_t i = tid; i < n; i += blockDim.x) A.list[0][o + i] = A.packed[A.tree_off[t] + i];
+        }
+    }
+    __syncthreads();
+    int cur = 0;
+    for (int l = 0; l < D; ++l) {
+        const uint32_t F = s_F, S = s_S;
+        if (F == 0) break;
+        const int sh = D - l;
+        const I Qc = ((I)3 * N) << (sh - 1);
+        const uint32_t* list = A.list[cur];
+        const uint32_t* off = A.f_off[cur];
+        for (uint32_t i = tid; i < 4 * F; i += blockDim.x) A.cv[i] = 0;
+        __syncthreads();
+        // pass 1: child votes
+        for (uint32_t i = tid; i < S; i += blockDim.x) {
+            uint32_t lo = 0, hi = F - 1;                // region of pair i: last r with off[r] <= i
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) / 2;
+                if (off[mid] <= i) lo = mid; else hi = mid - 1;
+            }
+            const uint32_t r = lo, w = list[i];
+            const bool beta = A.tree_beta[A.f_tree[cur][r]] != 0;
+            const I ex = (I)(beta ? (w & 0xFFFFu) : (w >> 16)), ey = (I)(beta ? (w >> 16) : (w & 0xFFFFu));
+            const I i0 = (I)A.f_a[cur][r] << sh, j0 = (I)A.f_c[cur][r] << sh;
+            const I g = ex * (((I)1 << D) - 2 * i0) + (ey << D) + (N << D) - (I)3 * N * j0;   // G(SW)
+            const I Pc = ex << sh, Uc = Pc + Qc;
+            // children NE, NW, SW, SE: SW values g - Pc - Qc, g - Qc, g, g - Pc
+            const I gq[4] = {g - Pc - Qc, g - Qc, g, g - Pc};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (gq[q] > 0 && gq[q] <= Uc) atomicAdd(A.cv + 4 * r + q, 1u);
+        }
+        __syncthreads();
+        // children: records of all, split flags, next frontier / leaves
+        const bool leaf = l + 1 == D;
+        unsigned long long my_v = 0, my_sv = 0;          // this thread's votes / votes of split children
+        for (uint32_t k = tid; k < 4 * F; k += blockDim.x) {
+            const uint32_t r = k >> 2, q = k & 3, v = A.cv[k];
+            const uint32_t ca = 2 * A.f_a[cur][r] + quad_da((int)q), cb = 2 * A.f_c[cur][r] + quad_dc((int)q);
+            A.rec[l + 1][k] = {A.f_tree[cur][r], ca, cb, v};
+            const bool split = (uint64_t)v > A.T;
+            A.cursor[k] = split ? 1u : 0u;                   // split flag, scanned below
+            my_v += v;
+            if (split) my_sv += v;
+        }
+        // block sums of the votes (every visited child) and of the split children's votes
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+            my_v += __shfl_xor_sync(0xFFFFFFFFu, my_v, d);
+            my_sv += __shfl_xor_sync(0xFFFFFFFFu, my_sv, d);
+        }
+        if ((tid & 31) == 0) { s_v[tid >> 5] = my_v; s_sv[tid >> 5] = my_sv; }
+        if (tid == 0) {
+            A.counts[l + 1] = 4 * F;
+            A.stats[kStatVisited0 + l + 1] = 4ull * F;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long bv = 0, bsv = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { bv += s_v[w]; bsv += s_sv[w]; }
+            votes += bv;
+            if (!leaf) tests += 4 * bsv;                     // 4 code evaluations per voter of a split region
+        }
+        const uint32_t nf = block_scan(A.cursor, 4 * F, s_warp);       // cursor[k] = next index
+        // next frontier, list offsets from the votes of the split children
+        const int nxt = cur ^ 1;
+        for (uint32_t k = tid; k < 4 * F; k += blockDim.x) {
+            const uint32_t v = A.cv[k];
+            if ((uint64_t)v > A.T) {
+                const uint32_t f = A.cursor[k], r = k >> 2, q = k & 3;
+                const uint32_t ca = 2 * A.f_a[cur][r] + quad_da((int)q), cb = 2 * A.f_c[cur][r] + quad_dc((int)q);
+                if (leaf) {
+                    A.leaves[f] = {A.f_tree[cur][r], ca, cb, v};
+                } else {
+                    A.f_tree[nxt][f] = A.f_tree[cur][r]; A.f_a[nxt][f] = ca; A.f_c[nxt][f] = cb;
+                    A.f_off[nxt][f] = v;                   // scanned into offsets below
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (leaf) {
+                A.counts[D + 1] = nf;
+                A.stats[kStatLeaves] = nf;
+            } else {
+                A.stats[kStatSplit0 + l + 1] = nf;
+            }
+        }
+        if (leaf) break;
+        const uint32_t S2 = block_scan(A.f_off[nxt], nf, s_warp);
+        if (tid == 0) { A.f_off[nxt][nf] = S2; s_F = nf; s_S = S2; }
+        // cursors of the split children: next-frontier index per child, kNone otherwise
+        for (uint32_t k = tid; k < 4 * F; k += blockDim.x) {
+            const uint32_t f = A.cursor[k];
+            A.cursor[k] = (uint64_t)A.cv[k] > A.T ? f : kNone;
+        }
+        __syncthreads();
+        for (uint32_t k = tid; k < nf; k += blockDim.x) A.cv[k] = 0;      // reuse: append cursors
+        __syncthreads();
+        // pass 2: append each candidate to the lists of the split children it crosses
+        for (uint32_t i = tid; i < S; i += blockDim.x) {
+            uint32_t lo = 0, hi = F - 1;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) / 2;
+                if (off[mid] <= i) lo = mid; else hi = mid - 1;
+            }
+            const uint32_t r = lo, w = list[i];
+            const bool beta = A.tree_beta[A.f_tree[cur][r]] != 0;
+            const I ex = (I)(beta ? (w & 0xFFFFu) : (w >> 16)), ey = (I)(beta ? (w >> 16) : (w & 0xFFFFu));
+            const I i0 = (I)A.f_a[cur][r] << sh, j0 = (I)A.f_c[cur][r] << sh;
+            const I g = ex * (((I)1 << D) - 2 * i0) + (ey << D) + (N << D) - (I)3 * N * j0;
+            const I Pc = ex << sh, Uc = Pc + Qc;
+            const I gq[4] = {g - Pc - Qc, g - Qc, g, g - Pc};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t f = A.cursor[4 * r + q];
+                if (f != kNone && gq[q] > 0 && gq[q] <= Uc)
+                    A.list[nxt][A.f_off[nxt][f] + atomicAdd(A.cv + f, 1u)] = w;
+            }
+        }
+        __syncthreads();
+        cur = nxt;
+    }
+    if (tid == 0) {
+        A.stats[kStatTests] = tests;
+        A.stats[kStatVotes] = votes;
+    }
+}
+
+uint64_t small_smem_bytes(uint32_t S, uint32_t F) { return 4ull * (2ull * S + 8ull * (F + 1) + 8ull * F); }
+
+cudaError_t launch_small(const SmallArgs& a, bool int64, cudaStream_t st) {
+    const int smem = (int)small_smem_bytes(a.smem_S, a.smem_F);
+    if (int64) {
+        cudaFuncSetAttribute(k_small<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_small<int64_t><<<1, 1024, smem, st>>>(a);
+    } else {
+        cudaFuncSetAttribute(k_small<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_small<int32_t><<<1, 1024, smem, st>>>(a);
+    }
+    return cudaGetLastError();
+}
+
 using PassKernel = void (*)(const PassArgs);
 
 static PassKernel tail16_kernel(bool int64, bool pref) {

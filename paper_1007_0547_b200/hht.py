@@ -44,7 +44,8 @@ class HHTError(RuntimeError):
 class Opts(C.Structure):
     _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("halves", C.c_uint32),
                 ("record_levels", C.c_uint32), ("force_int64", C.c_uint32), ("profile", C.c_uint32),
-                ("tail_depth", C.c_uint32), ("prefetch", C.c_uint32), ("variant", C.c_uint32),
+                ("tail_depth", C.c_uint32), ("prefetch", C.c_uint32), ("latency_path", C.c_uint32),
+                ("variant", C.c_uint32),
                 ("mem_budget", C.c_size_t),
                 ("nccl_id", C.c_void_p), ("group", C.c_void_p)]
 
@@ -59,7 +60,7 @@ class Stats(C.Structure):
                 ("visited", C.c_uint64 * 64), ("split", C.c_uint64 * 64), ("h2d_bytes", C.c_uint64),
                 ("d2h_bytes", C.c_uint64), ("levels", C.c_uint32), ("int_bits", C.c_uint32),
                 ("ranges", C.c_uint32), ("images", C.c_uint32), ("ms", C.c_double),
-                ("leaves_streamed", C.c_uint64)]
+                ("leaves_streamed", C.c_uint64), ("latency_path", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class Launch(C.Structure):
@@ -179,7 +180,7 @@ class HHT:
     def __init__(self, device: int = 0, halves: int = ALPHA | BETA, record_levels: bool = True,
                  force_int64: bool = False, profile: bool = False, mem_budget: int = 0,
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, tail_depth: int = 0,
-                 prefetch: int = 0, variant: int = 0, group: Optional["Group"] = None):
+                 prefetch: int = 0, variant: int = 0, group: Optional["Group"] = None, latency_path: int = 0):
         self._lib = load()
         o = Opts()
         self._lib.hht_default_opts(C.byref(o))
@@ -188,6 +189,7 @@ class HHT:
         o.mem_budget = mem_budget
         o.tail_depth = tail_depth
         o.prefetch = prefetch
+        o.latency_path = latency_path
         o.variant = variant
         self._id = None
         if group is not None:
@@ -342,7 +344,8 @@ class HHT:
         return {"tests": s.tests, "votes": s.votes, "leaves": s.leaves, "pairs": s.pairs,
                 "visited": list(s.visited)[:L], "split": list(s.split)[:L], "h2d_bytes": s.h2d_bytes,
                 "d2h_bytes": s.d2h_bytes, "levels": L, "int_bits": s.int_bits, "ranges": s.ranges,
-                "images": s.images, "ms": s.ms, "leaves_streamed": s.leaves_streamed}
+                "images": s.images, "ms": s.ms, "leaves_streamed": s.leaves_streamed,
+                "latency_path": s.latency_path}
 
     def profile(self) -> dict:
         p = Profile()

@@ -1,0 +1,68 @@
+"""Single-image latency on one B200: wall time of one hht_detect call (device-resident points,
+results on the device) and its device time, for the one-launch latency path and the multi-kernel
+path, on config 1 and the paper-scale scenes (32-256 px). Median of --reps calls after warm-up.
+
+    python scripts/latency_bench.py --out profiles/r01_latency.md
+"""
+import argparse
+import os
+import statistics
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_1007_0547_b200 import hht, synth  # noqa: E402
+
+
+def measure(pts, N, D, T, halves, latency_path, reps):
+    h = hht.HHT(halves=halves, latency_path=latency_path)
+    d = torch.from_numpy(pts).cuda()
+    for _ in range(5):
+        h.detect(d, N, D, T)
+    wall, dev = [], []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        h.detect(d, N, D, T)
+        wall.append(1e3 * (time.perf_counter() - t0))
+        dev.append(h.stats()["ms"])
+    return statistics.median(wall), statistics.median(dev), h.stats()["leaves"], h.stats()["latency_path"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=200)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    cases = []
+    cfg = synth.CONFIGS[1]
+    pts, _ = synth.config_image(1)
+    cases.append(("config1 64x64, 220 pts, D=6, T=20, ALPHA", pts, cfg.N, cfg.D, cfg.T, cfg.halves))
+    for N in (32, 64, 128, 256):
+        p, _ = synth.scene(N, 5, max(4, N // 2 + N // 8), 1, max(1, N * N // 50), False, 0x7AB1E1, 100 * N + 1, 7)
+        cases.append((f"{N}x{N} scene, {p.shape[0]} pts, D={N.bit_length() - 1}, T={N // 2}, both", p, N,
+                      N.bit_length() - 1, N // 2, hht.ALPHA | hht.BETA))
+    rows = []
+    for name, p, N, D, T, halves in cases:
+        lw, ld, nl, used = measure(p, N, D, T, halves, 1, a.reps)
+        mw, md, _, _ = measure(p, N, D, T, halves, 2, a.reps)
+        rows.append((name + ("" if used else " (not admitted: multi-kernel)"), nl, lw, ld, mw, md))
+        print(rows[-1], flush=True)
+    lines = ["# Single-image latency on one B200", "",
+             f"Median of {a.reps} hht_detect calls (points already on the device, results left on the device): "
+             "wall time of the call and its device time (CUDA events), one-launch latency path (k_small) "
+             "vs the multi-kernel path. The paper's Table 1 reports 31-484 us per image for its algorithm "
+             "on a 3 GHz Pentium IV at 32-256 px (its images, PAPER.md:274-292).", "",
+             "| input | leaves | auto path wall us | device us | multi-kernel wall us | device us |",
+             "|---|---|---|---|---|---|"]
+    for name, nl, lw, ld, mw, md in rows:
+        lines.append(f"| {name} | {nl} | {1e3 * lw:.0f} | {1e3 * ld:.0f} | {1e3 * mw:.0f} | {1e3 * md:.0f} |")
+    txt = "\n".join(lines) + "\n"
+    print(txt)
+    if a.out:
+        open(a.out, "w").write(txt)
+
+
+if __name__ == "__main__":
+    main()

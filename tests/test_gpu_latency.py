@@ -1,0 +1,91 @@
+"""The one-launch latency path (k_small; opts.latency_path): tiny detections run every level inside
+one 1024-thread block. Its records, leaves and statistics must equal the oracle's and the
+multi-kernel path's, bit for bit."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1007_0547_b200 import hht, synth
+from tests.hht_compare import compare_all
+
+pytestmark = pytest.mark.gpu
+
+AB = hht.ALPHA | hht.BETA
+
+
+def eligible(n_per_tree, D, T):
+    """Mirror of the library's admission rule (hht_driver.cu small_bounds / small_eligible)."""
+    S = max(sum(n_per_tree) * ((1 << D) - 1), 1)
+    F = min(S // (T + 1) + len(n_per_tree) + 1, S + 1)
+    return 4 * (2 * S + 8 * (F + 1) + 8 * F) <= 220 * 1024
+
+
+def _dev(pts, dev):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(pts, dtype=np.int32)).to(dev)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_latency_path_random(seed, cuda_device):
+    rng = np.random.default_rng(2100 + seed)
+    N = int(rng.choice([4, 7, 16, 33, 64, 128, 256]))
+    D = int(rng.integers(1, 7))
+    T = int(rng.choice([1, 2, 3, 8, 20]))
+    halves = [AB, hht.ALPHA, hht.BETA][seed % 3]
+    pts = synth.random_scene(2200 + seed, N, max_lines=4, max_noise=int(rng.choice([10, 100, 400])))
+    ref = oracle.detect(pts, N, D, T, halves)
+    h = hht.HHT(halves=halves, force_int64=bool(seed % 4 == 0))
+    h.detect(_dev(pts, cuda_device), N, D, T)
+    st = h.stats()
+    ntrees = bin(halves).count("1")
+    assert st["latency_path"] == (1 if eligible([len(pts)] * ntrees, D, T) else 0)
+    compare_all(h, ref, halves, D)
+    assert (st["tests"], st["votes"], st["leaves"]) == (ref.tests, ref.votes, ref.leaves.shape[0])
+    hm = hht.HHT(halves=halves, latency_path=2)
+    hm.detect(_dev(pts, cuda_device), N, D, T)
+    sm = hm.stats()
+    assert sm["latency_path"] == 0
+    assert (sm["visited"], sm["split"]) == (st["visited"], st["split"])
+
+
+@pytest.mark.parametrize("cid", [1])
+def test_latency_path_config(cid, cuda_device):
+    cfg = synth.CONFIGS[cid]
+    pts, _ = synth.config_image(cid)
+    h = hht.HHT(halves=cfg.halves)
+    h.detect(_dev(pts, cuda_device), cfg.N, cfg.D, cfg.T)
+    assert h.stats()["latency_path"] == 1
+    compare_all(h, oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves), cfg.halves, cfg.D)
+
+
+@pytest.mark.parametrize("case", ["empty", "below_threshold", "identical", "d1", "n1", "batch"])
+def test_latency_path_edges(case, cuda_device):
+    N, D, T = 16, 4, 2
+    if case == "batch":
+        imgs = [synth.random_scene(2300 + k, 32, max_lines=3, max_noise=k * 30) for k in range(5)]
+        imgs[1] = imgs[1][:0]
+        offs = np.zeros(6, dtype=np.int64)
+        offs[1:] = np.cumsum([len(p) for p in imgs])
+        h = hht.HHT(halves=AB)
+        sink = np.zeros((4096, 5), np.uint32)
+        h.set_leaf_sink(sink)
+        h.detect_batch(_dev(np.concatenate(imgs), cuda_device), offs, 32, 5, 3)
+        assert h.stats()["latency_path"] == 1
+        for b, p in enumerate(imgs):
+            compare_all(h, oracle.detect(p, 32, 5, 3, AB), AB, 5, image=b)
+        n = h.stats()["leaves_streamed"]
+        assert n == h.stats()["leaves"] and np.array_equal(sink[:n].astype(np.int64), h.leaves(-1))
+        return
+    if case == "empty":
+        pts = np.zeros((0, 2), np.int32)
+    elif case == "below_threshold":
+        pts = np.array([[1, 2], [3, 4]], np.int32)
+    elif case == "identical":
+        pts, T = np.array([[5, 9]] * 300, np.int32), 100
+    elif case == "d1":
+        pts, D = synth.random_scene(3, 16, max_noise=40), 1
+    else:
+        pts, N, D, T = np.array([[0, 0]] * 5, np.int32), 1, 3, 1
+    h = hht.HHT(halves=AB)
+    h.detect(_dev(pts, cuda_device), N, D, T)
+    compare_all(h, oracle.detect(pts, N, D, T, AB), AB, D)

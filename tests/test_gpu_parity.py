@@ -31,6 +31,7 @@ def _dev(pts, dev):
 
 
 def _run(pts, N, D, T, halves, dev, **kw):
+    kw.setdefault("latency_path", 2)      # the multi-kernel path; the one-launch path: test_gpu_latency.py
     h = hht.HHT(halves=halves, **kw)
     h.detect(_dev(pts, dev), N, D, T)
     return h
