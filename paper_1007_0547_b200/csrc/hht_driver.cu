@@ -472,10 +472,19 @@ hht_status run_pass(hht_ctx* x, int mode, const PassArgs& a, uint64_t pairs, uin
     return HHT_OK;
 }
 
-// Choose [q0, q1) over the level-lc frontier; W > 1 agrees on the smallest proposal.
-hht_status choose_range(hht_ctx* x, int lc, uint32_t q0, uint64_t cap_entries, bool all, RangeInfo* out) {
+// Choose [q0, q1) over the level-lc frontier; W > 1 agrees on the smallest proposal. The frontier
+// holds the split children of parents R_(lc-1)[r0, r1). When those parents are the whole parent
+// frontier, everything fits and one rank runs, the range is the whole level and its bounds are
+// known on the host (no kernel, no synchronisation); the chunk range then covers all parents.
+hht_status choose_range(hht_ctx* x, int lc, uint32_t q0, uint64_t cap_entries, bool all, RangeInfo* out,
+                        uint32_t r0, uint32_t r1) {
     Level& C = x->lv[lc];
     Level& P = x->lv[lc - 1];
+    if (!multi(x) && q0 == 0 && r0 == 0 && r1 == P.F && (all || C.S <= cap_entries)) {
+        *out = RangeInfo{C.F, 0, C.S, 0, P.C, P.S};
+        CK(launch_set_bounds((uint64_t*)x->bounds.p, 0, P.C, x->st));
+        return HHT_OK;
+    }
     const int id = prof_begin(x, 6, 0);
     CK(launch_range((const uint64_t*)C.off.p, (const uint32_t*)C.parent.p, C.F, q0, cap_entries,
                     all ? C.F : 0, (const uint64_t*)P.off.p, (const uint64_t*)P.choff.p,
@@ -571,8 +580,11 @@ hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_chil
     CK(cudaMemsetAsync(x->dense.p, 0, (size_t)n * kTail16Cells * 4, x->st));
     TRY(ensure(x, x->fusedctr, 256));
     CK(cudaMemsetAsync(x->fusedctr.p, 0, 16, x->st));
-    CK(launch_bounds((const uint64_t*)P.off.p, (const uint64_t*)P.choff.p, (const uint32_t*)P.len.p, r0, r1, l == 0,
-                     (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->range_m, x->st));
+    // streamed pairs: host-known when the parents are the whole level, else from the device
+    const bool host_pairs = r0 == 0 && r1 == P.F;
+    if (!host_pairs)
+        CK(launch_bounds((const uint64_t*)P.off.p, (const uint64_t*)P.choff.p, (const uint32_t*)P.len.p, r0, r1,
+                         l == 0, (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->range_m, x->st));
     PassArgs a = pass_args(x, P, l);
     a.nf = all_children ? nullptr : (const uint32_t*)C.nf.p;
     a.nf_rbase = r0;
@@ -588,10 +600,13 @@ hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_chil
     const int id = prof_begin(x, 3, 0);
     CK(launch_fused(x->int64, a, x->fused_grid[x->int64 ? 1 : 0], x->st));
     prof_end(x, id);
-    CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)((char*)x->fusedctr.p + 8), 2, x->st));
-    TRY(sync(x));
-    const uint64_t pairs = read_mapped(x->range_h).pairs;
-    const uint64_t child_pairs = read_mapped(x->misc_h);
+    uint64_t pairs = P.S, child_pairs = 0;
+    if (!host_pairs || id >= 0) {      // the device counters are read only when needed
+        CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)((char*)x->fusedctr.p + 8), 2, x->st));
+        TRY(sync(x));
+        if (!host_pairs) pairs = read_mapped(x->range_h).pairs;
+        child_pairs = read_mapped(x->misc_h);
+    }
     if (id >= 0) {
         x->pev[id].bytes = pairs * 4 + (uint64_t)n * kTail16Cells * 4;
         // raster steps: 16 leaf columns x 8 instructions per (line, child) pair (see tail()), plus the
@@ -625,7 +640,7 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
     if (lc == x->D - 1) {
         // count-only pass: level-D votes of the children of R_(D-1), then the leaves.
         RangeInfo ri{};
-        TRY(choose_range(x, lc, 0, 0, true, &ri));
+        TRY(choose_range(x, lc, 0, 0, true, &ri, r0, r1));
         TRY(ensure(x, C.votes, 16ull * Fc));
         CK(cudaMemsetAsync(C.votes.p, 0, 16ull * Fc, x->st));
         PassArgs a = pass_args(x, P, l);
@@ -649,7 +664,7 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         const size_t avail = x->budget > active ? x->budget - active : 0;
         const uint64_t cap = (lc == x->D - 2 ? avail : avail / 3) / 4;
         RangeInfo ri{};
-        TRY(choose_range(x, lc, q0, cap, false, &ri));
+        TRY(choose_range(x, lc, q0, cap, false, &ri, r0, r1));
         const uint32_t q1 = (uint32_t)ri.q1;
         const uint64_t entries = ri.s_hi - ri.s_lo;
         if (entries * 4 > avail)

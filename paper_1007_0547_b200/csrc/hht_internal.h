@@ -153,6 +153,7 @@ cudaError_t launch_range(const uint64_t* c_off, const uint32_t* c_parent, uint32
                          const uint64_t* p_choff, const uint32_t* p_len, int p_is_root, RangeInfo* info,
                          uint64_t* chunk_bounds, RangeInfo* info_h, cudaStream_t st);
 cudaError_t launch_copy_u32(uint32_t* dst, const uint32_t* src, uint32_t n, cudaStream_t st);
+cudaError_t launch_set_bounds(uint64_t* bounds, uint64_t lo, uint64_t hi, cudaStream_t st);
 int pass_blocks_per_sm(int mode, bool int64, bool pref, bool circle);
 int tail_blocks_per_sm(bool int64);
 cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_beta, uint32_t H, uint32_t* out,

@@ -1603,6 +1603,15 @@ __global__ void k_bounds(const uint64_t* off, const uint64_t* choff, const uint3
     if (info_h) *info_h = *info;      // mapped host copy: read after a stream sync, no copy engine
 }
 
+__global__ void k_set_bounds(uint64_t* b, uint64_t lo, uint64_t hi) {
+    if (threadIdx.x == 0) { b[0] = lo; b[1] = hi; }
+}
+
+cudaError_t launch_set_bounds(uint64_t* bounds, uint64_t lo, uint64_t hi, cudaStream_t st) {
+    k_set_bounds<<<1, 32, 0, st>>>(bounds, lo, hi);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
                           int is_root, RangeInfo* info, uint64_t* chunk_bounds, RangeInfo* info_h, cudaStream_t st) {
     k_bounds<<<1, 32, 0, st>>>(off, choff, len, r0, r1, is_root, info, chunk_bounds, info_h);

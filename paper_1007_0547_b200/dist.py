@@ -33,7 +33,7 @@ def make_shard(points: np.ndarray, offsets: np.ndarray, rank: int, world: int) -
     Batch (B > 1): whole images, no collective (each rank owns an independent set of trees)."""
     offsets = np.asarray(offsets, dtype=np.int64)
     B = offsets.shape[0] - 1
-    if B > 1 and world > 1:
+    if B > 1:
         lo, hi = shard(B, rank, world)
         p = np.ascontiguousarray(points[offsets[lo]:offsets[hi]])
         return Shard(p, offsets[lo:hi + 1] - offsets[lo], 1, lo, "images")

@@ -105,3 +105,18 @@ def test_two_rank_gloo_host_path():
     for r in range(world):
         assert "error" not in res[r], res[r]
         assert res[r]["additivity"] and res[r]["mismatch_detected"]
+
+
+def test_single_rank_batch_keeps_image_offsets():
+    """One rank, a batch of images: the shard is the whole batch with its own offsets (each image
+    its own trees), never the images concatenated into one point set."""
+    from paper_1007_0547_b200 import dist as hd, synth
+    imgs = [synth.random_scene(200 + b, 16, max_noise=20) for b in range(4)]
+    offs = np.zeros(5, dtype=np.int64)
+    offs[1:] = np.cumsum([len(p) for p in imgs])
+    allp = np.concatenate(imgs).astype(np.int32)
+    sb = hd.make_shard(allp, offs, 0, 1)
+    assert sb.mode == "images" and sb.comm_world == 1 and sb.image_lo == 0
+    assert np.array_equal(sb.offsets, offs) and np.array_equal(sb.points, allp)
+    single = hd.make_shard(imgs[0], [0, len(imgs[0])], 0, 1)
+    assert single.mode == "points" and np.array_equal(single.offsets, [0, len(imgs[0])])
