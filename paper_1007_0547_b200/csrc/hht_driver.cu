@@ -449,15 +449,15 @@ PassArgs pass_args(hht_ctx* x, Level& P, int level) {
     a.D = x->D;
     a.N = x->N;
     a.one = 1;
-    a.tab_stride = 256;   // k_tail16: table slot stride per entry (32 lane copies x 8 B)
-    // floor(y / 3N) = umulhi(y, m) >> (l - 1) for 0 <= y < 2^31, with l = ceil(log2 3N) and
-    // m = ceil(2^(31+l) / 3N) < 2^32 (3N is never a power of two); see floor_div3n_clamp16
+    // 16x16 raster fixed point (Raster16): 2^fx_s >= 32 * 3N > G_SW - 1 of any line crossing a
+    // level-(D-4) region; fx_m = ceil(2^(24+fx_s) / 3N) < 2^30 + 1, fx_mlo = floor(...)
     {
         const uint64_t n3 = 3ull * (uint64_t)x->N;
-        int l = 0;
-        while ((1ull << l) < n3) ++l;
-        a.div_m = (uint32_t)(((1ull << (31 + l)) + n3 - 1) / n3);
-        a.div_s = (uint32_t)(l - 1);
+        int s = 0;
+        while ((1ull << s) < 32 * n3) ++s;
+        a.fx_s = (uint32_t)s;
+        a.fx_m = (uint32_t)(((1ull << (24 + s)) + n3 - 1) / n3);
+        a.fx_mlo = (uint32_t)((1ull << (24 + s)) / n3);
     }
     return a;
 }

@@ -88,8 +88,7 @@ struct PassArgs {
     uint32_t* c_cursor;            // [q1 - q0] append cursors
     uint32_t* c_list;              // output lists
     uint32_t one;                  // == 1 (runtime value: keeps the count adds on the FMA pipe)
-    uint32_t tab_stride;           // == 256 (runtime value, see mad_u32): k_tail16 table entry stride
-    uint32_t div_m, div_s;         // floor(y / 3N) = umulhi(y, div_m) >> div_s for 0 <= y < 2^31
+    uint32_t fx_m, fx_mlo, fx_s;   // 16x16 raster fixed point: ceil / floor(2^(24+fx_s) / 3N), 2^fx_s >= 96N
     uint32_t* votes;               // MODE_COUNT: [4 * nparents] (4*(r - nf_rbase) + q)
                                    // else:       [4 * (q1 - q0)] (4*(nf - q0) + q')
                                    // tails: 256-cell leaf grids per region

@@ -58,30 +58,6 @@ __device__ __forceinline__ void mad_if(bool c, uint32_t& acc, uint32_t one, uint
         : "+r"(acc) : "r"((uint32_t)c), "r"(one), "r"(k));
 }
 
-// a*b + c as an integer multiply-add: keeps pointer / threshold updates on the FMA pipe (the ALU pipe
-// is the binding unit of the raster loops); b is a runtime value so ptxas cannot turn it into a
-// shift + add on the ALU pipe.
-__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t r;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-    return r;
-}
-__device__ __forceinline__ int32_t mad_i(uint32_t a, int32_t b, int32_t c) {
-    int32_t r;
-    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-    return r;
-}
-__device__ __forceinline__ int64_t mad_i(uint32_t a, int64_t b, int64_t c) {
-    int64_t r;
-    asm("mad.lo.s64 %0, %1, %2, %3;" : "=l"(r) : "l"((int64_t)a), "l"(b), "l"(c));
-    return r;
-}
-template <typename I>
-__device__ __forceinline__ uint32_t sign_bit(I v) {
-    using UI = typename Unsigned<I>::type;
-    return (uint32_t)((UI)v >> (8 * sizeof(I) - 1));
-}
-
 // quad index of (da, dc): NE(1,1)=0, NW(0,1)=1, SW(0,0)=2, SE(1,0)=3
 __host__ __device__ constexpr int quad_of(int da, int dc) { return dc ? (da ? 0 : 1) : (da ? 3 : 2); }
 
@@ -577,19 +553,37 @@ __global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
 // each block's 16 counter words are reduced across the warp with a butterfly reduce-scatter
 // (16 shuffles) that leaves every lane with the warp totals of 2 cells.
 // ---------------------------------------------------------------------------------------------
-constexpr int kTab16 = 68;  // (k + 16) * 2 + drop, k in -16..17
+// Fixed-point raster state. For a line of the batch, y_u = G(i0 + u, j0) - 1 at lattice column u of
+// the leaf grid and f_u = floor(y_u / 3N): the line is above lattice corner (u, v) (G > 0) iff
+// v <= f_u, so it crosses cell (u, v) (G_SW > 0 >= G_NE) iff f_(u+1) <= v <= f_u, rows clipped to
+// 0..15 (2ex < 3N, so f drops by 0 or 1 per column). The raster carries Y_u ~ 2^24 (y_u / 3N + 64)
+// in 32 bits: its top byte is f_u + 64, extracted with one PRMT that also inserts the lane's
+// table-copy offset, and the table entry of column u is addressed by the byte sum
+// (f_u + 64) + (f_(u+1) + 64) (= 2 f_u - drop + 128), so a column step is: Y -= P, PRMT, one
+// 3-input add, LDS.64.
+// Exactness: every line of a batch crosses the 16x16 region, so 0 <= y_0 < 16 (2ex +
+// 3N) < 32 * 3N <= 2^fx_s. Y_0 = floor(y_0 fx_m / 2^fx_s) + 1 with fx_m = ceil(2^(24+fx_s) / 3N)
+// exceeds the exact value 2^24 y_0 / 3N by (0, 2); P = floor(2ex fx_mlo / 2^fx_s) with fx_mlo =
+// floor(2^(24+fx_s) / 3N) falls below 2^24 2ex / 3N by [0, 2). So Y_u - 2^24 y_u / 3N lies in
+// (0, 2 + 2u) subset (0, 34) for u <= 16, while a non-multiple of 3N sits at least 2^24 / 3N > 34
+// units (3N < 493447) from the next multiple: floor(Y_u / 2^24) - 64 = f_u exactly. f_u stays in
+// [-16, 26] (f_0 <= 26, one drop per column), so the top byte is never wrapped.
+constexpr int kTab16Lo = 90;    // table entries e = (f_u + 64) + (f_(u+1) + 64) in [90, 192)
+constexpr int kTab16 = 102;
 
 // Column mask of the 16x16 tail as 4-bit counters, one table copy per lane. Logical row
 // v = 8h + 2b + par (h: word, b: byte, par: nibble within the byte) is stored at word h ^ L4, byte
 // b ^ L0, nibble par ^ L3, where Lx is bit x of the lane that owns the copy: the three lane-bit
-// swaps are exactly the register swaps the butterfly reduce-scatter in k_tail16 would otherwise do
-// with selects (levels xor 16, xor 8 and the final xor 1). A lane adds at most kItems = 8 per cell
-// per column block, so nibbles do not overflow; they are widened to bytes before the reduction.
-__device__ __forceinline__ uint2 tab16_entry(int t, int lane) {
-    const int k = t / 2 - 16, d = t & 1;
+// swaps are exactly the register swaps the butterfly reduce-scatter in Raster16 would otherwise do
+// with selects (levels xor 16, xor 8 and the final xor 1). A lane adds at most 7 per cell per column
+// block, so nibbles do not overflow; they are widened to bytes during the reduction.
+__device__ __forceinline__ uint2 tab16_entry(int e, int lane) {
+    const int t = e + kTab16Lo - 128;                  // f_u + f_(u+1) = 2 f_u - drop
+    const int f = t >= 0 ? (t + 1) / 2 : -((-t) / 2);  // f_u = ceil(t / 2)
+    const int fn = t - f;                              // f_(u+1)
     uint32_t w[2] = {0, 0};
-    if (k >= 1) {
-        const int vhi = min(k, 16) - 1, vlo = max(k - d - 1, 0);
+    {
+        const int vhi = min(f, 15), vlo = max(fn, 0);  // crossed rows f_(u+1) .. f_u
         for (int v = vlo; v <= vhi; ++v) {
             const int hp = (v >> 3) ^ ((lane >> 4) & 1);
             const int bp = ((v >> 1) & 3) ^ (lane & 1);
@@ -600,48 +594,27 @@ __device__ __forceinline__ uint2 tab16_entry(int t, int lane) {
     return make_uint2(w[0], w[1]);
 }
 
-// Per-line raster state at the SW corner of R: y = G_SW - 1 (>= 0 for every listed line: it crosses
-// R), f = min(floor(y / 3N), 16) (for int32, a multiply-high by the host-computed reciprocal, exact
-// for 0 <= y < 2^31; for int64 a branch-free binary search), then z = y - f*3N and the table
-// address of entry (k = f + 1, drop 0) in this lane's copy. Lanes past the chunk's end point at
-// the all-zero entries of k = 0.
-template <typename I>
-__device__ __forceinline__ I floor_div3n_clamp16(I y, I N3, uint32_t div_m, uint32_t div_s) {
-    if (sizeof(I) == 4) {
-        const uint32_t q = __umulhi((uint32_t)y, div_m) >> div_s;
-        return (I)min(q, 16u);
-    } else {
-        I f = (y >= (I)8 * N3) ? (I)8 : (I)0;
-        f += (y >= (f + 4) * N3) ? (I)4 : (I)0;
-        f += (y >= (f + 2) * N3) ? (I)2 : (I)0;
-        f += (y >= (f + 1) * N3) ? (I)1 : (I)0;
-        return (y >= (I)16 * N3) ? (I)16 : f;
-    }
-}
-
-// The 16x16 raster of one batch of <= 256 lines (8 per lane) over the leaf grid of one level-(D-4)
-// region (a, c), accumulated into `dst` (256 u32 counters, [16 * column + row]) with one atomic per
+// The 16x16 raster of one batch of <= 32 ITEMS lines over the leaf grid of one level-(D-4) region
+// (a, c), accumulated into `dst` (256 u32 counters, [16 * column + row]) with one atomic per
 // (lane, cell pair) per column block. Shared by the dense tail (batches = chunks of the region's
-// list) and the fused tail (batches = full shared-memory queues of a child of a level-(D-5) region).
+// list) and the fused tail (batches = full shared-memory stacks of a child of a level-(D-5) region).
 template <typename I>
 struct Raster16 {
-    uint32_t ta_zero, ta_base, cdrop, ck2n, ck2, red_u, red_row, div_m, div_s;
+    const char* tab_lo;            // s_tab - kTab16Lo entries: entry e, copy c at tab_lo + 256 e + 8 c
+    uint32_t lane4, red_u, red_row, fx_m, fx_mlo, fx_s;
     int D;
     I N, N3;
 
     __device__ __forceinline__ void init(const PassArgs& A, const uint2* s_tab, int lane) {
-        const uint32_t tab_sm = (uint32_t)__cvta_generic_to_shared(s_tab + lane);
-        cdrop = A.tab_stride;                       // 256, -512, 512 (runtime values, see mad_u32)
-        ck2n = 0u - 2u * A.tab_stride;
-        ck2 = 2u * A.tab_stride;
-        ta_zero = tab_sm + 256u * 32u;              // entry (k = 0, drop 0)
-        ta_base = tab_sm + 256u * 34u;              // entry (k = 1, drop 0)
+        tab_lo = reinterpret_cast<const char*>(s_tab) - kTab16Lo * 256;
+        lane4 = 4u * (uint32_t)lane;                 // two of them add up to the lane's copy offset
         // cells this lane holds after the reduce-scatter: column 4b + u, u = L1 + 2 L2; rows
         // 8 L4 + 2 L0 + L3 (+ 4)
         red_u = ((lane >> 1) & 1) + 2 * ((lane >> 2) & 1);
         red_row = 8 * ((lane >> 4) & 1) + 2 * (lane & 1) + ((lane >> 3) & 1);
-        div_m = A.div_m;
-        div_s = A.div_s;
+        fx_m = A.fx_m;
+        fx_mlo = A.fx_mlo;
+        fx_s = A.fx_s;
         D = A.D;
         N = (I)A.N;
         N3 = (I)3 * N;
@@ -660,21 +633,20 @@ struct Raster16 {
         // byte selectors: ex = low half-word of the packed entry for BETA (x <-> y), high for ALPHA
         const uint32_t sel_ex = beta ? 0x4410u : 0x4432u, sel_ey = beta ? 0x4432u : 0x4410u;
 
-        // per-line raster state carried across the 4 column blocks: z = y - (k-1)*3N (height of the
-        // line above its row's floor at the current lattice column; a column drops iff z < 0), the
-        // shared-memory address of table entry (k, 0) in this lane's copy, and the column step 2ex
-        I z[ITEMS], P8[ITEMS];
-        uint32_t ta[ITEMS];
+        // per-line state carried across the 4 column blocks: Y (fixed point, see above), its
+        // per-column decrement P, and the PRMT'd top byte of the previous column's Y
+        uint32_t Y[ITEMS], P[ITEMS], ak[ITEMS];
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             const uint32_t w = p[it];
             const I ex = (I)__byte_perm(w, 0, sel_ex);
             const I ey = (I)__byte_perm(w, 0, sel_ey);
-            const I yy = ex * alpha + (ey << D) + beta_m1;         // G(SW corner of R) - 1 >= 0
-            const I f = floor_div3n_clamp16<I>(yy, N3, div_m, div_s);
-            P8[it] = 2 * ex;
-            z[it] = yy - f * N3;
-            ta[it] = (lane + kWarp * it < cnt) ? mad_u32((uint32_t)f, ck2, ta_base) : ta_zero;
+            const uint32_t y0 = (uint32_t)(ex * alpha + (ey << D) + beta_m1);    // G(SW corner) - 1
+            const bool valid = lane + kWarp * it < cnt;
+            // lanes past the batch: f = -1 in every column (all-zero entries)
+            Y[it] = valid ? (uint32_t)(((uint64_t)y0 * fx_m) >> fx_s) + 0x40000001u : 0x3F000000u;
+            P[it] = valid ? (uint32_t)(((uint64_t)(2u * (uint32_t)ex) * fx_mlo) >> fx_s) : 0u;
+            ak[it] = __byte_perm(Y[it], lane4, 0x5534u);
         }
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
@@ -685,15 +657,12 @@ struct Raster16 {
             for (int it = 0; it < ITEMS; ++it) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const I zz = z[it] - P8[it];
-                    const uint32_t dr = sign_bit<I>(zz);                // drop: the line left its row
-                    uint32_t mx, my;
-                    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mx), "=r"(my)
-                                 : "r"(mad_u32(dr, cdrop, ta[it])));
-                    acc[2 * u + 0] += mx;
-                    acc[2 * u + 1] += my;
-                    ta[it] = mad_u32(dr, ck2n, ta[it]);                 // k -= drop
-                    z[it] = mad_i(dr, N3, zz);                          // threshold -= drop * 3N
+                    Y[it] -= P[it];
+                    const uint32_t an = __byte_perm(Y[it], lane4, 0x5534u);   // (f + 64) << 8 | 4 lane
+                    const uint2 m = *reinterpret_cast<const uint2*>(tab_lo + (ak[it] + an));
+                    ak[it] = an;
+                    acc[2 * u + 0] += m.x;
+                    acc[2 * u + 1] += m.y;
                 }
             }
             // butterfly reduce-scatter over the lanes: xor 16 pairs the two physical words of a

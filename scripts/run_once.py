@@ -38,7 +38,7 @@ log = h.launches()
 by = {}
 for cls, b, ms in log:
     by.setdefault(cls, []).append((b, ms))
-for cls in ("count", "write", "tail"):
+for cls in ("count", "write", "tail", "split", "gather", "other"):
     xs = by.get(cls, [])
     if xs:
         print(cls, "launches", len(xs), "first bytes", xs[0][0], "bytes[:16]", [b for b, _ in xs[:16]])

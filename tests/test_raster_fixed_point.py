@@ -1,0 +1,55 @@
+"""Model check of the 16x16 raster's fixed-point arithmetic (csrc/hht_kernels.cu, Raster16; DESIGN.md
+§4): the kernel's integer formulas, restated here, reproduce floor(y_u / 3N) exactly at every
+column of every line that crosses a level-(D-4) region, and its table (indexed by the sum of two
+consecutive floors) selects exactly the cells the paper's corner test marks as crossed
+(G_SW > 0 >= G_NE). Pure integer host arithmetic; no GPU, no oracle."""
+import random
+
+import pytest
+
+
+def fx_consts(N):
+    """The host constants of pass_args (csrc/hht_driver.cu)."""
+    n3 = 3 * N
+    s = 0
+    while (1 << s) < 32 * n3:
+        s += 1
+    return s, ((1 << (24 + s)) + n3 - 1) // n3, (1 << (24 + s)) // n3
+
+
+def rows_of_entry(t):
+    """Rows of table entry t = f_u + f_(u+1) (tab16_entry)."""
+    f = (t + 1) // 2 if t >= 0 else -((-t) // 2)
+    fn = t - f
+    return set(range(max(fn, 0), min(f, 15) + 1))
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 16, 64, 511, 512, 1000, 4096, 8192, 32767])
+def test_fixed_point_floor_exact(N):
+    s, m, mlo = fx_consts(N)
+    assert m < (1 << 32) and (1 << 24) // (3 * N) > 34
+    n3 = 3 * N
+    r = random.Random(N)
+    for trial in range(4000):
+        ex = r.randrange(N)
+        lim = 16 * (2 * ex + n3)                  # G_SW - 1 of a line crossing the 16x16 region
+        y0 = r.randrange(lim) if trial % 3 else (r.randrange(27) * n3) % lim
+        Y = ((y0 * m) >> s) + 0x40000001
+        P = (2 * ex * mlo) >> s
+        for u in range(17):
+            Yu = (Y - u * P) & 0xFFFFFFFF
+            assert (Yu >> 24) - 64 == (y0 - u * 2 * ex) // n3, (N, ex, y0, u)
+
+
+@pytest.mark.parametrize("N", [4, 16, 512, 8192])
+def test_table_rows_match_corner_test(N):
+    n3 = 3 * N
+    r = random.Random(7 + N)
+    for _ in range(1500):
+        ex = r.randrange(N)
+        y0 = r.randrange(16 * (2 * ex + n3))
+        for u in range(16):
+            yu, yn = y0 - 2 * ex * u, y0 - 2 * ex * (u + 1)
+            direct = {v for v in range(16) if yu - n3 * v >= 0 and yn - n3 * (v + 1) < 0}
+            assert rows_of_entry(yu // n3 + yn // n3) == direct
+    assert rows_of_entry(-2) == set()             # lanes past the batch: f = -1 in every column
