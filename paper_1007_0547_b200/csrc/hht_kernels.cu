@@ -556,20 +556,22 @@ __global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
 // Fixed-point raster state. For a line of the batch, y_u = G(i0 + u, j0) - 1 at lattice column u of
 // the leaf grid and f_u = floor(y_u / 3N): the line is above lattice corner (u, v) (G > 0) iff
 // v <= f_u, so it crosses cell (u, v) (G_SW > 0 >= G_NE) iff f_(u+1) <= v <= f_u, rows clipped to
-// 0..15 (2ex < 3N, so f drops by 0 or 1 per column). The raster carries Y_u ~ 2^24 (y_u / 3N + 64)
-// in 32 bits: its top byte is f_u + 64, extracted with one PRMT that also inserts the lane's
-// table-copy offset, and the table entry of column u is addressed by the byte sum
-// (f_u + 64) + (f_(u+1) + 64) (= 2 f_u - drop + 128), so a column step is: Y -= P, PRMT, one
-// 3-input add, LDS.64.
+// 0..15 (2ex < 3N, so f drops by 0 or 1 per column). The raster carries Y_u ~ 2^24 (y_u / 3N + B)
+// in 32 bits, B a per-block bias: its top byte is f_u + B. One PRMT per column boundary turns Y_u
+// into X_u = (f_u + B) << 8 | 4 lane, plus (at even boundaries) the table's 64 KB-aligned base H,
+// and the table entry of column u (t = f_u + f_(u+1) = 2 f_u - drop, lane copy) sits at
+// X_u + X_(u+1) = H + 256 (t + 2B) + 8 lane: a column step is Y -= P, PRMT, one 2-input add (an
+// integer multiply-add by a runtime 1, FMA pipe), LDS.64.
 // Exactness: every line of a batch crosses the 16x16 region, so 0 <= y_0 < 16 (2ex +
 // 3N) < 32 * 3N <= 2^fx_s. Y_0 = floor(y_0 fx_m / 2^fx_s) + 1 with fx_m = ceil(2^(24+fx_s) / 3N)
 // exceeds the exact value 2^24 y_0 / 3N by (0, 2); P = floor(2ex fx_mlo / 2^fx_s) with fx_mlo =
 // floor(2^(24+fx_s) / 3N) falls below 2^24 2ex / 3N by [0, 2). So Y_u - 2^24 y_u / 3N lies in
 // (0, 2 + 2u) subset (0, 34) for u <= 16, while a non-multiple of 3N sits at least 2^24 / 3N > 34
-// units (3N < 493447) from the next multiple: floor(Y_u / 2^24) - 64 = f_u exactly. f_u stays in
-// [-16, 26] (f_0 <= 26, one drop per column), so the top byte is never wrapped.
-constexpr int kTab16Lo = 90;    // table entries e = (f_u + 64) + (f_(u+1) + 64) in [90, 192)
-constexpr int kTab16 = 102;
+// units (3N < 493447) from the next multiple: floor(Y_u / 2^24) - B = f_u exactly. f_u stays in
+// [-16, 26] (f_0 <= 26, one drop per column) and B in [17, 145], so the top byte never wraps.
+constexpr int kTab16TLo = -34;  // table entries t = f_u + f_(u+1) in [-34, 56)
+constexpr int kTab16 = 90;
+constexpr int kTab16Slots = (kTab16 + 2) * 32;   // + 2 entries of slack for the placement below
 
 // Column mask of the 16x16 tail as 4-bit counters, one table copy per lane. Logical row
 // v = 8h + 2b + par (h: word, b: byte, par: nibble within the byte) is stored at word h ^ L4, byte
@@ -577,8 +579,7 @@ constexpr int kTab16 = 102;
 // swaps are exactly the register swaps the butterfly reduce-scatter in Raster16 would otherwise do
 // with selects (levels xor 16, xor 8 and the final xor 1). A lane adds at most 7 per cell per column
 // block, so nibbles do not overflow; they are widened to bytes during the reduction.
-__device__ __forceinline__ uint2 tab16_entry(int e, int lane) {
-    const int t = e + kTab16Lo - 128;                  // f_u + f_(u+1) = 2 f_u - drop
+__device__ __forceinline__ uint2 tab16_entry(int t, int lane) {
     const int f = t >= 0 ? (t + 1) / 2 : -((-t) / 2);  // f_u = ceil(t / 2)
     const int fn = t - f;                              // f_(u+1)
     uint32_t w[2] = {0, 0};
@@ -594,20 +595,47 @@ __device__ __forceinline__ uint2 tab16_entry(int e, int lane) {
     return make_uint2(w[0], w[1]);
 }
 
+// The raster's table (static shared memory of the kernels that raster) and its placement: with S
+// its shared address, H = S rounded down to 64 KB and 2B the smallest even number >= ceil((S - H) /
+// 256) - kTab16TLo, entry t of lane copy c lives at H + 256 (t + 2B) + 8 c, inside the array
+// (0 <= H + 256 (kTab16TLo + 2B) - S < 512).
+__shared__ uint2 s_tab16[kTab16Slots];
+
+struct Tab16Place {
+    uint32_t H, B;
+};
+
+__device__ __forceinline__ Tab16Place tab16_place() {
+    const uint32_t S = (uint32_t)__cvta_generic_to_shared(s_tab16);
+    const uint32_t H = S & 0xFFFF0000u;
+    uint32_t twoB = ((S - H + 255u) >> 8) + (uint32_t)(-kTab16TLo);
+    twoB += twoB & 1u;
+    return {H, twoB >> 1};
+}
+
+__device__ __forceinline__ void fill_tab16() {
+    const Tab16Place pl = tab16_place();
+    const uint32_t first = pl.H + 256u * (uint32_t)(kTab16TLo + 2 * (int)pl.B);
+    for (int i = threadIdx.x; i < kTab16 * 32; i += blockDim.x) {
+        const uint2 e = tab16_entry(kTab16TLo + (i >> 5), i & 31);
+        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" :: "r"(first + 8u * (uint32_t)i), "r"(e.x), "r"(e.y) : "memory");
+    }
+}
+
 // The 16x16 raster of one batch of <= 32 ITEMS lines over the leaf grid of one level-(D-4) region
 // (a, c), accumulated into `dst` (256 u32 counters, [16 * column + row]) with one atomic per
 // (lane, cell pair) per column block. Shared by the dense tail (batches = chunks of the region's
 // list) and the fused tail (batches = full shared-memory stacks of a child of a level-(D-5) region).
 template <typename I>
 struct Raster16 {
-    const char* tab_lo;            // s_tab - kTab16Lo entries: entry e, copy c at tab_lo + 256 e + 8 c
-    uint32_t lane4, red_u, red_row, fx_m, fx_mlo, fx_s;
+    uint32_t lane_h, bias, red_u, red_row, fx_m, fx_mlo, fx_s, one;
     int D;
     I N, N3;
 
-    __device__ __forceinline__ void init(const PassArgs& A, const uint2* s_tab, int lane) {
-        tab_lo = reinterpret_cast<const char*>(s_tab) - kTab16Lo * 256;
-        lane4 = 4u * (uint32_t)lane;                 // two of them add up to the lane's copy offset
+    __device__ __forceinline__ void init(const PassArgs& A, int lane) {
+        const Tab16Place pl = tab16_place();
+        lane_h = pl.H | (4u * (uint32_t)lane);       // byte 0: half the lane's copy offset; bytes 2-3: H
+        bias = (pl.B << 24) + 1u;                    // Y_0 = floor(...) + 1 + B 2^24
         // cells this lane holds after the reduce-scatter: column 4b + u, u = L1 + 2 L2; rows
         // 8 L4 + 2 L0 + L3 (+ 4)
         red_u = ((lane >> 1) & 1) + 2 * ((lane >> 2) & 1);
@@ -615,9 +643,16 @@ struct Raster16 {
         fx_m = A.fx_m;
         fx_mlo = A.fx_mlo;
         fx_s = A.fx_s;
+        one = A.one;
         D = A.D;
         N = (I)A.N;
         N3 = (I)3 * N;
+    }
+
+    // X_j of column boundary j: (f_j + B) << 8 | 4 lane, plus H at even j (exactly one of two
+    // neighbouring boundaries carries the table base)
+    __device__ __forceinline__ uint32_t boundary(uint32_t Yj, int j) const {
+        return __byte_perm(Yj, lane_h, (j & 1) ? 0x5534u : 0x7634u);
     }
 
     // ITEMS lines per lane (a batch of <= 32 ITEMS). ITEMS <= 7 keeps every per-lane cell count
@@ -634,8 +669,8 @@ struct Raster16 {
         const uint32_t sel_ex = beta ? 0x4410u : 0x4432u, sel_ey = beta ? 0x4432u : 0x4410u;
 
         // per-line state carried across the 4 column blocks: Y (fixed point, see above), its
-        // per-column decrement P, and the PRMT'd top byte of the previous column's Y
-        uint32_t Y[ITEMS], P[ITEMS], ak[ITEMS];
+        // per-column decrement P, and X of the previous column boundary
+        uint32_t Y[ITEMS], P[ITEMS], X[ITEMS];
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             const uint32_t w = p[it];
@@ -644,9 +679,9 @@ struct Raster16 {
             const uint32_t y0 = (uint32_t)(ex * alpha + (ey << D) + beta_m1);    // G(SW corner) - 1
             const bool valid = lane + kWarp * it < cnt;
             // lanes past the batch: f = -1 in every column (all-zero entries)
-            Y[it] = valid ? (uint32_t)(((uint64_t)y0 * fx_m) >> fx_s) + 0x40000001u : 0x3F000000u;
+            Y[it] = valid ? (uint32_t)(((uint64_t)y0 * fx_m) >> fx_s) + bias : bias - (1u << 24) - 1u;
             P[it] = valid ? (uint32_t)(((uint64_t)(2u * (uint32_t)ex) * fx_mlo) >> fx_s) : 0u;
-            ak[it] = __byte_perm(Y[it], lane4, 0x5534u);
+            X[it] = boundary(Y[it], 0);
         }
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
@@ -658,11 +693,13 @@ struct Raster16 {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     Y[it] -= P[it];
-                    const uint32_t an = __byte_perm(Y[it], lane4, 0x5534u);   // (f + 64) << 8 | 4 lane
-                    const uint2 m = *reinterpret_cast<const uint2*>(tab_lo + (ak[it] + an));
-                    ak[it] = an;
-                    acc[2 * u + 0] += m.x;
-                    acc[2 * u + 1] += m.y;
+                    const uint32_t xn = boundary(Y[it], 1 + u);   // boundary 4b + u + 1 (4b is even)
+                    uint32_t addr, mx, my;
+                    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(X[it]), "r"(one), "r"(xn));
+                    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mx), "=r"(my) : "r"(addr));
+                    X[it] = xn;
+                    acc[2 * u + 0] += mx;
+                    acc[2 * u + 1] += my;
                 }
             }
             // butterfly reduce-scatter over the lanes: xor 16 pairs the two physical words of a
@@ -711,12 +748,11 @@ template <typename I, bool PREF>
 __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) {
     // table entry e of lane copy c at slot 32e + c: an LDS.64 serves 16 lanes per wavefront and
     // every lane reads its own bank pair, so lookups never conflict whatever entries lanes need
-    __shared__ uint2 s_tab[kTab16 * 32];
-    for (int t = threadIdx.x; t < kTab16 * 32; t += blockDim.x) s_tab[t] = tab16_entry(t >> 5, t & 31);
+    fill_tab16();
     __syncthreads();
     const int lane = threadIdx.x & 31;
     Raster16<I> R;
-    R.init(A, s_tab, lane);
+    R.init(A, lane);
     chunk_loop<PREF>(A, lane, [&](const ChunkDesc& d, const uint32_t (&p)[kItems]) {
         R.template run<kItems>(p, (int)d.cnt, d.a, d.c, d.beta, A.votes + (uint64_t)(d.r - A.nf_rbase) * kTail16Cells, lane);
     });
@@ -735,20 +771,19 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
 constexpr int kQ = 512;                           // stack capacity per child: < 224 left + <= 256 pushed
 constexpr int kFusedItems = 7;                    // raster batches of 7 lines per lane (224 entries)
 constexpr uint32_t kFusedBatch = kWarp * kFusedItems;
-constexpr int kFusedSmem = kTab16 * 32 * 8 + 8 * 4 * kQ * 4;
+constexpr int kFusedSmem = 8 * 4 * kQ * 4;       // dynamic: the stacks (the table is static)
 
 template <typename I>
 __global__ void __launch_bounds__(256, 2) k_fused(const PassArgs A) {
     extern __shared__ uint4 s_dyn[];
-    uint2* s_tab = reinterpret_cast<uint2*>(s_dyn);
-    uint32_t* s_q = reinterpret_cast<uint32_t*>(s_tab + kTab16 * 32);
-    for (int t = threadIdx.x; t < kTab16 * 32; t += blockDim.x) s_tab[t] = tab16_entry(t >> 5, t & 31);
+    uint32_t* s_q = reinterpret_cast<uint32_t*>(s_dyn);
+    fill_tab16();
     __syncthreads();
     const int lane = threadIdx.x & 31;
     uint32_t* Q = s_q + (threadIdx.x >> 5) * (4 * kQ);
     const uint32_t q_sa = (uint32_t)__cvta_generic_to_shared(Q);
     Raster16<I> R;
-    R.init(A, s_tab, lane);
+    R.init(A, lane);
     const int D = A.D;
     const int sh = D - A.level;                       // == 5: parent side 32 lattice steps
     const I N = (I)A.N;

@@ -34,11 +34,12 @@ def test_fixed_point_floor_exact(N):
         ex = r.randrange(N)
         lim = 16 * (2 * ex + n3)                  # G_SW - 1 of a line crossing the 16x16 region
         y0 = r.randrange(lim) if trial % 3 else (r.randrange(27) * n3) % lim
-        Y = ((y0 * m) >> s) + 0x40000001
+        B = r.randrange(17, 146)                  # the per-block bias (tab16_place)
+        Y = ((y0 * m) >> s) + 1 + (B << 24)
         P = (2 * ex * mlo) >> s
         for u in range(17):
             Yu = (Y - u * P) & 0xFFFFFFFF
-            assert (Yu >> 24) - 64 == (y0 - u * 2 * ex) // n3, (N, ex, y0, u)
+            assert (Yu >> 24) - B == (y0 - u * 2 * ex) // n3, (N, ex, y0, u)
 
 
 @pytest.mark.parametrize("N", [4, 16, 512, 8192])
@@ -53,3 +54,28 @@ def test_table_rows_match_corner_test(N):
             direct = {v for v in range(16) if yu - n3 * v >= 0 and yn - n3 * (v + 1) < 0}
             assert rows_of_entry(yu // n3 + yn // n3) == direct
     assert rows_of_entry(-2) == set()             # lanes past the batch: f = -1 in every column
+
+
+def test_table_placement():
+    """tab16_place / fill_tab16 / Raster16::boundary: for any 8-byte aligned table address S, the
+    entries H + 256 (t + 2B) + 8 c (t in [-34, 56), c < 32) lie inside the array, B keeps every top
+    byte f + B (f in [-17, 26]) inside 1..255, and X_u + X_(u+1) (one of them carrying H) is that
+    address."""
+    t_lo, n_tab, slots = -34, 90, (90 + 2) * 32
+    r = random.Random(3)
+    for _ in range(20000):
+        S = r.randrange(0, 1 << 24) * 8 + (r.randrange(4) << 24)
+        H = S & 0xFFFF0000
+        two_b = ((S - H + 255) >> 8) - t_lo
+        two_b += two_b & 1
+        B = two_b >> 1
+        assert 17 <= B <= 145
+        first = H + 256 * (t_lo + 2 * B)
+        assert S <= first and first + 256 * n_tab <= S + 8 * slots
+        lane = r.randrange(32)
+        f0 = r.randrange(-16, 27)
+        f1 = f0 - r.randrange(2)
+        lane_h = H | (4 * lane)
+        x0 = ((f0 + B) << 8) | (lane_h & 0xFF) | (lane_h & 0xFFFF0000)   # even boundary: with H
+        x1 = ((f1 + B) << 8) | (lane_h & 0xFF)                           # odd boundary
+        assert 0 < f1 + B < 256 and x0 + x1 == first + 256 * (f0 + f1 - t_lo) + 8 * lane
