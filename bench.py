@@ -284,9 +284,16 @@ def main():
         sms, mhz, mhz_src = _issue_clock(local)
         ipeak = sms * 4 * 32 * mhz * 1e6 / 1e12
         ach = (d["ops"] / nl) / (avg_ms / 1e3) / 1e12
+        # the raster's other bound: one 8-byte column-mask lookup per lane step (ops = 8 per step)
+        # against the shared-memory data path, 128 B / clock / SM
+        speak = sms * 128 * mhz * 1e6 / 1e12
+        sach = (d["ops"] / 8 * 8 / nl) / (avg_ms / 1e3) / 1e12
+        smem = {"achieved": sach, "peak": speak, "unit": "TB/s", "frac": sach / speak,
+                "peak_source": f"{sms} SMs x 128 B x {mhz:.0f} MHz",
+                "algorithmic_bytes_per_launch": d["ops"] / nl, "note": "table lookups only (8 B per lane step)"}
         roofline = {"bound": "alu", "achieved": ach, "peak": ipeak, "unit": "Tinstr/s", "frac": ach / ipeak,
                     "traffic": traffic, "peak_source": f"{sms} SMs x 4 SMSP x 32 lanes x {mhz:.0f} MHz ({mhz_src})",
-                    "algorithmic_instr_per_launch": d["ops"] / nl, **common, "hbm": hbm}
+                    "algorithmic_instr_per_launch": d["ops"] / nl, **common, "hbm": hbm, "smem": smem}
     else:
         roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                     "frac": achieved_gbs / peak, "traffic": traffic, "peak_source": peak_kind,

@@ -103,6 +103,7 @@ struct hht_ctx {
     int tail_grid[2] = {};
     int tail16_grid[2] = {};
     int fused_grid[2] = {};
+    int split_grid = 0;             // resident k_split blocks (persistent tile loop)
     bool pref_pass = true, pref_tail = true;   // opts.prefetch (0 = auto)
     bool circle = false;                       // opts.variant == HHT_FHT_CIRCLE
     int grid_circle[3][2] = {};
@@ -414,7 +415,7 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
     a.ntiles = ntiles;
     const uint64_t bytes = (uint64_t)Fp * (16 + (VL != V ? 16 : 0) + 12 + (leaf ? 0 : 16) + (record ? 64 : 0));
     const int id = prof_begin(x, 4, bytes);
-    CK(launch_split(a, x->st));
+    CK(launch_split(a, x->split_grid, x->st));
     prof_end(x, id);
     TRY(sync(x));
     const Totals t = read_mapped(x->totals_h);
@@ -1226,6 +1227,7 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     for (int w = 0; w < 2; ++w) x->tail_grid[w] = x->sms * tail_blocks_per_sm(w == 1);
     for (int w = 0; w < 2; ++w) x->tail16_grid[w] = x->sms * tail16_blocks_per_sm(w == 1, x->pref_tail);
     for (int w = 0; w < 2; ++w) x->fused_grid[w] = x->sms * fused_blocks_per_sm(w == 1);
+    x->split_grid = x->sms * split_blocks_per_sm();
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return fail(HHT_ECUDA);
     x->budget = o.mem_budget ? o.mem_budget : (size_t)(0.70 * (double)fr);

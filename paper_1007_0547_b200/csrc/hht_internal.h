@@ -142,7 +142,8 @@ struct RangeInfo {
 cudaError_t launch_stage(const int32_t* pts, uint64_t n, int N, uint32_t* packed, uint32_t* err,
                          cudaStream_t st);
 cudaError_t launch_pass(int mode, bool int64, bool pref, bool circle, const PassArgs& a, int grid, cudaStream_t st);
-cudaError_t launch_split(const SplitArgs& a, cudaStream_t st);
+cudaError_t launch_split(const SplitArgs& a, int resident_blocks, cudaStream_t st);
+int split_blocks_per_sm();
 constexpr uint32_t kSplitPrescanTiles = 1024;   // reduce-then-scan split from this many tiles on
 cudaError_t launch_chunk_map(const uint64_t* choff, const uint64_t* off, const uint32_t* len, const uint32_t* a,
                              const uint32_t* c, const uint32_t* tree, const uint8_t* tree_beta, uint32_t F,

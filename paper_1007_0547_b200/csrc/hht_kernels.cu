@@ -1747,221 +1747,246 @@ __device__ __forceinline__ void publish(TileDesc* t, Agg v, uint32_t status) {
 
 }  // namespace
 
+// Persistent blocks walk the tiles (pass 0: in the order a device counter hands them out, so every
+// tile a look-back waits on is held by a running block; passes 1-2: strided); the per-block vote /
+// leaf / test statistics are flushed with one set of atomics per block instead of per tile.
 __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
     __shared__ Agg s_warp[kSplitThreads / 32];
     __shared__ Agg s_prefix;
     __shared__ uint32_t s_tile;
-    __shared__ unsigned long long s_stat[3];    // votes, split-or-leaf count, 4 * split votes
-    __shared__ uint4 s_rec[kSplitThreads / 32][128];   // per-warp record staging (4 per parent)
+    __shared__ uint4 s_rec[kSplitThreads / 32][128];   // per-warp record staging (4 per parent, swizzled)
     __shared__ uint4 s_leaf[kSplitThreads / 32][128];  // per-warp leaf staging (leaf level)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) {
-        // dynamic tile order for the look-back (predecessors are running); static for the 2 passes
-        s_tile = A.pass == 0 ? atomicAdd(A.tile_counter, 1u) : blockIdx.x;
-        s_stat[0] = s_stat[1] = s_stat[2] = 0;
-    }
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const uint32_t p = tile * kSplitThreads + tid;
-    const bool valid = p < A.Fp;
+    unsigned long long st_votes = 0, st_split = 0, st_tests = 0, st_visited = 0;   // lane-0 partials
 
-    uint4 V = make_uint4(0, 0, 0, 0), VL = V;
-    uint32_t tree = 0, pa = 0, pc = 0;
-    if (valid) {
-        V = __ldg(reinterpret_cast<const uint4*>(A.V) + p);
-        VL = (A.VL == A.V) ? V : __ldg(reinterpret_cast<const uint4*>(A.VL) + p);
-        tree = __ldg(A.p_tree + p);
-        pa = __ldg(A.p_a + p);
-        pc = __ldg(A.p_c + p);
-    }
-    if (valid && A.derive_ne) {   // votes(parent) = votes(SW child) + votes(NE child)
-        V.x = __ldg(A.p_votes + p) - V.z;
-        VL.x = __ldg(A.p_len + p) - VL.z;
-    }
-    const uint32_t v[4] = {V.x, V.y, V.z, V.w};
-    const uint32_t vl[4] = {VL.x, VL.y, VL.z, VL.w};
-    uint32_t flag[4], len[4], nch[4];
-    Agg mine = {0, 0, 0};
-    unsigned long long my_votes = 0, my_tests = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        flag[q] = (valid && (uint64_t)v[q] > A.T) ? 1u : 0u;          // strict: votes > THRESHOLD
-        len[q] = (flag[q] && A.need_lists) ? vl[q] : 0u;   // list entries on this rank
-        nch[q] = (len[q] + kChunk - 1) / kChunk;
-        mine.F += flag[q];
-        mine.C += nch[q];
-        mine.S += len[q];
-        my_votes += v[q];
-        if (flag[q]) my_tests += 4ull * v[q];
-    }
+    for (uint32_t iter = 0;; ++iter) {
+        if (tid == 0) s_tile = A.pass == 0 ? atomicAdd(A.tile_counter, 1u) : blockIdx.x + iter * gridDim.x;
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        if (tile >= A.ntiles) break;
+        const uint32_t p = tile * kSplitThreads + tid;
+        const bool valid = p < A.Fp;
 
-    // block scan
-    const Agg incl = warp_inclusive(mine, lane);
-    if (lane == 31) s_warp[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-        Agg w = lane < kSplitThreads / 32 ? s_warp[lane] : Agg{0, 0, 0};
-        const Agg wi = warp_inclusive(w, lane);
-        if (lane < kSplitThreads / 32) s_warp[lane] = {wi.F - w.F, wi.C - w.C, wi.S - w.S};  // exclusive
-        const Agg block_total = {__shfl_sync(kFull, wi.F, 31), __shfl_sync(kFull, wi.C, 31), shfl_u64(wi.S, 31)};
-        Agg excl = {0, 0, 0};
-        if (A.pass == 1) {                            // aggregates only (k_split_scan orders the tiles)
-            if (lane == 0) {
-                A.tiles[tile].aggF = block_total.F;
-                A.tiles[tile].aggC = block_total.C;
-                A.tiles[tile].aggS = block_total.S;
-            }
-        } else if (A.pass == 2) {                     // the exclusive tile prefix is precomputed
-            excl = {A.tiles[tile].incF, A.tiles[tile].incC, A.tiles[tile].incS};
-        } else if (tile == 0) {
-            // decoupled look-back (warp-wide window of 32 predecessors)
-            if (lane == 0) publish(A.tiles + 0, block_total, 2);
-        } else {
-            if (lane == 0) publish(A.tiles + tile, block_total, 1);
-            int64_t pred = (int64_t)tile - 1;
-            while (true) {
-                const int64_t t = pred - lane;
-                uint32_t st = 2;
-                Agg val = {0, 0, 0};
-                if (t >= 0) {
-                    TileDesc* d = A.tiles + t;
-                    // relaxed spin (no L1 invalidation per poll), then one acquire fence: the
-                    // payload was stored before the status with release semantics
-                    do { st = dev_u32(d->status).load(cuda::memory_order_relaxed); } while (st == 0);
-                    cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
-                    if (st == 1) {
-                        val = {dev_u32(d->aggF).load(cuda::memory_order_relaxed),
-                               dev_u32(d->aggC).load(cuda::memory_order_relaxed),
-                               dev_u64(d->aggS).load(cuda::memory_order_relaxed)};
-                    } else {
-                        val = {dev_u32(d->incF).load(cuda::memory_order_relaxed),
-                               dev_u32(d->incC).load(cuda::memory_order_relaxed),
-                               dev_u64(d->incS).load(cuda::memory_order_relaxed)};
-                    }
-                }
-                const uint32_t pm = __ballot_sync(kFull, st == 2);
-                const int stop = pm ? __ffs(pm) - 1 : 31;    // nearest predecessor with a prefix
-                if (lane > stop) val = {0, 0, 0};
-                excl = agg_add(excl, warp_total(val));
-                if (pm) break;
-                pred -= 32;
-            }
-            if (lane == 0) publish(A.tiles + tile, agg_add(excl, block_total), 2);
-        }
-        if (lane == 0) {
-            s_prefix = excl;
-            if (A.pass == 0 && tile == A.ntiles - 1) {
-                const Agg tot = agg_add(excl, block_total);
-                A.totals->F = tot.F;
-                A.totals->S = tot.S;
-                A.totals->C = tot.C;
-                if (!A.leaf_level) {
-                    A.out.off[tot.F] = tot.S;
-                    A.out.choff[tot.F] = tot.C;
-                }
+        uint4 V = make_uint4(0, 0, 0, 0), VL = V;
+        uint32_t tree = 0, pa = 0, pc = 0;
+        if (valid) {
+            V = __ldg(reinterpret_cast<const uint4*>(A.V) + p);
+            VL = (A.VL == A.V) ? V : __ldg(reinterpret_cast<const uint4*>(A.VL) + p);
+            if (A.pass != 1) {
+                tree = __ldg(A.p_tree + p);
+                pa = __ldg(A.p_a + p);
+                pc = __ldg(A.p_c + p);
             }
         }
-    }
-    __syncthreads();
-    if (A.pass == 1) return;
-    const Agg base = agg_add(agg_add(s_prefix, s_warp[wid]), Agg{incl.F - mine.F, incl.C - mine.C, incl.S - mine.S});
-
-    // the warp's leaves are the contiguous range [f_w, f_w + n_w): staged, then stored coalesced
-    const uint32_t f_w = __shfl_sync(kFull, base.F, 0);
-    if (valid) {
-        uint32_t f = base.F, cc = base.C;
-        uint64_t s = base.S;
-        uint32_t nf4[4];
-        uint64_t so[4];
+        if (valid && A.derive_ne) {   // votes(parent) = votes(SW child) + votes(NE child)
+            V.x = __ldg(A.p_votes + p) - V.z;
+            VL.x = __ldg(A.p_len + p) - VL.z;
+        }
+        const uint32_t v[4] = {V.x, V.y, V.z, V.w};
+        const uint32_t vl[4] = {VL.x, VL.y, VL.z, VL.w};
+        uint32_t flag[4], len[4], nch[4];
+        Agg mine = {0, 0, 0};
+        unsigned long long my_votes = 0, my_tests = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const uint32_t ca = 2 * pa + quad_da(q), cb = 2 * pc + quad_dc(q);
-            nf4[q] = kNone;
-            so[q] = s;
-            if (flag[q]) {
-                if (A.leaf_level) {
-                    s_leaf[wid][f - f_w] = make_uint4(tree, ca, cb, v[q]);
-                } else {
-                    nf4[q] = f;
-                    A.out.tree[f] = tree;
-                    A.out.a[f] = ca;
-                    A.out.c[f] = cb;
-                    A.out.parent[f] = A.parent_base + p;
-                    A.out.len[f] = vl[q];
-                    A.out.votes[f] = v[q];
-                    A.out.off[f] = s;
-                    A.out.choff[f] = cc;
-                }
-                f += 1;
-                s += len[q];
-                cc += nch[q];
-            }
-            if (A.record) s_rec[wid][4 * lane + q] = make_uint4(tree, ca, cb, v[q]);
+            flag[q] = (valid && (uint64_t)v[q] > A.T) ? 1u : 0u;          // strict: votes > THRESHOLD
+            len[q] = (flag[q] && A.need_lists) ? vl[q] : 0u;   // list entries on this rank
+            nch[q] = (len[q] + kChunk - 1) / kChunk;
+            mine.F += flag[q];
+            mine.C += nch[q];
+            mine.S += len[q];
+            my_votes += v[q];
+            if (flag[q]) my_tests += 4ull * v[q];
         }
-        if (!A.leaf_level) {
-            reinterpret_cast<uint4*>(A.nf)[p] = make_uint4(nf4[0], nf4[1], nf4[2], nf4[3]);
-            if (A.need_lists) {
-                ulonglong2* o = reinterpret_cast<ulonglong2*>(A.nfoff + 4 * (uint64_t)p);
-                o[0] = make_ulonglong2(so[0], so[1]);
-                o[1] = make_ulonglong2(so[2], so[3]);
-            }
-        }
-    }
-    if (A.record) {
-        // the warp's 4 x 32 records (2 KB, contiguous in HBM) go out as fully coalesced 16-byte stores
-        __syncwarp();
-        const uint32_t p0 = tile * kSplitThreads + wid * 32;
-        const uint32_t nrec = p0 < A.Fp ? 4 * min(32u, A.Fp - p0) : 0;
-        uint4* dst = reinterpret_cast<uint4*>(A.rec) + 4 * (uint64_t)p0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t k = lane + 32 * i;
-            if (k < nrec) dst[k] = s_rec[wid][k];
-        }
-    }
-    if (A.leaf_level) {
-        __syncwarp();
-        const uint32_t n_w = __shfl_sync(kFull, base.F + mine.F, 31) - f_w;
-        uint4* dst = reinterpret_cast<uint4*>(A.leaves) + f_w;
-        for (uint32_t k = lane; k < n_w; k += 32) dst[k] = s_leaf[wid][k];
-    }
 
-    // stats
-    unsigned long long sv = my_votes, sf = mine.F, stt = my_tests;
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
-        sv += __shfl_xor_sync(kFull, sv, d);
-        sf += __shfl_xor_sync(kFull, sf, d);
-        stt += __shfl_xor_sync(kFull, stt, d);
-    }
-    if (lane == 0) {
-        atomicAdd(&s_stat[0], sv);
-        atomicAdd(&s_stat[1], sf);
-        atomicAdd(&s_stat[2], stt);
-    }
-    __syncthreads();
-    if (tid == 0) {
-        atomicAdd(A.stats + kStatVotes, s_stat[0]);
-        if (A.leaf_level) {
-            atomicAdd(A.stats + kStatLeaves, s_stat[1]);
-        } else {
-            atomicAdd(A.stats + kStatSplit0 + A.child_level, s_stat[1]);
-            atomicAdd(A.stats + kStatTests, s_stat[2]);
+        // block scan
+        const Agg incl = warp_inclusive(mine, lane);
+        if (lane == 31) s_warp[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            Agg w = lane < kSplitThreads / 32 ? s_warp[lane] : Agg{0, 0, 0};
+            const Agg wi = warp_inclusive(w, lane);
+            if (lane < kSplitThreads / 32) s_warp[lane] = {wi.F - w.F, wi.C - w.C, wi.S - w.S};  // exclusive
+            const Agg block_total = {__shfl_sync(kFull, wi.F, 31), __shfl_sync(kFull, wi.C, 31), shfl_u64(wi.S, 31)};
+            Agg excl = {0, 0, 0};
+            if (A.pass == 1) {                            // aggregates only (k_split_scan orders the tiles)
+                if (lane == 0) {
+                    A.tiles[tile].aggF = block_total.F;
+                    A.tiles[tile].aggC = block_total.C;
+                    A.tiles[tile].aggS = block_total.S;
+                }
+            } else if (A.pass == 2) {                     // the exclusive tile prefix is precomputed
+                excl = {A.tiles[tile].incF, A.tiles[tile].incC, A.tiles[tile].incS};
+            } else if (tile == 0) {
+                // decoupled look-back (warp-wide window of 32 predecessors)
+                if (lane == 0) publish(A.tiles + 0, block_total, 2);
+            } else {
+                if (lane == 0) publish(A.tiles + tile, block_total, 1);
+                int64_t pred = (int64_t)tile - 1;
+                while (true) {
+                    const int64_t t = pred - lane;
+                    uint32_t st = 2;
+                    Agg val = {0, 0, 0};
+                    if (t >= 0) {
+                        TileDesc* d = A.tiles + t;
+                        // relaxed spin (no L1 invalidation per poll), then one acquire fence: the
+                        // payload was stored before the status with release semantics
+                        do { st = dev_u32(d->status).load(cuda::memory_order_relaxed); } while (st == 0);
+                        cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
+                        if (st == 1) {
+                            val = {dev_u32(d->aggF).load(cuda::memory_order_relaxed),
+                                   dev_u32(d->aggC).load(cuda::memory_order_relaxed),
+                                   dev_u64(d->aggS).load(cuda::memory_order_relaxed)};
+                        } else {
+                            val = {dev_u32(d->incF).load(cuda::memory_order_relaxed),
+                                   dev_u32(d->incC).load(cuda::memory_order_relaxed),
+                                   dev_u64(d->incS).load(cuda::memory_order_relaxed)};
+                        }
+                    }
+                    const uint32_t pm = __ballot_sync(kFull, st == 2);
+                    const int stop = pm ? __ffs(pm) - 1 : 31;    // nearest predecessor with a prefix
+                    if (lane > stop) val = {0, 0, 0};
+                    excl = agg_add(excl, warp_total(val));
+                    if (pm) break;
+                    pred -= 32;
+                }
+                if (lane == 0) publish(A.tiles + tile, agg_add(excl, block_total), 2);
+            }
+            if (lane == 0) {
+                s_prefix = excl;
+                if (A.pass == 0 && tile == A.ntiles - 1) {
+                    const Agg tot = agg_add(excl, block_total);
+                    A.totals->F = tot.F;
+                    A.totals->S = tot.S;
+                    A.totals->C = tot.C;
+                    if (!A.leaf_level) {
+                        A.out.off[tot.F] = tot.S;
+                        A.out.choff[tot.F] = tot.C;
+                    }
+                }
+            }
         }
-        const uint64_t nvalid = (A.Fp > tile * kSplitThreads) ? min((uint64_t)kSplitThreads, (uint64_t)A.Fp - tile * kSplitThreads) : 0;
-        atomicAdd(A.stats + kStatVisited0 + A.child_level, 4ull * nvalid);
+        __syncthreads();
+        if (A.pass != 1) {
+            const Agg base = agg_add(agg_add(s_prefix, s_warp[wid]), Agg{incl.F - mine.F, incl.C - mine.C, incl.S - mine.S});
+
+            // the warp's leaves are the contiguous range [f_w, f_w + n_w): staged, then stored coalesced
+            const uint32_t f_w = __shfl_sync(kFull, base.F, 0);
+            // record (lane, q) at slot 4 lane + (q ^ ((lane >> 1) & 3)): for each q the 32 lanes' 16-byte
+            // stores hit 8 distinct bank groups per quarter-warp (conflict-free)
+            const uint32_t swz = (lane >> 1) & 3;
+            if (valid) {
+                uint32_t f = base.F, cc = base.C;
+                uint64_t s = base.S;
+                uint32_t nf4[4];
+                uint64_t so[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t ca = 2 * pa + quad_da(q), cb = 2 * pc + quad_dc(q);
+                    nf4[q] = kNone;
+                    so[q] = s;
+                    if (flag[q]) {
+                        if (A.leaf_level) {
+                            s_leaf[wid][f - f_w] = make_uint4(tree, ca, cb, v[q]);
+                        } else {
+                            nf4[q] = f;
+                            A.out.tree[f] = tree;
+                            A.out.a[f] = ca;
+                            A.out.c[f] = cb;
+                            A.out.parent[f] = A.parent_base + p;
+                            A.out.len[f] = vl[q];
+                            A.out.votes[f] = v[q];
+                            A.out.off[f] = s;
+                            A.out.choff[f] = cc;
+                        }
+                        f += 1;
+                        s += len[q];
+                        cc += nch[q];
+                    }
+                    if (A.record) s_rec[wid][4 * lane + (q ^ swz)] = make_uint4(tree, ca, cb, v[q]);
+                }
+                if (!A.leaf_level) {
+                    reinterpret_cast<uint4*>(A.nf)[p] = make_uint4(nf4[0], nf4[1], nf4[2], nf4[3]);
+                    if (A.need_lists) {
+                        ulonglong2* o = reinterpret_cast<ulonglong2*>(A.nfoff + 4 * (uint64_t)p);
+                        o[0] = make_ulonglong2(so[0], so[1]);
+                        o[1] = make_ulonglong2(so[2], so[3]);
+                    }
+                }
+            }
+            if (A.record) {
+                // the warp's 4 x 32 records (2 KB, contiguous in HBM) go out as fully coalesced 16-byte stores
+                __syncwarp();
+                const uint32_t p0 = tile * kSplitThreads + wid * 32;
+                const uint32_t nrec = p0 < A.Fp ? 4 * min(32u, A.Fp - p0) : 0;
+                uint4* dst = reinterpret_cast<uint4*>(A.rec) + 4 * (uint64_t)p0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t k = lane + 32 * i;             // record k: parent k / 4, quad k % 4
+                    const uint32_t slot = (k & ~3u) + ((k & 3u) ^ (((k >> 2) >> 1) & 3u));
+                    if (k < nrec) dst[k] = s_rec[wid][slot];
+                }
+            }
+            if (A.leaf_level) {
+                __syncwarp();
+                const uint32_t n_w = __shfl_sync(kFull, base.F + mine.F, 31) - f_w;
+                uint4* dst = reinterpret_cast<uint4*>(A.leaves) + f_w;
+                for (uint32_t k = lane; k < n_w; k += 32) dst[k] = s_leaf[wid][k];
+            }
+
+            // stats (lane 0 of every warp keeps the warp's running partials)
+            unsigned long long sv = my_votes, sf = mine.F, stt = my_tests;
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) {
+                sv += __shfl_xor_sync(kFull, sv, d);
+                sf += __shfl_xor_sync(kFull, sf, d);
+                stt += __shfl_xor_sync(kFull, stt, d);
+            }
+            st_votes += sv;
+            st_split += sf;
+            st_tests += stt;
+            if (wid == 0) {
+                const uint64_t t0 = (uint64_t)tile * kSplitThreads;
+                st_visited += 4ull * ((A.Fp > t0) ? min((uint64_t)kSplitThreads, (uint64_t)A.Fp - t0) : 0);
+            }
+        }
+        __syncthreads();   // s_tile, s_warp, s_prefix and the stages are reused by the next tile
+    }
+    if (A.pass != 1 && lane == 0) {
+        if (st_votes) atomicAdd(A.stats + kStatVotes, st_votes);
+        if (A.leaf_level) {
+            if (st_split) atomicAdd(A.stats + kStatLeaves, st_split);
+        } else {
+            if (st_split) atomicAdd(A.stats + kStatSplit0 + A.child_level, st_split);
+            if (st_tests) atomicAdd(A.stats + kStatTests, st_tests);
+        }
+        if (st_visited) atomicAdd(A.stats + kStatVisited0 + A.child_level, st_visited);
     }
 }
 
 // One block: exclusive scan of the tile aggregates of pass 1 into tiles[t].inc*, totals, sentinels.
+// Warp w owns the contiguous tile segment [w seg, (w + 1) seg) and walks it 32 tiles at a time
+// (coalesced loads, a warp scan per step, a running carry); the 32 segment totals are then scanned
+// and every warp adds its segment's offset in a second walk.
 __global__ void __launch_bounds__(1024) k_split_scan(const SplitArgs A) {
     __shared__ Agg s_w[32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t per = (A.ntiles + 1023) / 1024, t0 = tid * per, t1 = min(A.ntiles, t0 + per);
-    Agg mine = {0, 0, 0};
-    for (uint32_t t = t0; t < t1; ++t) mine = agg_add(mine, Agg{A.tiles[t].aggF, A.tiles[t].aggC, A.tiles[t].aggS});
-    const Agg incl = warp_inclusive(mine, lane);
-    if (lane == 31) s_w[wid] = incl;
+    const uint32_t seg = (A.ntiles + 31) / 32;
+    const uint32_t t0 = wid * seg, t1 = min(A.ntiles, t0 + seg);
+    Agg carry = {0, 0, 0};
+    for (uint32_t b = t0; b < t1; b += 32) {
+        const uint32_t t = b + lane;
+        Agg a = {0, 0, 0};
+        if (t < t1) a = {A.tiles[t].aggF, A.tiles[t].aggC, A.tiles[t].aggS};
+        const Agg incl = warp_inclusive(a, lane);
+        if (t < t1) {
+            A.tiles[t].incF = carry.F + incl.F - a.F;
+            A.tiles[t].incC = carry.C + incl.C - a.C;
+            A.tiles[t].incS = carry.S + incl.S - a.S;
+        }
+        carry = agg_add(carry, Agg{__shfl_sync(kFull, incl.F, 31), __shfl_sync(kFull, incl.C, 31), shfl_u64(incl.S, 31)});
+    }
+    if (lane == 0) s_w[wid] = carry;
     __syncthreads();
     if (wid == 0) {
         const Agg w = s_w[lane];
@@ -1978,32 +2003,39 @@ __global__ void __launch_bounds__(1024) k_split_scan(const SplitArgs A) {
         }
     }
     __syncthreads();
-    Agg run = agg_add(s_w[wid], Agg{incl.F - mine.F, incl.C - mine.C, incl.S - mine.S});
-    for (uint32_t t = t0; t < t1; ++t) {
-        const Agg a = {A.tiles[t].aggF, A.tiles[t].aggC, A.tiles[t].aggS};
-        A.tiles[t].incF = run.F;
-        A.tiles[t].incC = run.C;
-        A.tiles[t].incS = run.S;
-        run = agg_add(run, a);
+    const Agg off = s_w[wid];
+    if (off.F | off.C | off.S) {
+        for (uint32_t t = t0 + lane; t < t1; t += 32) {
+            A.tiles[t].incF += off.F;
+            A.tiles[t].incC += off.C;
+            A.tiles[t].incS += off.S;
+        }
     }
 }
 
-cudaError_t launch_split(const SplitArgs& a, cudaStream_t st) {
+int split_blocks_per_sm() {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_split, kSplitThreads, 0);
+    return n > 0 ? n : 1;
+}
+
+cudaError_t launch_split(const SplitArgs& a, int resident_blocks, cudaStream_t st) {
     if (a.ntiles == 0) return cudaSuccess;
+    const unsigned grid = a.ntiles < (uint32_t)resident_blocks ? a.ntiles : (unsigned)resident_blocks;
     if (a.ntiles < kSplitPrescanTiles) {
         SplitArgs b = a;
         b.pass = 0;
-        k_split<<<a.ntiles, kSplitThreads, 0, st>>>(b);
+        k_split<<<grid, kSplitThreads, 0, st>>>(b);
         return cudaGetLastError();
     }
     // reduce-then-scan: with many tiles the look-back's first wave walks back over ~1000 running
     // tiles and holds their warps at the barrier; two passes over V cost 16 B per parent more
     SplitArgs b = a;
     b.pass = 1;
-    k_split<<<a.ntiles, kSplitThreads, 0, st>>>(b);
+    k_split<<<grid, kSplitThreads, 0, st>>>(b);
     k_split_scan<<<1, 1024, 0, st>>>(b);
     b.pass = 2;
-    k_split<<<a.ntiles, kSplitThreads, 0, st>>>(b);
+    k_split<<<grid, kSplitThreads, 0, st>>>(b);
     return cudaGetLastError();
 }
 
