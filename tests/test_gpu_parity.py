@@ -277,3 +277,26 @@ def test_leaf_sink_streaming(budget, torch_dev):
     h.set_leaf_sink(None)
     h.detect(d, cfg.N, cfg.D, cfg.T)
     assert h.stats()["leaves_streamed"] == 0
+
+
+@pytest.mark.parametrize("tail_depth", [4, 5])
+@pytest.mark.parametrize("N", [1, 2, 3, 5, 1023, 4095, 16383, 32767])
+def test_raster_fixed_point_extremes(N, tail_depth, torch_dev):
+    """The 16x16 raster's fixed-point floors (csrc Raster16) at the extremes of 3N:
+    smallest N (fx_s = 7) and the largest image sizes (2^24 / 3N down to 170), against the oracle."""
+    D = 5 if N <= 5 else 8
+    if N <= 5:                                   # tiny images: every pixel, several times
+        xs, ys = np.meshgrid(np.arange(N), np.arange(N))
+        pts = np.repeat(np.stack([xs.ravel(), ys.ravel()], 1).astype(np.int32), 7, axis=0)
+    elif N < 16384:
+        pts = synth.random_scene(500 + N, N, max_lines=4, max_noise=400)
+    else:                                        # beyond the scene generator's range: noise + 2 lines
+        rng = np.random.default_rng(N)
+        i = np.arange(0, N, 37)
+        pts = np.concatenate([rng.integers(0, N, (600, 2)), np.stack([i, (3 * i) // 5 + 11], 1),
+                              np.stack([(2 * i) // 7 + 5, i], 1)]).astype(np.int32)
+    T = 2
+    ref = oracle.detect(pts, N, D, T, AB)
+    h = _run(pts, N, D, T, AB, torch_dev, tail_depth=tail_depth)
+    compare_all(h, ref, AB, D)
+    assert (h.stats()["tests"], h.stats()["votes"]) == (ref.tests, ref.votes)
