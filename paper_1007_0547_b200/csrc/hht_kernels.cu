@@ -112,10 +112,59 @@ cudaError_t launch_stage(const int32_t* pts, uint64_t n, int N, uint32_t* packed
 //   acc : MODE_COUNT: acc[0] byte q = votes of child q; else acc[q] byte q' = votes of grandchild
 //         q' of child q (count-ahead over the 4x4 level-(l+2) cells (u, v), SW value
 //         g - u*Pg - v*Qg; containment makes the child's own crossing implied).
+// Count-ahead raster (MODE_WRITE / MODE_COUNT2): the 4x4 level-(l+2) cells under a parent of side
+// s = 2^sh are rastered like the 16x16 leaf grid (see "Fixed-point raster state" at Raster16), on
+// y' = floor((g - 1) / 2^(sh-2)): with Pg = 2ex s/4 and Qg = 3N s/4, floor((y - u Pg) / Qg) =
+// floor((y' - 2ex u) / 3N) because u Pg is a multiple of 2^(sh-2), so the leaf raster's fixed point
+// (Y ~ 2^24 (y' / 3N + B), decrement P from 2ex) applies unchanged; y' < 4 (2ex + 3N) keeps the
+// floors f in [-5, 6] over the 5 column boundaries. Column u's crossed rows f_(u+1) .. f_u (clipped
+// to 0..3) come as 4 byte counters from a table indexed by t = f_u + f_(u+1), one 4-byte copy per lane.
+constexpr int kTab4TLo = -12;   // t in [-12, 14)
+constexpr int kTab4 = 26;
+__shared__ uint32_t s_tab4[(kTab4 + 2) * 64];     // entries 256 B apart (32 lane words + 128 B gap)
+
+struct Tab4Place {
+    uint32_t H, B;
+};
+
+__device__ __forceinline__ Tab4Place tab4_place() {
+    const uint32_t S = (uint32_t)__cvta_generic_to_shared(s_tab4);
+    const uint32_t H = S & 0xFFFF0000u;
+    uint32_t twoB = ((S - H + 255u) >> 8) + (uint32_t)(-kTab4TLo);
+    twoB += twoB & 1u;
+    return {H, twoB >> 1};
+}
+
+// entry t, lane copy c at H + 256 (t + 2B) + 4 c
+__device__ __forceinline__ void fill_tab4() {
+    const Tab4Place pl = tab4_place();
+    const uint32_t first = pl.H + 256u * (uint32_t)(kTab4TLo + 2 * (int)pl.B);
+    for (int i = threadIdx.x; i < kTab4 * 32; i += blockDim.x) {
+        const int t = kTab4TLo + (i >> 5);
+        const int f = t >= 0 ? (t + 1) / 2 : -((-t) / 2), fn = t - f;
+        uint32_t w = 0;
+        for (int v = max(fn, 0); v <= min(f, 3); ++v) w |= 1u << (8 * v);
+        asm volatile("st.shared.u32 [%0], %1;" :: "r"(first + 256u * (uint32_t)(i >> 5) + 4u * (uint32_t)(i & 31)), "r"(w) : "memory");
+    }
+}
+
+struct CARaster {
+    uint32_t lane_h, bias, fx_m, fx_mlo, fx_s;
+    __device__ __forceinline__ void init(const PassArgs& A, int lane) {
+        const Tab4Place pl = tab4_place();
+        lane_h = pl.H | (2u * (uint32_t)lane);     // two boundaries add up to the lane's word 4 lane
+        bias = (pl.B << 24) + 1u;
+        fx_m = A.fx_m;
+        fx_mlo = A.fx_mlo;
+        fx_s = A.fx_s;
+    }
+};
+
 template <typename I, int MODE, bool BETA>
 __device__ __forceinline__ void chunk_math(const uint32_t (&p)[kItems], int cnt, int lane, I alpha, I beta_m1,
                                            int D, int sh, I Qc, I Qg, uint32_t one, uint32_t& cm,
-                                           uint32_t (&acc)[4]) {
+                                           uint32_t (&acc)[4], const CARaster& CR) {
+    uint32_t col[4] = {0, 0, 0, 0};                   // count-ahead: col[u] byte v = cells (u, v)
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
         const uint32_t w = p[it];
@@ -138,27 +187,31 @@ __device__ __forceinline__ void chunk_math(const uint32_t (&p)[kItems], int cnt,
             }
         }
         if (MODE == MODE_WRITE || MODE == MODE_COUNT2) {
-            // 12 of the 16 cells: the NE grandchild of each child is derived later from
-            // votes(child) = votes(SW grandchild) + votes(NE grandchild).
-            const I Pg = Pc >> 1;
-            const I Ug = Pg + Qg;
-            int n = 0;
+            // the 4x4 level-(l+2) cells as a 4-column raster (CARaster above); invalid lanes keep
+            // f = -1 (all-zero entries)
+            const bool valid = gm1 >= 0;
+            const uint32_t y0 = (uint32_t)(gm1 >> (sh - 2));
+            uint32_t Y = valid ? (uint32_t)(((uint64_t)y0 * CR.fx_m) >> CR.fx_s) + CR.bias : CR.bias - (1u << 24) - 1u;
+            const uint32_t P = valid ? (uint32_t)(((uint64_t)(2u * (uint32_t)ex) * CR.fx_mlo) >> CR.fx_s) : 0u;
+            uint32_t X = __byte_perm(Y, CR.lane_h, 0x7634u);          // boundary 0 carries H
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const I hu = gm1 - (I)u * Pg;
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    if ((u & 1) && (v & 1)) continue;
-                    const int q = quad_of(u >> 1, v >> 1);
-                    const int qq = quad_of(u & 1, v & 1);
-                    const bool c = crosses<I>(hu - (I)v * Qg, Ug);
-                    if ((n++ & 1) == 0) {
-                        if (c) acc[q] += 1u << (8 * qq);                   // ALU pipe
-                    } else {
-                        mad_if(c, acc[q], one, 1u << (8 * qq));            // FMA pipe
-                    }
-                }
+                Y -= P;
+                const uint32_t xn = __byte_perm(Y, CR.lane_h, (u & 1) ? 0x7634u : 0x5534u);
+                uint32_t addr, m;
+                asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(X), "r"(one), "r"(xn));
+                asm("ld.shared.u32 %0, [%1];" : "=r"(m) : "r"(addr));
+                X = xn;
+                col[u] += m;
             }
+        }
+    }
+    if (MODE == MODE_WRITE || MODE == MODE_COUNT2) {
+        // acc[q] byte qq = cell (2 da_q + da_qq, 2 dc_q + dc_qq); quads NE(1,1) NW(0,1) SW(0,0) SE(1,0)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int da = quad_da(q), dc = quad_dc(q);
+            acc[q] = __byte_perm(col[2 * da], col[2 * da + 1], dc ? 0x6237u : 0x4015u);
         }
     }
 }
@@ -302,6 +355,12 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
     const uint32_t stage_sa = (uint32_t)__cvta_generic_to_shared(s_stage) + (threadIdx.x >> 5) * (4 * kChunk * 4);
     const uint32_t cell_q = ((uint32_t)lane * 11u) >> 5;          // lane L < 12: child q = L / 3
     const uint32_t cell_qq = (uint32_t)lane - 3u * cell_q + 1u;    // grandchild qq = 1 + L % 3
+    CARaster CR{};
+    if (!CIRCLE && (MODE == MODE_WRITE || MODE == MODE_COUNT2)) {
+        fill_tab4();
+        __syncthreads();
+        CR.init(A, lane);
+    }
 
     chunk_loop<PREF>(A, lane, [&](const ChunkDesc& d, const uint32_t (&p)[kItems]) {
         const int cnt = (int)d.cnt;
@@ -325,8 +384,8 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
             if (d.beta) chunk_math_circle<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, N, Qc, Qg, cm, acc);
             else chunk_math_circle<I, MODE, false>(p, cnt, lane, alpha, beta_m1, D, sh, N, Qc, Qg, cm, acc);
         } else {
-            if (d.beta) chunk_math<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc);
-            else chunk_math<I, MODE, false>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc);
+            if (d.beta) chunk_math<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc, CR);
+            else chunk_math<I, MODE, false>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc, CR);
         }
 
         if (MODE == MODE_COUNT) {
