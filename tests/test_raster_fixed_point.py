@@ -79,3 +79,31 @@ def test_table_placement():
         x0 = ((f0 + B) << 8) | (lane_h & 0xFF) | (lane_h & 0xFFFF0000)   # even boundary: with H
         x1 = ((f1 + B) << 8) | (lane_h & 0xFF)                           # odd boundary
         assert 0 < f1 + B < 256 and x0 + x1 == first + 256 * (f0 + f1 - t_lo) + 8 * lane
+
+
+@pytest.mark.parametrize("N", [1, 3, 64, 512, 8192, 32767])
+def test_count_ahead_raster_matches_cell_tests(N):
+    """k_pass count-ahead (chunk_math, CARaster): for a line crossing a parent of side 2^sh, the
+    4-column raster on y' = (g - 1) >> (sh - 2) with the leaf fixed point marks exactly the 4x4
+    grandchild cells (u, v) with 0 <= g - 1 - u Pg - v Qg < Pg + Qg (Pg = 2ex 2^(sh-2),
+    Qg = 3N 2^(sh-2)): the paper's corner test at level l + 2."""
+    s, m, mlo = fx_consts(N)
+    n3 = 3 * N
+    r = random.Random(11 + N)
+    for _ in range(3000):
+        sh = r.randrange(2, 16)
+        ex = r.randrange(N)
+        gm1 = r.randrange((1 << sh) * (2 * ex + n3))     # the line crosses the parent
+        B = r.randrange(6, 135)
+        y0 = gm1 >> (sh - 2)
+        Y = ((y0 * m) >> s) + 1 + (B << 24)
+        P = (2 * ex * mlo) >> s
+        f = [(((Y - u * P) & 0xFFFFFFFF) >> 24) - B for u in range(5)]
+        assert all(-5 <= x <= 6 for x in f)
+        pg, qg = 2 * ex << (sh - 2), n3 << (sh - 2)
+        for u in range(4):
+            t = f[u] + f[u + 1]
+            fu = (t + 1) // 2 if t >= 0 else -((-t) // 2)
+            rows = set(range(max(t - fu, 0), min(fu, 3) + 1))
+            direct = {v for v in range(4) if 0 <= gm1 - u * pg - v * qg < pg + qg}
+            assert rows == direct, (N, sh, ex, gm1, u)
