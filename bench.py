@@ -163,8 +163,8 @@ def run_reference(a):
     v = tot_tests / tot_s
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": 1e3 * tot_s / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": _workload(cfg),
+            "scaling": "weak" if cfg.images > 1 else "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic", "config": _workload(cfg),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"{a.steps} steps, each the oracle DFS over config{cfg.cid} stopped after "
                                        f"{per_step:.3g} code evaluations"},
