@@ -23,3 +23,8 @@ echo "tail capture rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pass -s $WSKIP -c 1 \
     -o gpurun_out/c5_write python scripts/run_once.py --config 5 > gpurun_out/ncu_write.log 2>&1
 echo "write capture rc=$?"
+# the largest count-ahead list pass (MODE_WRITE: write launch 6 of config 5, level 6 -> lists of 7, votes of 8)
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k regex:"k_pass<int, \\(int\\)1," -s 6 -c 1 \
+    -o gpurun_out/c5_write_ca python scripts/run_once.py --config 5 > gpurun_out/ncu_write_ca.log 2>&1
+echo "count-ahead capture rc=$?"

@@ -90,7 +90,8 @@ def main():
     wf = os.path.join(G, "write_skip.txt")
     if os.path.exists(wf):
         wskip = int(open(wf).read().split()[-1])
-    caps = {"tail": ("c5_tail", 0), "write": ("c5_write", wskip - 1)}   # write launch index = k_pass index - 1
+    # write launch index = k_pass index - 1; write_ca: the largest count-ahead pass (write launch 6)
+    caps = {"tail": ("c5_tail", 0), "write": ("c5_write", wskip - 1), "write_ca": ("c5_write_ca", 6)}
     for cls, (f, idx) in caps.items():
         rep = os.path.join(G, f + ".ncu-rep")
         if not os.path.exists(rep):
@@ -98,7 +99,8 @@ def main():
         d, text = raw(rep)
         open(os.path.join(P, f"{tag}_{f}_raw.csv"), "w").write(text)
         dram = d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
-        alg = lb.get(cls, [None] * (idx + 1))[idx]
+        lcls = "write" if cls.startswith("write") else cls
+        alg = lb.get(lcls, [None] * (idx + 1))[idx]
         traffic["config5"][cls] = {
             "traffic": dram, "algorithmic_bytes": alg, "traffic_over_algorithmic": dram / alg if alg else None,
             "duration_ms": d["gpu__time_duration.sum"],
