@@ -463,6 +463,12 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
             const uint32_t t02 = __reduce_add_sync(kFull, c0 | (c2 << 16));
             const uint32_t t13 = __reduce_add_sync(kFull, c1 | (c3 << 16));
             const uint32_t tq[4] = {t02 & 0xFFFFu, t13 & 0xFFFFu, t02 >> 16, t13 >> 16};
+            // reserve the runs first: the staging stores below cover the atomics' round trip
+            uint32_t my_base = 0;
+            if (lane < 4) {
+                const uint32_t t = lane == 0 ? tq[0] : lane == 1 ? tq[1] : lane == 2 ? tq[2] : tq[3];
+                if (t) my_base = atomicAdd(A.c_cursor + (my_nf - A.q0), t);
+            }
             uint32_t sa[4] = {stage_sa + 4 * (exc & 0xFFu), stage_sa + 4 * (kChunk + ((exc >> 8) & 0xFFu)),
                               stage_sa + 4 * (2 * kChunk + ((exc >> 16) & 0xFFu)),
                               stage_sa + 4 * (3 * kChunk + (exc >> 24))};
@@ -470,11 +476,6 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
             for (int it = 0; it < kItems; ++it) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) sts_if(cm & (1u << (4 * it + q)), sa[q], p[it]);
-            }
-            uint32_t my_base = 0;
-            if (lane < 4) {
-                const uint32_t t = lane == 0 ? tq[0] : lane == 1 ? tq[1] : lane == 2 ? tq[2] : tq[3];
-                if (t) my_base = atomicAdd(A.c_cursor + (my_nf - A.q0), t);
             }
             const uint64_t my_dst = my_off - A.c_list_base + my_base;
             __syncwarp();
