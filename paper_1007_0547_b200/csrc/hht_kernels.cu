@@ -609,9 +609,9 @@ __global__ void __launch_bounds__(256) k_tail(const PassArgs A) {
 // diagonal (SW..NE) leaves (the SW+NE identity applied recursively), so
 // votes(region of side 2^j leaves) = sum of its 2^j diagonal leaf counts.
 // The 64 per-lane counter words do not fit in registers, so the grid is processed in 4 column
-// blocks of 4 columns; each line's raster state (y, k, threshold) is carried across blocks, and
-// each block's 16 counter words are reduced across the warp with a butterfly reduce-scatter
-// (16 shuffles) that leaves every lane with the warp totals of 2 cells.
+// blocks of 4 columns; each line's raster state (Y, P, X below) is carried across blocks, and
+// each block's 8 nibble counter words are reduced across the warp with a butterfly reduce-scatter
+// (12 shuffles) that leaves every lane with the warp totals of 2 cells.
 // ---------------------------------------------------------------------------------------------
 // Fixed-point raster state. For a line of the batch, y_u = G(i0 + u, j0) - 1 at lattice column u of
 // the leaf grid and f_u = floor(y_u / 3N): the line is above lattice corner (u, v) (G > 0) iff
