@@ -120,6 +120,7 @@ struct hht_ctx {
     Buf fusedctr;                    // k_fused work counter (u32) + rastered-pair counter (u64)
     Buf img, edgeB, edgetiles;       // edge front end: staged image, BETA points, look-back words
     Buf small;                       // latency path scratch (k_small)
+    Buf small_g;                     // latency path lists / frontiers when they exceed shared memory
     bool edges_valid = false;        // x->packed holds the last hht_detect_image's edge points
     std::vector<uint64_t> tree_pt_off;   // last detect: tree t's points in x->packed (local)
     std::vector<uint32_t> tree_pt_n;
@@ -750,11 +751,17 @@ void small_bounds(const hht_ctx* x, uint64_t& S, uint64_t& F) {
     F = S / (x->T + 1) + x->ntrees + 1;
 }
 
-bool small_eligible(const hht_ctx* x) {
-    if (x->opts.latency_path == 2 || multi(x) || x->circle || x->D > 24 || x->ntrees > 4096) return false;
+// 0: multi-kernel path; 1: latency path with shared-memory scratch; 2: latency path with the two
+// candidate lists in device (L2-resident) memory and the frontier arrays in shared memory, for lists
+// up to kSmallGlobalMaxS entries (profiles/r01_latency.md)
+int small_mode(const hht_ctx* x) {
+    if (x->opts.latency_path == 2 || multi(x) || x->circle || x->D > 24 || x->ntrees > 4096) return 0;
     uint64_t S, F;
     small_bounds(x, S, F);
-    return S < (1ull << 32) && small_smem_bytes((uint32_t)S, (uint32_t)std::min<uint64_t>(F, S + 1)) <= kSmallSmemMax;
+    if (S >= (1ull << 32)) return 0;
+    const uint32_t Fc = (uint32_t)std::min<uint64_t>(F, S + 1);
+    if (small_smem_bytes((uint32_t)S, Fc) <= kSmallSmemMax) return 1;
+    return (S <= kSmallGlobalMaxS && small_frontier_bytes(Fc) <= kSmallSmemMax) ? 2 : 0;
 }
 
 hht_status detect_small(hht_ctx* x) {
@@ -784,6 +791,13 @@ hht_status detect_small(hht_ctx* x) {
         h_rec[l] = (Record*)x->rec[l].b.p;
     }
     TRY(grow(x, x->leaves, sizeof(LeafRec), 4 * Fmax));
+    a.global_scratch = small_mode(x) == 2 ? 1u : 0u;
+    if (a.global_scratch) {
+        // the two candidate lists in one device buffer (the frontier arrays stay in shared memory)
+        TRY(ensure(x, x->small_g, 8ull * Smax));
+        a.list[0] = (uint32_t*)x->small_g.p;
+        a.list[1] = a.list[0] + Smax;
+    }
     {   // one host-to-device copy of everything the launch needs (offsets, counts, zeroed counters,
         // record pointers), laid out exactly as in `x->small`
         std::vector<uint32_t> h(words, 0);
@@ -960,7 +974,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         CK(launch_stage(dev_pts, (uint64_t)n, N, (uint32_t*)x->packed.p, (uint32_t*)x->errflag.p, x->st));
         prof_end(x, id);
     }
-    if (small_eligible(x)) {
+    if (small_mode(x)) {
         // latency path: no synchronisation before the traversal; the range check is read with the
         // results (an out-of-range point still fails the call with HHT_ERANGE, nothing is returned)
         CK(cudaMemsetAsync(x->stats.p, 0, kStatCount * 8, x->st));
@@ -1598,7 +1612,7 @@ void hht_destroy(hht_ctx* x) {
     fr(x->leaves.b);
     for (Buf* b : {&x->stage_in, &x->packed, &x->errflag, &x->beta, &x->stats, &x->tiles, &x->tilectr, &x->totals,
                    &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv, &x->leafrows, &x->fusedctr, &x->img,
-                   &x->edgeB, &x->edgetiles, &x->small})
+                   &x->edgeB, &x->edgetiles, &x->small, &x->small_g})
         fr(*b);
     if (x->totals_h) cudaFreeHost(x->totals_h);
     if (x->range_h) cudaFreeHost(x->range_h);

@@ -222,10 +222,14 @@ struct SmallArgs {
     LeafRec* leaves;
     unsigned long long* stats;     // kStat* layout (tests, votes, leaves, split[l], visited[l])
     uint32_t* counts;              // [D + 2] records per level, then leaves (read by the host)
-    uint32_t smem_S, smem_F;       // shared-memory capacities: list entries, frontier regions
+    uint32_t smem_S, smem_F;       // scratch capacities: list entries, frontier regions
+    uint32_t global_scratch;       // 1: list[] are device (L2-resident) buffers set by the host, the
+                                   //    frontier arrays stay in shared memory; 0: all in shared memory
 };
 uint64_t small_smem_bytes(uint32_t S, uint32_t F);
+uint64_t small_frontier_bytes(uint32_t F);
 constexpr uint64_t kSmallSmemMax = 220 * 1024;
+constexpr uint64_t kSmallGlobalMaxS = 1ull << 16;   // device-list latency path: list bound (entries)
 cudaError_t launch_small(const SmallArgs& a, bool int64, cudaStream_t st);
 cudaError_t launch_fused(bool int64, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,

@@ -1374,10 +1374,14 @@ __global__ void __launch_bounds__(1024) k_small(SmallArgs A) {
     // ~12 dependent phases of a level cost shared-memory, not L2, round trips
     extern __shared__ uint4 s_small_dyn[];
     {
+        // frontier arrays always in shared memory; the two candidate lists too unless the host gave
+        // device buffers for them (global_scratch: lists too large for shared memory)
         uint32_t* w = reinterpret_cast<uint32_t*>(s_small_dyn);
         const uint32_t Sm = A.smem_S, Fm = A.smem_F;
-        A.list[0] = w; w += Sm;
-        A.list[1] = w; w += Sm;
+        if (!A.global_scratch) {
+            A.list[0] = w; w += Sm;
+            A.list[1] = w; w += Sm;
+        }
         for (int b = 0; b < 2; ++b) {
             A.f_tree[b] = w; w += Fm + 1;
             A.f_a[b] = w; w += Fm + 1;
@@ -1550,9 +1554,10 @@ __global__ void __launch_bounds__(1024) k_small(SmallArgs A) {
 }
 
 uint64_t small_smem_bytes(uint32_t S, uint32_t F) { return 4ull * (2ull * S + 8ull * (F + 1) + 8ull * F); }
+uint64_t small_frontier_bytes(uint32_t F) { return 4ull * (8ull * (F + 1) + 8ull * F); }
 
 cudaError_t launch_small(const SmallArgs& a, bool int64, cudaStream_t st) {
-    const int smem = (int)small_smem_bytes(a.smem_S, a.smem_F);
+    const int smem = (int)(a.global_scratch ? small_frontier_bytes(a.smem_F) : small_smem_bytes(a.smem_S, a.smem_F));
     if (int64) {
         cudaFuncSetAttribute(k_small<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         k_small<int64_t><<<1, 1024, smem, st>>>(a);

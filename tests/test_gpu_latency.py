@@ -14,10 +14,13 @@ AB = hht.ALPHA | hht.BETA
 
 
 def eligible(n_per_tree, D, T):
-    """Mirror of the library's admission rule (hht_driver.cu small_bounds / small_eligible)."""
+    """Mirror of the library's admission rule (hht_driver.cu small_bounds / small_mode): everything in
+    shared memory when it fits 220 KiB; else lists in device memory (up to 2^16 entries) with the
+    frontier arrays in shared memory."""
     S = max(sum(n_per_tree) * ((1 << D) - 1), 1)
     F = min(S // (T + 1) + len(n_per_tree) + 1, S + 1)
-    return 4 * (2 * S + 8 * (F + 1) + 8 * F) <= 220 * 1024
+    return (4 * (2 * S + 8 * (F + 1) + 8 * F) <= 220 * 1024
+            or (S <= (1 << 16) and 4 * (8 * (F + 1) + 8 * F) <= 220 * 1024))
 
 
 def _dev(pts, dev):
@@ -89,3 +92,22 @@ def test_latency_path_edges(case, cuda_device):
     h = hht.HHT(halves=AB)
     h.detect(_dev(pts, cuda_device), N, D, T)
     compare_all(h, oracle.detect(pts, N, D, T, AB), AB, D)
+
+
+@pytest.mark.parametrize("size,seed", [(48, 2), (48, 3), (48, 4), (64, 3), (64, 5), (64, 7)])
+def test_latency_path_device_scratch(size, seed, cuda_device):
+    """Scenes whose lists exceed shared memory but stay under 2^16 entries run the one-launch path
+    with the lists in device memory (frontier arrays in shared memory); identical to the oracle."""
+    D, T = 6, 8
+    pts = synth.random_scene(2400 + 10 * size + seed, size, max_lines=5, max_noise=size * 3)
+    n = [len(pts), len(pts)]
+    S = sum(n) * ((1 << D) - 1)
+    F = min(S // (T + 1) + 3, S + 1)
+    assert 4 * (2 * S + 8 * (F + 1) + 8 * F) > 220 * 1024 and eligible(n, D, T)   # the device-list mode
+    ref = oracle.detect(pts, size, D, T, AB)
+    h = hht.HHT(halves=AB)
+    h.detect(_dev(pts, cuda_device), size, D, T)
+    st = h.stats()
+    assert st["latency_path"] == 1, S
+    compare_all(h, ref, AB, D)
+    assert (st["tests"], st["votes"], st["leaves"]) == (ref.tests, ref.votes, ref.leaves.shape[0])
