@@ -75,9 +75,11 @@ typedef struct {
                                 depth-3 lists. Results are identical. */
     uint32_t prefetch;       /* pass/tail kernels: 0 = auto, 1 = fetch the next chunk's descriptor
                                 only, 2 = also its list entries (more registers); identical results */
-    uint32_t latency_path;   /* 0 = auto: a detection whose every per-level array fits one block's
-                                shared memory (about sum over trees of points x 2^depth <= 26k;
-                                one rank, exact test) runs as ONE kernel launch (k_small);
+    uint32_t latency_path;   /* 0 = auto: a small detection (one rank, exact test; bound on the
+                                lists: sum over trees of points x (2^depth - 1) entries) runs as ONE
+                                kernel launch of one block (k_small): all arrays in shared memory
+                                when they fit 220 KiB, else (bound <= 2^16 entries) the two lists
+                                in device memory and the frontier arrays in shared memory;
                                 1 = same; 2 = never (always the multi-kernel path) */
     uint32_t variant;        /* membership test: HHT_EXACT (0, default) = the paper's 4-bit corner
                                 code; HHT_FHT_CIRCLE (1) = the FHT comparison: the line meets the
