@@ -173,7 +173,7 @@ __device__ __forceinline__ void chunk_math(const uint32_t (&p)[kItems], int cnt,
         I gm1 = ex * alpha + (ey << D) + beta_m1;            // G(SW corner) - 1
         if (lane + kWarp * it >= cnt) gm1 = (I)-1;
         const I Pc = ex << sh;                                // ex * s
-        if (MODE != MODE_COUNT2) {
+        if (MODE == MODE_COUNT || MODE == MODE_WRITE_NC) {
             const I Uc = Pc + Qc;
             // child SW values: NE g-Pc-Qc, NW g-Qc, SW g, SE g-Pc
             const uint32_t bNE = crosses<I>(gm1 - Pc - Qc, Uc);
@@ -194,15 +194,26 @@ __device__ __forceinline__ void chunk_math(const uint32_t (&p)[kItems], int cnt,
             uint32_t Y = valid ? (uint32_t)(((uint64_t)y0 * CR.fx_m) >> CR.fx_s) + CR.bias : CR.bias - (1u << 24) - 1u;
             const uint32_t P = valid ? (uint32_t)(((uint64_t)(2u * (uint32_t)ex) * CR.fx_mlo) >> CR.fx_s) : 0u;
             uint32_t X = __byte_perm(Y, CR.lane_h, 0x7634u);          // boundary 0 carries H
+            uint32_t mc[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 Y -= P;
                 const uint32_t xn = __byte_perm(Y, CR.lane_h, (u & 1) ? 0x7634u : 0x5534u);
-                uint32_t addr, m;
+                uint32_t addr;
                 asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(X), "r"(one), "r"(xn));
-                asm("ld.shared.u32 %0, [%1];" : "=r"(m) : "r"(addr));
+                asm("ld.shared.u32 %0, [%1];" : "=r"(mc[u]) : "r"(addr));
                 X = xn;
-                col[u] += m;
+                col[u] += mc[u];
+            }
+            if (MODE == MODE_WRITE) {
+                // child bits from the same cells: a line crosses a child iff it crosses one of the
+                // child's 4 cells (the children tile it; SW + NE identity). Child (da, dc) = columns
+                // 2da, 2da+1 x rows 2dc, 2dc+1. Bytes of x: NE, NW, SW, SE (each 0/1); the multiply
+                // gathers byte k's bit to bit 28 + k.
+                const uint32_t a = mc[0] | mc[1], b = mc[2] | mc[3];
+                const uint32_t x = __byte_perm(a, b, 0x4026u) | __byte_perm(a, b, 0x5137u);
+                const uint32_t nib = (x * 0x10204080u) >> 28;
+                cm |= nib << (4 * it);
             }
         }
     }

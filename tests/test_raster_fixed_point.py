@@ -107,3 +107,23 @@ def test_count_ahead_raster_matches_cell_tests(N):
             rows = set(range(max(t - fu, 0), min(fu, 3) + 1))
             direct = {v for v in range(4) if 0 <= gm1 - u * pg - v * qg < pg + qg}
             assert rows == direct, (N, sh, ex, gm1, u)
+
+
+def _prmt(a, b, sel):
+    bs = [(a >> (8 * i)) & 255 for i in range(4)] + [(b >> (8 * i)) & 255 for i in range(4)]
+    return sum(bs[(sel >> (4 * k)) & 7] << (8 * k) for k in range(4))
+
+
+def test_count_ahead_child_bits_gather():
+    """k_pass MODE_WRITE derives the 4 child bits (NE, NW, SW, SE at bits 0..3) from the count-ahead
+    raster's column words (byte v of word u = cell (u, v) crossed): a child is crossed iff one of its
+    2x2 cells is (containment and the SW + NE identity). Exhaustive over the 2^16 cell patterns."""
+    for pat in range(1 << 16):
+        mc = [sum(((pat >> (4 * u + v)) & 1) << (8 * v) for v in range(4)) for u in range(4)]
+        a, b = mc[0] | mc[1], mc[2] | mc[3]
+        x = _prmt(a, b, 0x4026) | _prmt(a, b, 0x5137)
+        nib = ((x * 0x10204080) & 0xFFFFFFFF) >> 28
+
+        def anyc(da, dc):
+            return int(any((pat >> (4 * (2 * da + i) + 2 * dc + j)) & 1 for i in (0, 1) for j in (0, 1)))
+        assert nib == anyc(1, 1) | anyc(0, 1) << 1 | anyc(0, 0) << 2 | anyc(1, 0) << 3
