@@ -657,6 +657,7 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
     }
 
     uint32_t q0 = 0;
+    bool final_cut = false;          // the last range has been cut once already (leaf sink, below)
     while (q0 < Fc) {
         // list budget left for this level: everything not held by the active ancestor levels.
         // Buffer capacities persist across ranges and calls (steady state allocates nothing);
@@ -667,6 +668,19 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         const uint64_t cap = (lc == x->D - 2 ? avail : avail / 3) / 4;
         RangeInfo ri{};
         TRY(choose_range(x, lc, q0, cap, false, &ri, r0, r1));
+        // With a leaf sink, the leaves of the last range are copied to the host after all compute: when
+        // the detection's final piece at the last list level would be large, cut its last quarter into
+        // a range of its own, so that the copy of the rest overlaps that quarter's tail
+        if (x->sink && !final_cut && ri.q1 == Fc && q0 > 0 && r1 == P.F && no_count_ahead(x) &&
+            lc == x->D - 5 && Fc - q0 >= 64) {
+            final_cut = true;
+            const uint32_t qf = q0 + (Fc - q0) - (Fc - q0) / 8;
+            CK(launch_range((const uint64_t*)C.off.p, (const uint32_t*)C.parent.p, C.F, q0, cap, qf,
+                            (const uint64_t*)P.off.p, (const uint64_t*)P.choff.p, (const uint32_t*)P.len.p,
+                            lc == 1, (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->range_m, x->st));
+            TRY(sync(x));
+            ri = read_mapped(x->range_h);
+        }
         const uint32_t q1 = (uint32_t)ri.q1;
         const uint64_t entries = ri.s_hi - ri.s_lo;
         if (entries * 4 > avail)
