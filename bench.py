@@ -36,6 +36,7 @@ def _args():
     ap.add_argument("--impl", default="hht", choices=["hht", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--prefetch", type=int, default=0, help="0 auto, 1 descriptor only, 2 descriptor + entries")
+    ap.add_argument("--tail-depth", type=int, default=0, help="0 auto; 3-6 (include/hht.h hht_opts.tail_depth)")
     ap.add_argument("--variant", default="exact", choices=["exact", "fht"],
                     help="membership test: the paper's exact corner code, or the FHT circumcircle comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -199,7 +200,7 @@ def main():
         nccl_id = hdist.broadcast_bytes(hht.nccl_unique_id() if rank == 0 else None)
     h = hht.HHT(device=local, halves=cfg.halves, record_levels=True, profile=True,
                 rank=rank if comm_world > 1 else 0, world=comm_world, nccl_id=nccl_id, prefetch=a.prefetch,
-                variant=hht.FHT_CIRCLE if a.variant == "fht" else hht.EXACT)
+                tail_depth=a.tail_depth, variant=hht.FHT_CIRCLE if a.variant == "fht" else hht.EXACT)
     d_pts = torch.from_numpy(np.ascontiguousarray(my)).to(dev)
     B = my_offs.shape[0] - 1
 

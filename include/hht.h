@@ -69,8 +69,11 @@ typedef struct {
     uint32_t force_int64;    /* 1: use the int64 kernels even where int32 is exact (testing) */
     uint32_t profile;        /* 1: time every kernel launch with CUDA events (hht_result_profile) */
     uint32_t tail_depth;     /* dense leaf-grid tail: 0 = auto (5 when depth >= 5, else 4 when
-                                depth >= 4, else 3); 5 = 16x16 grids of level depth-4 rastered
-                                straight from level depth-5 lists (fused, no level depth-4 lists);
+                                depth >= 4, else 3); 6 (depth >= 6, exact test) = the fused tail
+                                streams each level depth-5 region's parent list from level depth-6
+                                (no level depth-5 or depth-4 lists); 5 = 16x16 grids of level
+                                depth-4 rastered straight from level depth-5 lists (fused, no
+                                level depth-4 lists);
                                 4 = 16x16 grids from level depth-4 lists; 3 = 8x8 grids from level
                                 depth-3 lists. Results are identical. */
     uint32_t prefetch;       /* pass/tail kernels: 0 = auto, 1 = fetch the next chunk's descriptor

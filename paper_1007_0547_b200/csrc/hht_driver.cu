@@ -161,11 +161,14 @@ struct hht_ctx {
 namespace {
 
 
-// Levels covered by the dense tail: lists exist down to level D - tail_depth. 5 (auto when D >= 5):
-// 16x16 leaf grids of level D-4, rastered straight from level D-5 lists by the fused tail;
-// 4: 16x16 grids from level D-4 lists; 3: 8x8 grids from level D-3 lists.
+// Levels covered by the dense tail: lists exist down to level D - tail_depth. 6: the fused tail
+// streams level D-6 lists and rasters the 16x16 leaf grids of the level-(D-4) grandchildren (no
+// level D-5 lists); 5 (auto when D >= 5): 16x16 leaf grids of level D-4, rastered straight from
+// level D-5 lists by the fused tail; 4: 16x16 grids from level D-4 lists; 3: 8x8 grids from level
+// D-3 lists.
 int tail_depth(const hht_ctx* x) {
     const int want = x->opts.tail_depth ? (int)x->opts.tail_depth : 5;
+    if (want >= 6 && x->D >= 6 && !x->circle) return 6;
     if (want >= 5 && x->D >= 5) return 5;
     return (want >= 4 && x->D >= 4) ? 4 : 3;
 }
@@ -173,6 +176,9 @@ int tail_depth(const hht_ctx* x) {
 // With the fused tail and D >= 6, the last list pass (parent level D-6) skips the count-ahead: the
 // fused tail rasters all children of the level-(D-5) regions and takes their votes from the grids.
 bool no_count_ahead(const hht_ctx* x) { return !x->circle && tail_depth(x) == 5 && x->D >= 6; }
+
+// The fused tail ends the list levels (tail_depth 5 or 6): the leaf sink's final cut applies there.
+bool fused_tail(const hht_ctx* x) { return !x->circle && x->D >= 6 && tail_depth(x) >= 5; }
 
 hht_status set_err(hht_ctx* x, hht_status s, const char* fmt, ...) {
     char buf[512];
@@ -571,7 +577,9 @@ hht_status gather_levels(hht_ctx* x, int L, int c0, uint32_t anc_base, Level& Ow
 // the previous pass's count-ahead), or, when `all_children` (that pass ran without count-ahead),
 // of all 4 children of each parent, whose votes are then the grids' diagonal sums and whose split
 // happens here. Levels l+2 .. D are split from the grids.
-hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_children) {
+// With `gp` (tail_depth 6), R_l has no lists: each work unit r streams the list of its parent in
+// gp = lv[l-1] (all_children only).
+hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_children, Level* gp = nullptr) {
     const int L = l + 1;
     Level& P = x->lv[l];
     Level& C = x->lv[L];
@@ -581,19 +589,24 @@ hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_chil
     TRY(ensure(x, x->dense, (size_t)n * kTail16Cells * 4));
     CK(cudaMemsetAsync(x->dense.p, 0, (size_t)n * kTail16Cells * 4, x->st));
     TRY(ensure(x, x->fusedctr, 256));
-    CK(cudaMemsetAsync(x->fusedctr.p, 0, 16, x->st));
+    CK(cudaMemsetAsync(x->fusedctr.p, 0, 24, x->st));
     // streamed pairs: host-known when the parents are the whole level, else from the device
-    const bool host_pairs = r0 == 0 && r1 == P.F;
-    if (!host_pairs)
+    const bool host_pairs = !gp && r0 == 0 && r1 == P.F;
+    if (!host_pairs && !gp)
         CK(launch_bounds((const uint64_t*)P.off.p, (const uint64_t*)P.choff.p, (const uint32_t*)P.len.p, r0, r1,
                          l == 0, (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->range_m, x->st));
-    PassArgs a = pass_args(x, P, l);
+    PassArgs a = pass_args(x, gp ? *gp : P, l);
     a.nf = all_children ? nullptr : (const uint32_t*)C.nf.p;
     a.nf_rbase = r0;
     a.q0 = 0;
     a.q1 = all_children ? n : C.F;
     a.votes = (uint32_t*)x->dense.p;
-    a.p_choff = (const uint64_t*)P.choff.p;
+    a.p_choff = (const uint64_t*)(gp ? gp->choff.p : P.choff.p);
+    if (gp) {
+        a.gp_parent = (const uint32_t*)P.parent.p;
+        a.gp_a = (const uint32_t*)P.a.p;
+        a.gp_c = (const uint32_t*)P.c.p;
+    }
     a.r_lo = r0;
     a.r_hi = r1;
     a.work = (uint32_t*)x->fusedctr.p;
@@ -604,9 +617,10 @@ hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_chil
     prof_end(x, id);
     uint64_t pairs = P.S, child_pairs = 0;
     if (!host_pairs || id >= 0) {      // the device counters are read only when needed
-        CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)((char*)x->fusedctr.p + 8), 2, x->st));
+        CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)((char*)x->fusedctr.p + 8), 4, x->st));
         TRY(sync(x));
-        if (!host_pairs) pairs = read_mapped(x->range_h).pairs;
+        if (gp) pairs = read_mapped(x->misc_h + 1);
+        else if (!host_pairs) pairs = read_mapped(x->range_h).pairs;
         child_pairs = read_mapped(x->misc_h);
     }
     if (id >= 0) {
@@ -627,13 +641,32 @@ hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_chil
     return gather_levels(x, L, L + 1, r0, x->lv[L], 4, (const uint32_t*)x->lv[L].parent.p);
 }
 
+// tail_depth 6 at l = D-6: lv[l] holds the lists of a parent range and lv[l+1] its split children
+// R_(l+1) (votes from the last count-ahead, no lists). The fused tail streams each child's parent
+// list and rasters the leaf grids of all 4 children of the child; R_(l+1) is processed in pieces
+// whose grids (4 KB per region) stay within a quarter of the list budget (at most 1 GiB).
+hht_status tail_grandparent(hht_ctx* x, int l) {
+    Level& C = x->lv[l + 1];
+    const uint32_t F = C.F;
+    const uint64_t per = 4ull * kTail16Cells * 4;
+    const uint64_t capn = std::max<uint64_t>(1, std::min<uint64_t>(x->budget / 4, 1ull << 30) / per);
+    for (uint32_t q0 = 0; q0 < F;) {
+        const uint32_t q1 = (uint32_t)std::min<uint64_t>(F, q0 + capn);
+        TRY(tail_fused(x, l + 1, q0, q1, true, &x->lv[l]));
+        q0 = q1;
+    }
+    return HHT_OK;
+}
+
 // Preconditions: lv[l] holds the lists of R_l[r0, r1) and lv[l+1] holds R_(l+1) = the split
 // children of R_l[r0, r1) with NF_(l+1). Processes everything below.
 hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
     const int lc = l + 1;
     if (lc >= x->D) return HHT_OK;
-    if (!x->circle && x->D >= 3 && l == x->D - tail_depth(x))
+    if (!x->circle && x->D >= 3 && l == x->D - tail_depth(x)) {
+        if (tail_depth(x) == 6) return tail_grandparent(x, l);
         return tail_depth(x) == 5 ? tail_fused(x, l, r0, r1, no_count_ahead(x)) : tail(x, l, r0, r1);
+    }
     Level& P = x->lv[l];
     Level& C = x->lv[lc];
     const uint32_t Fc = C.F;
@@ -671,8 +704,8 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         // With a leaf sink, the leaves of the last range are copied to the host after all compute: when
         // the detection's final piece at the last list level would be large, cut its last quarter into
         // a range of its own, so that the copy of the rest overlaps that quarter's tail
-        if (x->sink && !final_cut && ri.q1 == Fc && q0 > 0 && r1 == P.F && no_count_ahead(x) &&
-            lc == x->D - 5 && Fc - q0 >= 64) {
+        if (x->sink && !final_cut && ri.q1 == Fc && q0 > 0 && r1 == P.F && fused_tail(x) &&
+            lc == x->D - tail_depth(x) && Fc - q0 >= 64) {
             final_cut = true;
             const uint32_t qf = q0 + (Fc - q0) - (Fc - q0) / 8;
             CK(launch_range((const uint64_t*)C.off.p, (const uint32_t*)C.parent.p, C.F, q0, cap, qf,
@@ -1217,7 +1250,7 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     if (o.world > 1 && !o.nccl_id && !o.group) return HHT_EINVAL;
     if (o.group && (o.nccl_id || o.group->world != o.world)) return HHT_EINVAL;
     if (o.halves == 0 || (o.halves & ~3u)) return HHT_EINVAL;
-    if (!(o.tail_depth == 0 || (o.tail_depth >= 3 && o.tail_depth <= 5))) return HHT_EINVAL;
+    if (!(o.tail_depth == 0 || (o.tail_depth >= 3 && o.tail_depth <= 6))) return HHT_EINVAL;
     hht_ctx* x = new (std::nothrow) hht_ctx();
     if (!x) return HHT_ENOMEM;
     x->opts = o;

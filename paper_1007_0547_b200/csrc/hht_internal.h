@@ -96,8 +96,14 @@ struct PassArgs {
     const uint64_t* p_choff;       // parents' chunk offsets (their chunks are consecutive)
     uint32_t r_lo, r_hi;
     uint32_t* work;                // device counter, zero at launch
-    unsigned long long* child_pairs;   // device counter: (line, split child) pairs rastered
+    unsigned long long* child_pairs;   // device counters: [0] (line, child) pairs rastered, [1] entries streamed
     uint32_t all_children;         // k_fused: raster all 4 children of every parent, grid 4 (r - r_lo) + q
+    // k_fused from the grandparents' lists (tail_depth 6): work unit r of level l streams the list of
+    // its parent gp_parent[r] (level l-1 chunks/lists above) and takes its region from gp_a/gp_c;
+    // entries that do not cross r have no child bit set. nullptr: r's own list.
+    const uint32_t* gp_parent;
+    const uint32_t* gp_a;
+    const uint32_t* gp_c;
 };
 
 struct SplitArgs {

@@ -865,7 +865,10 @@ __global__ void __launch_bounds__(256, 2) k_fused(const PassArgs A) {
         if (lane == 0) r = atomicAdd(A.work, 1u);
         r = __shfl_sync(kFull, r, 0) + A.r_lo;
         if (r >= A.r_hi) break;
-        const uint64_t c_lo = __ldg(A.p_choff + r), c_hi = __ldg(A.p_choff + r + 1);
+        // the list streamed: r's own, or (tail_depth 6) its parent's, whose entries that miss r
+        // get no child bits (a line crossing a child of r crosses r)
+        const uint32_t lr = A.gp_parent ? __ldg(A.gp_parent + r) : r;
+        const uint64_t c_lo = __ldg(A.p_choff + lr), c_hi = __ldg(A.p_choff + lr + 1);
         if (c_lo == c_hi) continue;
         // lanes 0..3: grid index of child `lane` (+ q0): its next-frontier index when only split
         // children are rastered, 4 (r - r_lo) + lane when all are; kNone for skipped children
@@ -886,7 +889,9 @@ __global__ void __launch_bounds__(256, 2) k_fused(const PassArgs A) {
         }
         if (splitm == 0) continue;
         ChunkDesc d = load_desc(A.chunks, c_lo, c_hi);
-        const uint32_t pa = d.a, pc = d.c, beta = d.beta;
+        const uint32_t pa = A.gp_parent ? __ldg(A.gp_a + r) : d.a;
+        const uint32_t pc = A.gp_parent ? __ldg(A.gp_c + r) : d.c;
+        const uint32_t beta = d.beta;
         const I i0 = (I)pa << sh;
         const I j0 = (I)pc << sh;
         const I alpha = ((I)1 << D) - 2 * i0;
@@ -895,6 +900,7 @@ __global__ void __launch_bounds__(256, 2) k_fused(const PassArgs A) {
         uint32_t p[kItems];
         load_items(p, A.list, A.list_base, d, lane);
         uint64_t ch = c_lo;
+        uint32_t streamed = 0;                             // entries of this work unit (profiling)
         // One loop whose every iteration either rasters one stack (a full one, or once the parent's
         // chunks are exhausted any non-empty one) or pushes one chunk: the raster code is
         // instantiated once (four inlined copies measured 2x slower: instruction-cache misses).
@@ -923,6 +929,7 @@ __global__ void __launch_bounds__(256, 2) k_fused(const PassArgs A) {
             if (ch >= c_hi) break;
             // push chunk ch: child bits of its entries (split children only)
             const int cnt = (int)d.cnt;
+            streamed += (uint32_t)cnt;
             uint32_t cm = 0;
 #pragma unroll
             for (int it = 0; it < kItems; ++it) {
@@ -971,6 +978,7 @@ __global__ void __launch_bounds__(256, 2) k_fused(const PassArgs A) {
             d = load_desc(A.chunks, ch, c_hi);
             load_items(p, A.list, A.list_base, d, lane);
         }
+        if (lane == 0) atomicAdd(A.child_pairs + 1, (unsigned long long)streamed);
     }
 }
 

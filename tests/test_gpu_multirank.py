@@ -42,7 +42,8 @@ def _run_ranks(pts, N, D, T, halves, world, dev, **kw):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("kw", [{}, {"tail_depth": 4}, {"tail_depth": 3}, {"mem_budget": 256 << 10},
+@pytest.mark.parametrize("kw", [{}, {"tail_depth": 4}, {"tail_depth": 3}, {"tail_depth": 6},
+                                {"mem_budget": 256 << 10}, {"mem_budget": 256 << 10, "tail_depth": 6},
                                 {"variant": 1}])
 def test_multirank_c2(world, kw, cuda_device):
     cfg = synth.CONFIGS[2]
@@ -56,8 +57,8 @@ def test_multirank_c2(world, kw, cuda_device):
         st = h.stats()
         assert (st["tests"], st["votes"], st["leaves"]) == (ref.tests, ref.votes, ref.leaves.shape[0])
         pairs += st["pairs"]
-    if "mem_budget" in kw:
-        assert min(h.stats()["ranges"] for h in hs) > 4 * cfg.D
+    if "mem_budget" in kw:   # tail_depth 6 has no level D-5 lists, so fewer ranges
+        assert min(h.stats()["ranges"] for h in hs) > (3 if kw.get("tail_depth") == 6 else 4) * cfg.D
     for h in hs:
         h.close()
     g.close()

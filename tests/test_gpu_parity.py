@@ -213,10 +213,11 @@ def test_c2_structure_and_profile(torch_dev):
     assert prof["write"]["launches"] > 0 and prof["split"]["launches"] >= cfg.D
 
 
-@pytest.mark.parametrize("tail_depth", [3, 4, 5])
+@pytest.mark.parametrize("tail_depth", [3, 4, 5, 6])
 @pytest.mark.parametrize("seed", range(8))
 def test_tail_depth_variants(seed, tail_depth, torch_dev):
-    """The 8x8 (D-3), 16x16 (D-4) and fused 16x16-from-(D-5) tails give identical records and leaves."""
+    """The 8x8 (D-3), 16x16 (D-4), fused 16x16-from-(D-5) and fused 16x16-from-(D-6) tails give
+    identical records and leaves."""
     rng = np.random.default_rng(100 + seed)
     N = int(rng.choice([16, 33, 64, 200]))
     D = int(rng.integers(3, 9))
@@ -279,7 +280,7 @@ def test_leaf_sink_streaming(budget, torch_dev):
     assert h.stats()["leaves_streamed"] == 0
 
 
-@pytest.mark.parametrize("tail_depth", [4, 5])
+@pytest.mark.parametrize("tail_depth", [4, 5, 6])
 @pytest.mark.parametrize("N", [1, 2, 3, 5, 1023, 4095, 16383, 32767])
 def test_raster_fixed_point_extremes(N, tail_depth, torch_dev):
     """The 16x16 raster's fixed-point floors (csrc Raster16) at the extremes of 3N:
