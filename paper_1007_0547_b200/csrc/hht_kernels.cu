@@ -834,18 +834,32 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
 // raster of their split children (level D-4) in one kernel, without materialising level-(D-4)
 // lists. A warp owns one parent R at a time (dynamic, via an atomic counter) and walks its chunks:
 // each chunk's entries are tested against R's 4 children (the exact test of k_pass) and pushed onto
-// per-child stacks in shared memory (4 x 512 entries per warp); whenever a stack holds >= 256
-// entries, its top 256 are rastered over that child's leaf grid exactly as k_tail16 would raster a
-// 256-entry chunk of the child's list (the order of a list is irrelevant to its counts); the last
+// per-child stacks in shared memory (4 x kQ entries per warp); whenever a stack holds a full batch
+// (kFusedBatch entries), that batch from its top is rastered over that child's leaf grid exactly as k_tail16 would
+// raster a chunk of the child's list (the order of a list is irrelevant to its counts); the last
 // partial stacks are flushed when R is done. Entries never leave the SM between the two steps.
 // ---------------------------------------------------------------------------------------------
-constexpr int kQ = 512;                           // stack capacity per child: < 224 left + <= 256 pushed
-constexpr int kFusedItems = 7;                    // raster batches of 7 lines per lane (224 entries)
+// Block shape (C5 fused tail, one B200; build with -D to compare): 16 warps x 12 lines per lane
+// (one 512-thread block per SM: one raster table per SM, 384-entry batches) 132.5 ms; 16 x 11 133.2,
+// x 13 134.6, x 14 137.4, x 9 / x 10 137.0, x 15 141.0, x 8 141.8, x 7 140.9; 12 warps x 14 149.0;
+// 8 warps x 7 (two blocks per SM, 224-entry batches, the previous default) 142.2.
+#ifndef HHT_FUSED_WARPS
+#define HHT_FUSED_WARPS 16                        // warps per block (1 block/SM); 8: 2 blocks/SM
+#endif
+#ifndef HHT_FUSED_ITEMS
+#define HHT_FUSED_ITEMS 12                        // raster batches of 12 lines per lane (384 entries)
+#endif
+constexpr int kFusedWarps = HHT_FUSED_WARPS;
+constexpr int kFusedThreads = kWarp * kFusedWarps;
+constexpr int kFusedMinBlocks = kFusedWarps <= 8 ? 2 : 1;
+constexpr int kFusedItems = HHT_FUSED_ITEMS;
 constexpr uint32_t kFusedBatch = kWarp * kFusedItems;
-constexpr int kFusedSmem = 8 * 4 * kQ * 4;       // dynamic: the stacks (the table is static)
+// stack capacity per child: < kFusedBatch left + <= 256 pushed (512 for 224-entry batches)
+constexpr int kQ = ((int)kFusedBatch - 1 + 256 + 63) / 64 * 64;
+constexpr int kFusedSmem = kFusedWarps * 4 * kQ * 4;   // dynamic: the stacks (the table is static)
 
 template <typename I>
-__global__ void __launch_bounds__(256, 2) k_fused(const PassArgs A) {
+__global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const PassArgs A) {
     extern __shared__ uint4 s_dyn[];
     uint32_t* s_q = reinterpret_cast<uint32_t*>(s_dyn);
     fill_tab16();
@@ -986,17 +1000,17 @@ int fused_blocks_per_sm(bool int64) {
     int n = 0;
     if (int64) {
         cudaFuncSetAttribute(k_fused<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fused<int64_t>, 256, kFusedSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fused<int64_t>, kFusedThreads, kFusedSmem);
     } else {
         cudaFuncSetAttribute(k_fused<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fused<int32_t>, 256, kFusedSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fused<int32_t>, kFusedThreads, kFusedSmem);
     }
     return n > 0 ? n : 1;
 }
 
 cudaError_t launch_fused(bool int64, const PassArgs& a, int grid, cudaStream_t st) {
-    if (int64) k_fused<int64_t><<<grid, 256, kFusedSmem, st>>>(a);
-    else k_fused<int32_t><<<grid, 256, kFusedSmem, st>>>(a);
+    if (int64) k_fused<int64_t><<<grid, kFusedThreads, kFusedSmem, st>>>(a);
+    else k_fused<int32_t><<<grid, kFusedThreads, kFusedSmem, st>>>(a);
     return cudaGetLastError();
 }
 
