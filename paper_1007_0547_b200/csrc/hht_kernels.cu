@@ -732,6 +732,7 @@ struct Raster16 {
     template <int ITEMS>
     __device__ __forceinline__ void run(const uint32_t (&p)[ITEMS], int cnt, uint32_t ra, uint32_t rc, uint32_t beta,
                                         uint32_t* dst, int lane) const {
+        static_assert(ITEMS <= 15, "per-lane 4-bit cell counters hold at most 15 lines");
         const I i0 = (I)ra << 4;
         const I j0 = (I)rc << 4;
         const I alpha = ((I)1 << D) - 2 * i0;
@@ -842,9 +843,14 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
 // Block shape (C5 fused tail, one B200; build with -D to compare): 16 warps x 12 lines per lane
 // (one 512-thread block per SM: one raster table per SM, 384-entry batches) 132.5 ms; 16 x 11 133.2,
 // x 13 134.6, x 14 137.4, x 9 / x 10 137.0, x 15 141.0, x 8 141.8, x 7 140.9; 12 warps x 14 149.0;
-// 8 warps x 7 (two blocks per SM, 224-entry batches, the previous default) 142.2.
+// 8 warps x 7 (two blocks per SM, 224-entry batches, the previous default) 142.2. Loading a
+// chunk's entries when it is pushed instead of one chunk ahead (HHT_FUSED_JIT, 8 registers fewer
+// during the raster): 135.2 (12 lines), 139.0 (13), 141.4 (14).
 #ifndef HHT_FUSED_WARPS
 #define HHT_FUSED_WARPS 16                        // warps per block (1 block/SM); 8: 2 blocks/SM
+#endif
+#ifndef HHT_FUSED_JIT
+#define HHT_FUSED_JIT 0                           // 1: load a chunk's entries when pushed, not ahead
 #endif
 #ifndef HHT_FUSED_ITEMS
 #define HHT_FUSED_ITEMS 12                        // raster batches of 12 lines per lane (384 entries)
@@ -912,7 +918,9 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
         const I beta_m1 = (N << D) - (I)3 * N * j0 - 1;
         uint32_t top0 = 0, top1 = 0, top2 = 0, top3 = 0;   // stack heights (warp-uniform)
         uint32_t p[kItems];
+#if !HHT_FUSED_JIT
         load_items(p, A.list, A.list_base, d, lane);
+#endif
         uint64_t ch = c_lo;
         uint32_t streamed = 0;                             // entries of this work unit (profiling)
         // One loop whose every iteration either rasters one stack (a full one, or once the parent's
@@ -941,6 +949,9 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
                 continue;
             }
             if (ch >= c_hi) break;
+#if HHT_FUSED_JIT
+            load_items(p, A.list, A.list_base, d, lane);
+#endif
             // push chunk ch: child bits of its entries (split children only)
             const int cnt = (int)d.cnt;
             streamed += (uint32_t)cnt;
@@ -990,7 +1001,9 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
             // the next chunk's entries are in flight while the full stacks are rastered
             ++ch;
             d = load_desc(A.chunks, ch, c_hi);
+#if !HHT_FUSED_JIT
             load_items(p, A.list, A.list_base, d, lane);
+#endif
         }
         if (lane == 0) atomicAdd(A.child_pairs + 1, (unsigned long long)streamed);
     }
