@@ -728,7 +728,9 @@ struct Raster16 {
 
     // ITEMS lines per lane (a batch of <= 32 ITEMS). ITEMS <= 7 keeps every per-lane cell count
     // <= 7, so the first reduce-scatter level can add the 4-bit counters of two lanes before they
-    // are widened to bytes (sums <= 14): half the widening work and shuffles of that level.
+    // are widened to bytes (sums <= 14): half the widening work of that level. Larger batches
+    // (<= 15 lines: 4-bit counts) exchange the raw nibble words and widen both before adding, so
+    // that level still takes one shuffle per column.
     template <int ITEMS>
     __device__ __forceinline__ void run(const uint32_t (&p)[ITEMS], int cnt, uint32_t ra, uint32_t rc, uint32_t beta,
                                         uint32_t* dst, int lane) const {
@@ -788,11 +790,10 @@ struct Raster16 {
                 }
             } else {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {                 // widen, then xor 16 on bytes
-                    const uint32_t e0 = acc[2 * u] & 0x0F0F0F0Fu, eh = acc[2 * u + 1] & 0x0F0F0F0Fu;
-                    const uint32_t q0 = (acc[2 * u] >> 4) & 0x0F0F0F0Fu, qh = (acc[2 * u + 1] >> 4) & 0x0F0F0F0Fu;
-                    e1[u] = e0 + __shfl_xor_sync(kFull, eh, 16);
-                    o1[u] = q0 + __shfl_xor_sync(kFull, qh, 16);
+                for (int u = 0; u < 4; ++u) {                 // xor 16 on 4-bit counters, widen both, add
+                    const uint32_t h = __shfl_xor_sync(kFull, acc[2 * u + 1], 16);
+                    e1[u] = (acc[2 * u] & 0x0F0F0F0Fu) + (h & 0x0F0F0F0Fu);
+                    o1[u] = ((acc[2 * u] >> 4) & 0x0F0F0F0Fu) + ((h >> 4) & 0x0F0F0F0Fu);
                 }
             }
             uint32_t w4[4];
