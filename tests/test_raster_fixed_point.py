@@ -56,6 +56,35 @@ def test_table_rows_match_corner_test(N):
     assert rows_of_entry(-2) == set()             # lanes past the batch: f = -1 in every column
 
 
+@pytest.mark.parametrize("N,D", [(1, 5), (3, 5), (64, 6), (512, 9), (8192, 13), (32767, 15), (65536, 20)])
+def test_setup_multiply_high(N, D):
+    """Raster16::run's setup: y0 2^k (k = 32 - fx_s) formed in 32-bit modular arithmetic from the
+    per-batch constants (alpha 2^k, 2^(D+k) mod 2^32, (beta - 1) 2^k), then Y_0 = mulhi(y0 2^k, fx_m)
+    + bias and P = mulhi(ex 2^(k+1), fx_mlo) equal the 64-bit forms floor(y0 fx_m / 2^fx_s) and
+    floor(2ex fx_mlo / 2^fx_s) for every line crossing a level-(D-4) region (0 <= y0 < 2^fx_s)."""
+    s, m, mlo = fx_consts(N)
+    k = 32 - s
+    M = 0xFFFFFFFF
+    r = random.Random(N * 31 + D)
+    n3 = 3 * N
+    for _ in range(3000):
+        ra, rc = r.randrange(1 << (D - 4)), r.randrange(1 << (D - 4))
+        i0, j0 = ra << 4, rc << 4
+        ex, ey = r.randrange(N), r.randrange(N)
+        alpha = (1 << D) - 2 * i0
+        beta_m1 = (N << D) - n3 * j0 - 1
+        G1 = ex * alpha + (ey << D) + beta_m1          # G(SW corner) - 1, exact (any sign)
+        alpha_s = ((alpha & M) << k) & M
+        ey_s = (1 << (D + k)) & M if D + k < 32 else 0
+        beta_s = ((beta_m1 & M) << k) & M
+        y0s = (ex * alpha_s + ey * ey_s + beta_s) & M
+        assert y0s == (G1 << k) & M                    # so y0s = y0 2^k exactly when 0 <= y0 < 2^s
+        y0 = r.randrange(16 * (2 * ex + n3))           # a line crossing the region
+        assert y0 < (1 << s)
+        assert ((((y0 << k) & M) * m) >> 32) == (y0 * m) >> s
+        assert (((ex << (k + 1)) & M) * mlo) >> 32 == (2 * ex * mlo) >> s
+
+
 def test_table_placement():
     """tab16_place / fill_tab16 / Raster16::boundary: for any 8-byte aligned table address S, the
     entries H + 256 (t + 2B) + 8 c (t in [-34, 56), c < 32) lie inside the array, B keeps every top
