@@ -854,8 +854,10 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
 // raster a chunk of the child's list (the order of a list is irrelevant to its counts); the last
 // partial stacks are flushed when R is done. Entries never leave the SM between the two steps.
 // ---------------------------------------------------------------------------------------------
-// Block shape (C5 fused tail, one B200; build with -D to compare): 16 warps x 12 lines per lane
-// (one 512-thread block per SM: one raster table per SM, 384-entry batches) 132.5 ms; 16 x 11 133.2,
+// Block shape (C5 fused tail, one B200; build with -D to compare). With the current raster setup:
+// 16 warps x 13 lines per lane (one 512-thread block per SM: one raster table per SM, 416-entry
+// batches) 122.3 ms; x 12 123.8, x 11 126.4, x 10 128.3, x 14 128.3. First sweep (64-bit setup,
+// two-shuffle first reduce level): 16 x 12 132.5 ms; 16 x 11 133.2,
 // x 13 134.6, x 14 137.4, x 9 / x 10 137.0, x 15 141.0, x 8 141.8, x 7 140.9; 12 warps x 14 149.0;
 // 8 warps x 7 (two blocks per SM, 224-entry batches, the previous default) 142.2. Loading a
 // chunk's entries when it is pushed instead of one chunk ahead (HHT_FUSED_JIT, 8 registers fewer
@@ -867,7 +869,7 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
 #define HHT_FUSED_JIT 0                           // 1: load a chunk's entries when pushed, not ahead
 #endif
 #ifndef HHT_FUSED_ITEMS
-#define HHT_FUSED_ITEMS 12                        // raster batches of 12 lines per lane (384 entries)
+#define HHT_FUSED_ITEMS 13                        // raster batches of 13 lines per lane (416 entries)
 #endif
 constexpr int kFusedWarps = HHT_FUSED_WARPS;
 constexpr int kFusedThreads = kWarp * kFusedWarps;
