@@ -408,6 +408,9 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
     a.child_level = child_level;
     a.leaf_level = leaf;
     a.need_lists = need_lists;
+    // offsets are read by chunk maps and range selection: list levels, and level D-1 (the
+    // count-only pass selects its range there)
+    a.write_off = need_lists || child_level == x->D - 1;
     a.record = record;
     a.T = x->T;
     a.nf = (uint32_t*)C.nf.p;

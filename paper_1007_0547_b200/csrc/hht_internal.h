@@ -117,6 +117,8 @@ struct SplitArgs {
     int child_level;
     int leaf_level;                // child_level == D: emit leaves, no frontier
     int need_lists;                // child_level <= D-2: children will carry candidate lists
+    int write_off;                 // write the children's list / chunk offsets (lists, or a range
+                                   // selection reads them); other levels skip 16 B per child
     int record;
     uint64_t T;
     const uint32_t* p_votes;       // derive_ne: parents' global votes (range start)

@@ -2055,8 +2055,10 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
                             A.out.parent[f] = A.parent_base + p;
                             A.out.len[f] = vl[q];
                             A.out.votes[f] = v[q];
-                            A.out.off[f] = s;
-                            A.out.choff[f] = cc;
+                            if (A.write_off) {
+                                A.out.off[f] = s;
+                                A.out.choff[f] = cc;
+                            }
                         }
                         f += 1;
                         s += len[q];
