@@ -117,8 +117,10 @@ struct SplitArgs {
     int child_level;
     int leaf_level;                // child_level == D: emit leaves, no frontier
     int need_lists;                // child_level <= D-2: children will carry candidate lists
-    int write_off;                 // write the children's list / chunk offsets (lists, or a range
-                                   // selection reads them); other levels skip 16 B per child
+    int write_off;                 // write the children's list lengths, votes and list / chunk
+                                   // offsets (read by list passes, chunk maps, range selection and
+                                   // the derived-NE split: list levels and D-1); other levels skip
+                                   // 24 B per child
     int record;
     uint64_t T;
     const uint32_t* p_votes;       // derive_ne: parents' global votes (range start)

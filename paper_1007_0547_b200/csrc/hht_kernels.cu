@@ -2053,9 +2053,9 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
                             A.out.a[f] = ca;
                             A.out.c[f] = cb;
                             A.out.parent[f] = A.parent_base + p;
-                            A.out.len[f] = vl[q];
-                            A.out.votes[f] = v[q];
-                            if (A.write_off) {
+                            if (A.write_off) {               // read only at list levels / D-1
+                                A.out.len[f] = vl[q];
+                                A.out.votes[f] = v[q];
                                 A.out.off[f] = s;
                                 A.out.choff[f] = cc;
                             }
