@@ -37,7 +37,9 @@
  *     below  <=>  F < 0  <=>  2^D*b_c + x0*(2^D*m_c) - 2^D*y0 < 0.
  *
  * Parity pins: tests/test_oracle_pins.py (SPEC worked examples, Fig. 2 prose example, exact
- * rational cross-check, brute force, invariants, survey worked example).
+ * rational cross-check, brute force, invariants, survey worked example; both circumcircle variants
+ * against the minimised point-to-line distance in exact rationals, the horizontal-line closed form
+ * and the survey's L9 totals). scripts/mutate_oracle.py: every listed mutant fails a pin.
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -128,9 +130,34 @@ int oracle_circle_passes(int32_t x, int32_t y, int32_t half, int32_t N, int32_t 
     return lhs <= rhs;
 }
 
+/* The same FHT [9]-style test with the distance and the circumradius measured in
+ * the (m, b) units of the parameter space itself (reading R22): a level-l region is
+ * the rectangle of width w = 2s/2^D (in m) and height h = 3N*s/2^D (in b), its circumcircle has
+ * radius sqrt(w^2 + h^2)/2, and the line b + ex*m - ey = 0 lies at distance |F(centre)|/sqrt(1+ex^2)
+ * from the centre, F(m, b) = b + ex*m - ey (the negated F of PAPER.md:51). Squared and multiplied by
+ * 4^(D+1) > 0:  (2^(D+1) F(centre))^2 <= (1 + ex^2) * (4 s^2 + 9 N^2 s^2), where 2^(D+1)*F(centre) is
+ * exact in integers at the doubled centre (2*i0+s, 2*j0+s):
+ *     2^(D+1) m_c = -2^(D+1) + 2*i2,  2^(D+1) b_c = -N*2^(D+1) + 3N*j2.
+ * Exact in __int128 while (1 + N^2) * 4^D * (4 + 9 N^2) < 2^127 (N <= 2^16 and D <= 24). */
+int oracle_circle_mb_passes(int32_t x, int32_t y, int32_t half, int32_t N, int32_t D, int32_t level,
+                            int64_t a, int64_t c) {
+    int64_t ex, ey;
+    effective_point(x, y, half, &ex, &ey);
+    const int64_t s = (int64_t)1 << (D - level);
+    const int64_t i2 = 2 * a * s + s, j2 = 2 * c * s + s;             /* doubled centre */
+    const __int128 sc = (__int128)1 << (D + 1);                        /* 2^(D+1) */
+    const __int128 m2 = -sc + 2 * (__int128)i2;                        /* 2^(D+1) * m_c */
+    const __int128 b2 = -(__int128)N * sc + 3 * (__int128)N * j2;      /* 2^(D+1) * b_c */
+    const __int128 F2 = b2 + ex * m2 - sc * ey;                        /* 2^(D+1) * F(centre) */
+    const __int128 lhs = F2 * F2;
+    const __int128 rhs = (__int128)(1 + ex * ex) * s * s * (4 + 9 * (__int128)N * N);
+    return lhs <= rhs;
+}
+
 static int member(int variant, int32_t x, int32_t y, int32_t half, int32_t N, int32_t D,
                   int32_t level, int64_t a, int64_t c) {
     if (variant == 1) return oracle_circle_passes(x, y, half, N, D, level, a, c);
+    if (variant == 2) return oracle_circle_mb_passes(x, y, half, N, D, level, a, c);
     return oracle_votes_for(oracle_code(x, y, half, N, D, level, a, c));
 }
 

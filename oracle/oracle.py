@@ -48,6 +48,8 @@ def _load():
             lib.oracle_generic_code.restype = C.c_int
             lib.oracle_circle_passes.argtypes = [i32, i32, i32, i32, i32, i32, i64, i64]
             lib.oracle_circle_passes.restype = C.c_int
+            lib.oracle_circle_mb_passes.argtypes = [i32, i32, i32, i32, i32, i32, i64, i64]
+            lib.oracle_circle_mb_passes.restype = C.c_int
             lib.oracle_region_votes.argtypes = [p, i64, i32, i32, i32, i32, i64, i64, i32]
             lib.oracle_region_votes.restype = i64
             lib.oracle_dense_votes.argtypes = [p, i64, i32, i32, i32, i32, p]
@@ -97,6 +99,10 @@ def generic_code(m_num: int, m_den: int, b_num: int, b_den: int, x0: int, y0: in
 
 def circle_passes(x: int, y: int, half: int, N: int, D: int, level: int, a: int, c: int) -> int:
     return _load().oracle_circle_passes(x, y, half, N, D, level, a, c)
+
+
+def circle_mb_passes(x: int, y: int, half: int, N: int, D: int, level: int, a: int, c: int) -> int:
+    return _load().oracle_circle_mb_passes(x, y, half, N, D, level, a, c)
 
 
 def region_votes(points, half: int, N: int, D: int, level: int, a: int, c: int, variant: int = 0) -> int:
@@ -160,7 +166,8 @@ def _collect(lib, h, N, D, T, halves) -> OracleResult:
 def detect(points, N: int, D: int, T: int, halves: int = ALPHA | BETA, variant: int = 0,
            max_tests: int = 0) -> OracleResult:
     """Recursive DFS detector (removal off). variant 0 = exact 4-bit code,
-    1 = FHT circumcircle test. max_tests > 0 stops the walk once that many code evaluations were
+    1 = FHT circumcircle test in lattice units (square regions), 2 = FHT circumcircle test in
+    (m, b) units (2s/2^D x 3Ns/2^D rectangles; reading R22). max_tests > 0 stops the walk once that many code evaluations were
     done (bounded CPU-baseline samples; result.truncated is then True)."""
     p = _pts(points)
     lib = _load()

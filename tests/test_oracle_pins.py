@@ -322,3 +322,144 @@ def test_c1_recovers_generated_lines():
         j = int((b + cfg.N) * side / (3 * cfg.N))
         near = {(i + di, j + dj) for di in (-1, 0, 1) for dj in (-1, 0, 1)}
         assert near & cells, (t, i, j)
+
+
+# ---------------------------------------------------------------------------------------------
+# The circumcircle tests pinned to geometry computed another way ("calculates the
+# perpendicular distance to the line from the center of the region and compares it with the radius
+# of the circle circumscribing the region"). The oracle squares the point-line distance formula;
+# here the squared distance is the minimum over the line of the squared distance to the centre,
+# found by setting the derivative of a quadratic to zero, in exact rationals.
+# ---------------------------------------------------------------------------------------------
+
+def _min_sq_dist_lattice(ex, ey, N, D, i_c, j_c):
+    """min over points (i, j) of the lattice line 2ex*i + 3N*j = 2^D (ex+ey+N) of (i-i_c)^2 + (j-j_c)^2."""
+    K = Fraction((1 << D) * (ex + ey + N), 3 * N)
+    k = Fraction(2 * ex, 3 * N)                          # j(i) = K - k*i
+    i = (i_c + k * (K - j_c)) / (1 + k * k)              # d/di [(i-i_c)^2 + (K-k*i-j_c)^2] = 0
+    return (i - i_c) ** 2 + (K - k * i - j_c) ** 2
+
+
+def _min_sq_dist_mb(ex, ey, m_c, b_c):
+    """min over m of (m-m_c)^2 + (ey - ex*m - b_c)^2 (points (m, b) of the line b = ey - ex*m)."""
+    m = (m_c + ex * (ey - b_c)) / (1 + ex * ex)
+    return (m - m_c) ** 2 + (ey - ex * m - b_c) ** 2
+
+
+@pytest.mark.parametrize("N,D", [(5, 2), (8, 3), (16, 4), (6, 4)])
+def test_circle_lattice_units_matches_minimised_distance(N, D):
+    """Variant 1: the line meets the circle through the 4 corners of the s x s lattice square
+    (radius s/sqrt(2), centre (i0 + s/2, j0 + s/2)) iff its minimum squared distance <= s^2/2."""
+    rng = random.Random(N * 100 + D)
+    pts = [(x, y) for x in range(N) for y in range(N)]
+    if len(pts) > 80:
+        pts = rng.sample(pts, 80)
+    for x, y in pts:
+        for half in (oracle.ALPHA, oracle.BETA):
+            ex, ey = (x, y) if half == oracle.ALPHA else (y, x)
+            for lev in range(D + 1):
+                s = 1 << (D - lev)
+                for a in range(1 << lev):
+                    for c in range(1 << lev):
+                        d2 = _min_sq_dist_lattice(ex, ey, N, D, Fraction(2 * a * s + s, 2), Fraction(2 * c * s + s, 2))
+                        want = int(d2 <= Fraction(s * s, 2))
+                        assert oracle.circle_passes(x, y, half, N, D, lev, a, c) == want, (x, y, half, lev, a, c)
+
+
+def test_circle_lattice_units_horizontal_closed_form():
+    """ex = 0: the parameter line is horizontal, b = ey, i.e. lattice row j* = 2^D (ey+N)/(3N); the
+    circle of radius s/sqrt(2) around (., j_c) meets it iff 2 (j_c - j*)^2 <= s^2."""
+    for N, D in [(8, 3), (16, 4), (12, 5)]:
+        for ey in range(N):
+            jstar = Fraction((1 << D) * (ey + N), 3 * N)
+            for lev in range(D + 1):
+                s = 1 << (D - lev)
+                for c in range(1 << lev):
+                    jc = Fraction(2 * c * s + s, 2)
+                    want = int(2 * (jc - jstar) ** 2 <= s * s)
+                    for a in (0, (1 << lev) - 1):
+                        assert oracle.circle_passes(0, ey, oracle.ALPHA, N, D, lev, a, c) == want
+
+
+def test_circle_survey_l9_totals():
+    """SURVEY.md §0 L9 (the survey's independent enumeration): N=16, D=4 over all effective points
+    and all regions of all levels: 10,356 exact votes, 1,554 extra circle votes."""
+    g = _gold("survey_l9_circle_n16_d4.json")
+    N, D = g["N"], g["D"]
+    exact = extra = 0
+    for x in range(N):
+        for y in range(N):
+            for lev in range(D + 1):
+                for a in range(1 << lev):
+                    for c in range(1 << lev):
+                        e = oracle.code(x, y, oracle.ALPHA, N, D, lev, a, c) not in (0, 15)
+                        p = oracle.circle_passes(x, y, oracle.ALPHA, N, D, lev, a, c)
+                        assert p or not e
+                        exact += e
+                        extra += p and not e
+    assert (exact, extra) == (g["exact_votes"], g["extra_circle_votes"])
+
+
+@pytest.mark.parametrize("N,D", [(5, 2), (8, 3), (16, 4), (6, 4)])
+def test_circle_mb_units_matches_minimised_distance(N, D):
+    """Variant 2 (reading R22): the region is the rectangle [m0, m0 + 2s/2^D] x [b0, b0 + 3Ns/2^D]
+    with m0 = -1 + 2 i0/2^D, b0 = -N + 3N j0/2^D; its circumcircle has the centre of the rectangle
+    and radius^2 = (w^2 + h^2)/4; the line b = ey - ex*m meets it iff min squared distance <= radius^2."""
+    rng = random.Random(N * 1000 + D)
+    pts = [(x, y) for x in range(N) for y in range(N)]
+    if len(pts) > 80:
+        pts = rng.sample(pts, 80)
+    S = 1 << D
+    for x, y in pts:
+        for half in (oracle.ALPHA, oracle.BETA):
+            ex, ey = (x, y) if half == oracle.ALPHA else (y, x)
+            for lev in range(D + 1):
+                s = 1 << (D - lev)
+                w, h = Fraction(2 * s, S), Fraction(3 * N * s, S)
+                for a in range(1 << lev):
+                    for c in range(1 << lev):
+                        m_c = -1 + Fraction(2 * a * s, S) + w / 2
+                        b_c = -N + Fraction(3 * N * c * s, S) + h / 2
+                        want = int(_min_sq_dist_mb(ex, ey, m_c, b_c) <= (w * w + h * h) / 4)
+                        assert oracle.circle_mb_passes(x, y, half, N, D, lev, a, c) == want, (x, y, half, lev, a, c)
+
+
+@pytest.mark.parametrize("passes", ["circle_passes", "circle_mb_passes"])
+def test_circle_variants_contain_exact_and_nest(passes):
+    """Both circle tests accept every exactly-crossing line (the circle contains the region), and a
+    child's circumcircle lies inside its parent's (radius halves, centre moves by half the parent's
+    radius), so passing a child implies passing the parent: the candidate-list restriction of
+    PAPER.md:100-103 stays exact for both variants."""
+    f = getattr(oracle, passes)
+    for N, D in [(8, 3), (16, 4), (7, 3)]:
+        for ex in range(N):
+            for ey in range(N):
+                for lev in range(D + 1):
+                    for a in range(1 << lev):
+                        for c in range(1 << lev):
+                            p = f(ex, ey, oracle.ALPHA, N, D, lev, a, c)
+                            if oracle.code(ex, ey, oracle.ALPHA, N, D, lev, a, c) not in (0, 15):
+                                assert p
+                            if p and lev > 0:
+                                assert f(ex, ey, oracle.ALPHA, N, D, lev - 1, a >> 1, c >> 1)
+
+
+def test_circle_mb_reading_grows_with_size():
+    """Reading R22's qualitative consequence (Table 1 C_v grows with the image size):
+    in (m, b) units the circumcircle is wide compared with the region for steep parameter lines,
+    so the extra votes per exact vote grow with N on uniform scenes (strictly, for N = 8, 16, 32)."""
+    ratios = []
+    for N in (8, 16, 32):
+        D = N.bit_length() - 1
+        rng = np.random.default_rng(N)
+        pts = rng.integers(0, N, size=(3 * N, 2)).astype(np.int32)
+        ex_ = oracle.detect(pts, N, D, 1 << 30, oracle.ALPHA, variant=0)
+        tot_e = tot_c = 0
+        for lev in range(D + 1):
+            for a in range(1 << lev):
+                for c in range(1 << lev):
+                    tot_e += oracle.region_votes(pts, oracle.ALPHA, N, D, lev, a, c, 0)
+                    tot_c += oracle.region_votes(pts, oracle.ALPHA, N, D, lev, a, c, 2)
+        assert ex_.votes == pts.shape[0]
+        ratios.append(tot_c / tot_e)
+    assert ratios[0] < ratios[1] < ratios[2], ratios
