@@ -7,8 +7,12 @@ One step = one full detection (all levels, both halves, records + leaves) of the
 synthetic edge points, resident in HBM. N > 1 runs under torch.distributed.run: points are sharded
 contiguously across ranks, per-level votes are summed with NCCL inside libhht, the timed region is
 bracketed by barrier + synchronize on every rank and the MAX over ranks is reported.
-`--impl reference` times the CPU oracle (oracle/, the only other place bench.py executes it) on a
-bounded sample of the same workload.
+`cpu_baseline` and `--impl reference` time the CPU oracle (oracle/, as it stands; the only places
+bench.py executes it) on all host cores, one oracle process per core, over a seeded sample of the
+same workload: complete level-(D-7) subtrees of the detection (or whole images of a batch).
+`roofline` reports the dominant kernel against its binding roof (the fused tail: the shared-memory
+data path), with HBM figures beside it; ncu counters from profiles/ are attached
+only when they were captured on the same libhht.so build.
 """
 from __future__ import annotations
 
@@ -40,7 +44,8 @@ def _args():
     ap.add_argument("--variant", default="exact", choices=["exact", "fht"],
                     help="membership test: the paper's exact corner code, or the FHT circumcircle comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--oracle-tests", type=float, default=4e8, help="bounded oracle sample (code evaluations)")
+    ap.add_argument("--oracle-steps", type=int, default=1, help="cpu_baseline: sampled oracle steps (all cores)")
+    ap.add_argument("--force-int64", action="store_true", help="run the int64 kernel instantiation")
     return ap.parse_args()
 
 
@@ -133,44 +138,149 @@ def _dist_init(n_gpus):
     return rank, world, local
 
 
-def _cpu_baseline(pts, cfg, budget_tests):
-    """The oracle as it stands on one host core, over a bounded depth-first prefix of the same
-    detection (stops after `budget_tests` code evaluations)."""
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# --- the oracle as it stands, on all host cores, over a seeded sample of the same workload ---------
+# Each task is one complete level-k subtree of the detection (oracle.detect_subtree from the region
+# with ALL points as candidates; a region whose own votes exceed T has every ancestor above T by
+# containment, so its subtree is exactly part of the workload), or one whole image of a batch. The
+# subtree root's scan over all points is not workload and is not counted in tests (conservative).
+_W = {}
+
+
+def _worker_init(path):
+    import numpy as np
+    _W["pts"] = np.load(path, mmap_mode="r")
+
+
+def _worker_task(t):
     import oracle
-    t0 = time.perf_counter()
-    r = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves, max_tests=int(budget_tests))
-    dt = time.perf_counter() - t0
-    return {"value": r.tests / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle DFS over config{cfg.cid} image 0 (ALPHA tree first), stopped after "
-                      f"{r.tests:.3g} code evaluations ({dt:.1f} s, single thread, plain C -O2)",
-            "seconds": dt, "tests": r.tests}
+    import numpy as np
+    kind, lo, hi, N, D, T, halves, half, k, a, c = t
+    pts = np.ascontiguousarray(_W["pts"][lo:hi])
+    if kind == "image":
+        return oracle.detect(pts, N, D, T, halves).tests
+    return oracle.detect_subtree(pts, N, D, T, half, k, a, c).tests - pts.shape[0]
+
+
+class OracleSampler:
+    def __init__(self, cfg, pts, offs, workers=None):
+        import multiprocessing as mp
+        import tempfile
+        import numpy as np
+        self.cfg, self.offs = cfg, offs
+        ncpu = os.cpu_count() or 1
+        try:
+            import psutil
+            cap = max(1, int(psutil.virtual_memory().available // (1 << 30)))   # ~1 GB per worker
+        except Exception:  # noqa: BLE001
+            cap = ncpu
+        self.workers = workers or max(1, min(ncpu, cap))
+        d = "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir()
+        self.path = os.path.join(d, f"hht_bench_pts_{os.getpid()}.npy")
+        np.save(self.path, np.ascontiguousarray(pts))
+        self.pool = mp.get_context("spawn").Pool(self.workers, _worker_init, (self.path,))
+        self.k = max(0, cfg.D - 7)
+
+    def tasks(self, seed):
+        import numpy as np
+        cfg, rng = self.cfg, np.random.default_rng(1000 + seed)
+        B = self.offs.shape[0] - 1
+        if B > 1:
+            imgs = rng.choice(B, size=min(B, self.workers), replace=False)
+            return [("image", int(self.offs[b]), int(self.offs[b + 1]), cfg.N, cfg.D, cfg.T, cfg.halves, 0, 0, 0, 0)
+                    for b in imgs], f"{len(imgs)} whole images of the batch"
+        halves = [h for h in (1, 2) if cfg.halves & h]
+        side = 1 << self.k
+        n = 2 * self.workers
+        cells = rng.choice(len(halves) * side * side, size=min(n, len(halves) * side * side), replace=False)
+        out = []
+        for q in cells.tolist():
+            h, r = divmod(q, side * side)
+            out.append(("subtree", 0, int(self.offs[1]), cfg.N, cfg.D, cfg.T, cfg.halves, halves[h], self.k,
+                        r % side, r // side))
+        return out, f"{len(out)} seeded level-{self.k} subtrees (of {len(halves) * side * side})"
+
+    def step(self, seed):
+        tasks, what = self.tasks(seed)
+        t0 = time.perf_counter()
+        tests = sum(self.pool.map(_worker_task, tasks, chunksize=1))
+        return tests, time.perf_counter() - t0, what
+
+    def close(self):
+        self.pool.terminate()
+        try:
+            os.remove(self.path)
+        except OSError:
+            pass
+
+
+def _cpu_baseline(sampler, steps=1):
+    tot_t, tot_s, what = 0, 0.0, ""
+    for k in range(steps):
+        t, dt, what = sampler.step(k)
+        tot_t += t
+        tot_s += dt
+    cfg = sampler.cfg
+    return {"value": tot_t / tot_s, "unit": UNIT, "cores": sampler.workers, "kind": "oracle",
+            "cpu_model": _cpu_model(), "os_cpu_count": os.cpu_count(),
+            "sample": f"config{cfg.cid}: {what} per step x {steps}, one oracle process per core "
+                      f"(plain C -O2, oracle/ as it stands); tests = code evaluations below each subtree "
+                      f"root; {tot_t:.3g} tests in {tot_s:.1f} s wall",
+            "seconds": tot_s, "tests": tot_t}
 
 
 def run_reference(a):
-    rank, world, _ = (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0)
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import numpy as np
     from paper_1007_0547_b200 import synth
     cfg = synth.CONFIGS[a.config]
-    pts, _ = synth.config_image(a.config, 0)
-    per_step = max(a.oracle_tests / max(a.steps, 1), 2e7)
-    for _ in range(a.warmup):
-        _cpu_baseline(pts, cfg, min(per_step, 2e7))
-    tot_tests, tot_s = 0, 0.0
-    for _ in range(a.steps):
-        r = _cpu_baseline(pts, cfg, per_step)
-        tot_tests += r["tests"]
-        tot_s += r["seconds"]
+    if cfg.images > 1:
+        pts, offs = synth.config_batch(a.config)
+    else:
+        pts, _ = synth.config_image(a.config, 0)
+        offs = np.array([0, pts.shape[0]], dtype=np.int64)
+    smp = OracleSampler(cfg, pts, offs)
+    try:
+        for w in range(a.warmup):
+            smp.step(10_000 + w)
+        tot_tests, tot_s, what = 0, 0.0, ""
+        for k in range(a.steps):
+            t, dt, what = smp.step(k)
+            tot_tests += t
+            tot_s += dt
+    finally:
+        smp.close()
     v = tot_tests / tot_s
+    wl = _workload(cfg)
+    wl["points_per_image"] = int(offs[1] - offs[0])
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": 1e3 * tot_s / a.steps, "higher_is_better": True,
-            "scaling": "weak" if cfg.images > 1 else "strong", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic", "config": _workload(cfg),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{a.steps} steps, each the oracle DFS over config{cfg.cid} stopped after "
-                                       f"{per_step:.3g} code evaluations"},
+            "scaling": "weak" if cfg.images > 1 else "strong", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": wl,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": smp.workers, "kind": "oracle",
+                             "cpu_model": _cpu_model(), "os_cpu_count": os.cpu_count(),
+                             "sample": f"{a.steps} steps, each {what} of config{cfg.cid}, one oracle process "
+                                       f"per core; {tot_tests:.3g} tests in {tot_s:.1f} s"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _lib_sha256():
+    import hashlib
+    from paper_1007_0547_b200 import build as b
+    with open(b.LIB, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()
 
 
 def main():
@@ -200,7 +310,7 @@ def main():
         nccl_id = hdist.broadcast_bytes(hht.nccl_unique_id() if rank == 0 else None)
     h = hht.HHT(device=local, halves=cfg.halves, record_levels=True, profile=True,
                 rank=rank if comm_world > 1 else 0, world=comm_world, nccl_id=nccl_id, prefetch=a.prefetch,
-                tail_depth=a.tail_depth, variant=hht.FHT_CIRCLE if a.variant == "fht" else hht.EXACT)
+                tail_depth=a.tail_depth, force_int64=a.force_int64, variant=hht.FHT_CIRCLE if a.variant == "fht" else hht.EXACT)
     d_pts = torch.from_numpy(np.ascontiguousarray(my)).to(dev)
     B = my_offs.shape[0] - 1
 
@@ -261,40 +371,50 @@ def main():
     nl = max(d["launches"], 1)
     avg_ms = d["ms"] / nl
     achieved_gbs = (d["bytes"] / nl) / (avg_ms / 1e3) / 1e9 if d["launches"] else 0.0
-    # traffic: DRAM bytes of one launch of the same kernel class from the committed ncu --set full
-    # capture (profiles/ncu_traffic.json), with that launch's algorithmic bytes beside it
-    traffic, cap = None, {}
+    # traffic and pipe counters: one launch of the same kernel class from the committed ncu --set full
+    # capture (profiles/ncu_traffic.json), used only when it was taken on THIS build of libhht.so
+    traffic, cap, ncu_note = None, {}, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            cap = json.load(open(tpath)).get(f"config{cfg.cid}", {}).get(dom, {}) or {}
-            traffic = cap.get("traffic")
-        except Exception:
+            tj = json.load(open(tpath))
+            if tj.get("libhht_sha256") == _lib_sha256():
+                cap = tj.get(f"config{cfg.cid}", {}).get(dom, {}) or {}
+                traffic = cap.get("traffic")
+            else:
+                ncu_note = (f"profiles/ncu_traffic.json was captured on another build "
+                            f"({str(tj.get('libhht_sha256'))[:12]}); not used")
+        except Exception:  # noqa: BLE001
             cap = {}
     hbm = {"achieved": achieved_gbs, "peak": peak, "unit": "GB/s", "frac": achieved_gbs / peak,
            "peak_source": peak_kind, "algorithmic_bytes_per_launch": d["bytes"] / nl, "traffic": traffic,
            "traffic_launch_algorithmic_bytes": cap.get("algorithmic_bytes")}
-    ncu_pipes = ("ncu: issue active %.0f%%, ALU pipe %.0f%%, FMA pipe %.0f%%, DRAM %.0f%%"
-                 % (cap["issue_active_pct"], cap["alu_pipe_pct"], cap["fma_pipe_pct"], cap["dram_pct"])
-                 if cap.get("issue_active_pct") is not None else None)
+    if cap.get("issue_active_pct") is not None:
+        ncu_note = ("ncu (same build): issue active %.0f%%, ALU pipe %.0f%%, FMA pipe %.0f%%, DRAM %.0f%%"
+                    % (cap["issue_active_pct"], cap["alu_pipe_pct"], cap["fma_pipe_pct"], cap["dram_pct"]))
+        if cap.get("smem_wavefronts_pct") is not None:
+            ncu_note += ", shared-memory wavefronts %.0f%% (LSU data pipe %.0f%%)" % (
+                cap["smem_wavefronts_pct"], cap.get("lsu_data_pipe_pct") or float("nan"))
     common = {"kernel": dom, "kernel_share_of_step": d["ms"] / max(sum(step_ms), 1e-9),
-              "launches": d["launches"], "avg_launch_ms": avg_ms, "ncu": ncu_pipes}
+              "launches": d["launches"], "avg_launch_ms": avg_ms, "ncu": ncu_note}
     if d.get("ops"):
-        # integer-issue bound: algorithmic instructions of the raster steps per launch
-        # over the launch time, against the SM issue rate (1 warp instruction / clock / SMSP)
+        # The fused tail's binding roof is the shared-memory data path ("Algorithmic
+        # instructions"): every raster step (one line x one leaf column of a level-(D-4) region) is
+        # one 8-byte column-mask lookup per lane. The library counts ops = 8 per step, so the
+        # algorithmic lookup bytes per launch are ops / 8 steps x 8 B. Peak: 128 B / clock / SM.
         sms, mhz, mhz_src = _issue_clock(local)
-        ipeak = sms * 4 * 32 * mhz * 1e6 / 1e12
-        ach = (d["ops"] / nl) / (avg_ms / 1e3) / 1e12
-        # the raster's other bound: one 8-byte column-mask lookup per lane step (ops = 8 per step)
-        # against the shared-memory data path, 128 B / clock / SM
+        steps = d["ops"] / 8 / nl
         speak = sms * 128 * mhz * 1e6 / 1e12
-        sach = (d["ops"] / 8 * 8 / nl) / (avg_ms / 1e3) / 1e12
-        smem = {"achieved": sach, "peak": speak, "unit": "TB/s", "frac": sach / speak,
-                "peak_source": f"{sms} SMs x 128 B x {mhz:.0f} MHz",
-                "algorithmic_bytes_per_launch": d["ops"] / nl, "note": "table lookups only (8 B per lane step)"}
-        roofline = {"bound": "alu", "achieved": ach, "peak": ipeak, "unit": "Tinstr/s", "frac": ach / ipeak,
-                    "traffic": traffic, "peak_source": f"{sms} SMs x 4 SMSP x 32 lanes x {mhz:.0f} MHz ({mhz_src})",
-                    "algorithmic_instr_per_launch": d["ops"] / nl, **common, "hbm": hbm, "smem": smem}
+        sach = (steps * 8) / (avg_ms / 1e3) / 1e12
+        issue_peak = sms * 4 * 32 * mhz * 1e6 / 1e12
+        roofline = {"bound": "smem", "achieved": sach, "peak": speak, "unit": "TB/s", "frac": sach / speak,
+                    "traffic": traffic,
+                    "peak_source": f"shared-memory data path: {sms} SMs x 128 B/clock x {mhz:.0f} MHz ({mhz_src})",
+                    "algorithmic_bytes_per_launch": steps * 8, "raster_steps_per_launch": steps,
+                    "unit_of_work": "raster step = one (line, leaf column) of a level-(D-4) region: one 8-B lookup",
+                    **common, "hbm": hbm,
+                    "issue": {"raster_steps_per_s": steps / (avg_ms / 1e3), "peak_thread_instr_per_s": issue_peak * 1e12,
+                              "note": "the step itself is ~5 issue slots; see ncu issue active above"}}
     else:
         roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                     "frac": achieved_gbs / peak, "traffic": traffic, "peak_source": peak_kind,
@@ -332,12 +452,17 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        smp = None
         try:
-            cpu = _cpu_baseline(pts[offs[0]:offs[1]], cfg, a.oracle_tests)
+            smp = OracleSampler(cfg, pts, offs)
+            cpu = _cpu_baseline(smp, a.oracle_steps)
             cpu.pop("seconds", None)
             cpu.pop("tests", None)
         except Exception as e:  # noqa: BLE001
-            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
+        finally:
+            if smp is not None:
+                smp.close()
 
     if rank == 0:
         wl = _workload(cfg)

@@ -31,7 +31,11 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
            "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-           "lts__t_sector_hit_rate.pct"]
+           "lts__t_sector_hit_rate.pct",
+           "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+           "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+           "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-6, "us": 1e-3, "ms": 1,
          "msecond": 1, "usecond": 1e-3, "nsecond": 1e-6}
 
@@ -86,6 +90,9 @@ def main():
     lb = launch_bytes()
     traffic = {"config5": {}, "source": "ncu --set full --clock-control none, one launch per kernel class "
                "(scripts/gpu_profile.sh); algorithmic bytes of the same launch from hht_result_launches"}
+    shaf = os.path.join(G, "libhht.sha256")
+    # bench.py splices these counters into its line only when this hash equals the loaded library's
+    traffic["libhht_sha256"] = open(shaf).read().split()[0] if os.path.exists(shaf) else None
     wskip = 14
     wf = os.path.join(G, "write_skip.txt")
     if os.path.exists(wf):
@@ -112,11 +119,17 @@ def main():
                               d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")),
             "warps_active_pct": d.get("sm__warps_active.avg.pct_of_peak_sustained_active"),
             "registers": d.get("launch__registers_per_thread"),
+            "smem_wavefronts_pct": d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+            "lsu_data_pipe_pct": d.get("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+            "smem_ld_wavefronts": d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum"),
+            "smem_st_wavefronts": d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum"),
+            "smem_bank_conflicts": d.get("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
             "warp_instructions": d.get("smsp__inst_executed.sum")}
     json.dump(traffic, open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
     tot, cnt = launch_list()
     T = sum(tot.values())
-    lines = [f"# Round {a.round} GPU profile summary (config 5, one B200)", ""]
+    lines = [f"# Round {a.round} GPU profile summary (config 5, one B200)", "",
+             f"libhht.so sha256 of the profiled build: {traffic['libhht_sha256']}", ""]
     if os.path.exists(os.path.join(G, "bench_default.log")):
         b = json.loads(open(os.path.join(G, "bench_default.log")).read().strip().splitlines()[-1])
         lines += ["## bench.py (default: config 5, 5 steps, 3 warm-up)", "",
@@ -133,14 +146,14 @@ def main():
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         lines.append(f"| `{k}` | {cnt[k]} | {v:.1f} | {100 * v / T:.1f}% |")
     lines += ["", "## ncu --set full captures", "",
-              "| class | ms | DRAM bytes | algorithmic bytes | ratio | DRAM % | issue active % | ALU pipe % | FMA pipe % | LSU pipe % | warps active % | regs |",
-              "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+              "| class | ms | DRAM bytes | algorithmic bytes | ratio | DRAM % | issue active % | ALU pipe % | FMA pipe % | LSU pipe % | smem wavefronts % | warps active % | regs |",
+              "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     fmt = lambda v, f: (format(v, f) if isinstance(v, (int, float)) else "n/a")  # noqa: E731
     for cls, t in traffic["config5"].items():
         t = {k: (v if v is not None else float("nan")) for k, v in t.items()}
         lines.append(f"| {cls} | {t['duration_ms']:.2f} | {t['traffic']:.4g} | {t['algorithmic_bytes']} | "
                      f"{(t['traffic_over_algorithmic'] or 0):.3f} | {t['dram_pct']:.1f} | {t['issue_active_pct']:.1f} | "
-                     f"{t['alu_pipe_pct']:.1f} | {t['fma_pipe_pct']:.1f} | {t['lsu_pipe_pct']:.1f} | "
+                     f"{t['alu_pipe_pct']:.1f} | {t['fma_pipe_pct']:.1f} | {t['lsu_pipe_pct']:.1f} | {t['smem_wavefronts_pct']:.1f} | "
                      f"{t['warps_active_pct']:.1f} | {t['registers']:.0f} |")
     open(os.path.join(P, f"{tag}_summary.md"), "w").write("\n".join(lines) + "\n")
     import shutil

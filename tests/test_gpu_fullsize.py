@@ -69,8 +69,8 @@ def test_fullsize_config(cid, cuda_device):
     h = hht.HHT(halves=cfg.halves, profile=True)       # the bench's launch configuration
     h.detect_batch(torch.from_numpy(pts).to(cuda_device), offs, cfg.N, cfg.D, cfg.T)
     images = offs.shape[0] - 1
-    if os.path.exists(path):
-        _digest_check(h, cfg, images, json.load(open(path)))
+    assert os.path.exists(path), f"missing oracle digest {path} (scripts/write_golden.py --config {cid})"
+    _digest_check(h, cfg, images, json.load(open(path)))
     # structure of every tree (full output), sampled brute-force counts on image 0
     tests = 0
     for b in range(images if images <= 4 else 4):
@@ -83,3 +83,26 @@ def test_fullsize_config(cid, cuda_device):
     rng = np.random.default_rng(cid)
     p0 = pts[offs[0]:offs[1]]
     _sampled_brute(h, p0, cfg, 0, 3 if cid == 5 else 30, rng)
+
+
+@pytest.mark.parametrize("cid", [3, 5])
+def test_fullsize_e2e_leaf_sink(cid, cuda_device):
+    """bench.py's e2e configuration (profile on, pinned HOST points staged by the library, the
+    detected lines streamed to a pinned host sink during the call, default memory budget): the
+    streamed (image, half, i, j, votes) rows hash to the oracle digest's leaves, in order."""
+    import torch
+    cfg = synth.CONFIGS[cid]
+    gold = json.load(open(os.path.join(GOLD, f"c{cid}_digest.json")))
+    pts, _ = synth.config_image(cid)
+    offs = np.array([0, pts.shape[0]], dtype=np.int64)
+    host = torch.from_numpy(np.ascontiguousarray(pts)).pin_memory().numpy()
+    h = hht.HHT(halves=cfg.halves, profile=True)
+    sink = torch.empty((gold["leaves"] + 1024, 5), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+    h.set_leaf_sink(sink)
+    h.detect_batch(host, offs, cfg.N, cfg.D, cfg.T)
+    st = h.stats()
+    assert st["leaves_streamed"] == st["leaves"] == gold["leaves"]
+    rows = np.ascontiguousarray(sink[:gold["leaves"]].astype("<u4"))
+    assert hashlib.sha256(rows.tobytes()).hexdigest() == gold["leaves_sha256"]
+    assert st["tests"] == gold["tests"] and st["votes"] == gold["votes"]
+    h.close()
