@@ -56,6 +56,7 @@ typedef enum {
 
 #define HHT_EXACT 0u       /* opts.variant: the paper's exact corner-code test             */
 #define HHT_FHT_CIRCLE 1u  /* opts.variant: FHT circumcircle test (comparison) */
+#define HHT_FHT_CIRCLE_MB 2u  /* opts.variant: the same circle measured in (m, b) units (DESIGN R22) */
 
 typedef struct hht_ctx hht_ctx;   /* opaque */
 typedef struct hht_group hht_group;   /* opaque: in-process collective group (hht_group_create) */
@@ -87,7 +88,11 @@ typedef struct {
     uint32_t variant;        /* membership test: HHT_EXACT (0, default) = the paper's 4-bit corner
                                 code; HHT_FHT_CIRCLE (1) = the FHT comparison: the line meets the
                                 region's circumscribing circle (exact integers, see
-                                DESIGN.md). HHT_EOVERFLOW if 13 N^2 2^(2 depth - 1) >= 2^63 */
+                                DESIGN.md). HHT_EOVERFLOW if 13 N^2 2^(2 depth - 1) >= 2^63;
+                                HHT_FHT_CIRCLE_MB (2) = the same test with distance and radius in the
+                                (m, b) units of the 2s/2^D x 3Ns/2^D rectangles (reading R22):
+                                (2 G(centre))^2 <= (1 + ex^2)(4 + 9N^2) s^2, exact in 128 bits;
+                                HHT_EOVERFLOW if (1 + N^2)(4 + 9N^2) 4^(depth-1) >= 2^126 */
     size_t mem_budget;       /* device bytes for candidate lists; 0 = 80% of free memory at create.
                                 Levels whose lists do not fit are processed in depth-first ranges. */
     const void* nccl_id;     /* world > 1: 128-byte ncclUniqueId from hht_nccl_unique_id on rank 0,
@@ -98,7 +103,22 @@ typedef struct {
                                 multi-rank path makes (the same calls, in the same order, as with
                                 NCCL) is a host-staged allreduce among them. For testing the
                                 multi-rank logic on one GPU; the contexts may share a device. */
+    void* stream;            /* cudaStream_t the ctx enqueues all its work on, BORROWED (never
+                                destroyed by the library); NULL: the ctx creates its own stream.
+                                The legacy default stream is cudaStreamLegacy ((void*)1). Work the
+                                caller enqueued on that stream before a detect call is ordered
+                                before the detection (no host synchronisation needed). */
+    void* nccl_comm;         /* ncclComm_t of `world` ranks, BORROWED (never destroyed by the
+                                library); takes precedence over nccl_id; its size and rank must equal
+                                world and rank (HHT_EINVAL otherwise) */
 } hht_opts;
+
+/* Re-point the ctx at another BORROWED stream (cudaStream_t; NULL = back to the ctx's own stream,
+ * cudaStreamLegacy = (void*)1 for the legacy default stream) for the following calls. The previous
+ * stream is synchronised first. Lets a caller order a detection after its own producer kernels on
+ * its current stream without a host synchronisation (the Python binding passes torch's current
+ * stream). */
+hht_status hht_set_stream(hht_ctx* ctx, void* stream);
 
 /* One detected line: leaf (i, j) of tree (image, half) with votes > threshold. */
 typedef struct {

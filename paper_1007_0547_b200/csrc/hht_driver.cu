@@ -94,6 +94,8 @@ struct hht_ctx {
     hht_opts opts{};
     int sms = 148;
     cudaStream_t st = nullptr;
+    cudaStream_t own_st = nullptr;              // the ctx's own stream (st may be a borrowed one)
+    bool own_comm = true;                       // false: comm is the caller's (opts.nccl_comm)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, tb0 = nullptr, tb1 = nullptr, ee0 = nullptr, ee1 = nullptr;
     ncclComm_t comm = nullptr;
     hht_group* group = nullptr;        // borrowed (opts.group)
@@ -105,7 +107,8 @@ struct hht_ctx {
     int fused_grid[2] = {};
     int split_grid = 0;             // resident k_split blocks (persistent tile loop)
     bool pref_pass = true, pref_tail = true;   // opts.prefetch (0 = auto)
-    bool circle = false;                       // opts.variant == HHT_FHT_CIRCLE
+    bool circle = false;                       // opts.variant is a circumcircle test (1 or 2)
+    int circle_var = 0;                        // opts.variant: 1 lattice units, 2 (m, b) units
     int grid_circle[3][2] = {};
 
     // last call
@@ -477,7 +480,7 @@ hht_status run_pass(hht_ctx* x, int mode, const PassArgs& a, uint64_t pairs, uin
     const int cls = mode == MODE_COUNT ? 1 : ((mode == MODE_WRITE || mode == MODE_WRITE_NC) ? 2 : 3);
     const int id = prof_begin(x, cls, pairs * 4 + written * 4);
     const int grid = x->circle ? x->grid_circle[mode][x->int64 ? 1 : 0] : x->grid[mode][x->int64 ? 1 : 0];
-    CK(launch_pass(mode, x->int64, x->pref_pass || x->circle, x->circle, a, grid, x->st));
+    CK(launch_pass(mode, x->int64, x->pref_pass || x->circle, x->circle_var, a, grid, x->st));
     prof_end(x, id);
     x->stat.pairs += pairs;
     return HHT_OK;
@@ -782,10 +785,14 @@ hht_status check_args(hht_ctx* x, const int32_t* points, int64_t n_total, int32_
     const long double mag = 5.0L * (long double)N * (long double)(1ull << D);
     if (mag >= 4.6e18L) return set_err(x, HHT_EOVERFLOW, "5*N*2^depth >= 2^62: exact int64 arithmetic impossible");
     if (n_total > 0xFFFFFFFFll) return set_err(x, HHT_EINVAL, "more than 2^32-1 points per rank");
-    if (x->opts.variant > HHT_FHT_CIRCLE) return set_err(x, HHT_EINVAL, "unknown variant");
+    if (x->opts.variant > HHT_FHT_CIRCLE_MB) return set_err(x, HHT_EINVAL, "unknown variant");
     // circle test: the squared radius 2 s^2 (4 ex^2 + 9 N^2) of a child of the root must fit 63 bits
     if (x->opts.variant == HHT_FHT_CIRCLE && 13.0L * N * (long double)N * powl(2.0L, 2.0L * D - 1) >= 9.2e18L)
         return set_err(x, HHT_EOVERFLOW, "13 N^2 2^(2 depth - 1) >= 2^63: circle radius overflows 64 bits");
+    // (m, b)-unit circle: (1 + N^2)(4 + 9 N^2) s^2 for a child of the root (s = 2^(D-1)) in 126 bits
+    if (x->opts.variant == HHT_FHT_CIRCLE_MB &&
+        (1.0L + (long double)N * N) * (4.0L + 9.0L * N * (long double)N) * powl(2.0L, 2.0L * D - 2) >= powl(2.0L, 126))
+        return set_err(x, HHT_EOVERFLOW, "(1 + N^2)(4 + 9 N^2) 4^(depth-1) >= 2^126: (m, b) circle radius overflows");
     return HHT_OK;
 }
 
@@ -1250,8 +1257,8 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     hht_opts o;
     if (opts) o = *opts; else hht_default_opts(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return HHT_EINVAL;
-    if (o.world > 1 && !o.nccl_id && !o.group) return HHT_EINVAL;
-    if (o.group && (o.nccl_id || o.group->world != o.world)) return HHT_EINVAL;
+    if (o.world > 1 && !o.nccl_id && !o.nccl_comm && !o.group) return HHT_EINVAL;
+    if (o.group && (o.nccl_id || o.nccl_comm || o.group->world != o.world)) return HHT_EINVAL;
     if (o.halves == 0 || (o.halves & ~3u)) return HHT_EINVAL;
     if (!(o.tail_depth == 0 || (o.tail_depth >= 3 && o.tail_depth <= 6))) return HHT_EINVAL;
     hht_ctx* x = new (std::nothrow) hht_ctx();
@@ -1265,7 +1272,8 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     cudaDeviceProp prop{};
     if (cudaGetDeviceProperties(&prop, o.device) != cudaSuccess) return fail(HHT_ECUDA);
     x->sms = prop.multiProcessorCount;
-    if (cudaStreamCreateWithFlags(&x->st, cudaStreamNonBlocking) != cudaSuccess) return fail(HHT_ECUDA);
+    if (cudaStreamCreateWithFlags(&x->own_st, cudaStreamNonBlocking) != cudaSuccess) return fail(HHT_ECUDA);
+    x->st = o.stream ? (cudaStream_t)o.stream : x->own_st;
     if (cudaStreamCreateWithFlags(&x->cst, cudaStreamNonBlocking) != cudaSuccess) return fail(HHT_ECUDA);
     for (int k = 0; k < 2; ++k)
         if (cudaEventCreateWithFlags(&x->ev_conv[k], cudaEventDisableTiming) != cudaSuccess ||
@@ -1285,9 +1293,11 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     if (o.prefetch == 2) x->pref_pass = x->pref_tail = true;
     for (int m = 0; m < 4; ++m)
         for (int w = 0; w < 2; ++w) x->grid[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, x->pref_pass, false);
-    x->circle = o.variant == HHT_FHT_CIRCLE;
+    x->circle = o.variant == HHT_FHT_CIRCLE || o.variant == HHT_FHT_CIRCLE_MB;
+    x->circle_var = x->circle ? (int)o.variant : 0;
     for (int m = 0; m < 3; ++m)
-        for (int w = 0; w < 2; ++w) x->grid_circle[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, true, true);
+        for (int w = 0; w < 2; ++w)
+            x->grid_circle[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, true, x->circle_var ? x->circle_var : 1);
     for (int w = 0; w < 2; ++w) x->tail_grid[w] = x->sms * tail_blocks_per_sm(w == 1);
     for (int w = 0; w < 2; ++w) x->tail16_grid[w] = x->sms * tail16_blocks_per_sm(w == 1, x->pref_tail);
     for (int w = 0; w < 2; ++w) x->fused_grid[w] = x->sms * fused_blocks_per_sm(w == 1);
@@ -1308,7 +1318,15 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
         cudaHostGetDevicePointer((void**)&x->misc_m, x->misc_h, 0) != cudaSuccess)
         return fail(HHT_ECUDA);
     x->group = o.group;
-    if (o.nccl_id) {   // world > 1, or world == 1 with an id: every collective runs (1-rank comm)
+    if (o.nccl_comm) {   // the caller's communicator (borrowed)
+        int cnt = 0, rk = 0;
+        if (ncclCommCount((ncclComm_t)o.nccl_comm, &cnt) != ncclSuccess ||
+            ncclCommUserRank((ncclComm_t)o.nccl_comm, &rk) != ncclSuccess)
+            return fail(HHT_ENCCL);
+        if (cnt != o.world || rk != o.rank) return fail(HHT_EINVAL);
+        x->comm = (ncclComm_t)o.nccl_comm;
+        x->own_comm = false;
+    } else if (o.nccl_id) {   // world > 1, or world == 1 with an id: every collective runs (1-rank comm)
         ncclUniqueId id;
         memcpy(&id, o.nccl_id, sizeof id);
         if (ncclCommInitRank(&x->comm, o.world, id, o.rank) != ncclSuccess) return fail(HHT_ENCCL);
@@ -1673,9 +1691,18 @@ void hht_destroy(hht_ctx* x) {
     }
     for (cudaEvent_t e : {x->ev0, x->ev1, x->tb0, x->tb1, x->ee0, x->ee1})
         if (e) cudaEventDestroy(e);
-    if (x->comm) ncclCommDestroy(x->comm);
-    if (x->st) cudaStreamDestroy(x->st);
+    if (x->comm && x->own_comm) ncclCommDestroy(x->comm);
+    if (x->own_st) cudaStreamDestroy(x->own_st);
     delete x;
+}
+
+hht_status hht_set_stream(hht_ctx* x, void* stream) {
+    if (!x) return HHT_EINVAL;
+    const cudaStream_t next = stream ? (cudaStream_t)stream : x->own_st;
+    if (next == x->st) return HHT_OK;
+    CK(cudaStreamSynchronize(x->st));
+    x->st = next;
+    return HHT_OK;
 }
 
 }  // extern "C"

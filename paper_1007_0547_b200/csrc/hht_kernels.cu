@@ -315,7 +315,18 @@ __device__ __forceinline__ bool circle_in(I L2, uint64_t rhs) {
     }
 }
 
-template <typename I, int MODE, bool BETA>
+// Variant 2 (HHT_FHT_CIRCLE_MB, reading R22): the same circle measured in the (m, b) units of the
+// parameter space, where a region of lattice side s' is a 2s'/2^D x 3N s'/2^D rectangle. The line
+// b = ey - ex m lies at distance |F(centre)| / sqrt(1 + ex^2) from the centre and the circumradius
+// is sqrt(w^2 + h^2) / 2; squared and scaled by 4^(D+1): L2^2 <= (1 + ex^2)(4 + 9N^2) s'^2 with
+// the same L2 = 2 G(centre) = -2^(D+1) F(centre). Compared in 128-bit (the right side reaches
+// 2^126 at the largest admitted N, D; the driver rejects larger).
+__device__ __forceinline__ bool circle_in_mb(int64_t L2, unsigned __int128 rhs) {
+    const uint64_t a = (uint64_t)(L2 < 0 ? -L2 : L2);
+    return (unsigned __int128)a * a <= rhs;
+}
+
+template <typename I, int MODE, bool BETA, int VAR>
 __device__ __forceinline__ void chunk_math_circle(const uint32_t (&p)[kItems], int cnt, int lane, I alpha, I beta_m1,
                                                   int D, int sh, I N, I Qc, I Qg, uint32_t& cm, uint32_t (&acc)[4]) {
     const uint64_t nn9 = 9ull * (uint64_t)N * (uint64_t)N;
@@ -328,34 +339,41 @@ __device__ __forceinline__ void chunk_math_circle(const uint32_t (&p)[kItems], i
         // invalid lanes: L2 odd (2g = 1, ex = 0) against rhs = 0 never passes
         const I twog = valid ? 2 * (ex * alpha + (ey << D) + beta_m1 + 1) : (I)1;
         const uint64_t K = valid ? 4ull * (uint64_t)ex * (uint64_t)ex + nn9 : 0ull;   // 4ex^2 + 9N^2
+        // variant 2: (1 + ex^2)(4 + 9N^2) < 2^67 in 128 bits
+        const unsigned __int128 K2 = valid ? (unsigned __int128)(1ull + (uint64_t)ex * (uint64_t)ex) * (4ull + nn9)
+                                           : (unsigned __int128)0;
         const I Pc = ex << sh;
         if (MODE != MODE_COUNT2) {
-            const uint64_t rc = K << (2 * sh - 1);                  // 2 (s/2)^2 K
+            const uint64_t rc = VAR == 1 ? K << (2 * sh - 1) : 0ull;            // 2 (s/2)^2 K
+            const unsigned __int128 rc2 = VAR == 2 ? K2 << (2 * sh - 2) : 0;     // (s/2)^2 K2
             uint32_t b = 0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const I L2 = twog - Pc * (I)(2 * quad_da(q) + 1) - Qc * (I)(2 * quad_dc(q) + 1);
-                b |= (circle_in<I>(L2, rc) ? 1u : 0u) << (MODE == MODE_COUNT ? 8 * q : q);
+                const bool in = VAR == 1 ? circle_in<I>(L2, rc) : circle_in_mb((int64_t)L2, rc2);
+                b |= (in ? 1u : 0u) << (MODE == MODE_COUNT ? 8 * q : q);
             }
             if (MODE == MODE_COUNT) acc[0] += b;
             else cm |= b << (4 * it);
         }
         if (MODE != MODE_COUNT) {
-            const uint64_t rg = K << (2 * sh - 3);                  // 2 (s/4)^2 K
+            const uint64_t rg = VAR == 1 ? K << (2 * sh - 3) : 0ull;            // 2 (s/4)^2 K
+            const unsigned __int128 rg2 = VAR == 2 ? K2 << (2 * sh - 4) : 0;     // (s/4)^2 K2
             const I Pg = Pc >> 1;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
                     const I L2 = twog - Pg * (I)(2 * u + 1) - Qg * (I)(2 * v + 1);
-                    if (circle_in<I>(L2, rg)) acc[quad_of(u >> 1, v >> 1)] += 1u << (8 * quad_of(u & 1, v & 1));
+                    const bool in = VAR == 1 ? circle_in<I>(L2, rg) : circle_in_mb((int64_t)L2, rg2);
+                    if (in) acc[quad_of(u >> 1, v >> 1)] += 1u << (8 * quad_of(u & 1, v & 1));
                 }
             }
         }
     }
 }
 
-template <typename I, int MODE, bool PREF, bool CIRCLE>
+template <typename I, int MODE, bool PREF, int CIRCLE>
 __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
     constexpr bool kWrites = MODE == MODE_WRITE || MODE == MODE_WRITE_NC;
     __shared__ uint32_t s_stage[kWrites ? 8 * 4 * kChunk : 1];   // 4 KB per warp
@@ -394,8 +412,8 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
         uint32_t cm = 0;
         uint32_t acc[4] = {0, 0, 0, 0};
         if (CIRCLE) {
-            if (d.beta) chunk_math_circle<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, N, Qc, Qg, cm, acc);
-            else chunk_math_circle<I, MODE, false>(p, cnt, lane, alpha, beta_m1, D, sh, N, Qc, Qg, cm, acc);
+            if (d.beta) chunk_math_circle<I, MODE, true, CIRCLE>(p, cnt, lane, alpha, beta_m1, D, sh, N, Qc, Qg, cm, acc);
+            else chunk_math_circle<I, MODE, false, CIRCLE>(p, cnt, lane, alpha, beta_m1, D, sh, N, Qc, Qg, cm, acc);
         } else {
             if (d.beta) chunk_math<I, MODE, true>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc, CR);
             else chunk_math<I, MODE, false>(p, cnt, lane, alpha, beta_m1, D, sh, Qc, Qg, A.one, cm, acc, CR);
@@ -1817,28 +1835,30 @@ cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_
     return cudaGetLastError();
 }
 
-template <typename I, bool P, bool C>
+template <typename I, bool P, int C>
 static PassKernel pass_kernel_t(int mode) {
     if (mode == MODE_COUNT) return k_pass<I, MODE_COUNT, P, C>;
     if (mode == MODE_WRITE) return k_pass<I, MODE_WRITE, P, C>;
-    if (mode == MODE_WRITE_NC && !C) return k_pass<I, MODE_WRITE_NC, P, false>;
+    if (mode == MODE_WRITE_NC && !C) return k_pass<I, MODE_WRITE_NC, P, 0>;
     return k_pass<I, MODE_COUNT2, P, C>;
 }
 
-// The circumcircle variant is instantiated with the prefetching loop only.
-static PassKernel pass_kernel(int mode, bool int64, bool pref, bool circle = false) {
-    if (circle) return int64 ? pass_kernel_t<int64_t, true, true>(mode) : pass_kernel_t<int32_t, true, true>(mode);
-    if (int64) return pref ? pass_kernel_t<int64_t, true, false>(mode) : pass_kernel_t<int64_t, false, false>(mode);
-    return pref ? pass_kernel_t<int32_t, true, false>(mode) : pass_kernel_t<int32_t, false, false>(mode);
+// The circumcircle variants (1: lattice units, 2: (m, b) units) are instantiated with the
+// prefetching loop only.
+static PassKernel pass_kernel(int mode, bool int64, bool pref, int circle = 0) {
+    if (circle == 1) return int64 ? pass_kernel_t<int64_t, true, 1>(mode) : pass_kernel_t<int32_t, true, 1>(mode);
+    if (circle == 2) return int64 ? pass_kernel_t<int64_t, true, 2>(mode) : pass_kernel_t<int32_t, true, 2>(mode);
+    if (int64) return pref ? pass_kernel_t<int64_t, true, 0>(mode) : pass_kernel_t<int64_t, false, 0>(mode);
+    return pref ? pass_kernel_t<int32_t, true, 0>(mode) : pass_kernel_t<int32_t, false, 0>(mode);
 }
 
-int pass_blocks_per_sm(int mode, bool int64, bool pref, bool circle) {
+int pass_blocks_per_sm(int mode, bool int64, bool pref, int circle) {
     int n = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, pass_kernel(mode, int64, pref, circle), 256, 0);
     return n > 0 ? n : 1;
 }
 
-cudaError_t launch_pass(int mode, bool int64, bool pref, bool circle, const PassArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_pass(int mode, bool int64, bool pref, int circle, const PassArgs& a, int grid, cudaStream_t st) {
     pass_kernel(mode, int64, pref, circle)<<<grid, 256, 0, st>>>(a);
     return cudaGetLastError();
 }

@@ -17,6 +17,7 @@ ALPHA = 1
 BETA = 2
 EXACT = 0          # opts.variant: the paper's exact 4-bit corner-code test
 FHT_CIRCLE = 1     # opts.variant: FHT circumcircle test (the paper's comparison)
+FHT_CIRCLE_MB = 2  # opts.variant: the same circle in (m, b) units (reading R22)
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libhht.so")
@@ -29,7 +30,7 @@ EXPORTS = ["hht_default_opts", "hht_create", "hht_nccl_unique_id", "hht_detect",
            "hht_result_leaves", "hht_result_level", "hht_result_stats", "hht_result_profile",
            "hht_result_launches", "hht_timer_begin", "hht_timer_end", "hht_last_error", "hht_status_str",
            "hht_destroy", "hht_version", "hht_set_leaf_sink", "hht_group_create", "hht_group_destroy",
-           "hht_detect_trees", "hht_detect_image", "hht_result_edges", "hht_result_lines"]
+           "hht_detect_trees", "hht_detect_image", "hht_result_edges", "hht_result_lines", "hht_set_stream"]
 
 PROFILE_CLASSES = ["stage", "count", "write", "tail", "split", "gather", "other", "allreduce"]
 
@@ -47,7 +48,7 @@ class Opts(C.Structure):
                 ("tail_depth", C.c_uint32), ("prefetch", C.c_uint32), ("latency_path", C.c_uint32),
                 ("variant", C.c_uint32),
                 ("mem_budget", C.c_size_t),
-                ("nccl_id", C.c_void_p), ("group", C.c_void_p)]
+                ("nccl_id", C.c_void_p), ("group", C.c_void_p), ("stream", C.c_void_p), ("nccl_comm", C.c_void_p)]
 
 
 class Leaf(C.Structure):
@@ -107,6 +108,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hht_last_error": ([p], C.c_char_p),
         "hht_status_str": ([C.c_int], C.c_char_p),
         "hht_destroy": ([p], None),
+        "hht_set_stream": ([p, p], C.c_int),
         "hht_version": ([], C.c_char_p),
     }
     for name, (args, res) in sig.items():
@@ -149,8 +151,6 @@ def _as_points(points):
         if t.dtype != torch.int32:
             t = t.to(torch.int32)
         t = t.reshape(-1, 2).contiguous()
-        if t.is_cuda:
-            torch.cuda.current_stream(t.device).synchronize()   # producer work done before the library reads
         return t.data_ptr(), t.shape[0], t, t.is_cuda
     a = np.ascontiguousarray(np.asarray(points, dtype=np.int32).reshape(-1, 2))
     return a.ctypes.data, a.shape[0], a, False
@@ -180,7 +180,8 @@ class HHT:
     def __init__(self, device: int = 0, halves: int = ALPHA | BETA, record_levels: bool = True,
                  force_int64: bool = False, profile: bool = False, mem_budget: int = 0,
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, tail_depth: int = 0,
-                 prefetch: int = 0, variant: int = 0, group: Optional["Group"] = None, latency_path: int = 0):
+                 prefetch: int = 0, variant: int = 0, group: Optional["Group"] = None, latency_path: int = 0,
+                 stream: Optional[int] = None):
         self._lib = load()
         o = Opts()
         self._lib.hht_default_opts(C.byref(o))
@@ -191,6 +192,8 @@ class HHT:
         o.prefetch = prefetch
         o.latency_path = latency_path
         o.variant = variant
+        if stream is not None:            # borrowed cudaStream_t handle (int), e.g. torch.cuda.Stream.cuda_stream
+            o.stream = stream if stream else 1
         self._id = None
         if group is not None:
             o.group = group._g
@@ -208,6 +211,15 @@ class HHT:
     def _check(self, st: int):
         if st:
             raise HHTError(st, self._lib.hht_last_error(self._ctx).decode())
+
+    def _order_after(self, t):
+        """Device input: enqueue the library's work on torch's current stream of the tensor's device
+        (hht_set_stream, borrowed), so the kernels or copies that produced `t` are ordered before the
+        detection without a host synchronisation. Host input needs nothing (the library stages it)."""
+        import torch
+        if isinstance(t, torch.Tensor) and t.is_cuda:
+            s = torch.cuda.current_stream(t.device).cuda_stream
+            self._check(self._lib.hht_set_stream(self._ctx, C.c_void_p(s if s else 1)))   # 1: cudaStreamLegacy
 
     def close(self):
         if getattr(self, "_ctx", None):
@@ -229,12 +241,14 @@ class HHT:
     # --- compute -----------------------------------------------------------------------------
     def detect(self, points, N: int, depth: int, threshold: int) -> "HHT":
         ptr, n, keep, _ = _as_points(points)
+        self._order_after(keep)
         self._check(self._lib.hht_detect(self._ctx, C.c_void_p(ptr), n, N, depth, threshold))
         del keep
         return self
 
     def detect_batch(self, points, offsets: Sequence[int], N: int, depth: int, threshold: int) -> "HHT":
         ptr, n, keep, _ = _as_points(points)
+        self._order_after(keep)
         offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
         B = offs.shape[0] - 1
         self._check(self._lib.hht_detect_batch(self._ctx, C.c_void_p(ptr), offs.ctypes.data, B, N, depth,
@@ -256,6 +270,7 @@ class HHT:
         """Per-tree point sets: tree t (image t // H, half t % H in ALPHA, BETA order) gets
         points[tree_offsets[t]:tree_offsets[t+1]]."""
         ptr, n, keep, _ = _as_points(points)
+        self._order_after(keep)
         to = np.ascontiguousarray(np.asarray(tree_offsets, dtype=np.int64))
         H = bin(self.halves).count("1")
         assert to.ndim == 1 and (to.shape[0] - 1) % H == 0 and to[-1] == n
@@ -271,6 +286,7 @@ class HHT:
             assert img.dtype.itemsize == 1 and img.is_contiguous() and img.dim() == 2
             N, ptr, keep = int(img.shape[0]), img.data_ptr(), img
             assert img.shape[1] == N
+            self._order_after(img)          # the producer of a device image is ordered first
         else:
             keep = np.ascontiguousarray(img, dtype=np.uint8)
             assert keep.ndim == 2 and keep.shape[0] == keep.shape[1]

@@ -1,8 +1,9 @@
 """GPU parity of the FHT circumcircle variant: the same
 level-synchronous pipeline with the membership test "the line meets the region's circumscribing
-circle", compared bit-exactly with the oracle's variant 1 (oracle/hht_oracle.c
-oracle_circle_passes, pinned in tests/test_oracle_pins.py), plus the paper's claim that the circle
-test casts extra (false) votes: at every region both runs visit, circle votes >= exact votes."""
+circle", compared bit-exactly with the oracle's variants 1 (circle in lattice units,
+oracle_circle_passes) and 2 (circle in (m, b) units, oracle_circle_mb_passes; reading R22), both
+pinned in tests/test_oracle_pins.py, plus the paper's claim that the circle test casts extra
+(false) votes: at every region both runs visit, circle votes >= exact votes."""
 import numpy as np
 import pytest
 
@@ -20,18 +21,25 @@ def _dev(pts, dev):
     return torch.from_numpy(np.ascontiguousarray(pts, dtype=np.int32)).to(dev)
 
 
-def _run(pts, N, D, T, halves, dev, **kw):
-    h = hht.HHT(halves=halves, variant=hht.FHT_CIRCLE, **kw)
+VARS = [hht.FHT_CIRCLE, hht.FHT_CIRCLE_MB]
+
+
+def _run(pts, N, D, T, halves, dev, var=hht.FHT_CIRCLE, **kw):
+    h = hht.HHT(halves=halves, variant=var, **kw)
     h.detect(_dev(pts, dev), N, D, T)
     return h
 
 
-@pytest.mark.parametrize("cid", [1, 2])
-def test_config_parity_circle(cid, cuda_device):
+# variant 2 on config 2 costs the oracle ~3 min (9.3e9 tests: the (m, b) circle accepts far more)
+CFG_VARS = [(1, hht.FHT_CIRCLE), (2, hht.FHT_CIRCLE), (1, hht.FHT_CIRCLE_MB)]
+
+
+@pytest.mark.parametrize("cid,var", CFG_VARS)
+def test_config_parity_circle(cid, var, cuda_device):
     cfg = synth.CONFIGS[cid]
     pts, _ = synth.config_image(cid)
-    ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves, variant=1)
-    h = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, cuda_device)
+    ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves, variant=var)
+    h = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, cuda_device, var)
     compare_all(h, ref, cfg.halves, cfg.D)
     st = h.stats()
     assert (st["tests"], st["votes"], st["leaves"]) == (ref.tests, ref.votes, ref.leaves.shape[0])
@@ -53,17 +61,43 @@ def test_random_scenes_circle(seed, force64, cuda_device):
     assert st["int_bits"] == (64 if force64 else 32)
 
 
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("force64", [False, True])
+def test_random_scenes_circle_mb(seed, force64, cuda_device):
+    rng = np.random.default_rng(9100 + seed)
+    N = int(rng.choice([4, 7, 16, 33, 64, 128]))
+    D = int(rng.integers(1, 8))
+    T = int(rng.choice([2, 8, 20, 60]))
+    pts = synth.random_scene(9200 + seed, N, max_lines=4, max_noise=int(rng.choice([10, 100, 600])))
+    ref = oracle.detect(pts, N, D, T, AB, variant=2)
+    h = _run(pts, N, D, T, AB, cuda_device, hht.FHT_CIRCLE_MB, force_int64=force64)
+    compare_all(h, ref, AB, D)
+    st = h.stats()
+    assert (st["tests"], st["votes"]) == (ref.tests, ref.votes)
+    assert st["int_bits"] == (64 if force64 else 32)
+
+
 def test_circle_ranges_under_tiny_budget(cuda_device):
     cfg = synth.CONFIGS[2]
     pts, _ = synth.config_image(2)
     ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves, variant=1)
-    h = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, cuda_device, mem_budget=256 << 10)
+    h = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, cuda_device, hht.FHT_CIRCLE, mem_budget=256 << 10)
     compare_all(h, ref, cfg.halves, cfg.D)
     assert h.stats()["ranges"] > 4 * cfg.D
 
 
+def test_circle_mb_ranges_under_tiny_budget(cuda_device):
+    N, D, T = 128, 7, 40
+    pts = synth.random_scene(4242, N, max_lines=6, max_noise=800)
+    ref = oracle.detect(pts, N, D, T, AB, variant=2)
+    h = _run(pts, N, D, T, AB, cuda_device, hht.FHT_CIRCLE_MB, mem_budget=64 << 10)
+    compare_all(h, ref, AB, D)
+    assert h.stats()["ranges"] > 2 * D
+
+
+@pytest.mark.parametrize("var", VARS)
 @pytest.mark.parametrize("case", ["empty", "identical", "d1", "d2", "d3", "n1"])
-def test_circle_edge_cases(case, cuda_device):
+def test_circle_edge_cases(case, var, cuda_device):
     N, D, T = 16, 4, 2
     if case == "empty":
         pts = np.zeros((0, 2), np.int32)
@@ -74,20 +108,20 @@ def test_circle_edge_cases(case, cuda_device):
     else:
         D = int(case[1])
         pts = synth.random_scene(30 + D, 16, max_noise=60)
-    ref = oracle.detect(pts, N, D, T, AB, variant=1)
-    h = _run(pts, N, D, T, AB, cuda_device)
+    ref = oracle.detect(pts, N, D, T, AB, variant=var)
+    h = _run(pts, N, D, T, AB, cuda_device, var)
     compare_all(h, ref, AB, D)
 
 
-@pytest.mark.parametrize("cid", [1, 2])
-def test_circle_casts_extra_votes(cid, cuda_device):
+@pytest.mark.parametrize("cid,var", CFG_VARS)
+def test_circle_casts_extra_votes(cid, var, cuda_device):
     """North star: the circumcircle test (FHT) votes wherever the exact test does and more: at every
     region visited by both runs, votes_circle >= votes_exact; strictly more votes in total."""
     cfg = synth.CONFIGS[cid]
     pts, _ = synth.config_image(cid)
     he = hht.HHT(halves=cfg.halves)
     he.detect(_dev(pts, cuda_device), cfg.N, cfg.D, cfg.T)
-    hc = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, cuda_device)
+    hc = _run(pts, cfg.N, cfg.D, cfg.T, cfg.halves, cuda_device, var)
     for half in (1, 2):
         if not cfg.halves & half:
             continue
@@ -99,8 +133,9 @@ def test_circle_casts_extra_votes(cid, cuda_device):
     assert hc.stats()["votes"] > he.stats()["votes"]
 
 
-def test_circle_overflow_rejected(cuda_device):
-    h = hht.HHT(halves=AB, variant=hht.FHT_CIRCLE)
+@pytest.mark.parametrize("var", VARS)
+def test_circle_overflow_rejected(var, cuda_device):
+    h = hht.HHT(halves=AB, variant=var)
     with pytest.raises(hht.HHTError) as e:
         h.detect(_dev(np.array([[0, 0]], np.int32), cuda_device), 65536, 30, 2)
     assert e.value.name == "HHT_EOVERFLOW"

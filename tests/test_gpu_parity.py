@@ -57,10 +57,6 @@ def test_config_full_parity(cid, torch_dev):
     compare_all(h, ref, cfg.halves, cfg.D)
     st = h.stats()
     assert (st["tests"], st["votes"], st["leaves"]) == (ref.tests, ref.votes, ref.leaves.shape[0])
-    for half in (1, 2):
-        if cfg.halves & half:
-            for lev in range(cfg.D + 1):
-                pass
     assert st["int_bits"] == 32
 
 
