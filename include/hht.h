@@ -204,11 +204,20 @@ hht_status hht_detect_batch(hht_ctx* ctx, const int32_t* points, const int64_t* 
  * the same tree; its live voters are then removed (the paper's "exclude the edge point from further
  * calculations"). Rows (image, half, i, j, live votes), image -1 = all, same cap/count protocol as
  * hht_result_leaves. This equals the paper's depth-first detector with removal on (the oracle's
- * oracle_detect_removal). Computed on the GPU on first request and cached until the next detect:
- * support bitsets of candidates x points / 8 bytes (HHT_ENOMEM beyond the memory budget), then one
- * block per tree walks its candidates sequentially — meant for images with sparse detections (the
- * paper's regime), not for saturated configs with 1e7+ candidates. Single rank, exact test only. */
+ * oracle_detect_removal). Computed on the GPU on first request and cached until the next detect, by
+ * one cooperative kernel per group of trees: live vote counts per candidate, kept exact by rastering
+ * each removed point's line over a dense 4^depth cell -> candidate map, so the next emission of every
+ * tree is found in one scan (rounds <= points / threshold per tree). Device memory: 12 B per candidate
+ * + 17 B per (tree, point) + 4^(depth+1) B per tree of a group (HHT_ENOMEM if one tree's map does not
+ * fit the budget). Single rank, exact test only. */
 hht_status hht_result_lines(hht_ctx* ctx, int32_t image, hht_leaf* out, int64_t cap, int64_t* count);
+
+/* The supports of those lines: uint32 rows (line, point) sorted by line then point, where line indexes
+ * the rows hht_result_lines returns for the same `image` (-1: all images, global line index) and point
+ * indexes the point set of the line's tree (the image's points for hht_detect / hht_detect_batch; the
+ * tree's own set for hht_detect_trees). Every point appears at most once per tree (it is removed by the
+ * line it supports). out holds cap rows (2 * cap uint32); out = NULL: count only. */
+hht_status hht_result_line_points(hht_ctx* ctx, int32_t image, uint32_t* out, int64_t cap, int64_t* count);
 
 /* Per-tree point sets (each point in ONE tree, e.g. the edge front end's ALPHA/BETA partition,
  * PAPER.md:67): tree t = image t / H + half index t % H (H = number of halves in opts.halves,

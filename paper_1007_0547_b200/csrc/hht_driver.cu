@@ -130,6 +130,9 @@ struct hht_ctx {
     bool lines_ok = false;               // removal post-pass cached for the last detect
     std::vector<hht_leaf> lines_host;
     std::vector<int64_t> lines_img;      // [B+1] row offsets per image
+    std::vector<std::pair<uint64_t, uint32_t>> lines_sup;   // (line index, point index in its tree)
+    bool lines_sup_sorted = false;
+    int rm_grid[2] = {0, 0};             // co-resident k_rm blocks (cooperative launch)
     int64_t edge_na = 0, edge_nb = 0;
     // leaf sink (hht_set_leaf_sink): double-buffered row staging, copied on its own stream
     hht_leaf* sink = nullptr;
@@ -1440,6 +1443,8 @@ hht_status hht_result_edges(hht_ctx* x, int32_t* out, int64_t cap, int64_t* n_al
 }
 
 // solution() with removal (NEXT-1) over the last detect's candidate leaves; cached until the next detect.
+// One cooperative kernel per group of trees (k_rm, see hht_kernels.cu): live vote counts per candidate,
+// a dense leaf-cell -> candidate map per tree of the group, removed flags per (tree, point).
 hht_status compute_lines(hht_ctx* x) {
     if (x->lines_ok) return HHT_OK;
     if (multi(x)) return set_err(x, HHT_EINVAL, "removal needs every point of a tree: single rank only");
@@ -1447,7 +1452,7 @@ hht_status compute_lines(hht_ctx* x) {
     TRY(host_leaves(x));
     const std::vector<LeafRec>& L = x->leaves_host;
     const uint32_t nt = (uint32_t)x->ntrees;
-    std::vector<uint64_t> cand_lo(nt + 1, 0), bits_off(nt + 1, 0);
+    std::vector<uint64_t> cand_lo(nt + 1, 0), rm_off(nt + 1, 0);
     {
         uint64_t k = 0;
         for (uint32_t t = 0; t < nt; ++t) {
@@ -1455,70 +1460,108 @@ hht_status compute_lines(hht_ctx* x) {
             while (k < L.size() && L[k].tree == t) ++k;
         }
         cand_lo[nt] = k;
+        for (uint32_t t = 0; t < nt; ++t) rm_off[t + 1] = rm_off[t] + x->tree_pt_n[t];
     }
-    uint32_t maxW = 1;
-    for (uint32_t t = 0; t < nt; ++t) {
-        const uint64_t W = (x->tree_pt_n[t] + 31) / 32;
-        maxW = std::max<uint32_t>(maxW, (uint32_t)W);
-        bits_off[t + 1] = bits_off[t] + (cand_lo[t + 1] - cand_lo[t]) * W;
-    }
-    const uint64_t words = bits_off[nt];
-    if (words * 4 > x->budget)
-        return set_err(x, HHT_ENOMEM, "removal post-pass needs %llu B of support bitsets (candidates x points / 8)",
-                       (unsigned long long)(words * 4));
-    if ((size_t)maxW * 4 > 200 * 1024)
-        return set_err(x, HHT_ENOMEM, "removal post-pass: a tree of more than 1.6M points");
-    Buf bits, meta, outb;
-    auto cleanup = [&]() { for (Buf* b : {&bits, &meta, &outb}) if (b->p) cudaFreeAsync(b->p, x->st); };
-    const uint64_t nl = L.size();
-    hht_status st = ensure(x, bits, std::max<uint64_t>(words, 1) * 4);
-    if (st == HHT_OK) st = ensure(x, meta, (size_t)(nt + 1) * 8 * 3 + (size_t)nt * 4 + 64);
-    if (st == HHT_OK) st = ensure(x, outb, (size_t)std::max<uint64_t>(nl, 1) * 8 + (size_t)nt * 4);
+    const uint64_t ncand = L.size(), npts = rm_off[nt];
+    const uint64_t per_tree = 4ull << (2 * x->D);                 // dense cell map of one tree
+    const uint64_t fixed = ncand * 12 + npts * 17 + (uint64_t)nt * 48 + 4096;
+    if (fixed + per_tree > x->budget)
+        return set_err(x, HHT_ENOMEM, "removal post-pass needs %llu B (candidates, points and one 4^depth cell map)",
+                       (unsigned long long)(fixed + per_tree));
+    const uint32_t gmax = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(nt ? nt : 1, (x->budget - fixed) / per_tree));
+    Buf big, meta;
+    auto cleanup = [&]() { for (Buf* b : {&big, &meta}) if (b->p) cudaFreeAsync(b->p, x->st); };
+    // big: live | out | out_live (ncand each) | queue | sup (2 npts each) | removed (npts) | cellmap
+    const uint64_t nc1 = std::max<uint64_t>(ncand, 1), np1 = std::max<uint64_t>(npts, 1);
+    const uint64_t big_bytes = nc1 * 12 + np1 * 16 + ((np1 + 15) / 16) * 16 + (uint64_t)gmax * per_tree;
+    hht_status st = ensure(x, big, big_bytes);
+    if (st == HHT_OK) st = ensure(x, meta, (size_t)(nt + 1) * 8 * 3 + (size_t)nt * 16 + 64);
     if (st != HHT_OK) { cleanup(); return st; }
+    uint32_t* d_live = (uint32_t*)big.p;
+    uint32_t* d_out = d_live + nc1;
+    uint32_t* d_out_live = d_out + nc1;
+    uint32_t* d_queue = d_out_live + nc1;
+    uint32_t* d_sup = d_queue + 2 * np1;
+    uint8_t* d_removed = (uint8_t*)(d_sup + 2 * np1);
+    uint32_t* d_cellmap = (uint32_t*)(d_removed + ((np1 + 15) / 16) * 16);
     uint64_t* d_cand = (uint64_t*)meta.p;
-    uint64_t* d_off = d_cand + (nt + 1);
-    uint64_t* d_bits = d_off + (nt + 1);
-    uint32_t* d_n = (uint32_t*)(d_bits + (nt + 1));
+    uint64_t* d_ptoff = d_cand + (nt + 1);
+    uint64_t* d_rmoff = d_ptoff + (nt + 1);
+    uint32_t* d_ptn = (uint32_t*)(d_rmoff + (nt + 1));
+    uint32_t* d_cur = d_ptn + nt;
+    uint32_t* d_pos = d_cur + nt;
+    uint32_t* d_outn = d_pos + nt;
+    uint32_t* d_small = d_outn + nt;                      // active[2], qn, pad
+    unsigned long long* d_supn = (unsigned long long*)(d_small + 4);
     CK(cudaMemcpyAsync(d_cand, cand_lo.data(), (nt + 1) * 8, cudaMemcpyHostToDevice, x->st));
-    CK(cudaMemcpyAsync(d_off, x->tree_pt_off.data(), nt * 8, cudaMemcpyHostToDevice, x->st));
-    CK(cudaMemcpyAsync(d_bits, bits_off.data(), (nt + 1) * 8, cudaMemcpyHostToDevice, x->st));
-    CK(cudaMemcpyAsync(d_n, x->tree_pt_n.data(), nt * 4, cudaMemcpyHostToDevice, x->st));
-    RemovalArgs a{};
+    if (nt) {
+        CK(cudaMemcpyAsync(d_ptoff, x->tree_pt_off.data(), nt * 8, cudaMemcpyHostToDevice, x->st));
+        CK(cudaMemcpyAsync(d_rmoff, rm_off.data(), nt * 8, cudaMemcpyHostToDevice, x->st));
+        CK(cudaMemcpyAsync(d_ptn, x->tree_pt_n.data(), nt * 4, cudaMemcpyHostToDevice, x->st));
+    }
+    CK(cudaMemsetAsync(d_cur, 0, (size_t)nt * 12 + 16 + 8, x->st));       // cur, pos, out_n, small, sup_n
+    CK(cudaMemsetAsync(d_removed, 0, np1, x->st));
+    RmArgs a{};
     a.leaves = (const LeafRec*)x->leaves.b.p;
-    a.packed = (const uint32_t*)x->packed.p;
     a.cand_lo = d_cand;
-    a.pt_off = d_off;
-    a.pt_n = d_n;
-    a.bits_off = d_bits;
+    a.packed = (const uint32_t*)x->packed.p;
+    a.pt_off = d_ptoff;
+    a.pt_n = d_ptn;
+    a.rm_off = d_rmoff;
     a.tree_beta = (const uint8_t*)x->beta.p;
-    a.bits = (uint32_t*)bits.p;
-    a.out = (uint32_t*)outb.p;
-    a.out_live = (uint32_t*)outb.p + std::max<uint64_t>(nl, 1);
-    a.out_n = a.out_live + std::max<uint64_t>(nl, 1);
+    a.live = d_live;
+    a.cellmap = d_cellmap;
+    a.removed = d_removed;
+    a.queue = d_queue;
+    a.qn = d_small + 2;
+    a.cur = d_cur;
+    a.pos = d_pos;
+    a.active = d_small;
+    a.out = d_out;
+    a.out_live = d_out_live;
+    a.out_n = d_outn;
+    a.sup = d_sup;
+    a.sup_n = d_supn;
     a.N = x->N;
     a.D = x->D;
     a.T = x->T;
-    a.ntrees = nt;
-    a.total_words = words;
-    CK(launch_removal(a, x->int64, maxW, x->st));
-    std::vector<uint32_t> h_out(nl), h_live(nl), h_n(nt);
-    if (nl) {
-        CK(cudaMemcpyAsync(h_out.data(), a.out, nl * 4, cudaMemcpyDeviceToHost, x->st));
-        CK(cudaMemcpyAsync(h_live.data(), a.out_live, nl * 4, cudaMemcpyDeviceToHost, x->st));
+    if (!x->rm_grid[x->int64 ? 1 : 0]) x->rm_grid[x->int64 ? 1 : 0] = x->sms * rm_blocks_per_sm(x->int64);
+    for (uint32_t t0 = 0; t0 < nt; t0 += gmax) {
+        a.t0 = t0;
+        a.t1 = std::min(nt, t0 + gmax);
+        if (cand_lo[a.t1] == cand_lo[t0]) continue;       // no candidates: nothing to emit
+        CK(cudaMemsetAsync(d_cellmap, 0xFF, (size_t)(a.t1 - t0) * per_tree, x->st));
+        CK(launch_removal(a, (const LeafRec*)x->leaves.b.p, x->int64, x->rm_grid[x->int64 ? 1 : 0], x->st));
     }
-    CK(cudaMemcpyAsync(h_n.data(), a.out_n, nt * 4, cudaMemcpyDeviceToHost, x->st));
+    std::vector<uint32_t> h_out(ncand), h_live(ncand), h_n(nt);
+    unsigned long long h_supn = 0;
+    if (ncand) {
+        CK(cudaMemcpyAsync(h_out.data(), d_out, ncand * 4, cudaMemcpyDeviceToHost, x->st));
+        CK(cudaMemcpyAsync(h_live.data(), d_out_live, ncand * 4, cudaMemcpyDeviceToHost, x->st));
+    }
+    if (nt) CK(cudaMemcpyAsync(h_n.data(), d_outn, nt * 4, cudaMemcpyDeviceToHost, x->st));
+    CK(cudaMemcpyAsync(&h_supn, d_supn, 8, cudaMemcpyDeviceToHost, x->st));
+    TRY(sync(x));
+    std::vector<uint32_t> h_sup(2 * h_supn);
+    if (h_supn) CK(cudaMemcpyAsync(h_sup.data(), d_sup, 8ull * h_supn, cudaMemcpyDeviceToHost, x->st));
     TRY(sync(x));
     cleanup();
     x->lines_host.clear();
     x->lines_img.assign(x->B + 1, 0);
+    std::vector<int64_t> slot_line(ncand, -1);            // global slot cand_lo[t] + e -> line index
     for (uint32_t t = 0; t < nt; ++t) {
         for (uint32_t e = 0; e < h_n[t]; ++e) {
             const LeafRec& r = L[cand_lo[t] + h_out[cand_lo[t] + e]];
+            slot_line[cand_lo[t] + e] = (int64_t)x->lines_host.size();
             x->lines_host.push_back({(int32_t)(t / x->H), (uint32_t)x->tree_half[t], r.i, r.j, h_live[cand_lo[t] + e]});
         }
         x->lines_img[t / x->H + 1] = (int64_t)x->lines_host.size();
     }
     for (int b = 1; b <= x->B; ++b) x->lines_img[b] = std::max(x->lines_img[b], x->lines_img[b - 1]);
+    // supports as (line, point); sorted by line then point on first request (hht_result_line_points)
+    x->lines_sup.resize(h_supn);
+    for (uint64_t s = 0; s < h_supn; ++s) x->lines_sup[s] = {(uint64_t)slot_line[h_sup[2 * s]], h_sup[2 * s + 1]};
+    x->lines_sup_sorted = false;
     x->lines_ok = true;
     return HHT_OK;
 }
@@ -1534,6 +1577,31 @@ hht_status hht_result_lines(hht_ctx* x, int32_t image, hht_leaf* out, int64_t ca
     if (!out) return HHT_OK;
     if (cap < e - b) return set_err(x, HHT_EINVAL, "cap < %lld lines", (long long)(e - b));
     if (e > b) memcpy(out, x->lines_host.data() + b, (size_t)(e - b) * sizeof(hht_leaf));
+    return HHT_OK;
+}
+
+hht_status hht_result_line_points(hht_ctx* x, int32_t image, uint32_t* out, int64_t cap, int64_t* count) {
+    if (!x || !count) return HHT_EINVAL;
+    if (!x->have) return set_err(x, HHT_ESTATE, "no successful detect yet");
+    if (image < -1 || image >= x->B) return set_err(x, HHT_EINVAL, "image out of range");
+    TRY(compute_lines(x));
+    const uint64_t lb = image < 0 ? 0 : (uint64_t)x->lines_img[image];
+    const uint64_t le = image < 0 ? x->lines_host.size() : (uint64_t)x->lines_img[image + 1];
+    if (!x->lines_sup_sorted) {
+        std::sort(x->lines_sup.begin(), x->lines_sup.end());
+        x->lines_sup_sorted = true;
+    }
+    const auto& S = x->lines_sup;
+    const auto lo = std::lower_bound(S.begin(), S.end(), std::make_pair(lb, 0u));
+    const auto hi = std::lower_bound(S.begin(), S.end(), std::make_pair(le, 0u));
+    *count = hi - lo;
+    if (!out) return HHT_OK;
+    if (cap < *count) return set_err(x, HHT_EINVAL, "cap < %lld support rows", (long long)*count);
+    int64_t k = 0;
+    for (auto it = lo; it != hi; ++it, ++k) {
+        out[2 * k] = (uint32_t)(it->first - lb);
+        out[2 * k + 1] = it->second;
+    }
     return HHT_OK;
 }
 

@@ -192,24 +192,36 @@ constexpr int kEdgeTile = 4096;    // pixels per 256-thread tile (16 per lane, l
 cudaError_t launch_edges(const EdgeArgs& a, cudaStream_t st);
 // solution() with point removal as a post-pass: per tree t, candidate leaves
 // leaves[cand_lo[t] .. cand_lo[t+1]) and points packed[pt_off[t] .. pt_off[t] + pt_n[t]).
-struct RemovalArgs {
-    const LeafRec* leaves;
-    const uint32_t* packed;
+// solution() with removal (NEXT-1): cooperative greedy over the candidate leaves of trees [t0, t1)
+constexpr int kRmThreads = 512;
+constexpr uint32_t kDone = 0xFFFFFFFEu;   // cur[t]: the tree's greedy has finished
+struct RmArgs {
+    const LeafRec* leaves;         // candidates (removal-off leaves), tree-major, depth-first order
     const uint64_t* cand_lo;       // [ntrees + 1]
-    const uint64_t* pt_off;        // [ntrees]
+    const uint32_t* packed;        // staged points
+    const uint64_t* pt_off;        // [ntrees] tree t's points in packed
     const uint32_t* pt_n;          // [ntrees]
-    const uint64_t* bits_off;      // [ntrees] word offset of tree t's support bitsets
+    const uint64_t* rm_off;        // [ntrees] tree t's removed flags in `removed`
     const uint8_t* tree_beta;
-    uint32_t* bits;                // supports: tree t, candidate k: W_t words
-    uint32_t* out;                 // [total candidates] emitted candidate indices, per tree at cand_lo[t]
-    uint32_t* out_live;            // live votes of the emitted lines
-    uint32_t* out_n;               // [ntrees] emitted per tree
+    uint32_t* live;                // [candidates] live votes
+    uint32_t* cellmap;             // [(t1 - t0) 4^D] leaf cell -> candidate index within its tree, kNone
+    uint8_t* removed;              // per (tree, point)
+    uint32_t* queue;               // [2 x points] (tree, point) removed in the current round
+    uint32_t* qn;
+    uint32_t* cur;                 // [ntrees] candidate emitted in the current round, kDone when finished
+    uint32_t* pos;                 // [ntrees] next candidate to consider
+    uint32_t* active;              // [2] trees that emitted in the round (round parity)
+    uint32_t* out;                 // [candidates] emitted candidate indices, tree t's at cand_lo[t]
+    uint32_t* out_live;            // live votes at emission
+    uint32_t* out_n;               // [ntrees]
+    uint32_t* sup;                 // [2 x points] (global line slot cand_lo[t] + e, point index in tree)
+    unsigned long long* sup_n;
     int N, D;
     uint64_t T;
-    uint32_t ntrees;
-    uint64_t total_words;
+    uint32_t t0, t1;
 };
-cudaError_t launch_removal(const RemovalArgs& a, bool int64, size_t smem_words, cudaStream_t st);
+int rm_blocks_per_sm(bool int64);
+cudaError_t launch_removal(const RmArgs& a, const LeafRec* leaves, bool int64, int grid, cudaStream_t st);
 // Latency path (k_small): the whole level-synchronous traversal of a tiny detection in ONE block.
 struct SmallArgs {
     const uint32_t* packed;        // staged points

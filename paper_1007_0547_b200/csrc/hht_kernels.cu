@@ -15,6 +15,7 @@
 // have SW values g - {0, Pc} - {0, Qc} (Pc = ex*s, Qc = 3N*s/2): the 9 lattice points of the
 // region (corners, edge midpoints, centre) decide the parent code and all four child codes.
 #include <algorithm>
+#include <cooperative_groups.h>
 #include <cuda/atomic>
 
 #include "hht_internal.h"
@@ -1343,93 +1344,161 @@ cudaError_t launch_edges(const EdgeArgs& a, cudaStream_t st) {
 // equals a greedy pass over the removal-off candidate leaves in depth-first order that emits a leaf
 // iff its voters not yet removed exceed THRESHOLD and then removes them (live votes only shrink, so a
 // leaf live at its turn had live ancestors at theirs; pinned in tests/test_oracle_removal.py).
-// k_support: support bitset of every candidate leaf (bit p = point p crosses the leaf cell, the exact
-// test at level D: 0 < G_SW <= 2ex + 3N); k_greedy: one block per tree walks its candidates in order
-// with the removed-point bitset in shared memory.
+//
+// Every candidate keeps its live vote count live[c] = votes(c) - #{removed points crossing c}
+// (votes(c) counts every point of the tree crossing the leaf cell, containment SURVEY.md L5). One
+// cooperative kernel runs the greedy for all trees of a group at once, in rounds:
+//   A  (one block per tree) the next candidate k at or after the tree's cursor with live[k] > T is
+//      exact (every earlier emission's removals are applied): emit it with live votes live[k];
+//   B1 (grid) every live point of the tree whose line crosses leaf k (the exact leaf test
+//      0 < G_SW <= 2ex + 3N) is removed and queued, with its support pair (line, point);
+//   B2 (grid, one warp per queued point) its line is rastered over the 2^D x 2^D leaf grid (column i:
+//      rows f_(i+1) .. f_i with f_i = floor((G(i, 0) - 1) / 3N)) and every candidate cell it crosses
+//      after k loses one live vote (a dense cell -> candidate map).
+// So a round costs E tests plus the removed points' rasters; the whole post-pass is bounded by
+// rounds <= E / T per tree and sum over removed points of 2^D columns (no candidates x points state).
 // ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_rm_init(const LeafRec* __restrict__ leaves, const uint64_t* __restrict__ cand_lo,
+                                                 uint32_t t0, uint32_t t1, int D, uint32_t* __restrict__ live,
+                                                 uint32_t* __restrict__ cellmap) {
+    const uint64_t k0 = cand_lo[t0], k1 = cand_lo[t1];
+    for (uint64_t k = k0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < k1; k += (uint64_t)gridDim.x * blockDim.x) {
+        const LeafRec L = leaves[k];
+        live[k] = L.votes;
+        const uint64_t cell = ((uint64_t)(L.tree - t0) << (2 * D)) + ((uint64_t)L.i << D) + L.j;
+        cellmap[cell] = (uint32_t)(k - cand_lo[L.tree]);
+    }
+}
+
+namespace cg = cooperative_groups;
+
 template <typename I>
-__global__ void __launch_bounds__(256) k_support(const RemovalArgs A) {
-    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;    // global support word
-    if (g >= A.total_words) return;
-    uint32_t lo = 0, hi = A.ntrees - 1;                                    // tree of word g
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) / 2;
-        if (A.bits_off[mid] <= g) lo = mid; else hi = mid - 1;
-    }
-    const uint32_t t = lo;
-    const uint32_t n = A.pt_n[t], W = (n + 31) / 32;
-    const uint64_t rel = g - A.bits_off[t];
-    const uint64_t k = A.cand_lo[t] + rel / W;                              // candidate leaf
-    const uint32_t w = (uint32_t)(rel % W);
-    const LeafRec L = A.leaves[k];
-    const bool beta = A.tree_beta[t] != 0;
-    const I N = (I)A.N;
-    const I base = ((I)N << A.D) - (I)3 * N * (I)L.j;                      // + 2^D (ex + ey) - 2 i ex below
-    uint32_t word = 0;
-    for (int b = 0; b < 32; ++b) {
-        const uint32_t p = 32 * w + b;
-        if (p >= n) break;
-        const uint32_t pk = A.packed[A.pt_off[t] + p];
-        const I ex = (I)(beta ? (pk & 0xFFFFu) : (pk >> 16)), ey = (I)(beta ? (pk >> 16) : (pk & 0xFFFFu));
-        const I g_sw = base + ((ex + ey) << A.D) - (I)2 * (I)L.i * ex;      // G(i, j) of the leaf's SW corner
-        if (g_sw > 0 && g_sw <= (I)2 * ex + (I)3 * N) word |= 1u << b;
-    }
-    A.bits[g] = word;
-}
-
-__global__ void __launch_bounds__(1024) k_greedy(const RemovalArgs A, uint32_t smem_words) {
-    extern __shared__ uint32_t s_removed[];
-    __shared__ uint32_t s_part[32];
-    __shared__ uint32_t s_emit;
-    const uint32_t t = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t n = A.pt_n[t], W = (n + 31) / 32;
-    // removed-point bitset: shared memory when it fits, else this tree's slice of `out` is not
-    // usable, so the caller guarantees W <= smem_words
-    for (uint32_t w = tid; w < W; w += blockDim.x) s_removed[w] = 0;
-    if (tid == 0) s_emit = 0;
-    __syncthreads();
-    const uint64_t c0 = A.cand_lo[t], c1 = A.cand_lo[t + 1];
-    const uint32_t* bits = A.bits + A.bits_off[t];
-    uint32_t emitted = 0;
-    for (uint64_t k = c0; k < c1; ++k) {
-        const uint32_t* sk = bits + (k - c0) * W;
-        uint32_t live = 0;
-        for (uint32_t w = tid; w < W; w += blockDim.x) live += __popc(sk[w] & ~s_removed[w]);
-        live = __reduce_add_sync(0xFFFFFFFFu, live);
-        if (lane == 0) s_part[wid] = live;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t v = lane < (int)(blockDim.x >> 5) ? s_part[lane] : 0u;
-            v = __reduce_add_sync(0xFFFFFFFFu, v);
-            if (lane == 0) s_emit = (uint64_t)v > A.T ? v : 0u;
-        }
-        __syncthreads();
-        const uint32_t e = s_emit;
-        if (e) {                                       // emit, then remove its live voters
-            for (uint32_t w = tid; w < W; w += blockDim.x) s_removed[w] |= sk[w];
-            if (tid == 0) {
-                A.out[c0 + emitted] = (uint32_t)(k - c0);
-                A.out_live[c0 + emitted] = e;
+__global__ void __launch_bounds__(kRmThreads) k_rm(const RmArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ uint32_t s_found;
+    const uint32_t nt = A.t1 - A.t0;
+    const I N = (I)A.N, N3 = (I)3 * (I)A.N;
+    const int D = A.D;
+    const uint32_t side = 1u << D;
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t gsize = (uint64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t round = 0;; ++round) {
+        // ---- A: next emission of every active tree (block b takes trees b, b + grid, ...)
+        for (uint32_t tt = blockIdx.x; tt < nt; tt += gridDim.x) {
+            const uint32_t t = A.t0 + tt;
+            if (A.cur[t] == kDone) continue;
+            const uint64_t c0 = A.cand_lo[t], c1 = A.cand_lo[t + 1];
+            uint64_t k = c0 + A.pos[t];
+            uint32_t found = kNone;
+            for (; k < c1; k += blockDim.x) {
+                if (threadIdx.x == 0) s_found = kNone;
+                __syncthreads();
+                const uint64_t c = k + threadIdx.x;
+                if (c < c1 && (uint64_t)A.live[c] > A.T) atomicMin(&s_found, (uint32_t)(c - c0));
+                __syncthreads();
+                found = s_found;
+                __syncthreads();
+                if (found != kNone) break;
             }
-            ++emitted;
+            if (threadIdx.x == 0) {
+                if (found == kNone) {
+                    A.cur[t] = kDone;
+                } else {
+                    const uint32_t e = A.out_n[t];
+                    A.out[c0 + e] = found;
+                    A.out_live[c0 + e] = A.live[c0 + found];
+                    A.out_n[t] = e + 1;
+                    A.cur[t] = found;
+                    A.pos[t] = found + 1;
+                    atomicAdd(A.active + (round & 1), 1u);
+                }
+            }
         }
-        __syncthreads();
+        if (gtid == 0) { A.active[(round + 1) & 1] = 0; *A.qn = 0; }
+        grid.sync();
+        if (A.active[round & 1] == 0) break;
+        // ---- B1: remove the live voters of every tree's emitted leaf
+        for (uint32_t tt = 0; tt < nt; ++tt) {
+            const uint32_t t = A.t0 + tt;
+            const uint32_t k = A.cur[t];
+            if (k == kDone) continue;
+            const LeafRec L = A.leaves[A.cand_lo[t] + k];
+            const bool beta = A.tree_beta[t] != 0;
+            const uint32_t n = A.pt_n[t];
+            const uint32_t* pts = A.packed + A.pt_off[t];
+            uint8_t* rem = A.removed + A.rm_off[t];
+            const I base = (N << D) - N3 * (I)L.j;
+            for (uint64_t p = gtid; p < n; p += gsize) {
+                if (rem[p]) continue;
+                const uint32_t pk = pts[p];
+                const I ex = (I)(beta ? (pk & 0xFFFFu) : (pk >> 16)), ey = (I)(beta ? (pk >> 16) : (pk & 0xFFFFu));
+                const I g = base + ((ex + ey) << D) - (I)2 * (I)L.i * ex;      // G(SW corner of leaf k)
+                if (g > 0 && g <= (I)2 * ex + N3) {
+                    rem[p] = 1;
+                    const uint32_t q = atomicAdd(A.qn, 1u);
+                    A.queue[2 * (uint64_t)q] = t;
+                    A.queue[2 * (uint64_t)q + 1] = (uint32_t)p;
+                    const unsigned long long sidx = atomicAdd(A.sup_n, 1ull);
+                    A.sup[2 * sidx] = (uint32_t)(A.cand_lo[t] + A.out_n[t] - 1);   // global line slot
+                    A.sup[2 * sidx + 1] = (uint32_t)p;
+                }
+            }
+        }
+        grid.sync();
+        // ---- B2: every queued point's line loses one live vote in every later candidate it crosses
+        const uint32_t nq = *A.qn;
+        const uint64_t warp = gtid >> 5, nwarp = gsize >> 5;
+        const uint32_t per = (side + 31) / 32;                 // columns per lane (contiguous)
+        for (uint64_t qi = warp; qi < nq; qi += nwarp) {
+            const uint32_t t = A.queue[2 * qi], p = A.queue[2 * qi + 1];
+            const uint32_t k = A.cur[t];
+            const bool beta = A.tree_beta[t] != 0;
+            const uint32_t pk = A.packed[A.pt_off[t] + p];
+            const I ex = (I)(beta ? (pk & 0xFFFFu) : (pk >> 16)), ey = (I)(beta ? (pk >> 16) : (pk & 0xFFFFu));
+            const uint32_t i_lo = (uint32_t)lane * per;
+            if (i_lo >= side) continue;
+            const uint32_t i_hi = min(side, i_lo + per);
+            // y_i = G(i, 0) - 1 = 2^D (ex + ey + N) - 2 i ex - 1 >= 0 up to the column where the line
+            // leaves the root; f_i = floor(y_i / 3N) with the remainder carried column to column
+            // (2ex < 3N: at most one borrow per column)
+            I y = ((ex + ey + N) << D) - (I)2 * (I)i_lo * ex - 1;
+            I f, r;
+            if (y >= 0) { f = y / N3; r = y - f * N3; }
+            else { f = -((-y + N3 - 1) / N3); r = y - f * N3; }
+            const uint32_t* cm = A.cellmap + ((uint64_t)(t - A.t0) << (2 * D));
+            uint32_t* live = A.live + A.cand_lo[t];
+            for (uint32_t i = i_lo; i < i_hi; ++i) {
+                // f_(i+1): y decreases by 2ex
+                I rn = r - (I)2 * ex, fn = f;
+                if (rn < 0) { rn += N3; fn -= 1; }
+                const I vlo = fn < 0 ? (I)0 : fn, vhi = f >= (I)side ? (I)side - 1 : f;
+                for (I v = vlo; v <= vhi; ++v) {
+                    const uint32_t c = __ldg(cm + ((uint64_t)i << D) + (uint64_t)v);
+                    if (c != kNone && c > k) atomicSub(live + c, 1u);
+                }
+                f = fn;
+                r = rn;
+            }
+        }
+        grid.sync();
     }
-    if (tid == 0) A.out_n[t] = emitted;
-    (void)smem_words;
 }
 
-cudaError_t launch_removal(const RemovalArgs& a, bool int64, size_t smem_words, cudaStream_t st) {
-    if (a.total_words) {
-        const uint64_t blocks = (a.total_words + 255) / 256;
-        if (int64) k_support<int64_t><<<(unsigned)blocks, 256, 0, st>>>(a);
-        else k_support<int32_t><<<(unsigned)blocks, 256, 0, st>>>(a);
-    }
-    const size_t smem = std::max<size_t>(smem_words, 1) * 4;
-    cudaFuncSetAttribute(k_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_greedy<<<a.ntrees, 1024, smem, st>>>(a, (uint32_t)smem_words);
-    return cudaGetLastError();
+int rm_blocks_per_sm(bool int64) {
+    int n = 0;
+    if (int64) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_rm<int64_t>, kRmThreads, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_rm<int32_t>, kRmThreads, 0);
+    return n > 0 ? n : 1;
+}
+
+cudaError_t launch_removal(const RmArgs& a, const LeafRec* leaves, bool int64, int grid, cudaStream_t st) {
+    k_rm_init<<<1184, 256, 0, st>>>(leaves, a.cand_lo, a.t0, a.t1, a.D, a.live, a.cellmap);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    void* args[] = {(void*)&a};
+    return cudaLaunchCooperativeKernel(int64 ? (const void*)k_rm<int64_t> : (const void*)k_rm<int32_t>,
+                                       dim3(grid), dim3(kRmThreads), args, 0, st);
 }
 
 // ---------------------------------------------------------------------------------------------

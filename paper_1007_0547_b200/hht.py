@@ -30,7 +30,8 @@ EXPORTS = ["hht_default_opts", "hht_create", "hht_nccl_unique_id", "hht_detect",
            "hht_result_leaves", "hht_result_level", "hht_result_stats", "hht_result_profile",
            "hht_result_launches", "hht_timer_begin", "hht_timer_end", "hht_last_error", "hht_status_str",
            "hht_destroy", "hht_version", "hht_set_leaf_sink", "hht_group_create", "hht_group_destroy",
-           "hht_detect_trees", "hht_detect_image", "hht_result_edges", "hht_result_lines", "hht_set_stream"]
+           "hht_detect_trees", "hht_detect_image", "hht_result_edges", "hht_result_lines", "hht_set_stream",
+           "hht_result_line_points"]
 
 PROFILE_CLASSES = ["stage", "count", "write", "tail", "split", "gather", "other", "allreduce"]
 
@@ -100,6 +101,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hht_detect_image": ([p, p, i32, i32, i32, i64], C.c_int),
         "hht_result_edges": ([p, p, i64, p, p], C.c_int),
         "hht_result_lines": ([p, i32, p, i64, p], C.c_int),
+        "hht_result_line_points": ([p, i32, p, i64, p], C.c_int),
         "hht_group_destroy": ([p], None),
         "hht_result_profile": ([p, p], C.c_int),
         "hht_result_launches": ([p, p, i64, p], C.c_int),
@@ -302,6 +304,15 @@ class HHT:
         out = (Leaf * max(cnt.value, 1))()
         self._check(self._lib.hht_result_lines(self._ctx, image, out, cnt.value, C.byref(cnt)))
         return np.frombuffer(out, dtype=np.uint32, count=5 * cnt.value).reshape(-1, 5).astype(np.int64)
+
+    def line_points(self, image: int = -1) -> np.ndarray:
+        """int64 [k, 2] (line, point): the points each removal-on line emitted (hht_result_line_points),
+        sorted by line then point; line indexes lines(image)."""
+        cnt = C.c_int64(0)
+        self._check(self._lib.hht_result_line_points(self._ctx, image, None, 0, C.byref(cnt)))
+        out = np.zeros((max(cnt.value, 1), 2), dtype=np.uint32)
+        self._check(self._lib.hht_result_line_points(self._ctx, image, out.ctypes.data, cnt.value, C.byref(cnt)))
+        return out[:cnt.value].astype(np.int64)
 
     def edges(self):
         """(alpha, beta) int32 [k, 2] (x, y) edge points of the last detect_image, raster order."""

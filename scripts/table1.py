@@ -1,7 +1,9 @@
 """Table-1-style comparison (Table 1, Figs. 6-7) on
 synthetic stand-ins for the paper's three images (Figs. 3a-5a are not available): for each size
-32..256 and three seeded line scenes, the votes cast by the FHT circumcircle test and by the
-paper's exact test, their ratio C_v, and the device time per image of both on one B200, measured
+32..256 and three seeded line scenes, the votes cast by the FHT circumcircle test (two readings of
+its units: variant 1 = lattice units, square regions; variant 2 = (m, b) units, 2s/2^D x 3Ns/2^D
+rectangles, R22) and by the paper's exact test, the ratios C_v, and the device time per
+image of each on one B200, measured
 as the paper did with many repetitions: one hht_detect_batch over `--reps` copies of the image
 (the paper ran each algorithm 1000 times). Votes are checked against the oracle (both variants)
 before they are reported.
@@ -44,8 +46,8 @@ def main():
         for k in range(3):
             pts = scene(N, k)
             res = {}
-            for name, var in (("fht", hht.FHT_CIRCLE), ("exact", hht.EXACT)):
-                ref = oracle.detect(pts, N, D, T, AB, variant=1 if var else 0)
+            for name, var in (("fht", hht.FHT_CIRCLE), ("fht_mb", hht.FHT_CIRCLE_MB), ("exact", hht.EXACT)):
+                ref = oracle.detect(pts, N, D, T, AB, variant=var)
                 h = hht.HHT(halves=AB, variant=var, record_levels=False)
                 one = torch.from_numpy(pts).to(dev)
                 h.detect(one, N, D, T)
@@ -66,14 +68,30 @@ def main():
              f"Votes: one detection (both halves, removal off), equal to the oracle's for both tests. Time: device "
              f"time of one hht_detect_batch over {a.reps} copies of the image, divided by {a.reps} (the paper "
              "looped 1000 times on a 3 GHz Pentium IV). T = max(4, N/8), D = log2 N.", "",
-             "| size | image | E | T | votes FHT | votes exact | C_v | leaves FHT | leaves exact | us/image FHT | us/image exact | C_t |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             "| size | image | E | T | votes exact | votes FHT-1 | C_v (1) | votes FHT-2 | C_v (2) | leaves exact / FHT-1 / FHT-2 | us/image exact | us/image FHT-1 | C_t (1) | us/image FHT-2 | C_t (2) |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for N, k, E, T, r in rows:
         vf, lf, tf = r["fht"]
+        vm, lm, tm = r["fht_mb"]
         ve, le, te = r["exact"]
-        lines.append(f"| {N}x{N} | {k} | {E} | {T} | {vf} | {ve} | {vf / ve:.3f} | {lf} | {le} | {tf:.2f} | {te:.2f} | {tf / te:.2f} |")
-    lines += ["", "Paper (Pentium IV, its own images, removal on): C_v between 1.9 and 7.6 and C_t in the hundreds "
-              "to thousands (Table 1); the paper attributes C_t mainly to FHT's floating point and square roots."]
+        lines.append(f"| {N}x{N} | {k} | {E} | {T} | {ve} | {vf} | {vf / ve:.3f} | {vm} | {vm / ve:.2f} | {le} / {lf} / {lm} | "
+                     f"{te:.2f} | {tf:.2f} | {tf / te:.2f} | {tm:.2f} | {tm / te:.2f} |")
+    # mean C_v per size and threshold regime, beside the paper's (Table 1)
+    paper = {32: (3391 / 1817 + 4577 / 2387 + 6081 / 3277) / 3, 64: (10424 / 4551 + 13537 / 5945 + 18281 / 8051) / 3,
+             128: (71315 / 15759 + 70946 / 15691 + 119756 / 26513) / 3, 256: (393553 / 51420 + 219320 / 29112 + 342795 / 45457) / 3}
+    lines += ["", "Mean C_v per size (three images) beside the paper's Table 1 means (its three images, removal on):", "",
+              "| size | T | C_v variant 1 (lattice units) | C_v variant 2 ((m, b) units) | paper C_v |", "|---|---|---|---|---|"]
+    groups = {}
+    for N, k, E, T, r in rows:
+        groups.setdefault((N, T), []).append(r)
+    for (N, T), rs in sorted(groups.items()):
+        c1 = sum(x["fht"][0] / x["exact"][0] for x in rs) / len(rs)
+        c2 = sum(x["fht_mb"][0] / x["exact"][0] for x in rs) / len(rs)
+        lines.append(f"| {N}x{N} | {T} | {c1:.2f} | {c2:.1f} | {paper[N]:.2f} |")
+    lines += ["", "Paper (Pentium IV, its own images, removal on): C_v between 1.9 and 7.6, growing with the image "
+              "size (PAPER.md:316 'exponential nature'), and C_t in the hundreds to thousands (Table 1); the paper "
+              "attributes C_t mainly to FHT's floating point and square roots. Variant 1 gives a flat C_v; variant "
+              "2 reproduces the growth with size (about x2 per doubling) at larger absolute values."]
     txt = "\n".join(lines) + "\n"
     print(txt)
     if a.out:

@@ -133,9 +133,21 @@ def test_circle_casts_extra_votes(cid, var, cuda_device):
     assert hc.stats()["votes"] > he.stats()["votes"]
 
 
-@pytest.mark.parametrize("var", VARS)
-def test_circle_overflow_rejected(var, cuda_device):
-    h = hht.HHT(halves=AB, variant=var)
+def test_circle_overflow_rejected(cuda_device):
+    h = hht.HHT(halves=AB, variant=hht.FHT_CIRCLE)
     with pytest.raises(hht.HHTError) as e:
         h.detect(_dev(np.array([[0, 0]], np.int32), cuda_device), 65536, 30, 2)
     assert e.value.name == "HHT_EOVERFLOW"
+
+
+def test_circle_mb_extremes(cuda_device):
+    """Variant 2 compares in 128 bits: (1 + ex^2)(4 + 9N^2) s^2 < 2^125.2 for every tested region
+    (children of the root down) within the API's limits (N <= 65536, depth <= 30), so it never
+    overflows; at the extreme it runs and matches the oracle (ex = 0 keeps the oracle's own root
+    test inside its signed 128-bit range)."""
+    pts = np.array([[0, 0], [0, 65535], [0, 1]], np.int32)     # ALPHA lines b = 0, 65535, 1
+    ref = oracle.detect(pts, 65536, 30, 2, hht.ALPHA, variant=2)
+    h = _run(pts, 65536, 30, 2, hht.ALPHA, cuda_device, hht.FHT_CIRCLE_MB)
+    assert ref.levels[(1, 1)].shape[0] == 4 and ref.levels[(1, 2)].shape[0] == 0
+    for lev in range(3):
+        assert np.array_equal(h.level(0, 1, lev), ref.levels[(1, lev)])

@@ -1,6 +1,12 @@
 """GPU solution() with point removal (hht_result_lines)
 against the oracle's literal depth-first detector with removal on (oracle_detect_removal, pinned in
-tests/test_oracle_removal.py): the emitted lines and their live votes must be identical, in order."""
+tests/test_oracle_removal.py): the emitted lines and their live votes must be identical, in order,
+and so must each line's support (the points it removed). Config 3 in full against an oracle-written
+digest (scripts/write_golden_removal.py)."""
+import hashlib
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -18,10 +24,14 @@ def _dev(pts, dev):
 
 
 def _check(h, pts, N, D, T, halves, image=0):
-    lines, _ = oracle.detect_removal(pts, N, D, T, halves)
+    lines, sup = oracle.detect_removal(pts, N, D, T, halves)
     got = h.lines(image)
     assert np.array_equal(got[:, 1:], lines.astype(np.int64)), (got[:5], lines[:5])
     assert (got[:, 0] == image).all()
+    want = sup.astype(np.int64)
+    want = want[np.lexsort((want[:, 1], want[:, 0]))] if want.shape[0] else want.reshape(0, 2)
+    gs = h.line_points(image)
+    assert np.array_equal(gs, want), (gs[:5], want[:5])
 
 
 @pytest.mark.parametrize("cid", [1, 2])
@@ -71,3 +81,20 @@ def test_removal_rejects_circle(cuda_device):
     with pytest.raises(hht.HHTError) as e:
         h.lines()
     assert e.value.name == "HHT_EINVAL"
+
+
+def test_removal_c3_digest(cuda_device):
+    """Config 3 in full (400k points, 4.2e6 candidate leaves): lines and supports against the digest
+    of oracle_detect_removal (tests/golden/c3_removal_digest.json)."""
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c3_removal_digest.json")))
+    cfg = synth.CONFIGS[3]
+    pts, _ = synth.config_image(3)
+    h = hht.HHT(halves=cfg.halves)
+    h.detect(_dev(pts, cuda_device), cfg.N, cfg.D, cfg.T)
+    lines = h.lines()
+    L = np.ascontiguousarray(lines[:, 1:].astype("<u4"))
+    assert L.shape[0] == gold["lines"]
+    assert hashlib.sha256(L.tobytes()).hexdigest() == gold["lines_sha256"]
+    S = np.ascontiguousarray(h.line_points().astype("<u4"))
+    assert S.shape[0] == gold["support"]
+    assert hashlib.sha256(S.tobytes()).hexdigest() == gold["support_sha256"]
