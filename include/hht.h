@@ -208,7 +208,7 @@ hht_status hht_detect_batch(hht_ctx* ctx, const int32_t* points, const int64_t* 
  * one cooperative kernel per group of trees: live vote counts per candidate, kept exact by rastering
  * each removed point's line over a dense 4^depth cell -> candidate map, so the next emission of every
  * tree is found in one scan (rounds <= points / threshold per tree). Device memory: 12 B per candidate
- * + 17 B per (tree, point) + 4^(depth+1) B per tree of a group (HHT_ENOMEM if one tree's map does not
+ * + 25 B per (tree, point) + 4^(depth+1) B per tree of a group (HHT_ENOMEM if one tree's map does not
  * fit the budget). Single rank, exact test only. */
 hht_status hht_result_lines(hht_ctx* ctx, int32_t image, hht_leaf* out, int64_t cap, int64_t* count);
 

@@ -1464,16 +1464,17 @@ hht_status compute_lines(hht_ctx* x) {
     }
     const uint64_t ncand = L.size(), npts = rm_off[nt];
     const uint64_t per_tree = 4ull << (2 * x->D);                 // dense cell map of one tree
-    const uint64_t fixed = ncand * 12 + npts * 17 + (uint64_t)nt * 48 + 4096;
+    const uint64_t fixed = ncand * 12 + npts * 25 + (uint64_t)nt * 48 + 4096;
     if (fixed + per_tree > x->budget)
         return set_err(x, HHT_ENOMEM, "removal post-pass needs %llu B (candidates, points and one 4^depth cell map)",
                        (unsigned long long)(fixed + per_tree));
     const uint32_t gmax = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(nt ? nt : 1, (x->budget - fixed) / per_tree));
     Buf big, meta;
     auto cleanup = [&]() { for (Buf* b : {&big, &meta}) if (b->p) cudaFreeAsync(b->p, x->st); };
-    // big: live | out | out_live (ncand each) | queue | sup (2 npts each) | removed (npts) | cellmap
+    // big: live | out | out_live (ncand each) | queue (4 npts) | sup (2 npts) | removed (npts) | cellmap
     const uint64_t nc1 = std::max<uint64_t>(ncand, 1), np1 = std::max<uint64_t>(npts, 1);
-    const uint64_t big_bytes = nc1 * 12 + np1 * 16 + ((np1 + 15) / 16) * 16 + (uint64_t)gmax * per_tree;
+    const uint64_t qwords = 4 * np1 + 2ull * (nt + 1) + 4;          // queue; later rows + line bases
+    const uint64_t big_bytes = nc1 * 12 + qwords * 4 + np1 * 8 + ((np1 + 15) / 16) * 16 + (uint64_t)gmax * per_tree;
     hht_status st = ensure(x, big, big_bytes);
     if (st == HHT_OK) st = ensure(x, meta, (size_t)(nt + 1) * 8 * 3 + (size_t)nt * 16 + 64);
     if (st != HHT_OK) { cleanup(); return st; }
@@ -1481,7 +1482,7 @@ hht_status compute_lines(hht_ctx* x) {
     uint32_t* d_out = d_live + nc1;
     uint32_t* d_out_live = d_out + nc1;
     uint32_t* d_queue = d_out_live + nc1;
-    uint32_t* d_sup = d_queue + 2 * np1;
+    uint32_t* d_sup = d_queue + qwords;
     uint8_t* d_removed = (uint8_t*)(d_sup + 2 * np1);
     uint32_t* d_cellmap = (uint32_t*)(d_removed + ((np1 + 15) / 16) * 16);
     uint64_t* d_cand = (uint64_t*)meta.p;
@@ -1491,7 +1492,7 @@ hht_status compute_lines(hht_ctx* x) {
     uint32_t* d_cur = d_ptn + nt;
     uint32_t* d_pos = d_cur + nt;
     uint32_t* d_outn = d_pos + nt;
-    uint32_t* d_small = d_outn + nt;                      // active[2], qn, pad
+    uint32_t* d_small = d_outn + nt;                      // active[2], qn[2]
     unsigned long long* d_supn = (unsigned long long*)(d_small + 4);
     CK(cudaMemcpyAsync(d_cand, cand_lo.data(), (nt + 1) * 8, cudaMemcpyHostToDevice, x->st));
     if (nt) {
@@ -1513,6 +1514,7 @@ hht_status compute_lines(hht_ctx* x) {
     a.cellmap = d_cellmap;
     a.removed = d_removed;
     a.queue = d_queue;
+    a.queue_cap = np1;
     a.qn = d_small + 2;
     a.cur = d_cur;
     a.pos = d_pos;
@@ -1533,34 +1535,33 @@ hht_status compute_lines(hht_ctx* x) {
         CK(cudaMemsetAsync(d_cellmap, 0xFF, (size_t)(a.t1 - t0) * per_tree, x->st));
         CK(launch_removal(a, (const LeafRec*)x->leaves.b.p, x->int64, x->rm_grid[x->int64 ? 1 : 0], x->st));
     }
-    std::vector<uint32_t> h_out(ncand), h_live(ncand), h_n(nt);
+    std::vector<uint32_t> h_n(nt);
     unsigned long long h_supn = 0;
-    if (ncand) {
-        CK(cudaMemcpyAsync(h_out.data(), d_out, ncand * 4, cudaMemcpyDeviceToHost, x->st));
-        CK(cudaMemcpyAsync(h_live.data(), d_out_live, ncand * 4, cudaMemcpyDeviceToHost, x->st));
-    }
     if (nt) CK(cudaMemcpyAsync(h_n.data(), d_outn, nt * 4, cudaMemcpyDeviceToHost, x->st));
     CK(cudaMemcpyAsync(&h_supn, d_supn, 8, cudaMemcpyDeviceToHost, x->st));
     TRY(sync(x));
+    std::vector<uint64_t> line_base(nt + 1, 0);
+    for (uint32_t t = 0; t < nt; ++t) line_base[t + 1] = line_base[t] + h_n[t];
+    const uint64_t nlines = line_base[nt];
+    // rows (5 u32) and line bases reuse the queue area (qwords >= 5 nlines + 2 (nt + 1) + 2, since a
+    // line removes more than T >= 1 points: nlines <= npts / 2)
+    uint32_t* d_rows = d_queue;
+    uint64_t* d_lbase = (uint64_t*)(((uintptr_t)(d_rows + 5 * nlines) + 7) & ~(uintptr_t)7);
+    CK(cudaMemcpyAsync(d_lbase, line_base.data(), (nt + 1) * 8, cudaMemcpyHostToDevice, x->st));
+    if (ncand) CK(launch_rm_rows((const LeafRec*)x->leaves.b.p, d_cand, d_out, d_out_live, d_outn, d_lbase,
+                                 (const uint8_t*)x->beta.p, nt, (uint32_t)x->H, ncand, d_rows, d_sup, h_supn, x->st));
+    x->lines_host.resize(nlines);
     std::vector<uint32_t> h_sup(2 * h_supn);
+    if (nlines) CK(cudaMemcpyAsync(x->lines_host.data(), d_rows, nlines * sizeof(hht_leaf), cudaMemcpyDeviceToHost, x->st));
     if (h_supn) CK(cudaMemcpyAsync(h_sup.data(), d_sup, 8ull * h_supn, cudaMemcpyDeviceToHost, x->st));
     TRY(sync(x));
     cleanup();
-    x->lines_host.clear();
     x->lines_img.assign(x->B + 1, 0);
-    std::vector<int64_t> slot_line(ncand, -1);            // global slot cand_lo[t] + e -> line index
-    for (uint32_t t = 0; t < nt; ++t) {
-        for (uint32_t e = 0; e < h_n[t]; ++e) {
-            const LeafRec& r = L[cand_lo[t] + h_out[cand_lo[t] + e]];
-            slot_line[cand_lo[t] + e] = (int64_t)x->lines_host.size();
-            x->lines_host.push_back({(int32_t)(t / x->H), (uint32_t)x->tree_half[t], r.i, r.j, h_live[cand_lo[t] + e]});
-        }
-        x->lines_img[t / x->H + 1] = (int64_t)x->lines_host.size();
-    }
+    for (uint32_t t = 0; t < nt; ++t) x->lines_img[t / x->H + 1] = (int64_t)line_base[t + 1];
     for (int b = 1; b <= x->B; ++b) x->lines_img[b] = std::max(x->lines_img[b], x->lines_img[b - 1]);
     // supports as (line, point); sorted by line then point on first request (hht_result_line_points)
     x->lines_sup.resize(h_supn);
-    for (uint64_t s = 0; s < h_supn; ++s) x->lines_sup[s] = {(uint64_t)slot_line[h_sup[2 * s]], h_sup[2 * s + 1]};
+    for (uint64_t s = 0; s < h_supn; ++s) x->lines_sup[s] = {(uint64_t)h_sup[2 * s], h_sup[2 * s + 1]};
     x->lines_sup_sorted = false;
     x->lines_ok = true;
     return HHT_OK;

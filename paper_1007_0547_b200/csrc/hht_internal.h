@@ -193,7 +193,9 @@ cudaError_t launch_edges(const EdgeArgs& a, cudaStream_t st);
 // solution() with point removal as a post-pass: per tree t, candidate leaves
 // leaves[cand_lo[t] .. cand_lo[t+1]) and points packed[pt_off[t] .. pt_off[t] + pt_n[t]).
 // solution() with removal (NEXT-1): cooperative greedy over the candidate leaves of trees [t0, t1)
-constexpr int kRmThreads = 512;
+constexpr int kRmThreads = 1024;
+constexpr int kRmRedTrees = 16;          // k_rm: groups of at most this many trees search redundantly per block
+constexpr int kRmCols = 8;               // k_rm: leaf columns rastered per thread and removed point
 constexpr uint32_t kDone = 0xFFFFFFFEu;   // cur[t]: the tree's greedy has finished
 struct RmArgs {
     const LeafRec* leaves;         // candidates (removal-off leaves), tree-major, depth-first order
@@ -206,8 +208,9 @@ struct RmArgs {
     uint32_t* live;                // [candidates] live votes
     uint32_t* cellmap;             // [(t1 - t0) 4^D] leaf cell -> candidate index within its tree, kNone
     uint8_t* removed;              // per (tree, point)
-    uint32_t* queue;               // [2 x points] (tree, point) removed in the current round
-    uint32_t* qn;
+    uint32_t* queue;               // [2 rounds][queue_cap][2] (tree, point) removed in a round (parity)
+    uint32_t* qn;                  // [2] queue counts by round parity
+    uint64_t queue_cap;
     uint32_t* cur;                 // [ntrees] candidate emitted in the current round, kDone when finished
     uint32_t* pos;                 // [ntrees] next candidate to consider
     uint32_t* active;              // [2] trees that emitted in the round (round parity)
@@ -221,6 +224,9 @@ struct RmArgs {
     uint32_t t0, t1;
 };
 int rm_blocks_per_sm(bool int64);
+cudaError_t launch_rm_rows(const LeafRec* leaves, const uint64_t* cand_lo, const uint32_t* out, const uint32_t* out_live,
+                           const uint32_t* out_n, const uint64_t* line_base, const uint8_t* tree_beta, uint32_t nt,
+                           uint32_t H, uint64_t ncand, uint32_t* rows, uint32_t* sup, uint64_t nsup, cudaStream_t st);
 cudaError_t launch_removal(const RmArgs& a, const LeafRec* leaves, bool int64, int grid, cudaStream_t st);
 // Latency path (k_small): the whole level-synchronous traversal of a tiny detection in ONE block.
 struct SmallArgs {

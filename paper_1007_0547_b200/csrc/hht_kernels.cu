@@ -1372,123 +1372,259 @@ __global__ void __launch_bounds__(256) k_rm_init(const LeafRec* __restrict__ lea
 
 namespace cg = cooperative_groups;
 
-template <typename I>
+// RED (at most kRmRedTrees trees in the group): every block runs A for every tree redundantly on
+// identical data (no barrier between A and B1; block 0 writes the outputs), so a round costs two
+// grid barriers instead of three.
+template <typename I, bool RED>
 __global__ void __launch_bounds__(kRmThreads) k_rm(const RmArgs A) {
     cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t s_found;
+    __shared__ uint32_t s_cur[kRmRedTrees], s_pos[kRmRedTrees], s_outn[kRmRedTrees], s_fnd[kRmRedTrees];
     const uint32_t nt = A.t1 - A.t0;
     const I N = (I)A.N, N3 = (I)3 * (I)A.N;
     const int D = A.D;
     const uint32_t side = 1u << D;
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t gsize = (uint64_t)gridDim.x * blockDim.x;
-    const int lane = threadIdx.x & 31;
+    if (RED) {
+        for (uint32_t tt = threadIdx.x; tt < nt; tt += blockDim.x) {
+            s_cur[tt] = A.cur[A.t0 + tt];
+            s_pos[tt] = A.pos[A.t0 + tt];
+            s_outn[tt] = A.out_n[A.t0 + tt];
+        }
+        __syncthreads();
+    }
     for (uint32_t round = 0;; ++round) {
-        // ---- A: next emission of every active tree (block b takes trees b, b + grid, ...)
-        for (uint32_t tt = blockIdx.x; tt < nt; tt += gridDim.x) {
+        // ---- A: next emission of every active tree. RED: every block, all trees at once (thread j of
+        // tree tt = threadIdx % nt scans 4 consecutive candidates per step); else block b takes trees
+        // b, b + grid, ... one after another with the whole block.
+        uint32_t active = 0;
+        if (RED) {
+            const uint32_t tt = threadIdx.x % nt, j = threadIdx.x / nt, per = blockDim.x / nt;
             const uint32_t t = A.t0 + tt;
-            if (A.cur[t] == kDone) continue;
             const uint64_t c0 = A.cand_lo[t], c1 = A.cand_lo[t + 1];
-            uint64_t k = c0 + A.pos[t];
-            uint32_t found = kNone;
-            for (; k < c1; k += blockDim.x) {
-                if (threadIdx.x == 0) s_found = kNone;
+            if (threadIdx.x < nt) s_fnd[threadIdx.x] = kNone;
+            __syncthreads();
+            const bool mine_active = j < per && s_cur[tt] != kDone;
+            for (uint64_t step = 0;; ++step) {
+                const uint64_t k = c0 + s_pos[tt] + step * 4ull * per + 4ull * j;
+                if (mine_active && s_fnd[tt] == kNone) {
+                    uint32_t mine = kNone;
+#pragma unroll
+                    for (int q = 3; q >= 0; --q) {
+                        const uint64_t c = k + q;
+                        if (c < c1 && (uint64_t)A.live[c] > A.T) mine = (uint32_t)(c - c0);
+                    }
+                    if (mine != kNone) atomicMin(&s_fnd[tt], mine);
+                }
                 __syncthreads();
-                const uint64_t c = k + threadIdx.x;
-                if (c < c1 && (uint64_t)A.live[c] > A.T) atomicMin(&s_found, (uint32_t)(c - c0));
-                __syncthreads();
-                found = s_found;
-                __syncthreads();
-                if (found != kNone) break;
+                const bool more = j == 0 && mine_active && s_fnd[tt] == kNone &&
+                                  c0 + s_pos[tt] + (step + 1) * 4ull * per < c1;
+                if (!__syncthreads_or(more)) break;
             }
-            if (threadIdx.x == 0) {
-                if (found == kNone) {
-                    A.cur[t] = kDone;
-                } else {
-                    const uint32_t e = A.out_n[t];
-                    A.out[c0 + e] = found;
-                    A.out_live[c0 + e] = A.live[c0 + found];
-                    A.out_n[t] = e + 1;
-                    A.cur[t] = found;
-                    A.pos[t] = found + 1;
-                    atomicAdd(A.active + (round & 1), 1u);
+            if (threadIdx.x < nt) {
+                const uint32_t u = A.t0 + threadIdx.x, f = s_fnd[threadIdx.x];
+                if (s_cur[threadIdx.x] != kDone) {
+                    if (f == kNone) {
+                        s_cur[threadIdx.x] = kDone;
+                        if (blockIdx.x == 0) A.cur[u] = kDone;
+                    } else {
+                        if (blockIdx.x == 0) {
+                            const uint64_t cb = A.cand_lo[u];
+                            A.out[cb + s_outn[threadIdx.x]] = f;
+                            A.out_live[cb + s_outn[threadIdx.x]] = A.live[cb + f];
+                            A.out_n[u] = s_outn[threadIdx.x] + 1;
+                            A.cur[u] = f;
+                            A.pos[u] = f + 1;
+                        }
+                        s_cur[threadIdx.x] = f;
+                        s_pos[threadIdx.x] = f + 1;
+                        s_outn[threadIdx.x] += 1;
+                    }
+                }
+            }
+            __syncthreads();
+            for (uint32_t q = 0; q < nt; ++q) active += s_cur[q] != kDone;
+        } else {
+            for (uint32_t tt = blockIdx.x; tt < nt; tt += gridDim.x) {
+                const uint32_t t = A.t0 + tt;
+                if (A.cur[t] == kDone) continue;
+                const uint64_t c0 = A.cand_lo[t], c1 = A.cand_lo[t + 1];
+                uint32_t found = kNone;
+                // 4 consecutive candidates per thread per step; one barrier per step until one is live
+                for (uint64_t k = c0 + A.pos[t]; k < c1; k += 4ull * blockDim.x) {
+                    uint32_t mine = kNone;
+#pragma unroll
+                    for (int j = 3; j >= 0; --j) {
+                        const uint64_t c = k + 4ull * threadIdx.x + j;
+                        if (c < c1 && (uint64_t)A.live[c] > A.T) mine = (uint32_t)(c - c0);
+                    }
+                    if (__syncthreads_or(mine != kNone)) {
+                        if (threadIdx.x == 0) s_found = kNone;
+                        __syncthreads();
+                        if (mine != kNone) atomicMin(&s_found, mine);
+                        __syncthreads();
+                        found = s_found;
+                        __syncthreads();
+                        break;
+                    }
+                }
+                if (threadIdx.x == 0) {
+                    if (found == kNone) {
+                        A.cur[t] = kDone;
+                    } else {
+                        const uint32_t e = A.out_n[t];
+                        A.out[c0 + e] = found;
+                        A.out_live[c0 + e] = A.live[c0 + found];
+                        A.out_n[t] = e + 1;
+                        A.cur[t] = found;
+                        A.pos[t] = found + 1;
+                        atomicAdd(A.active + (round & 1), 1u);
+                    }
                 }
             }
         }
-        if (gtid == 0) { A.active[(round + 1) & 1] = 0; *A.qn = 0; }
-        grid.sync();
-        if (A.active[round & 1] == 0) break;
-        // ---- B1: remove the live voters of every tree's emitted leaf
-        for (uint32_t tt = 0; tt < nt; ++tt) {
+        if (gtid == 0) { A.active[(round + 1) & 1] = 0; A.qn[(round + 1) & 1] = 0; }
+        if (RED) {
+            if (active == 0) break;                // identical in every block
+        } else {
+            grid.sync();
+            if (A.active[round & 1] == 0) break;
+        }
+        uint32_t* qn = A.qn + (round & 1);
+        uint32_t* queue = A.queue + (round & 1) * 2 * (uint64_t)A.queue_cap;
+        // ---- B1: remove the live voters of every tree's emitted leaf. RED (few trees): the grid
+        // strides over each tree's points; else block b takes trees b, b + grid, ...
+        for (uint32_t tt = RED ? 0 : blockIdx.x; tt < nt; tt += RED ? 1 : gridDim.x) {
             const uint32_t t = A.t0 + tt;
-            const uint32_t k = A.cur[t];
+            const uint32_t k = RED ? s_cur[tt] : A.cur[t];
             if (k == kDone) continue;
+            const uint32_t slot = (uint32_t)(A.cand_lo[t] + (RED ? s_outn[tt] : A.out_n[t]) - 1);   // global line slot
             const LeafRec L = A.leaves[A.cand_lo[t] + k];
             const bool beta = A.tree_beta[t] != 0;
             const uint32_t n = A.pt_n[t];
             const uint32_t* pts = A.packed + A.pt_off[t];
             uint8_t* rem = A.removed + A.rm_off[t];
             const I base = (N << D) - N3 * (I)L.j;
-            for (uint64_t p = gtid; p < n; p += gsize) {
+            const uint64_t p0 = RED ? gtid : threadIdx.x, ps = RED ? gsize : blockDim.x;
+            for (uint64_t p = p0; p < n; p += ps) {
                 if (rem[p]) continue;
                 const uint32_t pk = pts[p];
                 const I ex = (I)(beta ? (pk & 0xFFFFu) : (pk >> 16)), ey = (I)(beta ? (pk >> 16) : (pk & 0xFFFFu));
                 const I g = base + ((ex + ey) << D) - (I)2 * (I)L.i * ex;      // G(SW corner of leaf k)
                 if (g > 0 && g <= (I)2 * ex + N3) {
                     rem[p] = 1;
-                    const uint32_t q = atomicAdd(A.qn, 1u);
-                    A.queue[2 * (uint64_t)q] = t;
-                    A.queue[2 * (uint64_t)q + 1] = (uint32_t)p;
+                    const uint32_t q = atomicAdd(qn, 1u);
+                    queue[2 * (uint64_t)q] = t;
+                    queue[2 * (uint64_t)q + 1] = (uint32_t)p;
                     const unsigned long long sidx = atomicAdd(A.sup_n, 1ull);
-                    A.sup[2 * sidx] = (uint32_t)(A.cand_lo[t] + A.out_n[t] - 1);   // global line slot
+                    A.sup[2 * sidx] = slot;
                     A.sup[2 * sidx + 1] = (uint32_t)p;
                 }
             }
         }
         grid.sync();
-        // ---- B2: every queued point's line loses one live vote in every later candidate it crosses
-        const uint32_t nq = *A.qn;
-        const uint64_t warp = gtid >> 5, nwarp = gsize >> 5;
-        const uint32_t per = (side + 31) / 32;                 // columns per lane (contiguous)
-        for (uint64_t qi = warp; qi < nq; qi += nwarp) {
-            const uint32_t t = A.queue[2 * qi], p = A.queue[2 * qi + 1];
-            const uint32_t k = A.cur[t];
+        // ---- B2: every queued point's line loses one live vote in every later candidate it crosses;
+        // one thread per (queued point, run of kRmCols leaf columns): rows f_(i+1) .. f_i of column i,
+        // f_i = floor((G(i, 0) - 1) / 3N) with the remainder carried column to column (2ex < 3N: at
+        // most one borrow per column); all cell-map loads of a run are issued before its atomics
+        const uint32_t nq = *qn;
+        const uint32_t runs = (side + kRmCols - 1) / kRmCols;
+        const uint64_t work = (uint64_t)nq * runs;
+        for (uint64_t wi = gtid; wi < work; wi += gsize) {
+            const uint32_t qi = (uint32_t)(wi / runs), run = (uint32_t)(wi - (uint64_t)qi * runs);
+            const uint32_t t = queue[2 * (uint64_t)qi], p = queue[2 * (uint64_t)qi + 1];
+            const uint32_t k = RED ? s_cur[t - A.t0] : A.cur[t];
             const bool beta = A.tree_beta[t] != 0;
             const uint32_t pk = A.packed[A.pt_off[t] + p];
             const I ex = (I)(beta ? (pk & 0xFFFFu) : (pk >> 16)), ey = (I)(beta ? (pk >> 16) : (pk & 0xFFFFu));
-            const uint32_t i_lo = (uint32_t)lane * per;
-            if (i_lo >= side) continue;
-            const uint32_t i_hi = min(side, i_lo + per);
-            // y_i = G(i, 0) - 1 = 2^D (ex + ey + N) - 2 i ex - 1 >= 0 up to the column where the line
-            // leaves the root; f_i = floor(y_i / 3N) with the remainder carried column to column
-            // (2ex < 3N: at most one borrow per column)
-            I y = ((ex + ey + N) << D) - (I)2 * (I)i_lo * ex - 1;
+            const uint32_t i_lo = run * kRmCols;
+            I y = ((ex + ey + N) << D) - (I)2 * (I)i_lo * ex - 1;   // G(i_lo, 0) - 1
             I f, r;
             if (y >= 0) { f = y / N3; r = y - f * N3; }
             else { f = -((-y + N3 - 1) / N3); r = y - f * N3; }
             const uint32_t* cm = A.cellmap + ((uint64_t)(t - A.t0) << (2 * D));
             uint32_t* live = A.live + A.cand_lo[t];
-            for (uint32_t i = i_lo; i < i_hi; ++i) {
-                // f_(i+1): y decreases by 2ex
+            uint32_t c0[kRmCols], c1[kRmCols];
+#pragma unroll
+            for (int u = 0; u < kRmCols; ++u) {
                 I rn = r - (I)2 * ex, fn = f;
                 if (rn < 0) { rn += N3; fn -= 1; }
+                const uint32_t i = i_lo + u;
                 const I vlo = fn < 0 ? (I)0 : fn, vhi = f >= (I)side ? (I)side - 1 : f;
-                for (I v = vlo; v <= vhi; ++v) {
-                    const uint32_t c = __ldg(cm + ((uint64_t)i << D) + (uint64_t)v);
-                    if (c != kNone && c > k) atomicSub(live + c, 1u);
-                }
+                // rows vlo .. vhi hold 0, 1 or 2 cells (f drops by at most one per column)
+                const bool ok0 = i < side && vlo <= vhi, ok1 = ok0 && vhi > vlo;
+                const uint64_t col = (uint64_t)i << D;
+                c0[u] = ok0 ? __ldg(cm + col + (uint64_t)vlo) : kNone;
+                c1[u] = ok1 ? __ldg(cm + col + (uint64_t)vhi) : kNone;
                 f = fn;
                 r = rn;
+            }
+#pragma unroll
+            for (int u = 0; u < kRmCols; ++u) {
+                if (c0[u] != kNone && c0[u] > k) atomicSub(live + c0[u], 1u);
+                if (c1[u] != kNone && c1[u] > k) atomicSub(live + c1[u], 1u);
             }
         }
         grid.sync();
     }
 }
 
+// Compact the emitted lines into hht_leaf rows (image, half, i, j, live) in tree order and the
+// supports into (line index, point) pairs: slot k = cand_lo[t] + e is line line_base[t] + e.
+__device__ __forceinline__ uint32_t rm_tree_of(const uint64_t* cand_lo, uint32_t nt, uint64_t k) {
+    uint32_t lo = 0, hi = nt - 1;                 // last t with cand_lo[t] <= k
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) / 2;
+        if (cand_lo[mid] <= k) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) k_rm_rows(const LeafRec* __restrict__ leaves, const uint64_t* __restrict__ cand_lo,
+                                                 const uint32_t* __restrict__ out, const uint32_t* __restrict__ out_live,
+                                                 const uint32_t* __restrict__ out_n, const uint64_t* __restrict__ line_base,
+                                                 const uint8_t* __restrict__ tree_beta, uint32_t nt, uint32_t H,
+                                                 uint64_t ncand, uint32_t* __restrict__ rows,
+                                                 uint32_t* __restrict__ sup, uint64_t nsup) {
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, gs = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = g; k < ncand; k += gs) {
+        const uint32_t t = rm_tree_of(cand_lo, nt, k);
+        const uint64_t e = k - cand_lo[t];
+        if (e >= out_n[t]) continue;
+        const LeafRec L = leaves[cand_lo[t] + out[k]];
+        uint32_t* r = rows + 5 * (line_base[t] + e);
+        r[0] = t / H;
+        r[1] = tree_beta[t] ? 2u : 1u;
+        r[2] = L.i;
+        r[3] = L.j;
+        r[4] = out_live[k];
+    }
+    for (uint64_t s = g; s < nsup; s += gs) {
+        const uint32_t slot = sup[2 * s];
+        const uint32_t t = rm_tree_of(cand_lo, nt, slot);
+        sup[2 * s] = (uint32_t)(line_base[t] + (slot - cand_lo[t]));
+    }
+}
+
+cudaError_t launch_rm_rows(const LeafRec* leaves, const uint64_t* cand_lo, const uint32_t* out, const uint32_t* out_live,
+                           const uint32_t* out_n, const uint64_t* line_base, const uint8_t* tree_beta, uint32_t nt,
+                           uint32_t H, uint64_t ncand, uint32_t* rows, uint32_t* sup, uint64_t nsup, cudaStream_t st) {
+    k_rm_rows<<<148 * 8, 256, 0, st>>>(leaves, cand_lo, out, out_live, out_n, line_base, tree_beta, nt, H, ncand, rows,
+                                       sup, nsup);
+    return cudaGetLastError();
+}
+
 int rm_blocks_per_sm(bool int64) {
-    int n = 0;
-    if (int64) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_rm<int64_t>, kRmThreads, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_rm<int32_t>, kRmThreads, 0);
+    int n = 0, m = 0;
+    if (int64) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_rm<int64_t, false>, kRmThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k_rm<int64_t, true>, kRmThreads, 0);
+    } else {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_rm<int32_t, false>, kRmThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k_rm<int32_t, true>, kRmThreads, 0);
+    }
+    n = std::min(n, m);
     return n > 0 ? n : 1;
 }
 
@@ -1497,8 +1633,10 @@ cudaError_t launch_removal(const RmArgs& a, const LeafRec* leaves, bool int64, i
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     void* args[] = {(void*)&a};
-    return cudaLaunchCooperativeKernel(int64 ? (const void*)k_rm<int64_t> : (const void*)k_rm<int32_t>,
-                                       dim3(grid), dim3(kRmThreads), args, 0, st);
+    const bool red = a.t1 - a.t0 <= (uint32_t)kRmRedTrees;
+    const void* fn = int64 ? (red ? (const void*)k_rm<int64_t, true> : (const void*)k_rm<int64_t, false>)
+                           : (red ? (const void*)k_rm<int32_t, true> : (const void*)k_rm<int32_t, false>);
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kRmThreads), args, 0, st);
 }
 
 // ---------------------------------------------------------------------------------------------
