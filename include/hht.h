@@ -81,10 +81,13 @@ typedef struct {
                                 only, 2 = also its list entries (more registers); identical results */
     uint32_t latency_path;   /* 0 = auto: a small detection (one rank, exact test; bound on the
                                 lists: sum over trees of points x (2^depth - 1) entries) runs as ONE
-                                kernel launch of one block (k_small): all arrays in shared memory
-                                when they fit 220 KiB, else (bound <= 2^16 entries) the two lists
-                                in device memory and the frontier arrays in shared memory;
-                                1 = same; 2 = never (always the multi-kernel path) */
+                                kernel launch: of one block (k_small) when all arrays fit 220 KiB of
+                                shared memory, or (bound <= 2^16 entries) with the two lists in
+                                device memory; else, for bounds up to 2^26 entries, as one
+                                cooperative launch over the whole GPU (k_mid, stats.latency_path 2);
+                                larger detections take the multi-kernel path. 1 = same as 0;
+                                2 = never (always the multi-kernel path); 3 = k_mid whenever its
+                                bounds admit the detection. Results are identical. */
     uint32_t variant;        /* membership test: HHT_EXACT (0, default) = the paper's 4-bit corner
                                 code; HHT_FHT_CIRCLE (1) = the FHT comparison: the line meets the
                                 region's circumscribing circle (exact integers, see
@@ -143,7 +146,8 @@ typedef struct {
     uint32_t images;
     double ms;               /* device time of the call (CUDA events on the ctx stream) */
     uint64_t leaves_streamed;   /* leaf rows written to the leaf sink (hht_set_leaf_sink) */
-    uint32_t latency_path;      /* 1 if the detection ran on the one-launch latency path */
+    uint32_t latency_path;      /* 1: one-block latency path (k_small); 2: one cooperative launch
+                                   (k_mid); 0: multi-kernel path */
     uint32_t reserved;
 } hht_stats;
 

@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhht.so")
-SOURCES = ["hht_kernels.cu", "hht_driver.cu"]
+SOURCES = ["hht_kernels.cu", "hht_mid.cu", "hht_driver.cu"]
 HEADERS = ["hht_internal.h", os.path.join(ROOT, "include", "hht.h")]
 
 

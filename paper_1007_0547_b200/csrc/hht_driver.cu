@@ -133,6 +133,7 @@ struct hht_ctx {
     std::vector<std::pair<uint64_t, uint32_t>> lines_sup;   // (line index, point index in its tree)
     bool lines_sup_sorted = false;
     int rm_grid[2] = {0, 0};             // co-resident k_rm blocks (cooperative launch)
+    int mid_grid[2] = {0, 0};            // co-resident k_mid blocks (cooperative launch)
     int64_t edge_na = 0, edge_nb = 0;
     // leaf sink (hht_set_leaf_sink): double-buffered row staging, copied on its own stream
     hht_leaf* sink = nullptr;
@@ -147,6 +148,11 @@ struct hht_ctx {
     Totals* totals_h = nullptr;
     RangeInfo* range_h = nullptr;
     uint64_t* misc_h = nullptr;
+    bool errflag_dirty = true;              // errflag may be non-zero (see detect_impl)
+    uint32_t* fin_h = nullptr;              // k_finish's mapped host block (one-launch paths)
+    uint32_t* fin_m = nullptr;
+    uint8_t* pin = nullptr;                 // pinned staging for small host<->device copies of one call
+    size_t pin_used = 0;
     Totals* totals_m = nullptr;      // device-side pointers of the same memory
     RangeInfo* range_m = nullptr;
     uint64_t* misc_m = nullptr;
@@ -341,6 +347,26 @@ T read_mapped(const T* p) {
     T t;
     memcpy(&t, (const void*)p, sizeof t);
     return t;
+}
+
+// Small copies of one call go through the ctx's pinned staging area (async DMA; a pageable copy costs
+// a host bounce and ~10 us each); the area is reused from the start by the next call, which is safe
+// because every call synchronises its stream before returning.
+constexpr size_t kPinBytes = 256 * 1024;
+void* pin_take(hht_ctx* x, size_t bytes) {
+    const size_t off = (x->pin_used + 15) & ~(size_t)15;
+    if (!x->pin || off + bytes > kPinBytes) return nullptr;
+    x->pin_used = off + bytes;
+    return x->pin + off;
+}
+hht_status h2d_small(hht_ctx* x, void* dst, const void* src, size_t bytes) {
+    void* p = pin_take(x, bytes);
+    if (p) {
+        memcpy(p, src, bytes);
+        src = p;
+    }
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, x->st));
+    return HHT_OK;
 }
 
 // Leaf sink: rows of leaves [first, first + n) -> host, overlapped with the traversal.
@@ -814,14 +840,98 @@ void small_bounds(const hht_ctx* x, uint64_t& S, uint64_t& F) {
 // 0: multi-kernel path; 1: latency path with shared-memory scratch; 2: latency path with the two
 // candidate lists in device (L2-resident) memory and the frontier arrays in shared memory, for lists
 // up to kSmallGlobalMaxS entries (profiles/r01_latency.md)
+hht_status finish_small(hht_ctx* x, const uint32_t* d_counts, int id, uint32_t path);
+
+// 3: the mid-size latency path (k_mid, hht_mid.cu): one cooperative launch over the GPU, lists and
+// frontier in device memory, for lists up to kMidMaxS entries (opts.latency_path 3 forces it when the
+// bounds admit it).
 int small_mode(const hht_ctx* x) {
     if (x->opts.latency_path == 2 || multi(x) || x->circle || x->D > 24 || x->ntrees > 4096) return 0;
     uint64_t S, F;
     small_bounds(x, S, F);
     if (S >= (1ull << 32)) return 0;
     const uint32_t Fc = (uint32_t)std::min<uint64_t>(F, S + 1);
+    const bool mid_ok = S <= kMidMaxS && (uint64_t)Fc + 1 <= (uint64_t)kMidMaxTiles * kMidThreads;
+    if (x->opts.latency_path == 3) return mid_ok ? 3 : 0;
     if (small_smem_bytes((uint32_t)S, Fc) <= kSmallSmemMax) return 1;
-    return (S <= kSmallGlobalMaxS && small_frontier_bytes(Fc) <= kSmallSmemMax) ? 2 : 0;
+    if (S <= kSmallGlobalMaxS && small_frontier_bytes(Fc) <= kSmallSmemMax) return 2;
+    return mid_ok ? 3 : 0;
+}
+
+hht_status detect_mid(hht_ctx* x) {
+    const int D = x->D;
+    const uint32_t nt = (uint32_t)x->ntrees;
+    uint64_t n = 0;
+    for (uint32_t t = 0; t < nt; ++t) n += x->tree_pt_n[t];
+    uint64_t Smax, Fmax;
+    small_bounds(x, Smax, Fmax);
+    Fmax = std::min<uint64_t>(Fmax, Smax + 1) + 1;
+    const uint64_t tiles = (Fmax + kMidThreads - 1) / kMidThreads;
+    // host-written block: tree offsets and counts, per-level counts, control words, record pointers
+    const uint64_t words = 3ull * nt + (D + 2) + 8 + 2ull * (D + 1) + 16;
+    TRY(ensure(x, x->small, words * 4));
+    uint32_t* w = (uint32_t*)x->small.p;
+    MidArgs a{};
+    uint64_t* d_off = (uint64_t*)w; w += 2ull * nt;
+    uint32_t* d_n = w; w += nt;
+    a.counts = w; w += D + 2;
+    a.ctl = w; w += 8;
+    w = (uint32_t*)(((uintptr_t)w + 7) & ~(uintptr_t)7);
+    Record** d_rec = (Record**)w;
+    std::vector<Record*> h_rec(D + 1);
+    for (int l = 0; l <= D; ++l) {
+        const uint64_t cap = l == 0 ? nt : 4 * Fmax;
+        TRY(grow(x, x->rec[l], sizeof(Record), cap));
+        h_rec[l] = (Record*)x->rec[l].b.p;
+    }
+    TRY(grow(x, x->leaves, sizeof(LeafRec), 4 * Fmax));
+    // device scratch: 2 lists (Smax) + 2 x 6 frontier arrays (Fmax + 1) + 2 x cv (4 Fmax) + cursor,
+    // loff, lcoff (4 Fmax) + app (Fmax) + tiles (3 tiles)
+    const uint64_t F1 = Fmax + 1;
+    const uint64_t Cmax = Smax / kChunk + Fmax + 1;       // chunks of one level: sum ceil(len / 256)
+    auto up4 = [](uint64_t w) { return (w + 3) & ~3ull; };   // every array 16-byte aligned (vector access)
+    const uint64_t swords = 2 * (8 * F1 + up4(4 * Fmax)) + 2 * up4(Smax) + 2 * up4(Cmax) + 3 * up4(4 * Fmax) +
+                            up4(Fmax) + up4(3 * tiles) + 64;
+    TRY(ensure(x, x->small_g, swords * 4));
+    uint32_t* g = (uint32_t*)x->small_g.p;               // 256-byte aligned
+    for (int b = 0; b < 2; ++b) {
+        a.fd[b] = (uint4*)g; g += 8 * F1;
+        a.cv[b] = g; g += up4(4 * Fmax);
+    }
+    a.list[0] = g; g += up4(Smax);
+    a.list[1] = g; g += up4(Smax);
+    for (int b = 0; b < 2; ++b) {
+        a.chunkmap[b] = g; g += up4(Cmax);
+    }
+    a.cursor = g; g += up4(4 * Fmax);
+    a.loff = g; g += up4(4 * Fmax);
+    a.lcoff = g; g += up4(4 * Fmax);
+    a.app = g; g += up4(Fmax);
+    a.tiles = g;
+    {
+        std::vector<uint32_t> h(words, 0);
+        memcpy(h.data(), x->tree_pt_off.data(), 8ull * nt);
+        memcpy(h.data() + 2ull * nt, x->tree_pt_n.data(), 4ull * nt);
+        memcpy((char*)h.data() + ((char*)d_rec - (char*)x->small.p), h_rec.data(), sizeof(Record*) * (D + 1));
+        TRY(h2d_small(x, x->small.p, h.data(), words * 4));
+    }
+    a.packed = (const uint32_t*)x->packed.p;
+    a.tree_off = d_off;
+    a.tree_n = d_n;
+    a.tree_beta = (const uint8_t*)x->beta.p;
+    a.ntrees = nt;
+    a.N = x->N;
+    a.D = D;
+    a.T = x->T;
+    a.record = x->opts.record_levels ? 1u : 0u;
+    a.rec = d_rec;
+    a.leaves = (LeafRec*)x->leaves.b.p;
+    a.stats = (unsigned long long*)x->stats.p;
+    if (!x->mid_grid[x->int64 ? 1 : 0]) x->mid_grid[x->int64 ? 1 : 0] = x->sms * mid_blocks_per_sm(x->int64);
+    const int id = prof_begin(x, 1, n * 4 * (uint64_t)(D + 1));
+    CK(launch_mid(a, x->int64, x->mid_grid[x->int64 ? 1 : 0], x->st));
+    prof_end(x, id);
+    return finish_small(x, a.counts, id, 2);
 }
 
 hht_status detect_small(hht_ctx* x) {
@@ -864,7 +974,7 @@ hht_status detect_small(hht_ctx* x) {
         memcpy(h.data(), x->tree_pt_off.data(), 8ull * nt);
         memcpy(h.data() + 2ull * nt, x->tree_pt_n.data(), 4ull * nt);
         memcpy((char*)h.data() + ((char*)d_rec - (char*)x->small.p), h_rec.data(), sizeof(Record*) * (D + 1));
-        CK(cudaMemcpyAsync(x->small.p, h.data(), words * 4, cudaMemcpyHostToDevice, x->st));
+        TRY(h2d_small(x, x->small.p, h.data(), words * 4));
     }
     a.packed = (const uint32_t*)x->packed.p;
     a.tree_off = d_off;
@@ -880,14 +990,22 @@ hht_status detect_small(hht_ctx* x) {
     const int id = prof_begin(x, 1, n * 4 * (uint64_t)(D + 1));
     CK(launch_small(a, x->int64, x->st));
     prof_end(x, id);
-    std::vector<uint32_t> counts(D + 2);
-    uint64_t st[kStatCount];
-    CK(cudaMemcpyAsync(counts.data(), a.counts, 4ull * (D + 2), cudaMemcpyDeviceToHost, x->st));
-    CK(cudaMemcpyAsync(st, x->stats.p, sizeof st, cudaMemcpyDeviceToHost, x->st));
-    CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)x->errflag.p, 1, x->st));
+    return finish_small(x, a.counts, id, 1);
+}
+
+// Results of a one-launch traversal (k_small, k_mid): per-level record counts, leaves and statistics
+// in one synchronisation, with the range check of the staged points.
+hht_status finish_small(hht_ctx* x, const uint32_t* d_counts, int id, uint32_t path) {
+    const int D = x->D;
+    CK(launch_finish(x->fin_m, d_counts, (uint32_t)(D + 2), (const unsigned long long*)x->stats.p,
+                     (uint32_t*)x->errflag.p, x->st));
     CK(cudaEventRecord(x->ev1, x->st));
     TRY(sync(x));
-    if ((uint32_t)read_mapped(x->misc_h)) return set_err(x, HHT_ERANGE, "a point lies outside [0, N)^2");
+    x->errflag_dirty = false;
+    std::atomic_thread_fence(std::memory_order_acquire);
+    const uint32_t* counts = x->fin_h + 1;
+    const uint64_t* st = (const uint64_t*)(x->fin_h + kFinishStatsWord);
+    if (x->fin_h[0]) return set_err(x, HHT_ERANGE, "a point lies outside [0, N)^2");
     for (int l = 0; l <= D; ++l) x->rec[l].n = x->opts.record_levels ? counts[l] : 0;
     x->leaves.n = counts[D + 1];
     x->stat.tests = st[kStatTests];
@@ -897,7 +1015,7 @@ hht_status detect_small(hht_ctx* x) {
         x->stat.visited[l] = st[kStatVisited0 + l];
         x->stat.split[l] = st[kStatSplit0 + l];
     }
-    x->stat.latency_path = 1;
+    x->stat.latency_path = path;
     TRY(stream_leaves(x, 0, x->leaves.n));
     if (x->sink) {
         CK(cudaStreamSynchronize(x->cst));
@@ -923,6 +1041,7 @@ hht_status detect_small(hht_ctx* x) {
 
 hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets, int32_t B, int32_t N,
                        int32_t D, int64_t T, const int64_t* tree_offsets = nullptr, bool prepacked = false) {
+    x->pin_used = 0;                  // the previous call synchronised: its staging is free
     // offsets: per image [B+1] (every point enters each of the image's trees); tree_offsets: per
     // tree [B*H+1] (tree t = image t/H, halves in ALPHA, BETA order; each point in one tree)
     if (!x) return HHT_EINVAL;
@@ -1017,7 +1136,10 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     } else {
         TRY(ensure(x, x->packed, std::max<int64_t>(n, 1) * 4));
     }
-    CK(cudaMemsetAsync(x->errflag.p, 0, 4, x->st));
+    // errflag is 0 on entry: zeroed at create, re-armed by k_finish (one-launch paths) and after the
+    // multi-kernel path's range check; a call that failed in between leaves it dirty
+    if (x->errflag_dirty) CK(cudaMemsetAsync(x->errflag.p, 0, 4, x->st));
+    x->errflag_dirty = true;
     if (n > 0 && !prepacked) {   // prepacked: x->packed already holds in-range points (edge front end)
         const int32_t* dev_pts = points;
         cudaPointerAttributes pa{};
@@ -1036,17 +1158,19 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     }
     if (small_mode(x)) {
         // latency path: no synchronisation before the traversal; the range check is read with the
-        // results (an out-of-range point still fails the call with HHT_ERANGE, nothing is returned)
-        CK(cudaMemsetAsync(x->stats.p, 0, kStatCount * 8, x->st));
+        // results (an out-of-range point still fails the call with HHT_ERANGE, nothing is returned);
+        // the kernels zero the statistics themselves
         std::vector<uint8_t> beta(x->ntrees);
         for (int t = 0; t < x->ntrees; ++t) beta[t] = x->tree_half[t] == HHT_BETA;
         TRY(ensure(x, x->beta, x->ntrees));
-        CK(cudaMemcpyAsync(x->beta.p, beta.data(), x->ntrees, cudaMemcpyHostToDevice, x->st));
-        return detect_small(x);
+        TRY(h2d_small(x, x->beta.p, beta.data(), x->ntrees));
+        return small_mode(x) == 3 ? detect_mid(x) : detect_small(x);
     }
     TRY(coll_allreduce(x, x->errflag.p, x->errflag.p, 1, C_U32, C_MAX));
     CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)x->errflag.p, 1, x->st));
+    CK(cudaMemsetAsync(x->errflag.p, 0, 4, x->st));        // re-armed for the next call
     TRY(sync(x));
+    x->errflag_dirty = false;
     if ((uint32_t)read_mapped(x->misc_h)) return set_err(x, HHT_ERANGE, "a point lies outside [0, N)^2");
 
     // stats accumulators
@@ -1314,11 +1438,14 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
         return fail(HHT_ENOMEM);
     if (cudaMallocHost((void**)&x->totals_h, sizeof(Totals)) != cudaSuccess ||
         cudaMallocHost((void**)&x->range_h, sizeof(RangeInfo)) != cudaSuccess ||
-        cudaMallocHost((void**)&x->misc_h, 64) != cudaSuccess)
+        cudaMallocHost((void**)&x->misc_h, 64) != cudaSuccess ||
+        cudaMallocHost((void**)&x->pin, kPinBytes) != cudaSuccess ||
+        cudaMallocHost((void**)&x->fin_h, kFinishBytes) != cudaSuccess)
         return fail(HHT_ECUDA);
     if (cudaHostGetDevicePointer((void**)&x->totals_m, x->totals_h, 0) != cudaSuccess ||
         cudaHostGetDevicePointer((void**)&x->range_m, x->range_h, 0) != cudaSuccess ||
-        cudaHostGetDevicePointer((void**)&x->misc_m, x->misc_h, 0) != cudaSuccess)
+        cudaHostGetDevicePointer((void**)&x->misc_m, x->misc_h, 0) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&x->fin_m, x->fin_h, 0) != cudaSuccess)
         return fail(HHT_ECUDA);
     x->group = o.group;
     if (o.nccl_comm) {   // the caller's communicator (borrowed)
@@ -1754,6 +1881,8 @@ void hht_destroy(hht_ctx* x) {
     if (x->totals_h) cudaFreeHost(x->totals_h);
     if (x->range_h) cudaFreeHost(x->range_h);
     if (x->misc_h) cudaFreeHost(x->misc_h);
+    if (x->pin) cudaFreeHost(x->pin);
+    if (x->fin_h) cudaFreeHost(x->fin_h);
     for (auto& e : x->pev) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);

@@ -63,6 +63,12 @@ struct Totals {          // written by the last split tile
 // Device-side stats accumulators (uint64): see kStat*.
 enum { kStatTests = 0, kStatVotes = 1, kStatLeaves = 2, kStatSplit0 = 8, kStatVisited0 = 8 + 64,
        kStatCount = 8 + 128 };
+// k_finish's mapped host block: word 0 the range flag, words 1.. the per-level counts (<= 64 + 2),
+// from word kFinishStatsWord the statistics (kStatCount u64)
+constexpr uint32_t kFinishStatsWord = 128;
+constexpr size_t kFinishBytes = kFinishStatsWord * 4 + kStatCount * 8;
+cudaError_t launch_finish(uint32_t* host, const uint32_t* counts, uint32_t ncounts, const unsigned long long* stats,
+                          uint32_t* errflag, cudaStream_t st);
 
 enum PassMode { MODE_COUNT = 0, MODE_WRITE = 1, MODE_COUNT2 = 2, MODE_WRITE_NC = 3 };   // NC: no count-ahead
 
@@ -259,6 +265,39 @@ uint64_t small_frontier_bytes(uint32_t F);
 constexpr uint64_t kSmallSmemMax = 220 * 1024;
 constexpr uint64_t kSmallGlobalMaxS = 1ull << 16;   // device-list latency path: list bound (entries)
 cudaError_t launch_small(const SmallArgs& a, bool int64, cudaStream_t st);
+// Mid-size latency path (hht_mid.cu): the whole traversal as one cooperative kernel over the GPU.
+constexpr int kMidThreads = 256;
+constexpr int kMidMinBlocks = 3;
+constexpr uint32_t kMidMaxTiles = 3072;        // tiles of kMidThreads children per level (S2 prefixes)
+constexpr uint64_t kMidMaxS = 1ull << 26;      // list bound (entries per level) admitted
+struct MidArgs {
+    const uint32_t* packed;        // staged points (level-0 lists)
+    const uint64_t* tree_off;      // [ntrees] first point of each tree in `packed`
+    const uint32_t* tree_n;        // [ntrees]
+    const uint8_t* tree_beta;
+    uint32_t ntrees;
+    int N, D;
+    uint64_t T;
+    uint32_t record;
+    // scratch, double-buffered by level parity (capacities from the host's bounds)
+    uint32_t* list[2];             // candidate lists (list[0] unused at level 0: the roots read `packed`)
+    uint4* fd[2];                  // [2 F] region descriptors (tree | beta << 31, a, c, start), (len, coff)
+    uint32_t* chunkmap[2];         // [chunks] chunk -> region (no search per work unit)
+    uint32_t* cv[2];               // [4 F] votes of the frontier's children
+    uint32_t* cursor;              // [4 F] child -> next-frontier index (tile-local flag scan in S1)
+    uint32_t* loff;                // [4 F] tile-local list offsets
+    uint32_t* lcoff;               // [4 F] tile-local chunk offsets
+    uint32_t* app;                 // [F] append cursors of the next lists
+    uint32_t* tiles;               // [3 x tiles] tile totals (split count, entries, chunks)
+    uint32_t* ctl;                 // [8] per buffer: F, chunks, entries
+    // outputs (as SmallArgs)
+    Record* const* rec;
+    LeafRec* leaves;
+    unsigned long long* stats;
+    uint32_t* counts;              // [D + 2] records per level, then leaves
+};
+int mid_blocks_per_sm(bool int64);
+cudaError_t launch_mid(const MidArgs& a, bool int64, int grid, cudaStream_t st);
 cudaError_t launch_fused(bool int64, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint32_t* len, uint32_t r0, uint32_t r1,
                           int is_root, RangeInfo* info, uint64_t* chunk_bounds, RangeInfo* info_h, cudaStream_t st);

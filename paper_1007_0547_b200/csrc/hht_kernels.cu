@@ -1714,6 +1714,8 @@ __global__ void __launch_bounds__(1024) k_small(SmallArgs A) {
     const I N = (I)A.N;
     const int D = A.D;
     unsigned long long tests = 0, votes = 0;          // thread 0 accumulates
+    for (int i = tid; i < kStatCount; i += blockDim.x) A.stats[i] = 0;   // the call's statistics start at 0
+    __syncthreads();
     // level 0: roots (every line crosses the root); split iff E > T (reading R6)
     if (tid == 0) {
         uint32_t F = 0, S = 0;
@@ -2010,6 +2012,25 @@ cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint
 // the copy engines, e.g. the leaf-sink transfers).
 __global__ void k_copy_u32(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint32_t n) {
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+// End of a one-launch traversal: the range flag, the per-level counts and the statistics into mapped
+// host memory (no device-to-host copies), and the flag re-armed for the next call.
+__global__ void k_finish(uint32_t* __restrict__ host, const uint32_t* __restrict__ counts, uint32_t ncounts,
+                         const unsigned long long* __restrict__ stats, uint32_t* __restrict__ errflag) {
+    if (threadIdx.x == 0) {
+        host[0] = *errflag;
+        *errflag = 0;
+    }
+    for (uint32_t i = threadIdx.x; i < ncounts; i += blockDim.x) host[1 + i] = counts[i];
+    unsigned long long* hs = reinterpret_cast<unsigned long long*>(host + kFinishStatsWord);
+    for (uint32_t i = threadIdx.x; i < kStatCount; i += blockDim.x) hs[i] = stats[i];
+}
+
+cudaError_t launch_finish(uint32_t* host, const uint32_t* counts, uint32_t ncounts, const unsigned long long* stats,
+                          uint32_t* errflag, cudaStream_t st) {
+    k_finish<<<1, 256, 0, st>>>(host, counts, ncounts, stats, errflag);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_copy_u32(uint32_t* dst, const uint32_t* src, uint32_t n, cudaStream_t st) {

@@ -2,7 +2,7 @@
 results on the device) and its device time, for the one-launch latency path and the multi-kernel
 path, on config 1 and the paper-scale scenes (32-256 px). Median of --reps calls after warm-up.
 
-    python scripts/latency_bench.py --out profiles/r01_latency.md
+    python scripts/latency_bench.py --out profiles/r02_latency.md
 """
 import argparse
 import os
@@ -17,7 +17,7 @@ from paper_1007_0547_b200 import hht, synth  # noqa: E402
 
 
 def measure(pts, N, D, T, halves, latency_path, reps):
-    h = hht.HHT(halves=halves, latency_path=latency_path)
+    h = hht.HHT(halves=halves, latency_path=latency_path, profile=True)
     d = torch.from_numpy(pts).cuda()
     for _ in range(5):
         h.detect(d, N, D, T)
@@ -27,7 +27,8 @@ def measure(pts, N, D, T, halves, latency_path, reps):
         h.detect(d, N, D, T)
         wall.append(1e3 * (time.perf_counter() - t0))
         dev.append(h.stats()["ms"])
-    return statistics.median(wall), statistics.median(dev), h.stats()["leaves"], h.stats()["latency_path"]
+    kern = sum(v["ms"] for v in h.profile().values())
+    return statistics.median(wall), statistics.median(dev), h.stats()["leaves"], h.stats()["latency_path"], kern
 
 
 def main():
@@ -39,25 +40,32 @@ def main():
     cfg = synth.CONFIGS[1]
     pts, _ = synth.config_image(1)
     cases.append(("config1 64x64, 220 pts, D=6, T=20, ALPHA", pts, cfg.N, cfg.D, cfg.T, cfg.halves))
+    cfg2 = synth.CONFIGS[2]
+    p2, _ = synth.config_image(2)
     for N in (32, 64, 128, 256):
         p, _ = synth.scene(N, 5, max(4, N // 2 + N // 8), 1, max(1, N * N // 50), False, 0x7AB1E1, 100 * N + 1, 7)
         cases.append((f"{N}x{N} scene, {p.shape[0]} pts, D={N.bit_length() - 1}, T={N // 2}, both", p, N,
                       N.bit_length() - 1, N // 2, hht.ALPHA | hht.BETA))
+    cases.append(("config2 512x512, 17107 pts, D=9, T=50, both", p2, cfg2.N, cfg2.D, cfg2.T, cfg2.halves))
     rows = []
+    names = {0: "multi-kernel", 1: "k_small", 2: "k_mid"}
     for name, p, N, D, T, halves in cases:
-        lw, ld, nl, used = measure(p, N, D, T, halves, 1, a.reps)
-        mw, md, _, _ = measure(p, N, D, T, halves, 2, a.reps)
-        rows.append((name + ("" if used else " (not admitted: multi-kernel)"), nl, lw, ld, mw, md))
+        lw, ld, nl, used, lk = measure(p, N, D, T, halves, 1, a.reps)
+        mw, md, _, _, mk = measure(p, N, D, T, halves, 2, a.reps)
+        rows.append((name, names[used], nl, lw, ld, lk, mw, md, mk))
         print(rows[-1], flush=True)
     lines = ["# Single-image latency on one B200", "",
              f"Median of {a.reps} hht_detect calls (points already on the device, results left on the device): "
-             "wall time of the call and its device time (CUDA events), one-launch latency path (k_small) "
-             "vs the multi-kernel path. The paper's Table 1 reports 31-484 us per image for its algorithm "
-             "on a 3 GHz Pentium IV at 32-256 px (its images, PAPER.md:274-292).", "",
-             "| input | leaves | auto path wall us | device us | multi-kernel wall us | device us |",
-             "|---|---|---|---|---|---|"]
-    for name, nl, lw, ld, mw, md in rows:
-        lines.append(f"| {name} | {nl} | {1e3 * lw:.0f} | {1e3 * ld:.0f} | {1e3 * mw:.0f} | {1e3 * md:.0f} |")
+             "wall time of the call, its device time (CUDA events from staging to results) and the time of its "
+             "kernels alone (events around each launch, last call), on the automatic path (the one-block "
+             "k_small, the one-launch cooperative k_mid, or the multi-kernel path) vs the multi-kernel path. "
+             "The paper's Table 1 reports 31-484 us per image for its algorithm on a 3 GHz Pentium IV at "
+             "32-256 px (its images, PAPER.md:274-292).", "",
+             "| input | auto path | leaves | auto wall us | device us | kernels us | multi-kernel wall us | device us | kernels us |",
+             "|---|---|---|---|---|---|---|---|---|"]
+    for name, path, nl, lw, ld, lk, mw, md, mk in rows:
+        lines.append(f"| {name} | {path} | {nl} | {1e3 * lw:.0f} | {1e3 * ld:.0f} | {1e3 * lk:.0f} | {1e3 * mw:.0f} | "
+                     f"{1e3 * md:.0f} | {1e3 * mk:.0f} |")
     txt = "\n".join(lines) + "\n"
     print(txt)
     if a.out:

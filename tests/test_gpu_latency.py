@@ -14,13 +14,16 @@ AB = hht.ALPHA | hht.BETA
 
 
 def eligible(n_per_tree, D, T):
-    """Mirror of the library's admission rule (hht_driver.cu small_bounds / small_mode): everything in
-    shared memory when it fits 220 KiB; else lists in device memory (up to 2^16 entries) with the
-    frontier arrays in shared memory."""
+    """Mirror of the library's admission rule (hht_driver.cu small_bounds / small_mode): 1 = k_small
+    (everything in shared memory when it fits 220 KiB; else lists in device memory up to 2^16 entries
+    with the frontier arrays in shared memory); 2 = k_mid (one cooperative launch, lists up to 2^26
+    entries per level); 0 = the multi-kernel path."""
     S = max(sum(n_per_tree) * ((1 << D) - 1), 1)
     F = min(S // (T + 1) + len(n_per_tree) + 1, S + 1)
-    return (4 * (2 * S + 8 * (F + 1) + 8 * F) <= 220 * 1024
-            or (S <= (1 << 16) and 4 * (8 * (F + 1) + 8 * F) <= 220 * 1024))
+    if (4 * (2 * S + 8 * (F + 1) + 8 * F) <= 220 * 1024
+            or (S <= (1 << 16) and 4 * (8 * (F + 1) + 8 * F) <= 220 * 1024)):
+        return 1
+    return 2 if (S <= (1 << 26) and F + 1 <= 3072 * 256 and D <= 24) else 0
 
 
 def _dev(pts, dev):
@@ -41,7 +44,7 @@ def test_latency_path_random(seed, cuda_device):
     h.detect(_dev(pts, cuda_device), N, D, T)
     st = h.stats()
     ntrees = bin(halves).count("1")
-    assert st["latency_path"] == (1 if eligible([len(pts)] * ntrees, D, T) else 0)
+    assert st["latency_path"] == eligible([len(pts)] * ntrees, D, T)
     compare_all(h, ref, halves, D)
     assert (st["tests"], st["votes"], st["leaves"]) == (ref.tests, ref.votes, ref.leaves.shape[0])
     hm = hht.HHT(halves=halves, latency_path=2)
@@ -111,3 +114,56 @@ def test_latency_path_device_scratch(size, seed, cuda_device):
     assert st["latency_path"] == 1, S
     compare_all(h, ref, AB, D)
     assert (st["tests"], st["votes"], st["leaves"]) == (ref.tests, ref.votes, ref.leaves.shape[0])
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_mid_path_random(seed, cuda_device):
+    """k_mid (opts.latency_path = 3 forces it): records, leaves and statistics bit-exact against the
+    oracle, and visited/split counts equal to the multi-kernel path's."""
+    rng = np.random.default_rng(3100 + seed)
+    N = int(rng.choice([4, 16, 33, 64, 128, 256, 512]))
+    D = int(rng.integers(1, 10))
+    T = int(rng.choice([1, 2, 5, 20, 60]))
+    halves = [AB, hht.ALPHA, hht.BETA][seed % 3]
+    pts = synth.random_scene(3200 + seed, N, max_lines=5, max_noise=int(rng.choice([10, 300, 3000])))
+    ref = oracle.detect(pts, N, D, T, halves)
+    h = hht.HHT(halves=halves, latency_path=3, force_int64=bool(seed % 4 == 1))
+    h.detect(_dev(pts, cuda_device), N, D, T)
+    st = h.stats()
+    assert st["latency_path"] == 2
+    compare_all(h, ref, halves, D)
+    assert (st["tests"], st["votes"], st["leaves"]) == (ref.tests, ref.votes, ref.leaves.shape[0])
+    hm = hht.HHT(halves=halves, latency_path=2)
+    hm.detect(_dev(pts, cuda_device), N, D, T)
+    sm = hm.stats()
+    assert (sm["visited"], sm["split"]) == (st["visited"], st["split"])
+
+
+def test_mid_path_config2_and_batch(cuda_device):
+    """Config 2 runs on k_mid by default (bounds admit it) and equals the oracle in full; a ragged
+    batch with an empty image too."""
+    cfg = synth.CONFIGS[2]
+    pts, _ = synth.config_image(2)
+    h = hht.HHT(halves=cfg.halves)
+    h.detect(_dev(pts, cuda_device), cfg.N, cfg.D, cfg.T)
+    assert h.stats()["latency_path"] == 2
+    ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves)
+    compare_all(h, ref, cfg.halves, cfg.D)
+    st = h.stats()
+    assert (st["tests"], st["votes"], st["leaves"]) == (ref.tests, ref.votes, ref.leaves.shape[0])
+    imgs = [synth.random_scene(3300 + k, 128, max_lines=3, max_noise=k * 400) for k in range(4)]
+    imgs[1] = imgs[1][:0]
+    offs = np.zeros(5, dtype=np.int64)
+    offs[1:] = np.cumsum([len(p) for p in imgs])
+    hb = hht.HHT(halves=AB, latency_path=3)
+    hb.detect_batch(_dev(np.concatenate(imgs), cuda_device), offs, 128, 7, 6)
+    assert hb.stats()["latency_path"] == 2
+    for b, p in enumerate(imgs):
+        compare_all(hb, oracle.detect(p, 128, 7, 6, AB), AB, 7, image=b)
+
+
+def test_mid_path_range_error(cuda_device):
+    h = hht.HHT(halves=AB, latency_path=3)
+    with pytest.raises(hht.HHTError) as e:
+        h.detect(_dev(np.array([[0, 0], [70, 1]], np.int32), cuda_device), 64, 6, 1)
+    assert e.value.name == "HHT_ERANGE"
