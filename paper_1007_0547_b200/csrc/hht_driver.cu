@@ -95,6 +95,17 @@ struct hht_ctx {
     int sms = 148;
     cudaStream_t st = nullptr;
     cudaStream_t own_st = nullptr;              // the ctx's own stream (st may be a borrowed one)
+    cudaStream_t cst2 = nullptr;                // W > 1: the fused tail's grid allreduce, overlapped
+    cudaEvent_t ev_tail = nullptr, ev_ar = nullptr;
+    Buf dense2[2];                              // W > 1: leaf grids of two consecutive ranges
+    int dense_slot = 0;
+    struct Deferred {                           // a fused-tail range whose grid allreduce is in flight
+        bool pending = false;
+        int l = 0;
+        uint32_t r0 = 0, r1 = 0, n = 0;
+        bool all_children = false;
+        uint32_t* grids = nullptr;
+    } deferred;
     bool own_comm = true;                       // false: comm is the caller's (opts.nccl_comm)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, tb0 = nullptr, tb1 = nullptr, ee0 = nullptr, ee1 = nullptr;
     ncclComm_t comm = nullptr;
@@ -299,20 +310,22 @@ void host_reduce(T* acc, const T* v, size_t n, CollOp op) {
 
 // Allreduce of `count` elements from device `send` into device `recv` (may alias), over NCCL or the
 // in-process group. Asynchronous on the ctx stream for NCCL; synchronous for the group.
-hht_status coll_allreduce(hht_ctx* x, const void* send, void* recv, size_t count, CollType t, CollOp op) {
+hht_status coll_allreduce(hht_ctx* x, const void* send, void* recv, size_t count, CollType t, CollOp op,
+                          cudaStream_t stream = nullptr) {
     if (!multi(x) || count == 0) return HHT_OK;
+    const cudaStream_t sm = stream ? stream : x->st;
     if (x->comm) {
         const ncclDataType_t dt = t == C_U32 ? ncclUint32 : t == C_U64 ? ncclUint64 : ncclInt64;
         const ncclRedOp_t ro = op == C_SUM ? ncclSum : op == C_MIN ? ncclMin : ncclMax;
-        CKN(ncclAllReduce(send, recv, count, dt, ro, x->comm, x->st));
+        CKN(ncclAllReduce(send, recv, count, dt, ro, x->comm, sm));
         return HHT_OK;
     }
     hht_group* g = x->group;
     const size_t es = t == C_U32 ? 4 : 8, bytes = count * es;
     const int r = x->opts.rank;
     g->slot[r].resize(bytes);
-    CK(cudaMemcpyAsync(g->slot[r].data(), send, bytes, cudaMemcpyDeviceToHost, x->st));
-    CK(cudaStreamSynchronize(x->st));
+    CK(cudaMemcpyAsync(g->slot[r].data(), send, bytes, cudaMemcpyDeviceToHost, sm));
+    CK(cudaStreamSynchronize(sm));
     g->barrier();                                  // every rank's contribution is staged
     std::vector<uint8_t> acc(g->slot[0]);
     for (int k = 1; k < g->world; ++k) {
@@ -322,8 +335,8 @@ hht_status coll_allreduce(hht_ctx* x, const void* send, void* recv, size_t count
         else host_reduce((int64_t*)acc.data(), (const int64_t*)g->slot[k].data(), count, op);
     }
     g->barrier();                                  // every rank has read every slot
-    CK(cudaMemcpyAsync(recv, acc.data(), bytes, cudaMemcpyHostToDevice, x->st));
-    CK(cudaStreamSynchronize(x->st));
+    CK(cudaMemcpyAsync(recv, acc.data(), bytes, cudaMemcpyHostToDevice, sm));
+    CK(cudaStreamSynchronize(sm));
     return HHT_OK;
 }
 
@@ -554,7 +567,7 @@ hht_status choose_range(hht_ctx* x, int lc, uint32_t q0, uint64_t cap_entries, b
 // R_L region; every deeper level is then split from votes gathered out of the grids (a region's
 // votes = the sum of its diagonal leaves), down to the leaves.
 hht_status gather_levels(hht_ctx* x, int L, int c0, uint32_t anc_base, Level& Own, int TK,
-                         const uint32_t* owner_parent = nullptr);
+                         const uint32_t* owner_parent = nullptr, const uint32_t* grids = nullptr);
 
 hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
     const int TK = x->D - L;
@@ -589,7 +602,8 @@ hht_status tail(hht_ctx* x, int L, uint32_t r0, uint32_t r1) {
 // Levels c0 .. D from the leaf grids of the grid owners R_L[anc_base, ...): parents R_(c-1), a
 // child's votes = the sum of its diagonal leaves, then the split of level c.
 hht_status gather_levels(hht_ctx* x, int L, int c0, uint32_t anc_base, Level& Own, int TK,
-                         const uint32_t* owner_parent) {
+                         const uint32_t* owner_parent, const uint32_t* grids) {
+    if (!grids) grids = (const uint32_t*)x->dense.p;
     for (int c = c0; c <= x->D; ++c) {
         Level& Pc = x->lv[c - 1];
         if (Pc.F == 0) return HHT_OK;
@@ -598,7 +612,7 @@ hht_status gather_levels(hht_ctx* x, int L, int c0, uint32_t anc_base, Level& Ow
         for (int h = 0; h < hops; ++h) chain.parent[h] = (const uint32_t*)x->lv[c - 1 - h].parent.p;
         TRY(ensure(x, x->gv, 16ull * Pc.F));
         const int g = prof_begin(x, 5, (16ull + 8 + 4ull * hops + 16ull * (1u << (x->D - c))) * Pc.F);
-        CK(launch_gather((const uint32_t*)x->dense.p, anc_base, (const uint32_t*)Own.a.p, (const uint32_t*)Own.c.p,
+        CK(launch_gather(grids, anc_base, (const uint32_t*)Own.a.p, (const uint32_t*)Own.c.p,
                          (const uint32_t*)Pc.a.p, (const uint32_t*)Pc.c.p, chain, hops, TK, x->D - c, Pc.F,
                          (uint32_t*)x->gv.p, owner_parent, x->st));
         prof_end(x, g);
@@ -614,6 +628,29 @@ hht_status gather_levels(hht_ctx* x, int L, int c0, uint32_t anc_base, Level& Ow
 // happens here. Levels l+2 .. D are split from the grids.
 // With `gp` (tail_depth 6), R_l has no lists: each work unit r streams the list of its parent in
 // gp = lv[l-1] (all_children only).
+// The grid work of a fused-tail range with all children rastered: votes of the level-L children as
+// diagonal sums, their split, then levels L+1 .. D from the grids.
+hht_status tail_grid_levels(hht_ctx* x, int l, uint32_t r0, uint32_t r1, uint32_t n, const uint32_t* grids) {
+    const int L = l + 1;
+    Level& P = x->lv[l];
+    TRY(ensure(x, x->gv, 16ull * (r1 - r0)));
+    const int g = prof_begin(x, 5, (uint64_t)n * 64 + 16ull * (r1 - r0));
+    CK(launch_grid_diag(grids, r1 - r0, (uint32_t*)x->gv.p, x->st));
+    prof_end(x, g);
+    TRY(do_split(x, L, P, r0, r1 - r0, (const uint32_t*)x->gv.p, (const uint32_t*)x->gv.p));
+    return gather_levels(x, L, L + 1, r0, x->lv[L], 4, (const uint32_t*)x->lv[L].parent.p, grids);
+}
+
+// W > 1: the previous range's leaf grids were summed over the ranks on a second stream while this
+// rank went on with the next range (its list pass and fused tail); finish that range now.
+hht_status flush_deferred(hht_ctx* x) {
+    if (!x->deferred.pending) return HHT_OK;
+    x->deferred.pending = false;
+    CK(cudaStreamWaitEvent(x->st, x->ev_ar, 0));
+    const auto d = x->deferred;
+    return tail_grid_levels(x, d.l, d.r0, d.r1, d.n, d.grids);
+}
+
 hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_children, Level* gp = nullptr) {
     const int L = l + 1;
     Level& P = x->lv[l];
@@ -621,8 +658,13 @@ hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_chil
     if (r1 == r0) return HHT_OK;
     const uint32_t n = all_children ? 4 * (r1 - r0) : C.F;
     if (n == 0) return HHT_OK;
-    TRY(ensure(x, x->dense, (size_t)n * kTail16Cells * 4));
-    CK(cudaMemsetAsync(x->dense.p, 0, (size_t)n * kTail16Cells * 4, x->st));
+    // W > 1 with all children rastered: the grid allreduce overlaps the next range (double-buffered
+    // grids, flush_deferred); else it is on the critical path
+    const bool defer = multi(x) && all_children && !gp;
+    Buf& gb = defer ? x->dense2[x->dense_slot] : x->dense;
+    TRY(ensure(x, gb, (size_t)n * kTail16Cells * 4));
+    uint32_t* grids = (uint32_t*)gb.p;
+    CK(cudaMemsetAsync(grids, 0, (size_t)n * kTail16Cells * 4, x->st));
     TRY(ensure(x, x->fusedctr, 256));
     CK(cudaMemsetAsync(x->fusedctr.p, 0, 24, x->st));
     // streamed pairs: host-known when the parents are the whole level, else from the device
@@ -635,7 +677,7 @@ hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_chil
     a.nf_rbase = r0;
     a.q0 = 0;
     a.q1 = all_children ? n : C.F;
-    a.votes = (uint32_t*)x->dense.p;
+    a.votes = grids;
     a.p_choff = (const uint64_t*)(gp ? gp->choff.p : P.choff.p);
     if (gp) {
         a.gp_parent = (const uint32_t*)P.parent.p;
@@ -665,15 +707,25 @@ hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_chil
         x->pev[id].ops = child_pairs * 16 * 8 + pairs * 4 * 2;
     }
     x->stat.pairs += pairs;
-    TRY(allreduce_sum_u32(x, (uint32_t*)x->dense.p, (size_t)n * kTail16Cells));
+    if (defer) {
+        TRY(flush_deferred(x));                       // the previous range, in range order
+        CK(cudaEventRecord(x->ev_tail, x->st));
+        CK(cudaStreamWaitEvent(x->cst2, x->ev_tail, 0));
+        TRY(coll_allreduce(x, grids, grids, (size_t)n * kTail16Cells, C_U32, C_SUM, x->cst2));
+        CK(cudaEventRecord(x->ev_ar, x->cst2));
+        x->deferred.pending = true;
+        x->deferred.l = l;
+        x->deferred.r0 = r0;
+        x->deferred.r1 = r1;
+        x->deferred.n = n;
+        x->deferred.all_children = true;
+        x->deferred.grids = grids;
+        x->dense_slot ^= 1;
+        return HHT_OK;
+    }
+    TRY(allreduce_sum_u32(x, grids, (size_t)n * kTail16Cells));
     if (!all_children) return gather_levels(x, L, L + 1, 0, C, 4);
-    // votes of the level-L children from their grids, then their split (creates lv[L])
-    TRY(ensure(x, x->gv, 16ull * (r1 - r0)));
-    const int g = prof_begin(x, 5, (uint64_t)n * 64 + 16ull * (r1 - r0));
-    CK(launch_grid_diag((const uint32_t*)x->dense.p, r1 - r0, (uint32_t*)x->gv.p, x->st));
-    prof_end(x, g);
-    TRY(do_split(x, L, P, r0, r1 - r0, (const uint32_t*)x->gv.p, (const uint32_t*)x->gv.p));
-    return gather_levels(x, L, L + 1, r0, x->lv[L], 4, (const uint32_t*)x->lv[L].parent.p);
+    return tail_grid_levels(x, l, r0, r1, n, grids);
 }
 
 // tail_depth 6 at l = D-6: lv[l] holds the lists of a parent range and lv[l+1] its split children
@@ -798,7 +850,9 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         TRY(descend(x, lc, q0, q1));
         q0 = q1;
     }
-    return HHT_OK;
+    // W > 1: a deferred fused-tail range reads this level's frontier (lv[lc]), which the caller's next
+    // range rebuilds: finish it before returning
+    return flush_deferred(x);
 }
 
 hht_status check_args(hht_ctx* x, const int32_t* points, int64_t n_total, int32_t N, int32_t D, int64_t T) {
@@ -1042,6 +1096,7 @@ hht_status finish_small(hht_ctx* x, const uint32_t* d_counts, int id, uint32_t p
 hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets, int32_t B, int32_t N,
                        int32_t D, int64_t T, const int64_t* tree_offsets = nullptr, bool prepacked = false) {
     x->pin_used = 0;                  // the previous call synchronised: its staging is free
+    x->deferred.pending = false;      // a failed previous call may have left one
     // offsets: per image [B+1] (every point enters each of the image's trees); tree_offsets: per
     // tree [B*H+1] (tree t = image t/H, halves in ALPHA, BETA order; each point in one tree)
     if (!x) return HHT_EINVAL;
@@ -1260,6 +1315,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         }
         TRY(do_split(x, 1, L0, 0, F0, (const uint32_t*)L0.votes.p, VL));
         TRY(descend(x, 0, 0, F0));
+        TRY(flush_deferred(x));              // W > 1: the last range's grid work
     }
 
     // stats
@@ -1402,6 +1458,10 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     if (cudaStreamCreateWithFlags(&x->own_st, cudaStreamNonBlocking) != cudaSuccess) return fail(HHT_ECUDA);
     x->st = o.stream ? (cudaStream_t)o.stream : x->own_st;
     if (cudaStreamCreateWithFlags(&x->cst, cudaStreamNonBlocking) != cudaSuccess) return fail(HHT_ECUDA);
+    if (cudaStreamCreateWithFlags(&x->cst2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x->ev_tail, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x->ev_ar, cudaEventDisableTiming) != cudaSuccess)
+        return fail(HHT_ECUDA);
     for (int k = 0; k < 2; ++k)
         if (cudaEventCreateWithFlags(&x->ev_conv[k], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&x->ev_copy[k], cudaEventDisableTiming) != cudaSuccess)
@@ -1863,6 +1923,11 @@ void hht_destroy(hht_ctx* x) {
         if (x->ev_copy[k]) cudaEventDestroy(x->ev_copy[k]);
     }
     if (x->cst) cudaStreamDestroy(x->cst);
+    if (x->cst2) { cudaStreamSynchronize(x->cst2); cudaStreamDestroy(x->cst2); }
+    if (x->ev_tail) cudaEventDestroy(x->ev_tail);
+    if (x->ev_ar) cudaEventDestroy(x->ev_ar);
+    for (Buf* b : {&x->dense2[0], &x->dense2[1]})
+        if (b->p) cudaFree(b->p);
     auto fr = [&](Buf& b) {
         if (b.p) cudaFree(b.p);
         b.p = nullptr;

@@ -90,3 +90,32 @@ def test_multirank_error_flag_is_collective(cuda_device):
     for h in hs:
         h.close()
     g.close()
+
+
+@pytest.mark.parametrize("budget", [0, 24 << 20])
+def test_multirank_c3_digest(budget, cuda_device):
+    """Config 3 on 2 ranks (points sharded), the fused tail's grid allreduce deferred onto a second
+    stream behind the next range; with a 24 MiB budget the traversal runs in nested depth-first
+    ranges. Every level's records and the leaves hash to the oracle's digest on both ranks."""
+    import hashlib
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c3_digest.json")))
+    cfg = synth.CONFIGS[3]
+    pts, _ = synth.config_image(3)
+    hs, g, errs = _run_ranks(pts, cfg.N, cfg.D, cfg.T, cfg.halves, 2, cuda_device, mem_budget=budget)
+    assert errs == [None, None], errs
+    for h in hs:
+        for half in (1, 2):
+            for lev in range(cfg.D + 1):
+                arr = np.ascontiguousarray(h.level(0, half, lev).astype("<u4"))
+                assert hashlib.sha256(arr.tobytes()).hexdigest() == gold["level_sha256"][f"{half}/{lev}"], (half, lev)
+        lv = np.ascontiguousarray(h.leaves(-1).astype("<u4"))
+        assert hashlib.sha256(lv.tobytes()).hexdigest() == gold["leaves_sha256"]
+        st = h.stats()
+        assert (st["tests"], st["votes"]) == (gold["tests"], gold["votes"])
+    if budget:
+        assert min(h.stats()["ranges"] for h in hs) > 2 * cfg.D
+    for h in hs:
+        h.close()
+    g.close()
