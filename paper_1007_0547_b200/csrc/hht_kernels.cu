@@ -374,6 +374,10 @@ __device__ __forceinline__ void chunk_math_circle(const uint32_t (&p)[kItems], i
     }
 }
 
+// (No minimum resident blocks: the compiler's allocation gives the count-ahead pass 64 registers and
+// the last list pass 57, 4 blocks/SM. Measured on C5: forcing 5 blocks/SM on the last pass (48
+// registers, 40 B of spills) 44.4 vs 40.3 ms of list passes; an explicit minimum of 1 let the
+// count-ahead pass grow to 115 registers, 2 blocks/SM, 50.4 ms.)
 template <typename I, int MODE, bool PREF, int CIRCLE>
 __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
     constexpr bool kWrites = MODE == MODE_WRITE || MODE == MODE_WRITE_NC;
@@ -2383,17 +2387,28 @@ __global__ void __launch_bounds__(1024) k_split_scan(const SplitArgs A) {
     const uint32_t seg = (A.ntiles + 31) / 32;
     const uint32_t t0 = wid * seg, t1 = min(A.ntiles, t0 + seg);
     Agg carry = {0, 0, 0};
-    for (uint32_t b = t0; b < t1; b += 32) {
-        const uint32_t t = b + lane;
-        Agg a = {0, 0, 0};
-        if (t < t1) a = {A.tiles[t].aggF, A.tiles[t].aggC, A.tiles[t].aggS};
-        const Agg incl = warp_inclusive(a, lane);
-        if (t < t1) {
-            A.tiles[t].incF = carry.F + incl.F - a.F;
-            A.tiles[t].incC = carry.C + incl.C - a.C;
-            A.tiles[t].incS = carry.S + incl.S - a.S;
+    // 4 x 32 aggregates loaded per step (independent loads in flight; the aggregates are never
+    // written by this kernel, so the read-only path is safe), then scanned in order
+    constexpr int kU = 4;
+    for (uint32_t b = t0; b < t1; b += 32 * kU) {
+        Agg a[kU];
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+            const uint32_t t = b + 32 * k + lane;
+            a[k] = {0, 0, 0};
+            if (t < t1) a[k] = {__ldg(&A.tiles[t].aggF), __ldg(&A.tiles[t].aggC), __ldg(&A.tiles[t].aggS)};
         }
-        carry = agg_add(carry, Agg{__shfl_sync(kFull, incl.F, 31), __shfl_sync(kFull, incl.C, 31), shfl_u64(incl.S, 31)});
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+            const uint32_t t = b + 32 * k + lane;
+            const Agg incl = warp_inclusive(a[k], lane);
+            if (t < t1) {
+                A.tiles[t].incF = carry.F + incl.F - a[k].F;
+                A.tiles[t].incC = carry.C + incl.C - a[k].C;
+                A.tiles[t].incS = carry.S + incl.S - a[k].S;
+            }
+            carry = agg_add(carry, Agg{__shfl_sync(kFull, incl.F, 31), __shfl_sync(kFull, incl.C, 31), shfl_u64(incl.S, 31)});
+        }
     }
     if (lane == 0) s_w[wid] = carry;
     __syncthreads();
