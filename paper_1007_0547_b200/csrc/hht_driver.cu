@@ -90,6 +90,11 @@ struct hht_group {
     }
 };
 
+#ifndef HHT_SINK_SLOTS
+#define HHT_SINK_SLOTS 2
+#endif
+constexpr int kSinkSlots = HHT_SINK_SLOTS;   // leaf-sink staging buffers (row conversion -> host copy)
+
 struct hht_ctx {
     hht_opts opts{};
     int sms = 148;
@@ -151,9 +156,9 @@ struct hht_ctx {
     int64_t sink_cap = 0;
     uint64_t sink_n = 0;
     cudaStream_t cst = nullptr;
-    Buf sinkrows[2];
-    cudaEvent_t ev_conv[2] = {nullptr, nullptr}, ev_copy[2] = {nullptr, nullptr};
-    bool copy_pending[2] = {false, false};
+    Buf sinkrows[kSinkSlots];
+    cudaEvent_t ev_conv[kSinkSlots] = {}, ev_copy[kSinkSlots] = {};
+    bool copy_pending[kSinkSlots] = {};
     int sink_slot = 0;
     // pinned host memory that kernels write directly (mapped, UVA): small per-split readbacks
     Totals* totals_h = nullptr;
@@ -387,7 +392,7 @@ hht_status stream_leaves(hht_ctx* x, uint64_t first, uint64_t n) {
     if (!x->sink || n == 0 || x->sink_n >= (uint64_t)x->sink_cap) return HHT_OK;
     const uint64_t k = std::min<uint64_t>(n, (uint64_t)x->sink_cap - x->sink_n);
     const int s = x->sink_slot;
-    x->sink_slot ^= 1;
+    x->sink_slot = (s + 1) % kSinkSlots;
     Buf& b = x->sinkrows[s];
     if (b.cap < k * sizeof(hht_leaf)) {
         if (x->copy_pending[s]) CK(cudaEventSynchronize(x->ev_copy[s]));   // before freeing its buffer
@@ -789,8 +794,10 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         RangeInfo ri{};
         TRY(choose_range(x, lc, q0, cap, false, &ri, r0, r1));
         // With a leaf sink, the leaves of the last range are copied to the host after all compute: when
-        // the detection's final piece at the last list level would be large, cut its last quarter into
-        // a range of its own, so that the copy of the rest overlaps that quarter's tail
+        // the detection's final piece at the last list level would be large, cut its last eighth into
+        // a range of its own, so that the copy of the rest overlaps that eighth's tail. (Halving the
+        // final piece repeatedly, 1/2, 1/4, ..., measured worse on C5: +1.5, +4.5, +8.7 ms e2e with 1, 3
+        // and 5 cuts, since a small piece leaves most warps of its fused tail idle.)
         if (x->sink && !final_cut && ri.q1 == Fc && q0 > 0 && r1 == P.F && fused_tail(x) &&
             lc == x->D - tail_depth(x) && Fc - q0 >= 64) {
             final_cut = true;
@@ -1335,7 +1342,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     x->stat.ms = ms;
     if (x->sink) {
         CK(cudaStreamSynchronize(x->cst));
-        x->copy_pending[0] = x->copy_pending[1] = false;
+        for (int k = 0; k < kSinkSlots; ++k) x->copy_pending[k] = false;
         x->stat.leaves_streamed = x->sink_n;
         x->stat.d2h_bytes += x->sink_n * sizeof(hht_leaf);
     }
@@ -1462,7 +1469,7 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
         cudaEventCreateWithFlags(&x->ev_tail, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&x->ev_ar, cudaEventDisableTiming) != cudaSuccess)
         return fail(HHT_ECUDA);
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < kSinkSlots; ++k)
         if (cudaEventCreateWithFlags(&x->ev_conv[k], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&x->ev_copy[k], cudaEventDisableTiming) != cudaSuccess)
             return fail(HHT_ECUDA);
@@ -1864,7 +1871,7 @@ hht_status hht_set_leaf_sink(hht_ctx* x, hht_leaf* host, int64_t cap) {
     if (!x) return HHT_EINVAL;
     if (host && cap < 0) return set_err(x, HHT_EINVAL, "cap < 0");
     if (x->cst) cudaStreamSynchronize(x->cst);
-    x->copy_pending[0] = x->copy_pending[1] = false;
+    for (int k = 0; k < kSinkSlots; ++k) x->copy_pending[k] = false;
     x->sink = host;
     x->sink_cap = host ? cap : 0;
     return HHT_OK;
@@ -1916,9 +1923,9 @@ void hht_destroy(hht_ctx* x) {
     if (!x) return;
     if (x->st) cudaStreamSynchronize(x->st);
     if (x->cst) cudaStreamSynchronize(x->cst);
-    for (Buf* b : {&x->sinkrows[0], &x->sinkrows[1]})
-        if (b->p) cudaFree(b->p);
-    for (int k = 0; k < 2; ++k) {
+    for (Buf& b : x->sinkrows)
+        if (b.p) cudaFree(b.p);
+    for (int k = 0; k < kSinkSlots; ++k) {
         if (x->ev_conv[k]) cudaEventDestroy(x->ev_conv[k]);
         if (x->ev_copy[k]) cudaEventDestroy(x->ev_copy[k]);
     }
