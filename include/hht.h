@@ -114,6 +114,9 @@ typedef struct {
     void* nccl_comm;         /* ncclComm_t of `world` ranks, BORROWED (never destroyed by the
                                 library); takes precedence over nccl_id; its size and rank must equal
                                 world and rank (HHT_EINVAL otherwise) */
+    uint32_t tail_units;     /* fused tail work units: 0 = auto (when a launch has fewer parents than
+                                8 x its warps, each parent's chunks are split into blocks so every
+                                warp has work to the end); 2 = one unit per parent. Identical results */
 } hht_opts;
 
 /* Re-point the ctx at another BORROWED stream (cudaStream_t; NULL = back to the ctx's own stream,

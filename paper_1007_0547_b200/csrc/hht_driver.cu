@@ -94,6 +94,11 @@ struct hht_group {
 #define HHT_SINK_SLOTS 2
 #endif
 constexpr int kSinkSlots = HHT_SINK_SLOTS;   // leaf-sink staging buffers (row conversion -> host copy)
+#ifndef HHT_UNITS_PER_WARP
+#define HHT_UNITS_PER_WARP 8
+#endif
+constexpr uint64_t kUnitsPerWarp = HHT_UNITS_PER_WARP;   // fused tail: split parents below this many per warp
+constexpr int kFusedThreadsHost = 512;                     // k_fused block size (hht_kernels.cu kFusedThreads)
 
 struct hht_ctx {
     hht_opts opts{};
@@ -135,7 +140,7 @@ struct hht_ctx {
     std::vector<uint8_t> tree_half;         // HHT_ALPHA / HHT_BETA per tree
     std::vector<int64_t> tree_E;            // global points per tree
 
-    Buf stage_in, packed, errflag, beta, stats, tiles, tilectr, totals, rng, bounds, vtmp, dense, gv, leafrows;
+    Buf stage_in, packed, errflag, beta, stats, tiles, tilectr, totals, rng, bounds, vtmp, dense, gv, leafrows, units;
     Buf fusedctr;                    // k_fused work counter (u32) + rastered-pair counter (u64)
     Buf img, edgeB, edgetiles;       // edge front end: staged image, BETA points, look-back words
     Buf small;                       // latency path scratch (k_small)
@@ -694,6 +699,19 @@ hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_chil
     a.work = (uint32_t*)x->fusedctr.p;
     a.child_pairs = (unsigned long long*)((char*)x->fusedctr.p + 8);
     a.all_children = all_children ? 1u : 0u;
+    // few parents for the warps (C3, small ranges): split each parent's chunks into work units so that
+    // every warp gets work until the end (a unit's partial raster batches are its only extra cost)
+    const uint64_t nwarps = (uint64_t)x->fused_grid[x->int64 ? 1 : 0] * (kFusedThreadsHost / 32);
+    if (!gp && x->opts.tail_units != 2 && (uint64_t)(r1 - r0) < kUnitsPerWarp * nwarps) {
+        const uint64_t target = kUnitsPerWarp * nwarps;
+        const uint64_t cap = target + (r1 - r0) + 1;        // sum of ceil(chunks_r / K) <= chunks / K + parents
+        TRY(ensure(x, x->units, cap * 8 + 16));
+        uint32_t* nk = (uint32_t*)((char*)x->units.p + cap * 8);
+        CK(launch_units(a.p_choff, r0, r1, (uint32_t)target, (uint2*)x->units.p, nk, x->st));
+        a.units = (const uint2*)x->units.p;
+        a.nunits = nk;
+        a.unit_k = nk + 1;
+    }
     const int id = prof_begin(x, 3, 0);
     CK(launch_fused(x->int64, a, x->fused_grid[x->int64 ? 1 : 0], x->st));
     prof_end(x, id);
@@ -1947,7 +1965,7 @@ void hht_destroy(hht_ctx* x) {
     for (auto& g : x->rec) fr(g.b);
     fr(x->leaves.b);
     for (Buf* b : {&x->stage_in, &x->packed, &x->errflag, &x->beta, &x->stats, &x->tiles, &x->tilectr, &x->totals,
-                   &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv, &x->leafrows, &x->fusedctr, &x->img,
+                   &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv, &x->leafrows, &x->fusedctr, &x->img, &x->units,
                    &x->edgeB, &x->edgetiles, &x->small, &x->small_g})
         fr(*b);
     if (x->totals_h) cudaFreeHost(x->totals_h);

@@ -110,7 +110,15 @@ struct PassArgs {
     const uint32_t* gp_parent;
     const uint32_t* gp_a;
     const uint32_t* gp_c;
+    // k_fused with split work units (fewer parents than warps x kUnitsPerWarp): unit u = (r, k) covers
+    // chunks [c_lo + k K, min(c_hi, c_lo + (k + 1) K)) of parent r, K = *unit_k (k_units); nullptr:
+    // one unit per parent
+    const uint2* units;
+    const uint32_t* nunits;
+    const uint32_t* unit_k;
 };
+cudaError_t launch_units(const uint64_t* p_choff, uint32_t r_lo, uint32_t r_hi, uint32_t target_units, uint2* units,
+                         uint32_t* nunits_k, cudaStream_t st);
 
 struct SplitArgs {
     const uint32_t* V;             // [4 * Fp] global child votes

@@ -920,15 +920,29 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
     const I Qc = ((I)3 * N) << (sh - 1);              // child b-step 3N * s/2
 
     while (true) {
-        uint32_t r = 0;
-        if (lane == 0) r = atomicAdd(A.work, 1u);
-        r = __shfl_sync(kFull, r, 0) + A.r_lo;
-        if (r >= A.r_hi) break;
+        uint32_t u = 0;
+        if (lane == 0) u = atomicAdd(A.work, 1u);
+        u = __shfl_sync(kFull, u, 0);
+        uint32_t r, sub = 0;
+        if (A.units) {                                 // split units: (parent, block of K chunks)
+            if (u >= *A.nunits) break;
+            const uint2 e = __ldg(A.units + u);
+            r = e.x;
+            sub = e.y;
+        } else {
+            r = u + A.r_lo;
+            if (r >= A.r_hi) break;
+        }
         // the list streamed: r's own, or (tail_depth 6) its parent's, whose entries that miss r
         // get no child bits (a line crossing a child of r crosses r)
         const uint32_t lr = GP ? __ldg(A.gp_parent + r) : r;
-        const uint64_t c_lo = __ldg(A.p_choff + lr), c_hi = __ldg(A.p_choff + lr + 1);
-        if (c_lo == c_hi) continue;
+        uint64_t c_lo = __ldg(A.p_choff + lr), c_hi = __ldg(A.p_choff + lr + 1);
+        if (A.units) {
+            const uint64_t K = *A.unit_k;
+            c_lo += (uint64_t)sub * K;
+            c_hi = min(c_hi, c_lo + K);
+        }
+        if (c_lo >= c_hi) continue;
         // lanes 0..3: grid index of child `lane` (+ q0): its next-frontier index when only split
         // children are rastered, 4 (r - r_lo) + lane when all are; kNone for skipped children
         uint32_t my_nf = kNone;
@@ -1069,6 +1083,53 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
         }
         if (lane == 0) atomicAdd(A.child_pairs + 1, (unsigned long long)streamed);
     }
+}
+
+// Work units of a fused-tail launch with few parents (hht_driver.cu tail_fused): K = max(4,
+// ceil(chunks / target)) chunks per unit, parent r of [r_lo, r_hi) split into ceil(chunks_r / K)
+// units (r, k), listed in parent order. One block; a chunked block scan over the parents.
+__global__ void __launch_bounds__(1024) k_units(const uint64_t* __restrict__ p_choff, uint32_t r_lo, uint32_t r_hi,
+                                                 uint32_t target, uint2* __restrict__ units, uint32_t* __restrict__ nk) {
+    __shared__ uint32_t s_w[33];
+    const uint64_t total = p_choff[r_hi] - p_choff[r_lo];
+    const uint32_t K = (uint32_t)max((uint64_t)4, (total + target - 1) / max(target, 1u));
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    uint32_t carry = 0;
+    for (uint32_t base = r_lo; base < r_hi; base += blockDim.x) {
+        const uint32_t r = base + tid;
+        const uint32_t n = r < r_hi ? (uint32_t)((p_choff[r + 1] - p_choff[r] + K - 1) / K) : 0u;
+        uint32_t inc = n;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, inc, d);
+            if (lane >= d) inc += t;
+        }
+        if (lane == 31) s_w[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            const uint32_t w = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0u;
+            uint32_t wi = w;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t t = __shfl_up_sync(kFull, wi, d);
+                if (lane >= d) wi += t;
+            }
+            if (lane < (int)(blockDim.x >> 5)) s_w[lane] = wi - w;
+            if (lane == 31) s_w[32] = wi;
+        }
+        __syncthreads();
+        const uint32_t off = carry + s_w[wid] + inc - n;
+        for (uint32_t k = 0; k < n; ++k) units[off + k] = make_uint2(r, k);
+        carry += s_w[32];
+        __syncthreads();
+    }
+    if (tid == 0) { nk[0] = carry; nk[1] = K; }
+}
+
+cudaError_t launch_units(const uint64_t* p_choff, uint32_t r_lo, uint32_t r_hi, uint32_t target_units, uint2* units,
+                         uint32_t* nunits_k, cudaStream_t st) {
+    k_units<<<1, 1024, 0, st>>>(p_choff, r_lo, r_hi, target_units, units, nunits_k);
+    return cudaGetLastError();
 }
 
 int fused_blocks_per_sm(bool int64) {

@@ -49,7 +49,8 @@ class Opts(C.Structure):
                 ("tail_depth", C.c_uint32), ("prefetch", C.c_uint32), ("latency_path", C.c_uint32),
                 ("variant", C.c_uint32),
                 ("mem_budget", C.c_size_t),
-                ("nccl_id", C.c_void_p), ("group", C.c_void_p), ("stream", C.c_void_p), ("nccl_comm", C.c_void_p)]
+                ("nccl_id", C.c_void_p), ("group", C.c_void_p), ("stream", C.c_void_p), ("nccl_comm", C.c_void_p),
+                ("tail_units", C.c_uint32)]
 
 
 class Leaf(C.Structure):
@@ -183,7 +184,7 @@ class HHT:
                  force_int64: bool = False, profile: bool = False, mem_budget: int = 0,
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, tail_depth: int = 0,
                  prefetch: int = 0, variant: int = 0, group: Optional["Group"] = None, latency_path: int = 0,
-                 stream: Optional[int] = None):
+                 stream: Optional[int] = None, tail_units: int = 0):
         self._lib = load()
         o = Opts()
         self._lib.hht_default_opts(C.byref(o))
@@ -194,6 +195,7 @@ class HHT:
         o.prefetch = prefetch
         o.latency_path = latency_path
         o.variant = variant
+        o.tail_units = tail_units
         if stream is not None:            # borrowed cudaStream_t handle (int), e.g. torch.cuda.Stream.cuda_stream
             o.stream = stream if stream else 1
         self._id = None

@@ -225,6 +225,24 @@ def test_tail_depth_variants(seed, tail_depth, torch_dev):
     assert (h.stats()["tests"], h.stats()["votes"]) == (ref.tests, ref.votes)
 
 
+@pytest.mark.parametrize("tail_units", [0, 2])
+@pytest.mark.parametrize("seed", range(6))
+def test_fused_tail_work_units(seed, tail_units, torch_dev):
+    """The fused tail with each parent's chunks split into work units (auto: fewer parents than
+    8 x warps) and with one unit per parent (tail_units 2) give identical records and leaves,
+    also under a small budget (many ranges, some with very few parents)."""
+    rng = np.random.default_rng(700 + seed)
+    N = int(rng.choice([64, 200, 256]))
+    D = int(rng.integers(6, 9))
+    T = int(rng.choice([1, 3, 8]))
+    pts = synth.random_scene(7100 + seed, N, max_lines=5, max_noise=int(rng.choice([500, 4000])))
+    ref = oracle.detect(pts, N, D, T, AB)
+    for budget in (0, 128 << 10):
+        h = _run(pts, N, D, T, AB, torch_dev, tail_units=tail_units, mem_budget=budget)
+        compare_all(h, ref, AB, D)
+        assert (h.stats()["tests"], h.stats()["votes"]) == (ref.tests, ref.votes)
+
+
 def test_nccl_collectives_one_rank(torch_dev):
     """world = 1 with an NCCL id runs every collective call site (argument check, per-image
     counts, range agreement, per-level vote allreduce, error flag) on a 1-rank communicator;
