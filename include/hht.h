@@ -78,7 +78,9 @@ typedef struct {
                                 4 = 16x16 grids from level depth-4 lists; 3 = 8x8 grids from level
                                 depth-3 lists. Results are identical. */
     uint32_t prefetch;       /* pass/tail kernels: 0 = auto, 1 = fetch the next chunk's descriptor
-                                only, 2 = also its list entries (more registers); identical results */
+                                only, 2 = also its list entries (more registers); 3 = list passes
+                                fill a per-warp ring of two shared-memory slots with 1-D bulk copies
+                                (cp.async.bulk + mbarrier) two chunks ahead; identical results */
     uint32_t latency_path;   /* 0 = auto: a small detection (one rank, exact test; bound on the
                                 lists: sum over trees of points x (2^depth - 1) entries) runs as ONE
                                 kernel launch: of one block (k_small) when all arrays fit 220 KiB of

@@ -128,6 +128,7 @@ struct hht_ctx {
     int fused_grid[2] = {};
     int split_grid = 0;             // resident k_split blocks (persistent tile loop)
     bool pref_pass = true, pref_tail = true;   // opts.prefetch (0 = auto)
+    int pf_pass = 1;                           // list passes: 0 descriptor only, 1 registers, 2 bulk-copy ring
     bool circle = false;                       // opts.variant is a circumcircle test (1 or 2)
     int circle_var = 0;                        // opts.variant: 1 lattice units, 2 (m, b) units
     int grid_circle[3][2] = {};
@@ -532,7 +533,7 @@ hht_status run_pass(hht_ctx* x, int mode, const PassArgs& a, uint64_t pairs, uin
     const int cls = mode == MODE_COUNT ? 1 : ((mode == MODE_WRITE || mode == MODE_WRITE_NC) ? 2 : 3);
     const int id = prof_begin(x, cls, pairs * 4 + written * 4);
     const int grid = x->circle ? x->grid_circle[mode][x->int64 ? 1 : 0] : x->grid[mode][x->int64 ? 1 : 0];
-    CK(launch_pass(mode, x->int64, x->pref_pass || x->circle, x->circle_var, a, grid, x->st));
+    CK(launch_pass(mode, x->int64, x->circle ? 1 : x->pf_pass, x->circle_var, a, grid, x->st));
     prof_end(x, id);
     x->stat.pairs += pairs;
     return HHT_OK;
@@ -831,13 +832,13 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         if (entries * 4 > avail)
             return set_err(x, HHT_ENOMEM, "level %d region list of %llu entries exceeds the list budget (%zu B free)",
                            lc, (unsigned long long)entries, avail);
-        if (entries * 4 > C.list_own.cap) {
+        if (entries * 4 + 64 > C.list_own.cap) {
             size_t deeper = 0;
             for (int k = lc + 1; k < (int)x->lv.size(); ++k) deeper += x->lv[k].list_own.cap;
             if (active + entries * 4 + deeper > x->budget)
                 for (int k = lc + 1; k < (int)x->lv.size(); ++k) TRY(release(x, x->lv[k].list_own));
             TRY(release(x, C.list_own));
-            TRY(ensure(x, C.list_own, std::max<uint64_t>(entries, 1) * 4, true));
+            TRY(ensure(x, C.list_own, std::max<uint64_t>(entries, 1) * 4 + 64, true));   // + bulk-copy slack
         }
         C.list = (const uint32_t*)C.list_own.p;
         C.list_base = ri.s_lo;
@@ -1214,7 +1215,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     if (prepacked) {
         if (x->packed.cap < (size_t)n * 4) return set_err(x, HHT_EINVAL, "internal: prepacked points exceed the buffer");
     } else {
-        TRY(ensure(x, x->packed, std::max<int64_t>(n, 1) * 4));
+        TRY(ensure(x, x->packed, std::max<int64_t>(n, 1) * 4 + 64));   // + bulk-copy slack
     }
     // errflag is 0 on entry: zeroed at create, re-armed by k_finish (one-launch paths) and after the
     // multi-kernel path's range check; a call that failed in between leaves it dirty
@@ -1503,13 +1504,14 @@ hht_status hht_create(hht_ctx** out, const hht_opts* opts) {
     }
     if (o.prefetch == 1) x->pref_pass = x->pref_tail = false;
     if (o.prefetch == 2) x->pref_pass = x->pref_tail = true;
+    x->pf_pass = o.prefetch == 3 ? 2 : (x->pref_pass ? 1 : 0);
     for (int m = 0; m < 4; ++m)
-        for (int w = 0; w < 2; ++w) x->grid[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, x->pref_pass, false);
+        for (int w = 0; w < 2; ++w) x->grid[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, x->pf_pass, 0);
     x->circle = o.variant == HHT_FHT_CIRCLE || o.variant == HHT_FHT_CIRCLE_MB;
     x->circle_var = x->circle ? (int)o.variant : 0;
     for (int m = 0; m < 3; ++m)
         for (int w = 0; w < 2; ++w)
-            x->grid_circle[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, true, x->circle_var ? x->circle_var : 1);
+            x->grid_circle[m][w] = x->sms * pass_blocks_per_sm(m, w == 1, 1, x->circle_var ? x->circle_var : 1);
     for (int w = 0; w < 2; ++w) x->tail_grid[w] = x->sms * tail_blocks_per_sm(w == 1);
     for (int w = 0; w < 2; ++w) x->tail16_grid[w] = x->sms * tail16_blocks_per_sm(w == 1, x->pref_tail);
     for (int w = 0; w < 2; ++w) x->fused_grid[w] = x->sms * fused_blocks_per_sm(w == 1);

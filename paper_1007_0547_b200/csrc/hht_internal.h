@@ -165,7 +165,7 @@ struct RangeInfo {
 // Launchers (hht_kernels.cu). All asynchronous on `st`.
 cudaError_t launch_stage(const int32_t* pts, uint64_t n, int N, uint32_t* packed, uint32_t* err,
                          cudaStream_t st);
-cudaError_t launch_pass(int mode, bool int64, bool pref, int circle, const PassArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_pass(int mode, bool int64, int pf, int circle, const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_split(const SplitArgs& a, int resident_blocks, cudaStream_t st);
 int split_blocks_per_sm();
 constexpr uint32_t kSplitPrescanTiles = 1024;   // reduce-then-scan split from this many tiles on
@@ -178,7 +178,7 @@ cudaError_t launch_range(const uint64_t* c_off, const uint32_t* c_parent, uint32
                          uint64_t* chunk_bounds, RangeInfo* info_h, cudaStream_t st);
 cudaError_t launch_copy_u32(uint32_t* dst, const uint32_t* src, uint32_t n, cudaStream_t st);
 cudaError_t launch_set_bounds(uint64_t* bounds, uint64_t lo, uint64_t hi, cudaStream_t st);
-int pass_blocks_per_sm(int mode, bool int64, bool pref, int circle);
+int pass_blocks_per_sm(int mode, bool int64, int pf, int circle);
 int tail_blocks_per_sm(bool int64);
 cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_beta, uint32_t H, uint32_t* out,
                              cudaStream_t st);

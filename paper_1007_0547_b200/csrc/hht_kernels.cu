@@ -291,6 +291,90 @@ __device__ __forceinline__ void chunk_loop(const PassArgs& A, int lane, Body bod
     }
 }
 
+// TMA variant of the work loop (opts.prefetch 3, list passes): a per-warp ring of two shared-memory
+// slots, each filled by one 1-D bulk copy (cp.async.bulk, one elected lane, completion counted on the
+// slot's mbarrier) with the 16-byte-aligned span of a chunk's entries. While chunk k is processed
+// from registers, the bulk copies of chunks k+1 and k+2 are in flight (2 KB per warp instead of the
+// register prefetch's 1 KB), and no registers hold them.
+constexpr uint32_t kTmaSlot = 1040;            // (3 + 256) words rounded up to 16 bytes
+constexpr uint32_t kTmaWarpBytes = 2 * kTmaSlot + 16;   // two slots + two mbarriers
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    } while (!done);
+}
+// lane 0: bulk-copy the aligned span of chunk d's entries into slot `dst` (nothing for an empty chunk)
+__device__ __forceinline__ void tma_chunk(const PassArgs& A, const ChunkDesc& d, uint32_t dst, uint32_t bar) {
+    if (d.cnt == 0) return;
+    const uint64_t e = d.e0 - A.list_base;
+    const uint32_t off = (uint32_t)(e & 3u);
+    const uint32_t bytes = ((off + d.cnt) * 4u + 15u) & ~15u;
+    const uint32_t* src = A.list + (e - off);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
+template <typename Body>
+__device__ __forceinline__ void chunk_loop_tma(const PassArgs& A, int lane, uint32_t ring, Body body) {
+    const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t c_lo = A.chunk_bounds[0], c_hi = A.chunk_bounds[1];
+    const uint32_t bar0 = ring + 2 * kTmaSlot, bar1 = bar0 + 8;
+    if (lane == 0) {
+        mbar_init(bar0, 1);
+        mbar_init(bar1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint64_t ch = c_lo + warp0;
+    ChunkDesc d0 = load_desc(A.chunks, ch, c_hi);             // chunk k (slot k & 1)
+    ChunkDesc d1 = load_desc(A.chunks, ch + nwarps, c_hi);    // chunk k + 1
+    if (lane == 0) {
+        tma_chunk(A, d0, ring, bar0);
+        tma_chunk(A, d1, ring + kTmaSlot, bar1);
+    }
+    ChunkDesc d2 = load_desc(A.chunks, ch + 2 * nwarps, c_hi);
+    uint32_t phase = 0;                                       // parity of the slot's current use
+    for (uint32_t k = 0; ch < c_hi; ch += nwarps, ++k) {
+        const uint32_t s = k & 1u;
+        const uint32_t slot = ring + s * kTmaSlot, bar = s ? bar1 : bar0;
+        uint32_t p[kItems];
+        if (d0.cnt) {
+            mbar_wait(bar, (phase >> s) & 1u);
+            phase ^= 1u << s;
+            const uint32_t off = (uint32_t)((d0.e0 - A.list_base) & 3u);
+#pragma unroll
+            for (int it = 0; it < kItems; ++it) {
+                const uint32_t w = off + (uint32_t)lane + kWarp * it;
+                uint32_t v = 0;
+                if (lane + kWarp * it < (int)d0.cnt) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(slot + 4u * w));
+                p[it] = v;
+            }
+        } else {
+#pragma unroll
+            for (int it = 0; it < kItems; ++it) p[it] = 0u;
+        }
+        __syncwarp();
+        // the slot is free again: refill it with chunk k + 2 (generic reads before async writes)
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tma_chunk(A, d2, slot, bar);
+        }
+        const ChunkDesc d3 = load_desc(A.chunks, ch + 3 * nwarps, c_hi);
+        body(d0, p);
+        d0 = d1;
+        d1 = d2;
+        d2 = d3;
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // FHT circumcircle variant ("calculates the perpendicular
 // distance to the line from the center of the region and compares it with the radius of the
@@ -378,8 +462,9 @@ __device__ __forceinline__ void chunk_math_circle(const uint32_t (&p)[kItems], i
 // the last list pass 57, 4 blocks/SM. Measured on C5: forcing 5 blocks/SM on the last pass (48
 // registers, 40 B of spills) 44.4 vs 40.3 ms of list passes; an explicit minimum of 1 let the
 // count-ahead pass grow to 115 registers, 2 blocks/SM, 50.4 ms.)
-template <typename I, int MODE, bool PREF, int CIRCLE>
+template <typename I, int MODE, int PF, int CIRCLE>
 __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
+    constexpr bool PREF = PF == 1;
     constexpr bool kWrites = MODE == MODE_WRITE || MODE == MODE_WRITE_NC;
     __shared__ uint32_t s_stage[kWrites ? 8 * 4 * kChunk : 1];   // 4 KB per warp
     const int lane = threadIdx.x & 31;
@@ -398,7 +483,7 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
         CR.init(A, lane);
     }
 
-    chunk_loop<PREF>(A, lane, [&](const ChunkDesc& d, const uint32_t (&p)[kItems]) {
+    auto body = [&](const ChunkDesc& d, const uint32_t (&p)[kItems]) {
         const int cnt = (int)d.cnt;
         const I i0 = (I)d.a << sh;
         const I j0 = (I)d.c << sh;
@@ -530,7 +615,13 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
             }
             __syncwarp();
         }
-    });
+    };
+    if constexpr (PF == 2) {
+        extern __shared__ uint4 s_tma_ring[];
+        chunk_loop_tma(A, lane, (uint32_t)__cvta_generic_to_shared(s_tma_ring) + (threadIdx.x >> 5) * kTmaWarpBytes, body);
+    } else {
+        chunk_loop<PREF>(A, lane, body);
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -2128,31 +2219,45 @@ cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_
     return cudaGetLastError();
 }
 
-template <typename I, bool P, int C>
+// The count-ahead pass keeps the register prefetch under mode 3: its bulk-copy loop needs 73 registers
+// (3 blocks/SM), measured slower (C5 list passes 43.4 vs 39.7 ms with both passes on the ring)
+#ifndef PF_WRITE_TMA
+#define PF_WRITE_TMA 1
+#endif
+template <typename I, int P, int C>
 static PassKernel pass_kernel_t(int mode) {
-    if (mode == MODE_COUNT) return k_pass<I, MODE_COUNT, P, C>;
-    if (mode == MODE_WRITE) return k_pass<I, MODE_WRITE, P, C>;
+    if (mode == MODE_COUNT) return k_pass<I, MODE_COUNT, P == 2 ? 1 : P, C>;
+    if (mode == MODE_WRITE) return k_pass<I, MODE_WRITE, P == 2 ? PF_WRITE_TMA : P, C>;
     if (mode == MODE_WRITE_NC && !C) return k_pass<I, MODE_WRITE_NC, P, 0>;
-    return k_pass<I, MODE_COUNT2, P, C>;
+    return k_pass<I, MODE_COUNT2, P == 2 ? 1 : P, C>;
 }
 
-// The circumcircle variants (1: lattice units, 2: (m, b) units) are instantiated with the
-// prefetching loop only.
-static PassKernel pass_kernel(int mode, bool int64, bool pref, int circle = 0) {
-    if (circle == 1) return int64 ? pass_kernel_t<int64_t, true, 1>(mode) : pass_kernel_t<int32_t, true, 1>(mode);
-    if (circle == 2) return int64 ? pass_kernel_t<int64_t, true, 2>(mode) : pass_kernel_t<int32_t, true, 2>(mode);
-    if (int64) return pref ? pass_kernel_t<int64_t, true, 0>(mode) : pass_kernel_t<int64_t, false, 0>(mode);
-    return pref ? pass_kernel_t<int32_t, true, 0>(mode) : pass_kernel_t<int32_t, false, 0>(mode);
+// pf: 0 = descriptor prefetch only, 1 = also the next chunk's entries in registers, 2 = bulk-copy ring
+// (list passes MODE_WRITE / MODE_WRITE_NC; the other modes use 1). The circumcircle variants (1:
+// lattice units, 2: (m, b) units) are instantiated with the register prefetch only.
+static PassKernel pass_kernel(int mode, bool int64, int pf, int circle = 0) {
+    if (circle == 1) return int64 ? pass_kernel_t<int64_t, 1, 1>(mode) : pass_kernel_t<int32_t, 1, 1>(mode);
+    if (circle == 2) return int64 ? pass_kernel_t<int64_t, 1, 2>(mode) : pass_kernel_t<int32_t, 1, 2>(mode);
+    if (int64) return pf == 2 ? pass_kernel_t<int64_t, 2, 0>(mode) : pf ? pass_kernel_t<int64_t, 1, 0>(mode) : pass_kernel_t<int64_t, 0, 0>(mode);
+    return pf == 2 ? pass_kernel_t<int32_t, 2, 0>(mode) : pf ? pass_kernel_t<int32_t, 1, 0>(mode) : pass_kernel_t<int32_t, 0, 0>(mode);
 }
 
-int pass_blocks_per_sm(int mode, bool int64, bool pref, int circle) {
+static int pass_dyn_smem(int mode, int pf, int circle) {
+    return (pf == 2 && !circle && (mode == MODE_WRITE_NC || (mode == MODE_WRITE && PF_WRITE_TMA == 2)))
+               ? 8 * (int)kTmaWarpBytes : 0;
+}
+
+int pass_blocks_per_sm(int mode, bool int64, int pf, int circle) {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, pass_kernel(mode, int64, pref, circle), 256, 0);
+    const PassKernel k = pass_kernel(mode, int64, pf, circle);
+    const int dyn = pass_dyn_smem(mode, pf, circle);
+    if (dyn) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, 256, dyn);
     return n > 0 ? n : 1;
 }
 
-cudaError_t launch_pass(int mode, bool int64, bool pref, int circle, const PassArgs& a, int grid, cudaStream_t st) {
-    pass_kernel(mode, int64, pref, circle)<<<grid, 256, 0, st>>>(a);
+cudaError_t launch_pass(int mode, bool int64, int pf, int circle, const PassArgs& a, int grid, cudaStream_t st) {
+    pass_kernel(mode, int64, pf, circle)<<<grid, 256, pass_dyn_smem(mode, pf, circle), st>>>(a);
     return cudaGetLastError();
 }
 

@@ -225,6 +225,24 @@ def test_tail_depth_variants(seed, tail_depth, torch_dev):
     assert (h.stats()["tests"], h.stats()["votes"]) == (ref.tests, ref.votes)
 
 
+@pytest.mark.parametrize("prefetch", [1, 2, 3])
+@pytest.mark.parametrize("seed", range(6))
+def test_prefetch_modes(seed, prefetch, torch_dev):
+    """The list passes' work loop with the descriptor prefetched only (1), with the next chunk's
+    entries in registers (2), and with a bulk-copy (cp.async.bulk + mbarrier) ring two chunks ahead
+    (3) give identical results, including many ranges (list bases) and int64."""
+    rng = np.random.default_rng(800 + seed)
+    N = int(rng.choice([64, 200, 256]))
+    D = int(rng.integers(6, 10))
+    T = int(rng.choice([1, 3, 8]))
+    pts = synth.random_scene(8100 + seed, N, max_lines=5, max_noise=int(rng.choice([500, 4000])))
+    ref = oracle.detect(pts, N, D, T, AB)
+    for budget in (0, 128 << 10):
+        h = _run(pts, N, D, T, AB, torch_dev, prefetch=prefetch, mem_budget=budget, force_int64=bool(seed % 2))
+        compare_all(h, ref, AB, D)
+        assert (h.stats()["tests"], h.stats()["votes"]) == (ref.tests, ref.votes)
+
+
 @pytest.mark.parametrize("tail_units", [0, 2])
 @pytest.mark.parametrize("seed", range(6))
 def test_fused_tail_work_units(seed, tail_units, torch_dev):
