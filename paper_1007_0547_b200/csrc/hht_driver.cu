@@ -464,12 +464,18 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
     a.child_level = child_level;
     a.leaf_level = leaf;
     a.need_lists = need_lists;
-    // offsets are read by chunk maps and range selection: list levels, and level D-1 (the
-    // count-only pass selects its range there)
-    a.write_off = need_lists || child_level == x->D - 1;
+    // offsets are read by chunk maps and range selection: list levels, and level D-1 when a
+    // count-only pass runs there (circle variants, depth < 3; the tails never read them). The child ->
+    // next-index map is read by the passes over the parents' lists (list levels) and that count-only
+    // pass; a leaf grid's gathers need neither.
+    const bool count_only = x->circle || x->D < 3;
+    a.write_off = need_lists || (child_level == x->D - 1 && count_only);
     a.record = record;
     a.T = x->T;
-    a.nf = (uint32_t*)C.nf.p;
+    // the pass over the deepest list level (a write pass, a fused tail rastering only split children,
+    // or the count-only pass) reads its children's map: levels up to one below the deepest lists
+    const int list_max = x->D - (count_only ? 2 : tail_depth(x));
+    a.nf = child_level <= list_max + 1 ? (uint32_t*)C.nf.p : nullptr;
     a.nfoff = need_lists ? (uint64_t*)C.nfoff.p : nullptr;
     a.out = C.frontier();
     a.rec = record ? (Record*)x->rec[child_level].b.p + x->rec[child_level].n : nullptr;

@@ -2485,7 +2485,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
                     if (A.record) s_rec[wid][4 * lane + (q ^ swz)] = make_uint4(tree, ca, cb, v[q]);
                 }
                 if (!A.leaf_level) {
-                    reinterpret_cast<uint4*>(A.nf)[p] = make_uint4(nf4[0], nf4[1], nf4[2], nf4[3]);
+                    if (A.nf) reinterpret_cast<uint4*>(A.nf)[p] = make_uint4(nf4[0], nf4[1], nf4[2], nf4[3]);
                     if (A.need_lists) {
                         ulonglong2* o = reinterpret_cast<ulonglong2*>(A.nfoff + 4 * (uint64_t)p);
                         o[0] = make_ulonglong2(so[0], so[1]);
