@@ -446,7 +446,7 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
     const bool record = x->opts.record_levels != 0;
     if (record) TRY(grow(x, x->rec[child_level], sizeof(Record), x->rec[child_level].n + nch));
     const uint32_t ntiles = (Fp + kSplitThreads - 1) / kSplitThreads;
-    TRY(ensure(x, x->tiles, (size_t)ntiles * sizeof(TileDesc)));
+    TRY(ensure(x, x->tiles, (size_t)(ntiles + kScanBlocks) * sizeof(TileDesc)));
     CK(cudaMemsetAsync(x->tiles.p, 0, (size_t)ntiles * sizeof(TileDesc), x->st));
     CK(cudaMemsetAsync(x->tilectr.p, 0, 4, x->st));
 
@@ -481,6 +481,7 @@ hht_status do_split(hht_ctx* x, int child_level, Level& P, uint32_t r0, uint32_t
     a.rec = record ? (Record*)x->rec[child_level].b.p + x->rec[child_level].n : nullptr;
     a.leaves = leaf ? (LeafRec*)x->leaves.b.p + x->leaves.n : nullptr;
     a.tiles = (TileDesc*)x->tiles.p;
+    a.scan_seg = (TileDesc*)x->tiles.p + ntiles;
     a.tile_counter = (uint32_t*)x->tilectr.p;
     a.stats = (unsigned long long*)x->stats.p;
     a.totals = x->totals_m;

@@ -146,6 +146,7 @@ struct SplitArgs {
     Record* rec;                   // records of child_level, rec[4*p + q]
     LeafRec* leaves;               // leaves[leaf index]
     TileDesc* tiles;
+    TileDesc* scan_seg;            // [kScanBlocks] segment descriptors of k_split_scan's look-back
     uint32_t* tile_counter;
     unsigned long long* stats;
     Totals* totals;
@@ -169,6 +170,7 @@ cudaError_t launch_pass(int mode, bool int64, int pf, int circle, const PassArgs
 cudaError_t launch_split(const SplitArgs& a, int resident_blocks, cudaStream_t st);
 int split_blocks_per_sm();
 constexpr uint32_t kSplitPrescanTiles = 1024;   // reduce-then-scan split from this many tiles on
+constexpr uint32_t kScanBlocks = 128;           // k_split_scan: at most this many segments (<= one block per SM)
 cudaError_t launch_chunk_map(const uint64_t* choff, const uint64_t* off, const uint32_t* len, const uint32_t* a,
                              const uint32_t* c, const uint32_t* tree, const uint8_t* tree_beta, uint32_t F,
                              ChunkDesc* chunks, cudaStream_t st);

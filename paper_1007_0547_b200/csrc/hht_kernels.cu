@@ -2543,63 +2543,109 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const SplitArgs A) {
     }
 }
 
-// One block: exclusive scan of the tile aggregates of pass 1 into tiles[t].inc*, totals, sentinels.
-// Warp w owns the contiguous tile segment [w seg, (w + 1) seg) and walks it 32 tiles at a time
-// (coalesced loads, a warp scan per step, a running carry); the 32 segment totals are then scanned
-// and every warp adds its segment's offset in a second walk.
-__global__ void __launch_bounds__(1024) k_split_scan(const SplitArgs A) {
-    __shared__ Agg s_w[32];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t seg = (A.ntiles + 31) / 32;
-    const uint32_t t0 = wid * seg, t1 = min(A.ntiles, t0 + seg);
-    Agg carry = {0, 0, 0};
-    // 4 x 32 aggregates loaded per step (independent loads in flight; the aggregates are never
-    // written by this kernel, so the read-only path is safe), then scanned in order
-    constexpr int kU = 4;
-    for (uint32_t b = t0; b < t1; b += 32 * kU) {
-        Agg a[kU];
-#pragma unroll
-        for (int k = 0; k < kU; ++k) {
-            const uint32_t t = b + 32 * k + lane;
-            a[k] = {0, 0, 0};
-            if (t < t1) a[k] = {__ldg(&A.tiles[t].aggF), __ldg(&A.tiles[t].aggC), __ldg(&A.tiles[t].aggS)};
-        }
-#pragma unroll
-        for (int k = 0; k < kU; ++k) {
-            const uint32_t t = b + 32 * k + lane;
-            const Agg incl = warp_inclusive(a[k], lane);
-            if (t < t1) {
-                A.tiles[t].incF = carry.F + incl.F - a[k].F;
-                A.tiles[t].incC = carry.C + incl.C - a[k].C;
-                A.tiles[t].incS = carry.S + incl.S - a[k].S;
-            }
-            carry = agg_add(carry, Agg{__shfl_sync(kFull, incl.F, 31), __shfl_sync(kFull, incl.C, 31), shfl_u64(incl.S, 31)});
-        }
-    }
-    if (lane == 0) s_w[wid] = carry;
+// Exclusive scan of the tile aggregates of pass 1 into tiles[t].inc*, totals and sentinels, by
+// kScanBlocks resident blocks: block b owns a contiguous segment of tiles, reduces it (coalesced),
+// gets its segment prefix from a warp-wide decoupled look-back over the earlier segments (all blocks
+// are resident: the grid is at most one block per SM), then scans its segment in 1024-tile steps.
+// (One block did this at ~10 MB of aggregates per C4 leaf-level split: 0.52 ms, bound by one SM's
+// bandwidth.)
+__device__ __forceinline__ Agg block_total_agg(Agg v, Agg* s_w) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const Agg w = warp_total(v);
+    if (lane == 0) s_w[wid] = w;
     __syncthreads();
+    Agg t = {0, 0, 0};
     if (wid == 0) {
-        const Agg w = s_w[lane];
-        const Agg wi = warp_inclusive(w, lane);
-        s_w[lane] = {wi.F - w.F, wi.C - w.C, wi.S - w.S};
-        if (lane == 31) {
-            A.totals->F = wi.F;
-            A.totals->S = wi.S;
-            A.totals->C = wi.C;
-            if (!A.leaf_level) {
-                A.out.off[wi.F] = wi.S;
-                A.out.choff[wi.F] = wi.C;
+        t = lane < (int)(blockDim.x >> 5) ? s_w[lane] : Agg{0, 0, 0};
+        t = warp_total(t);
+        if (lane == 0) s_w[32] = t;
+    }
+    __syncthreads();
+    t = s_w[32];
+    __syncthreads();
+    return t;
+}
+
+__global__ void __launch_bounds__(1024) k_split_scan(const SplitArgs A, TileDesc* seg_desc) {
+    __shared__ Agg s_w[33];
+    __shared__ Agg s_prefix;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t nseg = gridDim.x, seg = (A.ntiles + nseg - 1) / nseg;
+    const uint32_t t0 = min(A.ntiles, blockIdx.x * seg), t1 = min(A.ntiles, t0 + seg);
+    // 1. segment aggregate
+    Agg mine = {0, 0, 0};
+    for (uint32_t t = t0 + tid; t < t1; t += blockDim.x)
+        mine = agg_add(mine, Agg{__ldg(&A.tiles[t].aggF), __ldg(&A.tiles[t].aggC), __ldg(&A.tiles[t].aggS)});
+    const Agg segtot = block_total_agg(mine, s_w);
+    // 2. segment prefix: decoupled look-back over the earlier segments (warp 0)
+    if (wid == 0) {
+        Agg excl = {0, 0, 0};
+        if (blockIdx.x == 0) {
+            if (lane == 0) publish(seg_desc, segtot, 2);
+        } else {
+            if (lane == 0) publish(seg_desc + blockIdx.x, segtot, 1);
+            int64_t pred = (int64_t)blockIdx.x - 1;
+            while (true) {
+                const int64_t t = pred - lane;
+                uint32_t st = 2;
+                Agg val = {0, 0, 0};
+                if (t >= 0) {
+                    TileDesc* d = seg_desc + t;
+                    do { st = dev_u32(d->status).load(cuda::memory_order_relaxed); } while (st == 0);
+                    cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
+                    if (st == 1) val = {dev_u32(d->aggF).load(cuda::memory_order_relaxed), dev_u32(d->aggC).load(cuda::memory_order_relaxed),
+                                        dev_u64(d->aggS).load(cuda::memory_order_relaxed)};
+                    else val = {dev_u32(d->incF).load(cuda::memory_order_relaxed), dev_u32(d->incC).load(cuda::memory_order_relaxed),
+                                dev_u64(d->incS).load(cuda::memory_order_relaxed)};
+                }
+                const uint32_t pm = __ballot_sync(kFull, st == 2);
+                const int stop = pm ? __ffs(pm) - 1 : 31;
+                if (lane > stop) val = {0, 0, 0};
+                excl = agg_add(excl, warp_total(val));
+                if (pm) break;
+                pred -= 32;
+            }
+            if (lane == 0) publish(seg_desc + blockIdx.x, agg_add(excl, segtot), 2);
+        }
+        if (lane == 0) {
+            s_prefix = excl;
+            if (blockIdx.x == nseg - 1) {
+                const Agg tot = agg_add(excl, segtot);
+                A.totals->F = tot.F;
+                A.totals->S = tot.S;
+                A.totals->C = tot.C;
+                if (!A.leaf_level) {
+                    A.out.off[tot.F] = tot.S;
+                    A.out.choff[tot.F] = tot.C;
+                }
             }
         }
     }
     __syncthreads();
-    const Agg off = s_w[wid];
-    if (off.F | off.C | off.S) {
-        for (uint32_t t = t0 + lane; t < t1; t += 32) {
-            A.tiles[t].incF += off.F;
-            A.tiles[t].incC += off.C;
-            A.tiles[t].incS += off.S;
+    // 3. the segment's exclusive tile prefixes, 1024 tiles per step
+    Agg carry = s_prefix;
+    for (uint32_t base = t0; base < t1; base += blockDim.x) {
+        const uint32_t t = base + tid;
+        Agg a = {0, 0, 0};
+        if (t < t1) a = {__ldg(&A.tiles[t].aggF), __ldg(&A.tiles[t].aggC), __ldg(&A.tiles[t].aggS)};
+        const Agg incl = warp_inclusive(a, lane);
+        if (lane == 31) s_w[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            const Agg w = lane < (int)(blockDim.x >> 5) ? s_w[lane] : Agg{0, 0, 0};
+            const Agg wi = warp_inclusive(w, lane);
+            if (lane < (int)(blockDim.x >> 5)) s_w[lane] = {wi.F - w.F, wi.C - w.C, wi.S - w.S};
+            if (lane == 31) s_w[32] = wi;
         }
+        __syncthreads();
+        if (t < t1) {
+            const Agg wb = s_w[wid];
+            A.tiles[t].incF = carry.F + wb.F + incl.F - a.F;
+            A.tiles[t].incC = carry.C + wb.C + incl.C - a.C;
+            A.tiles[t].incS = carry.S + wb.S + incl.S - a.S;
+        }
+        carry = agg_add(carry, s_w[32]);
+        __syncthreads();
     }
 }
 
@@ -2623,7 +2669,9 @@ cudaError_t launch_split(const SplitArgs& a, int resident_blocks, cudaStream_t s
     SplitArgs b = a;
     b.pass = 1;
     k_split<<<grid, kSplitThreads, 0, st>>>(b);
-    k_split_scan<<<1, 1024, 0, st>>>(b);
+    const uint32_t nseg = std::min<uint32_t>(kScanBlocks, (a.ntiles + 1023) / 1024);
+    cudaMemsetAsync(a.scan_seg, 0, nseg * sizeof(TileDesc), st);
+    k_split_scan<<<nseg, 1024, 0, st>>>(b, a.scan_seg);
     b.pass = 2;
     k_split<<<grid, kSplitThreads, 0, st>>>(b);
     return cudaGetLastError();
