@@ -246,7 +246,10 @@ cudaError_t launch_rm_rows(const LeafRec* leaves, const uint64_t* cand_lo, const
 cudaError_t launch_removal(const RmArgs& a, const LeafRec* leaves, bool int64, int grid, cudaStream_t st);
 // Latency path (k_small): the whole level-synchronous traversal of a tiny detection in ONE block.
 struct SmallArgs {
-    const uint32_t* packed;        // staged points
+    uint32_t* packed;              // staged points (written here when `pts` is set)
+    const int2* pts;               // non-null: raw device points [npts], staged and range-checked in the
+    uint64_t npts;                 //   kernel (no separate stage launch); null: `packed` is already staged
+    uint32_t* fin;                 // mapped host block (k_finish's layout): range flag, counts, statistics
     const uint64_t* tree_off;      // [ntrees] first point of each tree in `packed`
     const uint32_t* tree_n;        // [ntrees] points of each tree
     const uint8_t* tree_beta;
@@ -254,13 +257,8 @@ struct SmallArgs {
     int N, D;
     uint64_t T;
     // scratch (capacities from the host's bounds)
-    uint32_t* list[2];             // candidate lists of the current / next frontier
-    uint32_t* f_tree[2];           // frontier (regions split at the current level) and next
-    uint32_t* f_a[2];
-    uint32_t* f_c[2];
-    uint32_t* f_off[2];            // [F + 1] list offsets
-    uint32_t* cv;                  // [4 F] child votes, then split flags / scan
-    uint32_t* cursor;              // [4 F] append cursors of the next lists
+    uint32_t* list[2];             // global_scratch: the two candidate lists (list[1] = list[0] + smem_S);
+                                   // the frontier arrays, votes and frontier indices are in shared memory
     // outputs
     Record* const* rec;            // [D + 1] per-level record arrays
     LeafRec* leaves;

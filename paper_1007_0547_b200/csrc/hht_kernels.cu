@@ -1840,208 +1840,316 @@ __device__ uint32_t block_scan(uint32_t* v, uint32_t n, uint32_t* s_warp) {
 }
 }  // namespace
 
+// frontier tree ids carry the tree's half in their top bit: no global load per region in the passes
+constexpr uint32_t kSmallBeta = 1u << 31;
+
+#ifdef HHT_SMALL_TRACE
+// phase timestamps of the last k_small launch (experiment builds only: scripts/build_variant.sh)
+__device__ unsigned long long g_small_trace[512];
+#define SMALL_MARK(k) do { if (threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_small_trace[k] = t_; } } while (0)
+extern "C" int hht_debug_small_trace(unsigned long long* host) {
+    return (int)cudaMemcpyFromSymbol(host, g_small_trace, sizeof g_small_trace);
+}
+#else
+#define SMALL_MARK(k) do { } while (0)
+#endif
+
 template <typename I>
-__global__ void __launch_bounds__(1024) k_small(SmallArgs A) {
-    __shared__ uint32_t s_warp[33];
-    __shared__ uint32_t s_F, s_S;
+__global__ void __launch_bounds__(1024) k_small(const SmallArgs A) {
+    __shared__ uint32_t s_warp[33], s_warp2[33];
+    __shared__ uint32_t s_F;
     __shared__ unsigned long long s_v[32], s_sv[32];
     // every per-level array lives in shared memory (the host admits only problems that fit), so the
-    // ~12 dependent phases of a level cost shared-memory, not L2, round trips
+    // dependent phases of a level cost shared-memory, not L2, round trips
     extern __shared__ uint4 s_small_dyn[];
-    {
-        // frontier arrays always in shared memory; the two candidate lists too unless the host gave
-        // device buffers for them (global_scratch: lists too large for shared memory)
-        uint32_t* w = reinterpret_cast<uint32_t*>(s_small_dyn);
-        const uint32_t Sm = A.smem_S, Fm = A.smem_F;
-        if (!A.global_scratch) {
-            A.list[0] = w; w += Sm;
-            A.list[1] = w; w += Sm;
-        }
-        for (int b = 0; b < 2; ++b) {
-            A.f_tree[b] = w; w += Fm + 1;
-            A.f_a[b] = w; w += Fm + 1;
-            A.f_c[b] = w; w += Fm + 1;
-            A.f_off[b] = w; w += Fm + 1;
-        }
-        A.cv = w; w += 4 * Fm;
-        A.cursor = w;
-    }
-    const int tid = threadIdx.x;
+    // layout: [list 0 | list 1] (unless the host gave device buffers: global_scratch), then per
+    // buffer b = 0, 1 the frontier arrays tree | a | c | off of FS = smem_F + 1 entries each, then the
+    // child votes and the children's frontier indices. Buffers are addressed as base + b * stride, so
+    // nothing indexes a pointer array with the level parity (that would live in local memory)
+    uint32_t* w = reinterpret_cast<uint32_t*>(s_small_dyn);
+    const uint32_t Sm = A.smem_S, FS = A.smem_F + 1;
+    uint32_t* list0 = A.list[0];
+    if (!A.global_scratch) { list0 = w; w += 2 * Sm; }
+    uint32_t* const fr = w;                              // frontier buffer 0, buffer 1 at fr + 4 FS
+    uint32_t* const cv = fr + 8 * FS;                    // [4 F] child votes
+    uint32_t* const cursor = cv + 4 * (FS - 1);          // [4 F] split child's frontier index or kNone
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     const I N = (I)A.N;
     const int D = A.D;
-    unsigned long long tests = 0, votes = 0;          // thread 0 accumulates
-    for (int i = tid; i < kStatCount; i += blockDim.x) A.stats[i] = 0;   // the call's statistics start at 0
-    __syncthreads();
+    unsigned long long my_v = 0, my_t = 0;              // this thread's share of the votes and tests
+    SMALL_MARK(0);
+    for (uint32_t i = tid; i < kStatCount; i += blockDim.x) A.stats[i] = 0;   // the call's statistics start at 0
+    for (uint32_t i = tid; i < (uint32_t)D + 2; i += blockDim.x) A.counts[i] = 0;   // levels never reached stay 0
+    // K0 in the same launch: stage and range-check the points (an out-of-range point fails
+    // the call before any traversal; the host reads the flag with the results)
+    if (A.pts) {
+        uint32_t bad = 0;
+        for (uint64_t i = tid; i < A.npts; i += blockDim.x) {
+            const int2 p = A.pts[i];
+            const bool ok = (unsigned)p.x < (unsigned)A.N && (unsigned)p.y < (unsigned)A.N;
+            bad |= !ok;
+            A.packed[i] = ok ? (((uint32_t)p.x << 16) | (uint32_t)p.y) : 0u;
+        }
+        if (__syncthreads_or(bad)) {
+            if (tid == 0) {
+                A.fin[0] = 1;
+                __threadfence_system();
+            }
+            return;
+        }
+    }
     // level 0: roots (every line crosses the root); split iff E > T (reading R6)
     if (tid == 0) {
         uint32_t F = 0, S = 0;
         for (uint32_t t = 0; t < A.ntrees; ++t) {
             const uint32_t E = A.tree_n[t];
             A.rec[0][t] = {t, 0, 0, E};
-            tests += E;
-            votes += E;
+            my_t += E;
+            my_v += E;
             if ((uint64_t)E > A.T) {
-                A.f_tree[0][F] = t; A.f_a[0][F] = 0; A.f_c[0][F] = 0; A.f_off[0][F] = S;
+                fr[F] = t | (A.tree_beta[t] ? kSmallBeta : 0u);
+                fr[FS + F] = 0;
+                fr[2 * FS + F] = 0;
+                fr[3 * FS + F] = S;
                 S += E;
                 ++F;
-                tests += 4ull * E;                        // the root's 4 child tests per point
-                A.stats[kStatSplit0] += 1;
+                my_t += 4ull * E;                         // the root's 4 child tests per point
             }
         }
-        A.f_off[0][F] = S;
+        fr[3 * FS + F] = S;
         A.counts[0] = A.ntrees;
-        A.stats[kStatVisited0] = A.ntrees;
         s_F = F;
-        s_S = S;
     }
     __syncthreads();
+    if (tid == 0) {                                       // after the zeroing above
+        A.stats[kStatVisited0] = A.ntrees;
+        A.stats[kStatSplit0] = s_F;
+    }
     // root lists: the trees' points, in frontier order
-    {
-        const uint32_t F = s_F;
-        for (uint32_t r = 0; r < F; ++r) {
-            const uint32_t t = A.f_tree[0][r], o = A.f_off[0][r], n = A.tree_n[t];
-            for (uint32_t i = tid; i < n; i += blockDim.x) A.list[0][o + i] = A.packed[A.tree_off[t] + i];
-        }
+    for (uint32_t r = 0; r < s_F; ++r) {
+        const uint32_t t = fr[r] & ~kSmallBeta, o = fr[3 * FS + r], n = A.tree_n[t];
+        const uint32_t* src = A.packed + A.tree_off[t];
+        for (uint32_t i = tid; i < n; i += blockDim.x) list0[o + i] = src[i];
     }
     __syncthreads();
-    int cur = 0;
+    SMALL_MARK(1);
     for (int l = 0; l < D; ++l) {
-        const uint32_t F = s_F, S = s_S;
+        const uint32_t F = s_F;
         if (F == 0) break;
+        const uint32_t cur = (uint32_t)l & 1u;
+        const uint32_t* const list = list0 + cur * Sm;
+        uint32_t* const nlist = list0 + (cur ^ 1u) * Sm;
+        const uint32_t* const ftree = fr + cur * 4 * FS;
+        const uint32_t* const fa = ftree + FS;
+        const uint32_t* const fc = ftree + 2 * FS;
+        const uint32_t* const off = ftree + 3 * FS;
+        uint32_t* const ntree = fr + (cur ^ 1u) * 4 * FS;
         const int sh = D - l;
         const I Qc = ((I)3 * N) << (sh - 1);
-        const uint32_t* list = A.list[cur];
-        const uint32_t* off = A.f_off[cur];
-        for (uint32_t i = tid; i < 4 * F; i += blockDim.x) A.cv[i] = 0;
-        __syncthreads();
-        // pass 1: child votes
-        for (uint32_t i = tid; i < S; i += blockDim.x) {
-            uint32_t lo = 0, hi = F - 1;                // region of pair i: last r with off[r] <= i
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi + 1) / 2;
-                if (off[mid] <= i) lo = mid; else hi = mid - 1;
+        SMALL_MARK(8 + 8 * l);
+        // pass 1 (level 0 only; deeper levels get their child votes from the previous level's pass 2):
+        // child votes. A warp owns whole regions (their pairs are contiguous in the list): the region's
+        // data is loaded once, no search per pair, and the warp sums the 4 child votes itself
+        if (l == 0) {
+            for (uint32_t r = wid; r < F; r += nw) {
+                const bool beta = (ftree[r] & kSmallBeta) != 0;
+                const I i0 = (I)fa[r] << sh, j0 = (I)fc[r] << sh;
+                const I alpha = ((I)1 << D) - 2 * i0, gb = (N << D) - (I)3 * N * j0;
+                uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+                for (uint32_t i = off[r] + lane; i < off[r + 1]; i += 32) {
+                    const uint32_t p = list[i];
+                    const I ex = (I)(beta ? (p & 0xFFFFu) : (p >> 16)), ey = (I)(beta ? (p >> 16) : (p & 0xFFFFu));
+                    const I g = ex * alpha + (ey << D) + gb;   // G(SW)
+                    const I Pc = ex << sh, Uc = Pc + Qc;
+                    // children NE, NW, SW, SE: SW values g - Pc - Qc, g - Qc, g, g - Pc
+                    v0 += g - Pc - Qc > 0 && g - Pc - Qc <= Uc;
+                    v1 += g - Qc > 0 && g - Qc <= Uc;
+                    v2 += g > 0 && g <= Uc;
+                    v3 += g - Pc > 0 && g - Pc <= Uc;
+                }
+                v0 = __reduce_add_sync(0xFFFFFFFFu, v0);
+                v1 = __reduce_add_sync(0xFFFFFFFFu, v1);
+                v2 = __reduce_add_sync(0xFFFFFFFFu, v2);
+                v3 = __reduce_add_sync(0xFFFFFFFFu, v3);
+                if (lane == 0) { cv[4 * r] = v0; cv[4 * r + 1] = v1; cv[4 * r + 2] = v2; cv[4 * r + 3] = v3; }
             }
-            const uint32_t r = lo, w = list[i];
-            const bool beta = A.tree_beta[A.f_tree[cur][r]] != 0;
-            const I ex = (I)(beta ? (w & 0xFFFFu) : (w >> 16)), ey = (I)(beta ? (w >> 16) : (w & 0xFFFFu));
-            const I i0 = (I)A.f_a[cur][r] << sh, j0 = (I)A.f_c[cur][r] << sh;
-            const I g = ex * (((I)1 << D) - 2 * i0) + (ey << D) + (N << D) - (I)3 * N * j0;   // G(SW)
-            const I Pc = ex << sh, Uc = Pc + Qc;
-            // children NE, NW, SW, SE: SW values g - Pc - Qc, g - Qc, g, g - Pc
-            const I gq[4] = {g - Pc - Qc, g - Qc, g, g - Pc};
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (gq[q] > 0 && gq[q] <= Uc) atomicAdd(A.cv + 4 * r + q, 1u);
+            __syncthreads();
         }
-        __syncthreads();
-        // children: records of all, split flags, next frontier / leaves
+        SMALL_MARK(9 + 8 * l);
+        // children, in one block scan of (split flag, split ? votes : 0): records of all, the next
+        // frontier with its list offsets (or the leaves at level D), and each child's frontier index
         const bool leaf = l + 1 == D;
-        unsigned long long my_v = 0, my_sv = 0;          // this thread's votes / votes of split children
-        for (uint32_t k = tid; k < 4 * F; k += blockDim.x) {
-            const uint32_t r = k >> 2, q = k & 3, v = A.cv[k];
-            const uint32_t ca = 2 * A.f_a[cur][r] + quad_da((int)q), cb = 2 * A.f_c[cur][r] + quad_dc((int)q);
-            A.rec[l + 1][k] = {A.f_tree[cur][r], ca, cb, v};
-            const bool split = (uint64_t)v > A.T;
-            A.cursor[k] = split ? 1u : 0u;                   // split flag, scanned below
-            my_v += v;
-            if (split) my_sv += v;
-        }
-        // block sums of the votes (every visited child) and of the split children's votes
+        Record* const rec = A.rec[l + 1];
+        uint32_t nf = 0, S2 = 0;                         // running totals of the scan
+        for (uint32_t base = 0; base < 4 * F; base += blockDim.x) {
+            const uint32_t k = base + tid, r = k >> 2, q = k & 3;
+            const bool ok = k < 4 * F;
+            const uint32_t v = ok ? cv[k] : 0u;
+            const bool split = ok && (uint64_t)v > A.T;
+            uint32_t tr = 0, ca = 0, cb = 0;
+            if (ok) {
+                tr = ftree[r];
+                ca = 2 * fa[r] + quad_da((int)q);
+                cb = 2 * fc[r] + quad_dc((int)q);
+                rec[k] = {tr & ~kSmallBeta, ca, cb, v};
+                my_v += v;
+                if (split && !leaf) my_t += 4ull * v;      // 4 code evaluations per voter of a split region
+            }
+            uint32_t in = split ? 1u : 0u, is = split ? v : 0u;
 #pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) {
-            my_v += __shfl_xor_sync(0xFFFFFFFFu, my_v, d);
-            my_sv += __shfl_xor_sync(0xFFFFFFFFu, my_sv, d);
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t tn = __shfl_up_sync(0xFFFFFFFFu, in, d), ts = __shfl_up_sync(0xFFFFFFFFu, is, d);
+                if (lane >= d) { in += tn; is += ts; }
+            }
+            if (lane == 31) { s_warp[wid] = in; s_warp2[wid] = is; }
+            __syncthreads();
+            if (wid == 0) {
+                const uint32_t wn = lane < nw ? s_warp[lane] : 0u, ws = lane < nw ? s_warp2[lane] : 0u;
+                uint32_t xn = wn, xs = ws;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t tn = __shfl_up_sync(0xFFFFFFFFu, xn, d), ts = __shfl_up_sync(0xFFFFFFFFu, xs, d);
+                    if (lane >= d) { xn += tn; xs += ts; }
+                }
+                if (lane < nw) { s_warp[lane] = xn - wn; s_warp2[lane] = xs - ws; }
+                if (lane == 31) { s_warp[32] = xn; s_warp2[32] = xs; }
+            }
+            __syncthreads();
+            const uint32_t f = nf + s_warp[wid] + in - 1;  // this child's frontier index when split
+            if (split) {
+                if (leaf) {
+                    A.leaves[f] = {tr & ~kSmallBeta, ca, cb, v};
+                } else {
+                    ntree[f] = tr;
+                    ntree[FS + f] = ca;
+                    ntree[2 * FS + f] = cb;
+                    ntree[3 * FS + f] = S2 + s_warp2[wid] + is - v;
+                }
+            }
+            if (ok && !leaf) cursor[k] = split ? f : kNone;
+            nf += s_warp[32];
+            S2 += s_warp2[32];
+            __syncthreads();                               // s_warp reuse; frontier complete for pass 2
         }
-        if ((tid & 31) == 0) { s_v[tid >> 5] = my_v; s_sv[tid >> 5] = my_sv; }
+        SMALL_MARK(10 + 8 * l);
         if (tid == 0) {
             A.counts[l + 1] = 4 * F;
             A.stats[kStatVisited0 + l + 1] = 4ull * F;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            unsigned long long bv = 0, bsv = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { bv += s_v[w]; bsv += s_sv[w]; }
-            votes += bv;
-            if (!leaf) tests += 4 * bsv;                     // 4 code evaluations per voter of a split region
-        }
-        const uint32_t nf = block_scan(A.cursor, 4 * F, s_warp);       // cursor[k] = next index
-        // next frontier, list offsets from the votes of the split children
-        const int nxt = cur ^ 1;
-        for (uint32_t k = tid; k < 4 * F; k += blockDim.x) {
-            const uint32_t v = A.cv[k];
-            if ((uint64_t)v > A.T) {
-                const uint32_t f = A.cursor[k], r = k >> 2, q = k & 3;
-                const uint32_t ca = 2 * A.f_a[cur][r] + quad_da((int)q), cb = 2 * A.f_c[cur][r] + quad_dc((int)q);
-                if (leaf) {
-                    A.leaves[f] = {A.f_tree[cur][r], ca, cb, v};
-                } else {
-                    A.f_tree[nxt][f] = A.f_tree[cur][r]; A.f_a[nxt][f] = ca; A.f_c[nxt][f] = cb;
-                    A.f_off[nxt][f] = v;                   // scanned into offsets below
-                }
-            }
-        }
-        __syncthreads();
-        if (tid == 0) {
             if (leaf) {
                 A.counts[D + 1] = nf;
                 A.stats[kStatLeaves] = nf;
             } else {
                 A.stats[kStatSplit0 + l + 1] = nf;
+                ntree[3 * FS + nf] = S2;
+                s_F = nf;
             }
         }
         if (leaf) break;
-        const uint32_t S2 = block_scan(A.f_off[nxt], nf, s_warp);
-        if (tid == 0) { A.f_off[nxt][nf] = S2; s_F = nf; s_S = S2; }
-        // cursors of the split children: next-frontier index per child, kNone otherwise
-        for (uint32_t k = tid; k < 4 * F; k += blockDim.x) {
-            const uint32_t f = A.cursor[k];
-            A.cursor[k] = (uint64_t)A.cv[k] > A.T ? f : kNone;
-        }
-        __syncthreads();
-        for (uint32_t k = tid; k < nf; k += blockDim.x) A.cv[k] = 0;      // reuse: append cursors
-        __syncthreads();
-        // pass 2: append each candidate to the lists of the split children it crosses
-        for (uint32_t i = tid; i < S; i += blockDim.x) {
-            uint32_t lo = 0, hi = F - 1;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi + 1) / 2;
-                if (off[mid] <= i) lo = mid; else hi = mid - 1;
-            }
-            const uint32_t r = lo, w = list[i];
-            const bool beta = A.tree_beta[A.f_tree[cur][r]] != 0;
-            const I ex = (I)(beta ? (w & 0xFFFFu) : (w >> 16)), ey = (I)(beta ? (w >> 16) : (w & 0xFFFFu));
-            const I i0 = (I)A.f_a[cur][r] << sh, j0 = (I)A.f_c[cur][r] << sh;
-            const I g = ex * (((I)1 << D) - 2 * i0) + (ey << D) + (N << D) - (I)3 * N * j0;
-            const I Pc = ex << sh, Uc = Pc + Qc;
-            const I gq[4] = {g - Pc - Qc, g - Qc, g, g - Pc};
+        // pass 2: append each candidate to the lists of the split children it crosses and count, as it
+        // goes, the votes of those children's own 4 children (the next level's pass 1). A warp owns
+        // whole regions, so it alone writes their split children's lists and votes: positions from
+        // ballots and running counts, no atomics. Per-lane grandchild counts are packed two per word:
+        // a region's list is below 2^16 entries here (lists hold < kSmallGlobalMaxS = 2^16 entries and
+        // pass 2 runs only for D >= 2, where a tree's list at a level is at most S / 3)
+        {
+            const I Qc1 = ((I)3 * N) << (sh - 2);          // the child level's Q (sh >= 2 here)
+            const uint32_t* const noff = ntree + 3 * FS;
+            for (uint32_t r = wid; r < F; r += nw) {
+                const bool beta = (ftree[r] & kSmallBeta) != 0;
+                const I i0 = (I)fa[r] << sh, j0 = (I)fc[r] << sh;
+                const I alpha = ((I)1 << D) - 2 * i0, gb = (N << D) - (I)3 * N * j0;
+                const uint4 fq4 = *reinterpret_cast<const uint4*>(cursor + 4 * r);
+                const uint32_t fq[4] = {fq4.x, fq4.y, fq4.z, fq4.w};
+                uint32_t pos[4], c01[4], c23[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t f = A.cursor[4 * r + q];
-                if (f != kNone && gq[q] > 0 && gq[q] <= Uc)
-                    A.list[nxt][A.f_off[nxt][f] + atomicAdd(A.cv + f, 1u)] = w;
+                for (int q = 0; q < 4; ++q) {
+                    pos[q] = fq[q] != kNone ? noff[fq[q]] : 0u;
+                    c01[q] = c23[q] = 0;
+                }
+                const uint32_t e = off[r + 1];
+                for (uint32_t i = off[r] + lane; i - lane < e; i += 32) {
+                    const bool ok = i < e;
+                    const uint32_t p = ok ? list[i] : 0u;
+                    const I ex = (I)(beta ? (p & 0xFFFFu) : (p >> 16)), ey = (I)(beta ? (p >> 16) : (p & 0xFFFFu));
+                    const I g = ex * alpha + (ey << D) + gb;
+                    const I Pc = ex << sh, Uc = Pc + Qc;
+                    const I Pc1 = ex << (sh - 1), Uc1 = Pc1 + Qc1;
+                    const I gq[4] = {g - Pc - Qc, g - Qc, g, g - Pc};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const bool app = ok && fq[q] != kNone && gq[q] > 0 && gq[q] <= Uc;
+                        const uint32_t b = __ballot_sync(0xFFFFFFFFu, app);
+                        if (app) {
+                            nlist[pos[q] + __popc(b & ((1u << lane) - 1u))] = p;
+                            const I h = gq[q];                 // G(SW) of child q: its children as in pass 1
+                            c01[q] += (h - Pc1 - Qc1 > 0 && h - Pc1 - Qc1 <= Uc1 ? 1u : 0u) |
+                                      (h - Qc1 > 0 && h - Qc1 <= Uc1 ? 0x10000u : 0u);
+                            c23[q] += (h > 0 && h <= Uc1 ? 1u : 0u) | (h - Pc1 > 0 && h - Pc1 <= Uc1 ? 0x10000u : 0u);
+                        }
+                        pos[q] += __popc(b);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (fq[q] == kNone) continue;            // warp-uniform
+                    const uint32_t x01 = __reduce_add_sync(0xFFFFFFFFu, c01[q]);
+                    const uint32_t x23 = __reduce_add_sync(0xFFFFFFFFu, c23[q]);
+                    if (lane == 0)
+                        *reinterpret_cast<uint4*>(cv + 4 * fq[q]) = make_uint4(x01 & 0xFFFFu, x01 >> 16, x23 & 0xFFFFu, x23 >> 16);
+                }
             }
         }
         __syncthreads();
-        cur = nxt;
+        SMALL_MARK(14 + 8 * l);
     }
+    SMALL_MARK(7);
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        my_v += __shfl_xor_sync(0xFFFFFFFFu, my_v, d);
+        my_t += __shfl_xor_sync(0xFFFFFFFFu, my_t, d);
+    }
+    if (lane == 0) { s_v[wid] = my_v; s_sv[wid] = my_t; }
+    __syncthreads();
     if (tid == 0) {
+        unsigned long long votes = 0, tests = 0;
+        for (uint32_t i = 0; i < nw; ++i) { votes += s_v[i]; tests += s_sv[i]; }
         A.stats[kStatTests] = tests;
         A.stats[kStatVotes] = votes;
     }
+    // k_finish in the same launch: counts and statistics straight into the mapped host block
+    __syncthreads();
+    if (A.fin) {
+        for (uint32_t i = tid; i < (uint32_t)D + 2; i += blockDim.x) A.fin[1 + i] = A.counts[i];
+        unsigned long long* hs = reinterpret_cast<unsigned long long*>(A.fin + kFinishStatsWord);
+        for (uint32_t i = tid; i < kStatCount; i += blockDim.x) hs[i] = A.stats[i];
+        if (tid == 0) A.fin[0] = 0;
+        __threadfence_system();
+    }
 }
 
-uint64_t small_smem_bytes(uint32_t S, uint32_t F) { return 4ull * (2ull * S + 8ull * (F + 1) + 8ull * F); }
+// S is rounded up to a multiple of 4 entries (the host passes smem_S rounded): 16-byte aligned votes and
+// frontier indices after the two lists
+uint64_t small_smem_bytes(uint32_t S, uint32_t F) { return 4ull * (2ull * ((S + 3ull) & ~3ull) + 8ull * (F + 1) + 8ull * F); }
 uint64_t small_frontier_bytes(uint32_t F) { return 4ull * (8ull * (F + 1) + 8ull * F); }
 
 cudaError_t launch_small(const SmallArgs& a, bool int64, cudaStream_t st) {
     const int smem = (int)(a.global_scratch ? small_frontier_bytes(a.smem_F) : small_smem_bytes(a.smem_S, a.smem_F));
-    if (int64) {
-        cudaFuncSetAttribute(k_small<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        k_small<int64_t><<<1, 1024, smem, st>>>(a);
-    } else {
-        cudaFuncSetAttribute(k_small<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        k_small<int32_t><<<1, 1024, smem, st>>>(a);
+    // the dynamic shared-memory opt-in is raised only when a call needs more than any before on this
+    // device (one attribute call per growth, not per launch)
+    static int opted[2][64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& have = opted[int64 ? 1 : 0][dev & 63];
+    if (smem > have) {
+        const cudaError_t e = int64 ? cudaFuncSetAttribute(k_small<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+                                    : cudaFuncSetAttribute(k_small<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        have = smem;
     }
+    if (int64)
+        k_small<int64_t><<<1, 1024, smem, st>>>(a);
+    else
+        k_small<int32_t><<<1, 1024, smem, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -56,8 +56,10 @@ def _sampled_brute(h, pts, cfg, image, nsamp, rng):
             assert ((i, j) in cells) == (v > cfg.T), (half, i, j, v)
 
 
-@pytest.mark.parametrize("cid", [3, 4, 5])
-def test_fullsize_config(cid, cuda_device):
+@pytest.mark.parametrize("cid,int64", [(3, False), (4, False), (5, False), (3, True), (4, True)])
+def test_fullsize_config(cid, int64, cuda_device):
+    """The bench's launch configuration (int32, where exact for every config), and the int64
+    instantiation north_star names on configs 3 and 4, against the oracle's digests."""
     import torch
     path = os.path.join(GOLD, f"c{cid}_digest.json")
     cfg = synth.CONFIGS[cid]
@@ -66,11 +68,14 @@ def test_fullsize_config(cid, cuda_device):
     else:
         pts, _ = synth.config_image(cid)
         offs = np.array([0, pts.shape[0]])
-    h = hht.HHT(halves=cfg.halves, profile=True)       # the bench's launch configuration
+    h = hht.HHT(halves=cfg.halves, profile=True, force_int64=int64)   # profile on: as bench.py runs
     h.detect_batch(torch.from_numpy(pts).to(cuda_device), offs, cfg.N, cfg.D, cfg.T)
+    assert h.stats()["int_bits"] == (64 if int64 else 32)
     images = offs.shape[0] - 1
     assert os.path.exists(path), f"missing oracle digest {path} (scripts/write_golden.py --config {cid})"
     _digest_check(h, cfg, images, json.load(open(path)))
+    if int64:
+        return
     # structure of every tree (full output), sampled brute-force counts on image 0
     tests = 0
     for b in range(images if images <= 4 else 4):

@@ -167,3 +167,42 @@ def test_mid_path_range_error(cuda_device):
     with pytest.raises(hht.HHTError) as e:
         h.detect(_dev(np.array([[0, 0], [70, 1]], np.int32), cuda_device), 64, 6, 1)
     assert e.value.name == "HHT_ERANGE"
+
+
+@pytest.mark.gpu
+def test_small_path_range_error_then_recovers(cuda_device):
+    """k_small stages and range-checks the points itself: an out-of-range point fails the call with
+    HHT_ERANGE on the one-block path, and the next call on the same context is exact."""
+    h = hht.HHT(halves=AB)
+    with pytest.raises(hht.HHTError) as e:
+        h.detect(_dev(np.array([[0, 0], [3, 64]], np.int32), cuda_device), 64, 6, 1)
+    assert e.value.name == "HHT_ERANGE"
+    pts = synth.random_scene(4100, 64, max_lines=3, max_noise=40)
+    h.detect(_dev(pts, cuda_device), 64, 6, 4)
+    assert h.stats()["latency_path"] == 1
+    compare_all(h, oracle.detect(pts, 64, 6, 4, AB), AB, 6)
+
+
+@pytest.mark.gpu
+def test_small_path_constant_blocks_across_shapes(cuda_device):
+    """The latency path skips re-uploading its constant blocks (tree offsets, record pointers, half
+    flags) when a call repeats the previous one's; alternating shapes, halves and batch sizes on one
+    context must still match the oracle every time."""
+    h = hht.HHT(halves=AB)
+    ha = hht.HHT(halves=hht.ALPHA)
+    scenes = [(synth.random_scene(4200 + k, N, max_lines=3, max_noise=30), N, D, T)
+              for k, (N, D, T) in enumerate([(64, 6, 4), (32, 5, 3), (64, 6, 4), (128, 7, 6), (32, 5, 3)])]
+    for rep in range(2):
+        for pts, N, D, T in scenes:
+            for ctx, halves in ((h, AB), (ha, hht.ALPHA)):
+                ctx.detect(_dev(pts, cuda_device), N, D, T)
+                assert ctx.stats()["latency_path"] in (1, 2)   # k_small, or k_mid (128 px: its block overwrites)
+                compare_all(ctx, oracle.detect(pts, N, D, T, halves), halves, D)
+    imgs = [synth.random_scene(4300 + k, 64, max_lines=2, max_noise=20) for k in range(3)]
+    for nb in (3, 2, 3):
+        offs = np.zeros(nb + 1, dtype=np.int64)
+        offs[1:] = np.cumsum([len(p) for p in imgs[:nb]])
+        h.detect_batch(_dev(np.concatenate(imgs[:nb]), cuda_device), offs, 64, 6, 4)
+        assert h.stats()["latency_path"] == 1
+        for b in range(nb):
+            compare_all(h, oracle.detect(imgs[b], 64, 6, 4, AB), AB, 6, image=b)
