@@ -178,7 +178,7 @@ struct hht_ctx {
         uint64_t gen = 0;
         std::vector<uint8_t> bytes;
     } cache_small, cache_beta;
-    uint32_t* fin_h = nullptr;              // k_finish's mapped host block (one-launch paths)
+    uint32_t* fin_h = nullptr;              // the one-launch paths' mapped host block (kFinish* layout)
     uint32_t* fin_m = nullptr;
     uint8_t* pin = nullptr;                 // pinned staging for small host<->device copies of one call
     size_t pin_used = 0;
@@ -948,7 +948,7 @@ void small_bounds(const hht_ctx* x, uint64_t& S, uint64_t& F) {
 // 0: multi-kernel path; 1: latency path with shared-memory scratch; 2: latency path with the two
 // candidate lists in device (L2-resident) memory and the frontier arrays in shared memory, for lists
 // up to kSmallGlobalMaxS entries (profiles/r01_latency.md)
-hht_status finish_small(hht_ctx* x, const uint32_t* d_counts, int id, uint32_t path);
+hht_status finish_small(hht_ctx* x, int id, uint32_t path);
 
 // 3: the mid-size latency path (k_mid, hht_mid.cu): one cooperative launch over the GPU, lists and
 // frontier in device memory, for lists up to kMidMaxS entries (opts.latency_path 3 forces it when the
@@ -966,7 +966,7 @@ int small_mode(const hht_ctx* x) {
     return mid_ok ? 3 : 0;
 }
 
-hht_status detect_mid(hht_ctx* x) {
+hht_status detect_mid(hht_ctx* x, const int32_t* dev_pts, uint64_t npts) {
     const int D = x->D;
     const uint32_t nt = (uint32_t)x->ntrees;
     uint64_t n = 0;
@@ -1021,10 +1021,13 @@ hht_status detect_mid(hht_ctx* x) {
         memcpy(h.data(), x->tree_pt_off.data(), 8ull * nt);
         memcpy(h.data() + 2ull * nt, x->tree_pt_n.data(), 4ull * nt);
         memcpy((char*)h.data() + ((char*)d_rec - (char*)x->small.p), h_rec.data(), sizeof(Record*) * (D + 1));
-        TRY(h2d_small(x, x->small.p, h.data(), words * 4));
-        x->cache_small.b = nullptr;        // zeroed control words: written every call
+        // counts: zeroed by k_mid; ctl[3] (range flag): 0 on upload, re-armed by k_mid
+        TRY(h2d_cached(x, x->cache_small, x->small, h.data(), words * 4));
     }
-    a.packed = (const uint32_t*)x->packed.p;
+    a.packed = (uint32_t*)x->packed.p;
+    a.pts = (const int2*)dev_pts;          // staged and range-checked by k_mid itself
+    a.npts = dev_pts ? npts : 0;
+    a.fin = x->fin_m;
     a.tree_off = d_off;
     a.tree_n = d_n;
     a.tree_beta = (const uint8_t*)x->beta.p;
@@ -1040,7 +1043,7 @@ hht_status detect_mid(hht_ctx* x) {
     const int id = prof_begin(x, 1, n * 4 * (uint64_t)(D + 1));
     CK(launch_mid(a, x->int64, x->mid_grid[x->int64 ? 1 : 0], x->st));
     prof_end(x, id);
-    return finish_small(x, a.counts, id, 2);
+    return finish_small(x, id, 2);
 }
 
 hht_status detect_small(hht_ctx* x, const int32_t* dev_pts, uint64_t npts) {
@@ -1102,16 +1105,13 @@ hht_status detect_small(hht_ctx* x, const int32_t* dev_pts, uint64_t npts) {
     const int id = prof_begin(x, 1, n * 4 * (uint64_t)(D + 1));
     CK(launch_small(a, x->int64, x->st));
     prof_end(x, id);
-    return finish_small(x, nullptr, id, 1);
+    return finish_small(x, id, 1);
 }
 
 // Results of a one-launch traversal (k_small, k_mid): per-level record counts, leaves and statistics
 // in one synchronisation, with the range check of the staged points.
-hht_status finish_small(hht_ctx* x, const uint32_t* d_counts, int id, uint32_t path) {
+hht_status finish_small(hht_ctx* x, int id, uint32_t path) {
     const int D = x->D;
-    if (d_counts)      // null: k_small wrote the block itself
-        CK(launch_finish(x->fin_m, d_counts, (uint32_t)(D + 2), (const unsigned long long*)x->stats.p,
-                         (uint32_t*)x->errflag.p, x->st));
     CK(cudaEventRecord(x->ev1, x->st));
     TRY(sync(x));
     x->errflag_dirty = false;
@@ -1250,11 +1250,12 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
     } else {
         TRY(ensure(x, x->packed, std::max<int64_t>(n, 1) * 4 + 64));   // + bulk-copy slack
     }
-    // k_small stages and range-checks the points itself (no k_stage launch, no errflag)
+    // the one-launch paths (k_small, k_mid) stage and range-check the points themselves (no k_stage
+    // launch, no errflag)
     const int smode = small_mode(x);
-    const bool stage_in_small = smode == 1 || smode == 2;
-    // errflag is 0 on entry: zeroed at create, re-armed by k_finish (one-launch paths) and after the
-    // multi-kernel path's range check; a call that failed in between leaves it dirty
+    const bool stage_in_small = smode != 0;
+    // errflag is 0 on entry: zeroed at create, re-armed after the multi-kernel path's range check; a
+    // call that failed in between leaves it dirty
     if (!stage_in_small) {
         if (x->errflag_dirty) CK(cudaMemsetAsync(x->errflag.p, 0, 4, x->st));
         x->errflag_dirty = true;
@@ -1288,7 +1289,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         for (int t = 0; t < x->ntrees; ++t) beta[t] = x->tree_half[t] == HHT_BETA;
         TRY(ensure(x, x->beta, x->ntrees));
         TRY(h2d_cached(x, x->cache_beta, x->beta, beta.data(), x->ntrees));
-        return smode == 3 ? detect_mid(x) : detect_small(x, small_pts, (uint64_t)n);
+        return smode == 3 ? detect_mid(x, small_pts, (uint64_t)n) : detect_small(x, small_pts, (uint64_t)n);
     }
     TRY(coll_allreduce(x, x->errflag.p, x->errflag.p, 1, C_U32, C_MAX));
     CK(launch_copy_u32((uint32_t*)x->misc_m, (const uint32_t*)x->errflag.p, 1, x->st));

@@ -63,12 +63,11 @@ struct Totals {          // written by the last split tile
 // Device-side stats accumulators (uint64): see kStat*.
 enum { kStatTests = 0, kStatVotes = 1, kStatLeaves = 2, kStatSplit0 = 8, kStatVisited0 = 8 + 64,
        kStatCount = 8 + 128 };
-// k_finish's mapped host block: word 0 the range flag, words 1.. the per-level counts (<= 64 + 2),
-// from word kFinishStatsWord the statistics (kStatCount u64)
+// The one-launch paths' mapped host block (SmallArgs / MidArgs::fin), written by the kernel itself:
+// word 0 the range flag, words 1.. the per-level counts (<= 64 + 2), from word kFinishStatsWord the
+// statistics (kStatCount u64)
 constexpr uint32_t kFinishStatsWord = 128;
 constexpr size_t kFinishBytes = kFinishStatsWord * 4 + kStatCount * 8;
-cudaError_t launch_finish(uint32_t* host, const uint32_t* counts, uint32_t ncounts, const unsigned long long* stats,
-                          uint32_t* errflag, cudaStream_t st);
 
 enum PassMode { MODE_COUNT = 0, MODE_WRITE = 1, MODE_COUNT2 = 2, MODE_WRITE_NC = 3 };   // NC: no count-ahead
 
@@ -249,7 +248,7 @@ struct SmallArgs {
     uint32_t* packed;              // staged points (written here when `pts` is set)
     const int2* pts;               // non-null: raw device points [npts], staged and range-checked in the
     uint64_t npts;                 //   kernel (no separate stage launch); null: `packed` is already staged
-    uint32_t* fin;                 // mapped host block (k_finish's layout): range flag, counts, statistics
+    uint32_t* fin;                 // mapped host block (kFinish* layout): range flag, counts, statistics
     const uint64_t* tree_off;      // [ntrees] first point of each tree in `packed`
     const uint32_t* tree_n;        // [ntrees] points of each tree
     const uint8_t* tree_beta;
@@ -271,7 +270,10 @@ struct SmallArgs {
 uint64_t small_smem_bytes(uint32_t S, uint32_t F);
 uint64_t small_frontier_bytes(uint32_t F);
 constexpr uint64_t kSmallSmemMax = 220 * 1024;
-constexpr uint64_t kSmallGlobalMaxS = 1ull << 16;   // device-list latency path: list bound (entries)
+#ifndef HHT_SMALL_GLOBAL_MAX_LOG2
+#define HHT_SMALL_GLOBAL_MAX_LOG2 16
+#endif
+constexpr uint64_t kSmallGlobalMaxS = 1ull << HHT_SMALL_GLOBAL_MAX_LOG2;   // device-list latency path: list bound (entries)
 cudaError_t launch_small(const SmallArgs& a, bool int64, cudaStream_t st);
 // Mid-size latency path (hht_mid.cu): the whole traversal as one cooperative kernel over the GPU.
 constexpr int kMidThreads = 256;
@@ -279,7 +281,10 @@ constexpr int kMidMinBlocks = 3;
 constexpr uint32_t kMidMaxTiles = 3072;        // tiles of kMidThreads children per level (S2 prefixes)
 constexpr uint64_t kMidMaxS = 1ull << 26;      // list bound (entries per level) admitted
 struct MidArgs {
-    const uint32_t* packed;        // staged points (level-0 lists)
+    uint32_t* packed;              // staged points (level-0 lists; written here when `pts` is set)
+    const int2* pts;               // non-null: raw device points [npts], staged and range-checked in the
+    uint64_t npts;                 //   kernel (no separate stage launch); null: `packed` is already staged
+    uint32_t* fin;                 // mapped host block (kFinish* layout): range flag, counts, statistics
     const uint64_t* tree_off;      // [ntrees] first point of each tree in `packed`
     const uint32_t* tree_n;        // [ntrees]
     const uint8_t* tree_beta;
@@ -297,7 +302,7 @@ struct MidArgs {
     uint32_t* lcoff;               // [4 F] tile-local chunk offsets
     uint32_t* app;                 // [F] append cursors of the next lists
     uint32_t* tiles;               // [3 x tiles] tile totals (split count, entries, chunks)
-    uint32_t* ctl;                 // [8] per buffer: F, chunks, entries
+    uint32_t* ctl;                 // [8] per buffer: F, chunks, entries; ctl[3]: range flag (0 between calls)
     // outputs (as SmallArgs)
     Record* const* rec;
     LeafRec* leaves;

@@ -52,13 +52,6 @@ __device__ __forceinline__ uint32_t byte_counter(uint32_t c02, uint32_t c13, int
     return (((which & 1) ? c13 : c02) >> (16 * (which >> 1))) & 0xFFFFu;
 }
 
-// if (c) acc += one * k, as a predicated integer multiply-add (issued on the FMA pipe; `one` is a
-// runtime 1 so ptxas cannot strength-reduce it to an ALU add).
-__device__ __forceinline__ void mad_if(bool c, uint32_t& acc, uint32_t one, uint32_t k) {
-    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p mad.lo.u32 %0, %2, %3, %0;\n\t}"
-        : "+r"(acc) : "r"((uint32_t)c), "r"(one), "r"(k));
-}
-
 // quad index of (da, dc): NE(1,1)=0, NW(0,1)=1, SW(0,0)=2, SE(1,0)=3
 __host__ __device__ constexpr int quad_of(int da, int dc) { return dc ? (da ? 0 : 1) : (da ? 3 : 2); }
 
@@ -1804,42 +1797,6 @@ cudaError_t launch_removal(const RmArgs& a, const LeafRec* leaves, bool int64, i
 // their records and the next frontier (strict votes > T) or the leaves at level D, and a
 // second pass appends each candidate to the lists of the split children it crosses.
 // ---------------------------------------------------------------------------------------------
-namespace {
-// exclusive block scan of n values in place (one block of blockDim.x threads), returns the total
-__device__ uint32_t block_scan(uint32_t* v, uint32_t n, uint32_t* s_warp) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    uint32_t carry = 0;
-    for (uint32_t base = 0; base < n; base += blockDim.x) {
-        const uint32_t i = base + tid;
-        const uint32_t x = i < n ? v[i] : 0u;
-        uint32_t inc = x;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-            if (lane >= d) inc += t;
-        }
-        if (lane == 31) s_warp[wid] = inc;
-        __syncthreads();
-        if (wid == 0) {
-            const uint32_t w = lane < nw ? s_warp[lane] : 0u;
-            uint32_t wi = w;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, wi, d);
-                if (lane >= d) wi += t;
-            }
-            if (lane < nw) s_warp[lane] = wi - w;
-            if (lane == 31) s_warp[32] = wi;            // chunk total
-        }
-        __syncthreads();
-        if (i < n) v[i] = carry + s_warp[wid] + inc - x;
-        carry += s_warp[32];
-        __syncthreads();
-    }
-    return carry;
-}
-}  // namespace
-
 // frontier tree ids carry the tree's half in their top bit: no global load per region in the passes
 constexpr uint32_t kSmallBeta = 1u << 31;
 
@@ -2048,9 +2005,9 @@ __global__ void __launch_bounds__(1024) k_small(const SmallArgs A) {
         // pass 2: append each candidate to the lists of the split children it crosses and count, as it
         // goes, the votes of those children's own 4 children (the next level's pass 1). A warp owns
         // whole regions, so it alone writes their split children's lists and votes: positions from
-        // ballots and running counts, no atomics. Per-lane grandchild counts are packed two per word:
-        // a region's list is below 2^16 entries here (lists hold < kSmallGlobalMaxS = 2^16 entries and
-        // pass 2 runs only for D >= 2, where a tree's list at a level is at most S / 3)
+        // ballots and running counts, no atomics. Per-lane grandchild counts are packed two per word
+        // (a lane sees at most 1/32 of a region's list, and lists here are far below 2^21 entries) and
+        // unpacked before the warp sums them
         {
             const I Qc1 = ((I)3 * N) << (sh - 2);          // the child level's Q (sh >= 2 here)
             const uint32_t* const noff = ntree + 3 * FS;
@@ -2092,10 +2049,11 @@ __global__ void __launch_bounds__(1024) k_small(const SmallArgs A) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     if (fq[q] == kNone) continue;            // warp-uniform
-                    const uint32_t x01 = __reduce_add_sync(0xFFFFFFFFu, c01[q]);
-                    const uint32_t x23 = __reduce_add_sync(0xFFFFFFFFu, c23[q]);
-                    if (lane == 0)
-                        *reinterpret_cast<uint4*>(cv + 4 * fq[q]) = make_uint4(x01 & 0xFFFFu, x01 >> 16, x23 & 0xFFFFu, x23 >> 16);
+                    const uint32_t x0 = __reduce_add_sync(0xFFFFFFFFu, c01[q] & 0xFFFFu);
+                    const uint32_t x1 = __reduce_add_sync(0xFFFFFFFFu, c01[q] >> 16);
+                    const uint32_t x2 = __reduce_add_sync(0xFFFFFFFFu, c23[q] & 0xFFFFu);
+                    const uint32_t x3 = __reduce_add_sync(0xFFFFFFFFu, c23[q] >> 16);
+                    if (lane == 0) *reinterpret_cast<uint4*>(cv + 4 * fq[q]) = make_uint4(x0, x1, x2, x3);
                 }
             }
         }
@@ -2116,7 +2074,7 @@ __global__ void __launch_bounds__(1024) k_small(const SmallArgs A) {
         A.stats[kStatTests] = tests;
         A.stats[kStatVotes] = votes;
     }
-    // k_finish in the same launch: counts and statistics straight into the mapped host block
+    // results in the same launch: counts and statistics straight into the mapped host block (fin)
     __syncthreads();
     if (A.fin) {
         for (uint32_t i = tid; i < (uint32_t)D + 2; i += blockDim.x) A.fin[1 + i] = A.counts[i];
@@ -2276,25 +2234,6 @@ cudaError_t launch_bounds(const uint64_t* off, const uint64_t* choff, const uint
 // the copy engines, e.g. the leaf-sink transfers).
 __global__ void k_copy_u32(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint32_t n) {
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-}
-
-// End of a one-launch traversal: the range flag, the per-level counts and the statistics into mapped
-// host memory (no device-to-host copies), and the flag re-armed for the next call.
-__global__ void k_finish(uint32_t* __restrict__ host, const uint32_t* __restrict__ counts, uint32_t ncounts,
-                         const unsigned long long* __restrict__ stats, uint32_t* __restrict__ errflag) {
-    if (threadIdx.x == 0) {
-        host[0] = *errflag;
-        *errflag = 0;
-    }
-    for (uint32_t i = threadIdx.x; i < ncounts; i += blockDim.x) host[1 + i] = counts[i];
-    unsigned long long* hs = reinterpret_cast<unsigned long long*>(host + kFinishStatsWord);
-    for (uint32_t i = threadIdx.x; i < kStatCount; i += blockDim.x) hs[i] = stats[i];
-}
-
-cudaError_t launch_finish(uint32_t* host, const uint32_t* counts, uint32_t ncounts, const unsigned long long* stats,
-                          uint32_t* errflag, cudaStream_t st) {
-    k_finish<<<1, 256, 0, st>>>(host, counts, ncounts, stats, errflag);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_copy_u32(uint32_t* dst, const uint32_t* src, uint32_t n, cudaStream_t st) {

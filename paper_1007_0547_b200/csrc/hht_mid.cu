@@ -251,9 +251,22 @@ __global__ void __launch_bounds__(kMidThreads, kMidMinBlocks) k_mid(const MidArg
     const uint64_t gsize = (uint64_t)gridDim.x * blockDim.x;
     const uint32_t warp = (uint32_t)(gtid >> 5), nwarps = (uint32_t)(gsize >> 5);
     const int D = A.D;
+    // ---- K0 in the same launch: stage and range-check the points; the flag is read after
+    // the first grid barrier, and an out-of-range point ends the call before any traversal
+    if (A.pts) {
+        uint32_t bad = 0;
+        for (uint64_t i = gtid; i < A.npts; i += gsize) {
+            const int2 p = A.pts[i];
+            const bool ok = (unsigned)p.x < (unsigned)A.N && (unsigned)p.y < (unsigned)A.N;
+            bad |= !ok;
+            A.packed[i] = ok ? (((uint32_t)p.x << 16) | (uint32_t)p.y) : 0u;
+        }
+        if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(A.ctl + 3, 1u);
+    }
     // ---- level 0: the roots (every line crosses the root); split iff E > T (R6)
     if (blockIdx.x == 0) {
         for (int i = threadIdx.x; i < kStatCount; i += blockDim.x) A.stats[i] = 0;   // the call's statistics
+        for (int i = threadIdx.x; i < D + 2; i += blockDim.x) A.counts[i] = 0;     // levels never reached stay 0
         __syncthreads();
         const uint32_t nt = A.ntrees;
         unsigned long long tests = 0, votes = 0;
@@ -288,6 +301,15 @@ __global__ void __launch_bounds__(kMidThreads, kMidMinBlocks) k_mid(const MidArg
         }
     }
     grid.sync();
+    if (A.pts && *(volatile uint32_t*)(A.ctl + 3)) {        // every thread reads the same flag
+        grid.sync();                                         // ... before it is re-armed
+        if (gtid == 0) {
+            A.ctl[3] = 0;
+            A.fin[0] = 1;
+            __threadfence_system();
+        }
+        return;
+    }
     mid_pass<I, true>(A, 0, 0, A.ctl[1], warp, nwarps, lane, false);
     grid.sync();
     for (int l = 0; l < D; ++l) {
@@ -413,6 +435,14 @@ __global__ void __launch_bounds__(kMidThreads, kMidMinBlocks) k_mid(const MidArg
         // ---- W: append to the split children's lists, count their grandchildren
         if (Fn) mid_pass<I, false>(A, l, cur, C, warp, nwarps, lane, l + 2 < D);
         grid.sync();
+    }
+    // ---- results in the same launch: counts and statistics straight into the mapped host block (fin)
+    if (A.fin && blockIdx.x == 0) {
+        for (int i = threadIdx.x; i < D + 2; i += blockDim.x) A.fin[1 + i] = A.counts[i];
+        unsigned long long* hs = reinterpret_cast<unsigned long long*>(A.fin + kFinishStatsWord);
+        for (int i = threadIdx.x; i < kStatCount; i += blockDim.x) hs[i] = A.stats[i];
+        if (threadIdx.x == 0) A.fin[0] = 0;
+        __threadfence_system();
     }
 }
 }  // namespace
