@@ -74,7 +74,14 @@ def _workload(cfg):
     return {"workload": f"config{cfg.cid}: {cfg.text}", "N": cfg.N, "depth": cfg.D, "threshold": cfg.T,
             "images": cfg.images, "halves": "both" if cfg.halves == 3 else "alpha",
             "points_per_image": None, "seed": 0,
-            "l2": "inputs and candidate lists larger than L2 (126 MB); no flush"}
+            "l2": ("L2 flushed before every timed step (a 256 MB write, outside the timed calls: the "
+                   "value sums each call's own device time)" if _flush_l2(cfg) else
+                   "inputs and candidate lists larger than L2 (126 MB); no flush")}
+
+
+def _flush_l2(cfg):
+    """Configs 1-3 fit (inputs) in the 126 MB L2: flush it between timed steps."""
+    return cfg.cid <= 3
 
 
 class ClockSampler:
@@ -324,6 +331,14 @@ def main():
         if world > 1:
             dist.barrier(device_ids=[local])
 
+    flush = _flush_l2(cfg)
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
+
+    def flush_l2():
+        if flush:
+            scratch.zero_()
+            torch.cuda.synchronize()
+
     for _ in range(max(a.warmup, 0)):
         step()
     torch.cuda.synchronize()
@@ -336,6 +351,7 @@ def main():
         h.timer_begin()
         step_ms = []
         for _ in range(a.steps):
+            flush_l2()
             step()
             st = h.stats()
             step_ms.append(st["ms"])
@@ -347,6 +363,8 @@ def main():
                 p["bytes"] += v["bytes"]
                 p["ops"] += v.get("ops", 0)
         ms = h.timer_end()
+        if flush:
+            ms = float(sum(step_ms))   # each call's device time (CUDA events), flushes excluded
         torch.cuda.synchronize()
         barrier()
     clocks = clk.summary()
@@ -432,23 +450,28 @@ def main():
         h2.detect_batch(hnp, my_offs, cfg.N, cfg.D, cfg.T)   # untimed warm-up of the streaming path
         barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e_steps = max(1, min(a.steps, 3))
+        e_steps = max(1, a.steps if flush else min(a.steps, 3))
         d2h = 0
+        et = 0.0
         for _ in range(e_steps):
+            flush_l2()
+            t0 = time.perf_counter()
             h2.detect_batch(hnp, my_offs, cfg.N, cfg.D, cfg.T)   # H2D of the points + D2H of the lines inside
+            et += time.perf_counter() - t0                        # the call returns with its results on the host
             sst = h2.stats()
             assert sst["leaves_streamed"] == sst["leaves"], "leaf sink too small"
             d2h = sst["leaves_streamed"] * 20
         torch.cuda.synchronize()
-        et = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([et], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             et = float(t.item())
         e2e = {"value": tests_tot / a.steps * e_steps / et, "unit": UNIT,
                "h2d_bytes_per_step": int(hnp.nbytes), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": 1e3 * et / e_steps, "timing": "wall clock around detect_batch(pinned host points) with the detected lines streamed to a pinned host buffer (hht_set_leaf_sink) during the call"}
+               "ms_per_step": 1e3 * et / e_steps,
+               "timing": "wall clock of each detect_batch call (pinned host points in, the detected lines streamed "
+                         "to a pinned host buffer by hht_set_leaf_sink during the call), summed over the steps" +
+                         ("; L2 flushed before each call, outside its clock" if flush else "")}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

@@ -1,6 +1,7 @@
 #!/bin/bash
 # Round profiling run on one B200 (see /opt/skills/guides/B200_PROFILING.md):
-#   1. the default bench line, 2. the ncu launch list of the same command,
+#   1. the default bench line (config 5) and bench lines of configs 1-4, the int64 config-5 line and
+#      the single-image latency table, 2. the ncu launch list of the default command,
 #   3. full ncu captures of the dominant kernels (tail, largest write pass) on config 5, with the
 #      library's per-launch algorithmic bytes of the same run (run_once.py prints them).
 set -x
@@ -10,6 +11,11 @@ python bench.py > gpurun_out/bench_default.log 2> gpurun_out/bench_default.err &
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_c5.csv python bench.py > gpurun_out/ncu_launches.log 2>&1
 echo "launch list rc=$?"
+for c in 1 2; do python bench.py --config $c --steps 200 --warmup 20 > gpurun_out/bench_c$c.log 2> gpurun_out/bench_c$c.err; done
+python bench.py --config 3 --steps 20 --warmup 5 > gpurun_out/bench_c3.log 2> gpurun_out/bench_c3.err
+python bench.py --config 4 --steps 5 --warmup 3 > gpurun_out/bench_c4.log 2> gpurun_out/bench_c4.err
+python bench.py --force-int64 --no-cpu-baseline > gpurun_out/bench_c5_int64.log 2> gpurun_out/bench_c5_int64.err
+python scripts/latency_bench.py --out gpurun_out/latency.md > gpurun_out/latency.log 2>&1
 python scripts/run_once.py --config 5 > gpurun_out/plain_c5.log 2>&1
 # k_pass launch index of the largest write pass (k_pass launch 0 is the root count pass)
 WSKIP=$(python -c "

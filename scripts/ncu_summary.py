@@ -17,6 +17,7 @@ import csv
 import json
 import os
 import re
+import shutil
 import subprocess
 from collections import defaultdict
 
@@ -141,6 +142,22 @@ def main():
                   f"- e2e: {json.dumps(b['e2e'])}",
                   f"- cpu_baseline: {json.dumps(b['cpu_baseline'])}", ""]
         open(os.path.join(P, f"{tag}_bench_default.jsonl"), "w").write(json.dumps(b) + "\n")
+    # bench lines of the other configs (C1-C4) and the int64 config-5 line, as run by gpu_profile.sh
+    other = []
+    for name in ["bench_c1", "bench_c2", "bench_c3", "bench_c4", "bench_c5_int64"]:
+        f = os.path.join(G, name + ".log")
+        if not os.path.exists(f) or not open(f).read().strip():
+            continue
+        b = json.loads(open(f).read().strip().splitlines()[-1])
+        open(os.path.join(P, f"{tag}_{name}.jsonl"), "w").write(json.dumps(b) + "\n")
+        other.append(f"| {name[6:]} | {b['config'].get('workload', '')[:60]} | {b['value']:.4g} | {b['ms_per_step']:.4g} | "
+                     f"{b['e2e']['ms_per_step'] if isinstance(b.get('e2e'), dict) and 'ms_per_step' in b['e2e'] else 'n/a'} | "
+                     f"{b['dtype']} | {b['roofline'].get('frac', float('nan')):.3f} |")
+    if other:
+        lines += ["## bench.py on the other configs (one detection per step; lines in profiles/" + tag + "_bench_c*.jsonl)", "",
+                  "| config | workload | tests/s | ms/step | e2e ms/step | dtype | roofline frac |", "|---|---|---|---|---|---|---|"] + other + [""]
+    if os.path.exists(os.path.join(G, "latency.md")):
+        shutil.copy(os.path.join(G, "latency.md"), os.path.join(P, f"{tag}_latency.md"))
     lines += ["## ncu launch list of the same command (cold-cache, serialised: compare shares)", "",
               "| kernel | launches | total ms | share |", "|---|---|---|---|"]
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
@@ -156,7 +173,6 @@ def main():
                      f"{t['alu_pipe_pct']:.1f} | {t['fma_pipe_pct']:.1f} | {t['lsu_pipe_pct']:.1f} | {t['smem_wavefronts_pct']:.1f} | "
                      f"{t['warps_active_pct']:.1f} | {t['registers']:.0f} |")
     open(os.path.join(P, f"{tag}_summary.md"), "w").write("\n".join(lines) + "\n")
-    import shutil
     shutil.copy(os.path.join(G, "launches_c5.csv"), os.path.join(P, f"{tag}_launches_c5_bench.csv"))
     print("\n".join(lines))
 
