@@ -89,7 +89,10 @@ typedef struct {
                                 cooperative launch over the whole GPU (k_mid, stats.latency_path 2);
                                 larger detections take the multi-kernel path. 1 = same as 0;
                                 2 = never (always the multi-kernel path); 3 = k_mid whenever its
-                                bounds admit the detection. Results are identical. */
+                                bounds admit the detection. Results are identical. The one-launch
+                                paths also stage and range-check the points in that launch (an
+                                out-of-range point still fails the call with HHT_ERANGE and no
+                                results) and write the statistics to mapped host memory. */
     uint32_t variant;        /* membership test: HHT_EXACT (0, default) = the paper's 4-bit corner
                                 code; HHT_FHT_CIRCLE (1) = the FHT comparison: the line meets the
                                 region's circumscribing circle (exact integers, see
