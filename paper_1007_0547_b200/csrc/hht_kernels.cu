@@ -2725,25 +2725,40 @@ cudaError_t launch_split(const SplitArgs& a, int resident_blocks, cudaStream_t s
 }
 
 // ---------------------------------------------------------------------------------------------
-// Chunk map: chunk -> region for a frontier (one warp per region).
+// Chunk map: chunk -> region for a frontier. A persistent grid of W warps: with F >= W regions
+// each warp walks regions wid, wid + W, ...; with fewer regions (the first levels: 2 root regions
+// of 62.5k chunks each on C5) each region gets wpr = W / F warps that interleave its chunks 16 at
+// a time, so a few huge lists do not leave one warp writing them alone (one warp per region had
+// cost 130-350 us per launch at levels 0-2 of C5).
 // ---------------------------------------------------------------------------------------------
+constexpr unsigned kChunkMapBlocks = 148 * 8;
 __global__ void __launch_bounds__(256) k_chunk_map(const uint64_t* __restrict__ choff, const uint64_t* __restrict__ off,
                                                    const uint32_t* __restrict__ len, const uint32_t* __restrict__ ra,
                                                    const uint32_t* __restrict__ rc, const uint32_t* __restrict__ tree,
-                                                   const uint8_t* __restrict__ tree_beta, uint32_t F,
+                                                   const uint8_t* __restrict__ tree_beta, uint32_t F, uint32_t wpr,
                                                    ChunkDesc* __restrict__ chunks) {
-    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t W = (gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (w >= F) return;
-    const uint64_t b = choff[w], e = choff[w + 1], o = off[w];
-    const uint32_t n = len[w], a = ra[w], c = rc[w], beta = tree_beta[tree[w]];
-    for (uint64_t k = b + lane; k < e; k += 32) {
-        const uint64_t j = (k - b) * kChunk;
-        const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, (uint64_t)n - j);
-        uint4* q = reinterpret_cast<uint4*>(chunks + k);
-        q[0] = make_uint4((uint32_t)w, cnt, a, c);
-        const uint64_t e0 = o + j;
-        q[1] = make_uint4((uint32_t)e0, (uint32_t)(e0 >> 32), beta, 0u);
+    // lane pair (2i, 2i+1) writes the two 16-byte halves of one descriptor: every store instruction
+    // covers 16 consecutive descriptors (512 contiguous bytes, whole sectors)
+    const uint32_t half = (uint32_t)lane & 1u;
+    const uint32_t part = wpr > 1 ? wid % wpr : 0u;
+    const uint32_t rstep = wpr > 1 ? W / wpr : W;
+    for (uint32_t w = wpr > 1 ? wid / wpr : wid; w < F; w += rstep) {
+        const uint64_t b = choff[w], e = choff[w + 1], o = off[w];
+        const uint32_t n = len[w], a = ra[w], c = rc[w], beta = tree_beta[tree[w]];
+        for (uint64_t k = b + 16 * (uint64_t)part + (lane >> 1); k < e; k += 16 * (uint64_t)wpr) {
+            const uint64_t j = (k - b) * kChunk;
+            uint4* q = reinterpret_cast<uint4*>(chunks + k) + half;
+            if (half == 0) {
+                const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, (uint64_t)n - j);
+                *q = make_uint4(w, cnt, a, c);
+            } else {
+                const uint64_t e0 = o + j;
+                *q = make_uint4((uint32_t)e0, (uint32_t)(e0 >> 32), beta, 0u);
+            }
+        }
     }
 }
 
@@ -2751,8 +2766,9 @@ cudaError_t launch_chunk_map(const uint64_t* choff, const uint64_t* off, const u
                              const uint32_t* c, const uint32_t* tree, const uint8_t* tree_beta, uint32_t F,
                              ChunkDesc* chunks, cudaStream_t st) {
     if (F == 0) return cudaSuccess;
-    const uint64_t blocks = ((uint64_t)F * 32 + 255) / 256;
-    k_chunk_map<<<(unsigned)blocks, 256, 0, st>>>(choff, off, len, a, c, tree, tree_beta, F, chunks);
+    const uint32_t W = kChunkMapBlocks * 256 / 32;
+    const uint32_t wpr = F >= W ? 1u : W / F;
+    k_chunk_map<<<kChunkMapBlocks, 256, 0, st>>>(choff, off, len, a, c, tree, tree_beta, F, wpr, chunks);
     return cudaGetLastError();
 }
 
