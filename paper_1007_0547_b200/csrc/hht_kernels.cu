@@ -165,20 +165,26 @@ __device__ __forceinline__ void chunk_math(const uint32_t (&p)[kItems], int cnt,
         const I ex = (I)(BETA ? (w & 0xFFFFu) : (w >> 16));
         const I ey = (I)(BETA ? (w >> 16) : (w & 0xFFFFu));
         I gm1 = ex * alpha + (ey << D) + beta_m1;            // G(SW corner) - 1
-        if (lane + kWarp * it >= cnt) gm1 = (I)-1;
+        if (MODE != MODE_WRITE_NC && lane + kWarp * it >= cnt) gm1 = (I)-1;
         const I Pc = ex << sh;                                // ex * s
-        if (MODE == MODE_COUNT || MODE == MODE_WRITE_NC) {
+        if (MODE == MODE_WRITE_NC) {
+            // every entry of a region's own list crosses it, so y = G_SW - 1 lies in [0, 2 Uc) and
+            // the NE child (y >= Uc) is crossed exactly when the SW child (y < Uc) is not (the
+            // SW + NE identity); NW and SE keep their exact tests. Lanes past the chunk are masked
+            // once per chunk below (the fused tail's push does the same).
+            const I Uc = Pc + Qc;
+            const uint32_t b = (crosses<I>(gm1, Uc) ? 4u : 1u) | (crosses<I>(gm1 - Qc, Uc) << 1) |
+                               (crosses<I>(gm1 - Pc, Uc) << 3);
+            cm |= b << (4 * it);
+        }
+        if (MODE == MODE_COUNT) {
             const I Uc = Pc + Qc;
             // child SW values: NE g-Pc-Qc, NW g-Qc, SW g, SE g-Pc
             const uint32_t bNE = crosses<I>(gm1 - Pc - Qc, Uc);
             const uint32_t bNW = crosses<I>(gm1 - Qc, Uc);
             const uint32_t bSW = crosses<I>(gm1, Uc);
             const uint32_t bSE = crosses<I>(gm1 - Pc, Uc);
-            if (MODE == MODE_COUNT) {
-                acc[0] += bNE | (bNW << 8) | (bSW << 16) | (bSE << 24);
-            } else {
-                cm |= (bNE | (bNW << 1) | (bSW << 2) | (bSE << 3)) << (4 * it);
-            }
+            acc[0] += bNE | (bNW << 8) | (bSW << 16) | (bSE << 24);
         }
         if (MODE == MODE_WRITE || MODE == MODE_COUNT2) {
             // the 4x4 level-(l+2) cells as a 4-column raster (CARaster above); invalid lanes keep
@@ -212,6 +218,11 @@ __device__ __forceinline__ void chunk_math(const uint32_t (&p)[kItems], int cnt,
                 cm |= nib << (4 * it);
             }
         }
+    }
+    if (MODE == MODE_WRITE_NC) {
+        const int nv = cnt - lane;                            // valid items of this lane: ceil(nv / 32)
+        const int kv = nv <= 0 ? 0 : min((nv + kWarp - 1) / kWarp, kItems);
+        cm &= kv >= kItems ? 0xFFFFFFFFu : ((1u << (4 * kv)) - 1u);
     }
     if (MODE == MODE_WRITE || MODE == MODE_COUNT2) {
         // acc[q] byte qq = cell (2 da_q + da_qq, 2 dc_q + dc_qq); quads NE(1,1) NW(0,1) SW(0,0) SE(1,0)
@@ -2241,19 +2252,34 @@ cudaError_t launch_copy_u32(uint32_t* dst, const uint32_t* src, uint32_t n, cuda
     return cudaGetLastError();
 }
 
-// Leaf records (tree, i, j, votes) -> the ABI's hht_leaf rows (image, half, i, j, votes).
+// Leaf records (tree, i, j, votes) -> the ABI's hht_leaf rows (image, half, i, j, votes). Each warp
+// converts 32 consecutive records and writes their 32 x 20 bytes as five fully coalesced 128-byte
+// stores through a warp-private shared-memory transpose (stride-5 words: conflict-free both ways);
+// five scattered 4-byte stores per row had touched 20 sectors per store instruction.
 __global__ void __launch_bounds__(256) k_leaf_rows(const LeafRec* __restrict__ in, uint64_t n,
                                                    const uint8_t* __restrict__ tree_beta, uint32_t H,
                                                    uint32_t* __restrict__ out) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += stride) {
-        const LeafRec r = in[k];
-        uint32_t* o = out + 5 * k;
-        o[0] = r.tree / H;
-        o[1] = tree_beta[r.tree] ? 2u : 1u;
-        o[2] = r.i;
-        o[3] = r.j;
-        o[4] = r.votes;
+    __shared__ uint32_t s_rows[8][5 * 32];
+    const int lane = threadIdx.x & 31;
+    uint32_t* sw = s_rows[threadIdx.x >> 5];
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; 32 * w < n; w += nw) {
+        const uint64_t k = 32 * w + lane;
+        if (k < n) {
+            const LeafRec r = in[k];
+            sw[5 * lane + 0] = r.tree / H;
+            sw[5 * lane + 1] = tree_beta[r.tree] ? 2u : 1u;
+            sw[5 * lane + 2] = r.i;
+            sw[5 * lane + 3] = r.j;
+            sw[5 * lane + 4] = r.votes;
+        }
+        __syncwarp();
+        const uint64_t words = 5 * min((uint64_t)32, n - 32 * w);
+        uint32_t* o = out + 160 * w;
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+            if ((uint64_t)(lane + 32 * q) < words) o[lane + 32 * q] = sw[lane + 32 * q];
+        __syncwarp();
     }
 }
 
