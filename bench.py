@@ -445,8 +445,13 @@ def main():
         hnp = host.numpy()
         h2.detect_batch(hnp, my_offs, cfg.N, cfg.D, cfg.T)   # warm
         nleaf = h2.stats()["leaves"]
-        lbuf = torch.empty((max(int(nleaf * 1.1) + 1024, 1024), 5), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
-        h2.set_leaf_sink(lbuf)          # detected lines stream to the pinned buffer during detection
+        packed = cfg.D <= 16            # 8-byte rows (i, j, votes) + per-tree offsets; else 20-byte hht_leaf rows
+        if packed:
+            lbuf = torch.empty(max(int(nleaf * 1.1) + 1024, 1024), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+            h2.set_leaf_sink_packed(lbuf)   # detected lines stream to the pinned buffer during detection
+        else:
+            lbuf = torch.empty((max(int(nleaf * 1.1) + 1024, 1024), 5), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+            h2.set_leaf_sink(lbuf)
         h2.detect_batch(hnp, my_offs, cfg.N, cfg.D, cfg.T)   # untimed warm-up of the streaming path
         barrier()
         torch.cuda.synchronize()
@@ -460,7 +465,7 @@ def main():
             et += time.perf_counter() - t0                        # the call returns with its results on the host
             sst = h2.stats()
             assert sst["leaves_streamed"] == sst["leaves"], "leaf sink too small"
-            d2h = sst["leaves_streamed"] * 20
+            d2h = sst["leaves_streamed"] * (8 if packed else 20)
         torch.cuda.synchronize()
         if world > 1:
             t = torch.tensor([et], dtype=torch.float64, device=dev)
@@ -470,7 +475,9 @@ def main():
                "h2d_bytes_per_step": int(hnp.nbytes), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * et / e_steps,
                "timing": "wall clock of each detect_batch call (pinned host points in, the detected lines streamed "
-                         "to a pinned host buffer by hht_set_leaf_sink during the call), summed over the steps" +
+                         "to a pinned host buffer during the call: " +
+                         ("hht_set_leaf_sink_packed, 8-byte (i, j, votes) rows" if packed else "hht_set_leaf_sink, 20-byte rows") +
+                         "), summed over the steps" +
                          ("; L2 flushed before each call, outside its clock" if flush else "")}
 
     cpu = None

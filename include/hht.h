@@ -168,6 +168,20 @@ typedef struct {
  * replaced or removed (host = NULL); page-locked memory gives real overlap. */
 hht_status hht_set_leaf_sink(hht_ctx* ctx, hht_leaf* host, int64_t cap);
 
+/* Packed leaf sink: as hht_set_leaf_sink, but each detected line is one 8-byte row
+ *     (uint64_t)i << 48 | (uint64_t)j << 32 | votes
+ * (2.5x fewer bytes over PCIe than hht_leaf rows), in the same order (tree by tree: image order, ALPHA
+ * before BETA, each tree in the paper's depth-first order); the tree of each row follows from
+ * hht_result_tree_offsets. Replaces any row sink (and vice versa); host = NULL removes it. A detect
+ * with depth > 16 and a packed sink set fails with HHT_EINVAL (i, j need 16 bits each). */
+hht_status hht_set_leaf_sink_packed(hht_ctx* ctx, uint64_t* host, int64_t cap);
+
+/* Leaf offsets per tree of the last detect: out[t] = index of tree t's first detected line in the
+ * hht_result_leaves(ctx, -1, ...) / leaf-sink order, t = 0 .. ntrees (out[ntrees] = total), tree
+ * t = image t / H, half index t % H (H = number of halves in opts.halves, ALPHA first). out holds
+ * cap >= ntrees + 1 values; out = NULL: *ntrees only. */
+hht_status hht_result_tree_offsets(hht_ctx* ctx, uint64_t* out, int64_t cap, int64_t* ntrees);
+
 /* Per-kernel-class timings of the last detect (opts.profile = 1), CUDA events per launch. */
 typedef struct {
     uint64_t launches[8];    /* 0 stage, 1 root count pass, 2 write pass (list compaction +

@@ -159,11 +159,13 @@ struct hht_ctx {
     int mid_grid[2] = {0, 0};            // co-resident k_mid blocks (cooperative launch)
     int64_t edge_na = 0, edge_nb = 0;
     // leaf sink (hht_set_leaf_sink): double-buffered row staging, copied on its own stream
-    hht_leaf* sink = nullptr;
+    void* sink = nullptr;                // hht_leaf rows, or packed 8-byte rows (sink_packed)
+    bool sink_packed = false;
     int64_t sink_cap = 0;
     uint64_t sink_n = 0;
     cudaStream_t cst = nullptr;
     Buf sinkrows[kSinkSlots];
+    Buf treeoff;                         // hht_result_tree_offsets
     cudaEvent_t ev_conv[kSinkSlots] = {}, ev_copy[kSinkSlots] = {};
     bool copy_pending[kSinkSlots] = {};
     int sink_slot = 0;
@@ -414,24 +416,30 @@ hht_status h2d_cached(hht_ctx* x, hht_ctx::H2dCache& c, Buf& b, const void* src,
     return HHT_OK;
 }
 
+size_t sink_row_bytes(const hht_ctx* x) { return x->sink_packed ? sizeof(uint64_t) : sizeof(hht_leaf); }
+
 // Leaf sink: rows of leaves [first, first + n) -> host, overlapped with the traversal.
 hht_status stream_leaves(hht_ctx* x, uint64_t first, uint64_t n) {
     if (!x->sink || n == 0 || x->sink_n >= (uint64_t)x->sink_cap) return HHT_OK;
     const uint64_t k = std::min<uint64_t>(n, (uint64_t)x->sink_cap - x->sink_n);
+    const size_t rb = sink_row_bytes(x);
     const int s = x->sink_slot;
     x->sink_slot = (s + 1) % kSinkSlots;
     Buf& b = x->sinkrows[s];
-    if (b.cap < k * sizeof(hht_leaf)) {
+    if (b.cap < k * rb) {
         if (x->copy_pending[s]) CK(cudaEventSynchronize(x->ev_copy[s]));   // before freeing its buffer
         x->copy_pending[s] = false;
-        TRY(ensure(x, b, k * sizeof(hht_leaf)));
+        TRY(ensure(x, b, k * rb));
     }
     if (x->copy_pending[s]) CK(cudaStreamWaitEvent(x->st, x->ev_copy[s], 0));   // buffer reuse
-    CK(launch_leaf_rows((const LeafRec*)x->leaves.b.p + first, k, (const uint8_t*)x->beta.p, x->H,
-                        (uint32_t*)b.p, x->st));
+    if (x->sink_packed)
+        CK(launch_leaf_packed((const LeafRec*)x->leaves.b.p + first, k, (uint64_t*)b.p, x->st));
+    else
+        CK(launch_leaf_rows((const LeafRec*)x->leaves.b.p + first, k, (const uint8_t*)x->beta.p, x->H,
+                            (uint32_t*)b.p, x->st));
     CK(cudaEventRecord(x->ev_conv[s], x->st));
     CK(cudaStreamWaitEvent(x->cst, x->ev_conv[s], 0));
-    CK(cudaMemcpyAsync(x->sink + x->sink_n, b.p, k * sizeof(hht_leaf), cudaMemcpyDefault, x->cst));
+    CK(cudaMemcpyAsync((uint8_t*)x->sink + x->sink_n * rb, b.p, k * rb, cudaMemcpyDefault, x->cst));
     CK(cudaEventRecord(x->ev_copy[s], x->cst));
     x->copy_pending[s] = true;
     x->sink_n += k;
@@ -916,6 +924,8 @@ hht_status check_args(hht_ctx* x, const int32_t* points, int64_t n_total, int32_
     if (((uintptr_t)points & 7) != 0) return set_err(x, HHT_EINVAL, "points must be 8-byte aligned");
     if (N < 1 || N > 65536) return set_err(x, HHT_EINVAL, "N must be in [1, 65536] (16-bit packed coordinates)");
     if (D < 1 || D > 30) return set_err(x, HHT_EINVAL, "depth must be in [1, 30]");
+    if (x->sink && x->sink_packed && D > 16)
+        return set_err(x, HHT_EINVAL, "a packed leaf sink needs depth <= 16 (16-bit i, j)");
     if (T < 1) return set_err(x, HHT_EINVAL, "threshold must be >= 1");
     if (x->opts.halves == 0 || (x->opts.halves & ~3u)) return set_err(x, HHT_EINVAL, "bad halves");
     // |G| < 5 N 2^D must fit the signed width
@@ -1133,7 +1143,7 @@ hht_status finish_small(hht_ctx* x, int id, uint32_t path) {
     if (x->sink) {
         CK(cudaStreamSynchronize(x->cst));
         x->stat.leaves_streamed = x->sink_n;
-        x->stat.d2h_bytes += x->sink_n * sizeof(hht_leaf);
+        x->stat.d2h_bytes += x->sink_n * sink_row_bytes(x);
     }
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, x->ev0, x->ev1));
@@ -1407,7 +1417,7 @@ hht_status detect_impl(hht_ctx* x, const int32_t* points, const int64_t* offsets
         CK(cudaStreamSynchronize(x->cst));
         for (int k = 0; k < kSinkSlots; ++k) x->copy_pending[k] = false;
         x->stat.leaves_streamed = x->sink_n;
-        x->stat.d2h_bytes += x->sink_n * sizeof(hht_leaf);
+        x->stat.d2h_bytes += x->sink_n * sink_row_bytes(x);
     }
     x->launch_log.clear();
     if (x->opts.profile) {
@@ -1931,14 +1941,31 @@ hht_status hht_result_level(hht_ctx* x, int32_t image, uint32_t half, int32_t le
     return HHT_OK;
 }
 
-hht_status hht_set_leaf_sink(hht_ctx* x, hht_leaf* host, int64_t cap) {
+static hht_status set_sink(hht_ctx* x, void* host, int64_t cap, bool packed) {
     if (!x) return HHT_EINVAL;
     if (host && cap < 0) return set_err(x, HHT_EINVAL, "cap < 0");
     if (x->cst) cudaStreamSynchronize(x->cst);
     for (int k = 0; k < kSinkSlots; ++k) x->copy_pending[k] = false;
     x->sink = host;
+    x->sink_packed = host && packed;
     x->sink_cap = host ? cap : 0;
     return HHT_OK;
+}
+
+hht_status hht_set_leaf_sink(hht_ctx* x, hht_leaf* host, int64_t cap) { return set_sink(x, host, cap, false); }
+
+hht_status hht_set_leaf_sink_packed(hht_ctx* x, uint64_t* host, int64_t cap) { return set_sink(x, host, cap, true); }
+
+hht_status hht_result_tree_offsets(hht_ctx* x, uint64_t* out, int64_t cap, int64_t* ntrees) {
+    if (!x || !ntrees) return HHT_EINVAL;
+    if (!x->have) return set_err(x, HHT_ESTATE, "no successful detect yet");
+    *ntrees = x->ntrees;
+    if (!out) return HHT_OK;
+    if (cap < (int64_t)x->ntrees + 1) return set_err(x, HHT_EINVAL, "cap %lld < %d tree offsets", (long long)cap, x->ntrees + 1);
+    TRY(ensure(x, x->treeoff, 8ull * (x->ntrees + 1)));
+    CK(launch_tree_offsets((const LeafRec*)x->leaves.b.p, x->leaves.n, (uint32_t)x->ntrees, (uint64_t*)x->treeoff.p, x->st));
+    CK(cudaMemcpyAsync(out, x->treeoff.p, 8ull * (x->ntrees + 1), cudaMemcpyDefault, x->st));
+    return sync(x);
 }
 
 hht_status hht_result_stats(hht_ctx* x, hht_stats* out) {
@@ -2011,7 +2038,7 @@ void hht_destroy(hht_ctx* x) {
     for (auto& g : x->rec) fr(g.b);
     fr(x->leaves.b);
     for (Buf* b : {&x->stage_in, &x->packed, &x->errflag, &x->beta, &x->stats, &x->tiles, &x->tilectr, &x->totals,
-                   &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv, &x->leafrows, &x->fusedctr, &x->img, &x->units,
+                   &x->rng, &x->bounds, &x->vtmp, &x->dense, &x->gv, &x->leafrows, &x->treeoff, &x->fusedctr, &x->img, &x->units,
                    &x->edgeB, &x->edgetiles, &x->small, &x->small_g})
         fr(*b);
     if (x->totals_h) cudaFreeHost(x->totals_h);

@@ -181,6 +181,8 @@ cudaError_t launch_copy_u32(uint32_t* dst, const uint32_t* src, uint32_t n, cuda
 cudaError_t launch_set_bounds(uint64_t* bounds, uint64_t lo, uint64_t hi, cudaStream_t st);
 int pass_blocks_per_sm(int mode, bool int64, int pf, int circle);
 int tail_blocks_per_sm(bool int64);
+cudaError_t launch_leaf_packed(const LeafRec* in, uint64_t n, uint64_t* out, cudaStream_t st);
+cudaError_t launch_tree_offsets(const LeafRec* in, uint64_t n, uint32_t ntrees, uint64_t* out, cudaStream_t st);
 cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_beta, uint32_t H, uint32_t* out,
                              cudaStream_t st);
 cudaError_t launch_tail(bool int64, const PassArgs& a, int grid, cudaStream_t st);

@@ -817,6 +817,9 @@ __device__ __forceinline__ void fill_tab16() {
 // (a, c), accumulated into `dst` (256 u32 counters, [16 * column + row]) with one atomic per
 // (lane, cell pair) per column block. Shared by the dense tail (batches = chunks of the region's
 // list) and the fused tail (batches = full shared-memory stacks of a child of a level-(D-5) region).
+#ifndef HHT_RASTER_XRECOMP
+#define HHT_RASTER_XRECOMP 0      // 1: X of a column block's first boundary recomputed from Y (not carried)
+#endif
 template <typename I>
 struct Raster16 {
     uint32_t lane_h, bias, red_u, red_row, fx_m, fx_mlo, fx_s, one;
@@ -872,7 +875,11 @@ struct Raster16 {
 
         // per-line state carried across the 4 column blocks: Y (fixed point, see above), its
         // per-column decrement P, and X of the previous column boundary
+#if HHT_RASTER_XRECOMP
+        uint32_t Y[ITEMS], P[ITEMS];                          // X recomputed at each block start
+#else
         uint32_t Y[ITEMS], P[ITEMS], X[ITEMS];
+#endif
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             const uint32_t w = p[it];
@@ -886,7 +893,9 @@ struct Raster16 {
             // lanes past the batch: f = -1 in every column (all-zero entries)
             Y[it] = valid ? yv : bias - (1u << 24) - 1u;
             P[it] = valid ? pv : 0u;
+#if !HHT_RASTER_XRECOMP
             X[it] = boundary(Y[it], 0);
+#endif
         }
 #pragma unroll   // a rolled column-block loop (half the code, 44 B of spills) measured 151.7 vs 120.9 ms
         for (int b = 0; b < 4; ++b) {
@@ -895,14 +904,19 @@ struct Raster16 {
             for (int i = 0; i < 8; ++i) acc[i] = 0;
 #pragma unroll
             for (int it = 0; it < ITEMS; ++it) {
+#if HHT_RASTER_XRECOMP
+                uint32_t Xc = boundary(Y[it], 0);                 // boundary 4b (even: carries H)
+#else
+                uint32_t& Xc = X[it];
+#endif
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     Y[it] -= P[it];
                     const uint32_t xn = boundary(Y[it], 1 + u);   // boundary 4b + u + 1 (4b is even)
                     uint32_t addr, mx, my;
-                    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(X[it]), "r"(one), "r"(xn));
+                    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(Xc), "r"(one), "r"(xn));
                     asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mx), "=r"(my) : "r"(addr));
-                    X[it] = xn;
+                    Xc = xn;
                     acc[2 * u + 0] += mx;
                     acc[2 * u + 1] += my;
                 }
@@ -2281,6 +2295,42 @@ __global__ void __launch_bounds__(256) k_leaf_rows(const LeafRec* __restrict__ i
             if ((uint64_t)(lane + 32 * q) < words) o[lane + 32 * q] = sw[lane + 32 * q];
         __syncwarp();
     }
+}
+
+// Leaf records -> packed 8-byte rows (hht_set_leaf_sink_packed): i << 48 | j << 32 | votes (depth <= 16).
+__global__ void __launch_bounds__(256) k_leaf_packed(const LeafRec* __restrict__ in, uint64_t n,
+                                                     unsigned long long* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += stride) {
+        const LeafRec r = in[k];
+        out[k] = ((unsigned long long)r.i << 48) | ((unsigned long long)r.j << 32) | r.votes;
+    }
+}
+
+cudaError_t launch_leaf_packed(const LeafRec* in, uint64_t n, uint64_t* out, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_leaf_packed<<<(unsigned)blocks, 256, 0, st>>>(in, n, reinterpret_cast<unsigned long long*>(out));
+    return cudaGetLastError();
+}
+
+// Per-tree leaf offsets: out[t] = first leaf record of tree >= t (records are in tree order), t = 0..ntrees.
+__global__ void __launch_bounds__(256) k_tree_offsets(const LeafRec* __restrict__ in, uint64_t n, uint32_t ntrees,
+                                                      unsigned long long* __restrict__ out) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > ntrees) return;
+    uint64_t lo = 0, hi = n;                      // lower bound of tree t
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) / 2;
+        if (in[mid].tree < t) lo = mid + 1; else hi = mid;
+    }
+    out[t] = lo;
+}
+
+cudaError_t launch_tree_offsets(const LeafRec* in, uint64_t n, uint32_t ntrees, uint64_t* out, cudaStream_t st) {
+    k_tree_offsets<<<(ntrees + 1 + 255) / 256, 256, 0, st>>>(in, n, ntrees, reinterpret_cast<unsigned long long*>(out));
+    return cudaGetLastError();
 }
 
 cudaError_t launch_leaf_rows(const LeafRec* in, uint64_t n, const uint8_t* tree_beta, uint32_t H, uint32_t* out,

@@ -31,7 +31,7 @@ EXPORTS = ["hht_default_opts", "hht_create", "hht_nccl_unique_id", "hht_detect",
            "hht_result_launches", "hht_timer_begin", "hht_timer_end", "hht_last_error", "hht_status_str",
            "hht_destroy", "hht_version", "hht_set_leaf_sink", "hht_group_create", "hht_group_destroy",
            "hht_detect_trees", "hht_detect_image", "hht_result_edges", "hht_result_lines", "hht_set_stream",
-           "hht_result_line_points"]
+           "hht_result_line_points", "hht_set_leaf_sink_packed", "hht_result_tree_offsets"]
 
 PROFILE_CLASSES = ["stage", "count", "write", "tail", "split", "gather", "other", "allreduce"]
 
@@ -97,6 +97,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "hht_result_level": ([p, i32, u32, i32, p, i64, p], C.c_int),
         "hht_result_stats": ([p, p], C.c_int),
         "hht_set_leaf_sink": ([p, p, i64], C.c_int),
+        "hht_set_leaf_sink_packed": ([p, p, i64], C.c_int),
+        "hht_result_tree_offsets": ([p, p, i64, p], C.c_int),
         "hht_group_create": ([p, i32], C.c_int),
         "hht_detect_trees": ([p, p, p, i32, i32, i32, i64], C.c_int),
         "hht_detect_image": ([p, p, i32, i32, i32, i64], C.c_int),
@@ -335,6 +337,27 @@ class HHT:
         assert out.dtype == np.uint32 and out.ndim == 2 and out.shape[1] == 5 and out.flags.c_contiguous
         self._sink = out
         self._check(self._lib.hht_set_leaf_sink(self._ctx, C.c_void_p(out.ctypes.data), out.shape[0]))
+
+    def set_leaf_sink_packed(self, out: Optional[np.ndarray]):
+        """Stream every later detect's leaf rows as packed uint64 (i << 48 | j << 32 | votes) into
+        `out` (a C-contiguous uint64 [cap] array, ideally pinned); None removes the sink. The tree of
+        each row follows from tree_offsets(). Needs depth <= 16."""
+        if out is None:
+            self._check(self._lib.hht_set_leaf_sink_packed(self._ctx, None, 0))
+            self._sink = None
+            return
+        assert out.dtype == np.uint64 and out.ndim == 1 and out.flags.c_contiguous
+        self._sink = out
+        self._check(self._lib.hht_set_leaf_sink_packed(self._ctx, C.c_void_p(out.ctypes.data), out.shape[0]))
+
+    def tree_offsets(self) -> np.ndarray:
+        """uint64 [ntrees + 1]: index of each tree's first detected line in the leaf order of the last
+        detect (tree t = image t / H, half index t % H, ALPHA first)."""
+        nt = C.c_int64()
+        self._check(self._lib.hht_result_tree_offsets(self._ctx, None, 0, C.byref(nt)))
+        out = np.zeros(nt.value + 1, dtype=np.uint64)
+        self._check(self._lib.hht_result_tree_offsets(self._ctx, C.c_void_p(out.ctypes.data), out.shape[0], C.byref(nt)))
+        return out
 
     def leaves(self, image: int = -1) -> np.ndarray:
         """int64 [L, 5]: (image, half, i, j, votes) in image, half, depth-first order."""

@@ -49,3 +49,12 @@ print("device points, sink:    wall %.1f ms, device %.1f ms" % wall(lambda: h.de
 print("host points,   sink:    wall %.1f ms, device %.1f ms" % wall(lambda: h.detect_batch(host, offs, cfg.N, cfg.D, cfg.T)))
 st = h.stats()
 print("leaves", st["leaves"], "streamed", st["leaves_streamed"], "ranges", st["ranges"])
+# the final-range cut alone: a sink with no room (the driver cuts the last range, copies nothing)
+h.set_leaf_sink(buf[:0])
+print("device points, sink cap 0 (cut, no copies): wall %.1f ms, device %.1f ms" % wall(lambda: h.detect_batch(dev, offs, cfg.N, cfg.D, cfg.T)))
+print("ranges", h.stats()["ranges"])
+pk = torch.empty(int(n * 1.1) + 1024, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+h.set_leaf_sink_packed(pk)
+print("device points, packed sink: wall %.1f ms, device %.1f ms" % wall(lambda: h.detect_batch(dev, offs, cfg.N, cfg.D, cfg.T)))
+print("host points,   packed sink: wall %.1f ms, device %.1f ms" % wall(lambda: h.detect_batch(host, offs, cfg.N, cfg.D, cfg.T)))
+h.set_leaf_sink(None)

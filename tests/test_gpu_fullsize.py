@@ -111,3 +111,27 @@ def test_fullsize_e2e_leaf_sink(cid, cuda_device):
     assert hashlib.sha256(rows.tobytes()).hexdigest() == gold["leaves_sha256"]
     assert st["tests"] == gold["tests"] and st["votes"] == gold["votes"]
     h.close()
+
+
+@pytest.mark.parametrize("cid", [3, 5])
+def test_fullsize_e2e_leaf_sink_packed(cid, cuda_device):
+    """bench.py's e2e configuration with the packed sink (8-byte rows + per-tree offsets): the rows,
+    expanded to (image, half, i, j, votes), hash to the oracle digest's leaves, in order."""
+    import torch
+    from tests.test_gpu_parity import _unpack_rows
+    cfg = synth.CONFIGS[cid]
+    gold = json.load(open(os.path.join(GOLD, f"c{cid}_digest.json")))
+    pts, _ = synth.config_image(cid)
+    offs = np.array([0, pts.shape[0]], dtype=np.int64)
+    host = torch.from_numpy(np.ascontiguousarray(pts)).pin_memory().numpy()
+    h = hht.HHT(halves=cfg.halves, profile=True)
+    sink = torch.empty(gold["leaves"] + 1024, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    h.set_leaf_sink_packed(sink)
+    h.detect_batch(host, offs, cfg.N, cfg.D, cfg.T)
+    st = h.stats()
+    assert st["leaves_streamed"] == st["leaves"] == gold["leaves"]
+    rows = _unpack_rows(sink[:gold["leaves"]], h.tree_offsets(), 2, cfg.halves)
+    rows = np.ascontiguousarray(rows.astype("<u4"))
+    assert hashlib.sha256(rows.tobytes()).hexdigest() == gold["leaves_sha256"]
+    assert st["tests"] == gold["tests"] and st["votes"] == gold["votes"]
+    h.close()

@@ -312,6 +312,58 @@ def test_leaf_sink_streaming(budget, torch_dev):
     assert h.stats()["leaves_streamed"] == 0
 
 
+def _unpack_rows(packed, offs, H, halves):
+    """packed uint64 rows + per-tree offsets -> (image, half, i, j, votes) rows (hht_leaf order)."""
+    hs = [x for x in (hht.ALPHA, hht.BETA) if halves & x]
+    tree = np.repeat(np.arange(len(offs) - 1), np.diff(offs.astype(np.int64)))
+    return np.stack([tree // H, np.array(hs, np.int64)[tree % H], (packed >> 48).astype(np.int64),
+                     ((packed >> 32) & 0xFFFF).astype(np.int64), (packed & 0xFFFFFFFF).astype(np.int64)], axis=1)
+
+
+@pytest.mark.parametrize("budget", [0, 256 << 10])
+def test_leaf_sink_packed(budget, torch_dev):
+    """hht_set_leaf_sink_packed: 8-byte rows (i << 48 | j << 32 | votes) streamed during the detect,
+    with hht_result_tree_offsets, reproduce hht_result_leaves(-1) row for row, across depth-first
+    ranges and for a ragged batch with empty images; 8 bytes per row over PCIe; depth > 16 refused."""
+    cfg = synth.CONFIGS[2]
+    pts, _ = synth.config_image(2)
+    h = hht.HHT(halves=cfg.halves, mem_budget=budget)
+    d = _dev(pts, torch_dev)
+    h.detect(d, cfg.N, cfg.D, cfg.T)
+    want = h.leaves(-1)
+    sink = np.zeros(want.shape[0] + 5, dtype=np.uint64)
+    h.set_leaf_sink_packed(sink)
+    h.detect(d, cfg.N, cfg.D, cfg.T)
+    st = h.stats()
+    assert st["leaves_streamed"] == st["leaves"] == want.shape[0]
+    offs = h.tree_offsets()
+    assert offs.shape[0] == 3 and offs[0] == 0 and offs[-1] == want.shape[0]
+    assert np.array_equal(_unpack_rows(sink[:want.shape[0]], offs, 2, cfg.halves), want)
+    assert st["d2h_bytes"] >= 8 * want.shape[0] and st["d2h_bytes"] < 20 * want.shape[0]
+    # a ragged batch (empty images included), ALPHA only
+    parts = [synth.random_scene(300 + k, 64, max_lines=3, max_noise=200) if k % 3 else np.zeros((0, 2), np.int32)
+             for k in range(7)]
+    allp = np.concatenate(parts).astype(np.int32)
+    bo = np.concatenate([[0], np.cumsum([len(q) for q in parts])]).astype(np.int64)
+    hb = hht.HHT(halves=hht.ALPHA, mem_budget=budget)
+    hb.detect_batch(_dev(allp, torch_dev), bo, 64, 6, 4)
+    want = hb.leaves(-1)
+    sink = np.zeros(max(want.shape[0], 1), dtype=np.uint64)
+    hb.set_leaf_sink_packed(sink)
+    hb.detect_batch(_dev(allp, torch_dev), bo, 64, 6, 4)
+    offs = hb.tree_offsets()
+    assert offs.shape[0] == 8
+    assert np.array_equal(_unpack_rows(sink[:want.shape[0]], offs, 1, hht.ALPHA), want)
+    for b in range(7):
+        assert offs[b + 1] - offs[b] == hb.leaves(b).shape[0]
+    with pytest.raises(hht.HHTError) as e:
+        hb.detect_batch(_dev(allp, torch_dev), bo, 64, 17, 4)
+    assert e.value.name == "HHT_EINVAL"
+    hb.set_leaf_sink_packed(None)
+    hb.detect_batch(_dev(allp, torch_dev), bo, 64, 6, 4)
+    assert hb.stats()["leaves_streamed"] == 0
+
+
 @pytest.mark.parametrize("tail_depth", [4, 5, 6])
 @pytest.mark.parametrize("N", [1, 2, 3, 5, 1023, 4095, 16383, 32767])
 def test_raster_fixed_point_extremes(N, tail_depth, torch_dev):
