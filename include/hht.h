@@ -121,7 +121,11 @@ typedef struct {
                                 world and rank (HHT_EINVAL otherwise) */
     uint32_t tail_units;     /* fused tail work units: 0 = auto (when a launch has fewer parents than
                                 8 x its warps, each parent's chunks are split into blocks so every
-                                warp has work to the end); 2 = one unit per parent. Identical results */
+                                warp has work to the end; with more parents, whole parents first and
+                                then the last (one per warp) in pieces of 32 chunks, so that the launch
+                                does not end waiting for the warps that took the last large parents);
+                                2 = one unit per parent; 3 = always the second scheme (tests).
+                                Identical results */
 } hht_opts;
 
 /* Re-point the ctx at another BORROWED stream (cudaStream_t; NULL = back to the ctx's own stream,

@@ -94,11 +94,23 @@ struct hht_group {
 #ifndef HHT_SINK_SLOTS
 #define HHT_SINK_SLOTS 2
 #endif
+#ifndef HHT_SINK_CUT_DIV
+#define HHT_SINK_CUT_DIV 8            // leaf sink: the final range's last 1/DIV becomes a range of its own (0: no cut)
+#endif
+constexpr uint32_t kSinkCutDiv = HHT_SINK_CUT_DIV;
 constexpr int kSinkSlots = HHT_SINK_SLOTS;   // leaf-sink staging buffers (row conversion -> host copy)
 #ifndef HHT_UNITS_PER_WARP
 #define HHT_UNITS_PER_WARP 8
 #endif
 constexpr uint64_t kUnitsPerWarp = HHT_UNITS_PER_WARP;   // fused tail: split parents below this many per warp
+#ifndef HHT_TAIL_SPLIT_PER_WARP
+#define HHT_TAIL_SPLIT_PER_WARP 1     // many parents: the last (this many x warps) parents are split ...
+#endif
+#ifndef HHT_TAIL_SPLIT_K
+#define HHT_TAIL_SPLIT_K 32           // ... into units of this many chunks (0: no split)
+#endif
+constexpr uint64_t kTailSplitPerWarp = HHT_TAIL_SPLIT_PER_WARP;
+constexpr uint32_t kTailSplitK = HHT_TAIL_SPLIT_K;
 constexpr int kFusedThreadsHost = 512;                     // k_fused block size (hht_kernels.cu kFusedThreads)
 
 struct hht_ctx {
@@ -739,12 +751,26 @@ hht_status tail_fused(hht_ctx* x, int l, uint32_t r0, uint32_t r1, bool all_chil
     // few parents for the warps (C3, small ranges): split each parent's chunks into work units so that
     // every warp gets work until the end (a unit's partial raster batches are its only extra cost)
     const uint64_t nwarps = (uint64_t)x->fused_grid[x->int64 ? 1 : 0] * (kFusedThreadsHost / 32);
-    if (!gp && x->opts.tail_units != 2 && (uint64_t)(r1 - r0) < kUnitsPerWarp * nwarps) {
+    if (!gp && x->opts.tail_units != 2 && x->opts.tail_units != 3 && (uint64_t)(r1 - r0) < kUnitsPerWarp * nwarps) {
         const uint64_t target = kUnitsPerWarp * nwarps;
         const uint64_t cap = target + (r1 - r0) + 1;        // sum of ceil(chunks_r / K) <= chunks / K + parents
         TRY(ensure(x, x->units, cap * 8 + 16));
         uint32_t* nk = (uint32_t*)((char*)x->units.p + cap * 8);
-        CK(launch_units(a.p_choff, r0, r1, (uint32_t)target, (uint2*)x->units.p, nk, x->st));
+        CK(launch_units(a.p_choff, r0, r1, (uint32_t)target, r0, 0, (uint2*)x->units.p, nk, x->st));
+        a.units = (const uint2*)x->units.p;
+        a.nunits = nk;
+        a.unit_k = nk + 1;
+    } else if (!gp && x->opts.tail_units != 2 && kTailSplitK > 0 && kTailSplitPerWarp > 0) {
+        // (tail_units 3 takes this path whatever the parent count: tests)
+        // many parents: whole parents first, then the last ones in pieces of kTailSplitK chunks (the
+        // end of the launch otherwise waits for the warps that took the last large parents)
+        const uint64_t ns = std::min<uint64_t>(r1 - r0, kTailSplitPerWarp * nwarps);
+        const uint32_t r_split = r1 - (uint32_t)ns;
+        // sum over the split parents of ceil(chunks_r / K) <= their chunks / K + ns <= P.C / K + ns
+        const uint64_t cap = (r_split - r0) + ns + P.C / kTailSplitK + 1;
+        TRY(ensure(x, x->units, cap * 8 + 16));
+        uint32_t* nk = (uint32_t*)((char*)x->units.p + cap * 8);
+        CK(launch_units(a.p_choff, r0, r1, 0, r_split, kTailSplitK, (uint2*)x->units.p, nk, x->st));
         a.units = (const uint2*)x->units.p;
         a.nunits = nk;
         a.unit_k = nk + 1;
@@ -853,10 +879,10 @@ hht_status descend(hht_ctx* x, int l, uint32_t r0, uint32_t r1) {
         // a range of its own, so that the copy of the rest overlaps that eighth's tail. (Halving the
         // final piece repeatedly, 1/2, 1/4, ..., measured worse on C5: +1.5, +4.5, +8.7 ms e2e with 1, 3
         // and 5 cuts, since a small piece leaves most warps of its fused tail idle.)
-        if (x->sink && !final_cut && ri.q1 == Fc && q0 > 0 && r1 == P.F && fused_tail(x) &&
+        if (kSinkCutDiv > 0 && x->sink && !final_cut && ri.q1 == Fc && q0 > 0 && r1 == P.F && fused_tail(x) &&
             lc == x->D - tail_depth(x) && Fc - q0 >= 64) {
             final_cut = true;
-            const uint32_t qf = q0 + (Fc - q0) - (Fc - q0) / 8;
+            const uint32_t qf = q0 + (Fc - q0) - (Fc - q0) / kSinkCutDiv;
             CK(launch_range((const uint64_t*)C.off.p, (const uint32_t*)C.parent.p, C.F, q0, cap, qf,
                             (const uint64_t*)P.off.p, (const uint64_t*)P.choff.p, (const uint32_t*)P.len.p,
                             lc == 1, (RangeInfo*)x->rng.p, (uint64_t*)x->bounds.p, x->range_m, x->st));

@@ -116,8 +116,9 @@ struct PassArgs {
     const uint32_t* nunits;
     const uint32_t* unit_k;
 };
-cudaError_t launch_units(const uint64_t* p_choff, uint32_t r_lo, uint32_t r_hi, uint32_t target_units, uint2* units,
-                         uint32_t* nunits_k, cudaStream_t st);
+constexpr uint32_t kUnitWhole = 0xFFFFFFFFu;   // work unit = the whole parent (k_units with k_split)
+cudaError_t launch_units(const uint64_t* p_choff, uint32_t r_lo, uint32_t r_hi, uint32_t target_units, uint32_t r_split,
+                         uint32_t k_split, uint2* units, uint32_t* nunits_k, cudaStream_t st);
 
 struct SplitArgs {
     const uint32_t* V;             // [4 * Fp] global child votes

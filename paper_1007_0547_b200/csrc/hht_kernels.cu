@@ -1046,7 +1046,7 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
         // get no child bits (a line crossing a child of r crosses r)
         const uint32_t lr = GP ? __ldg(A.gp_parent + r) : r;
         uint64_t c_lo = __ldg(A.p_choff + lr), c_hi = __ldg(A.p_choff + lr + 1);
-        if (A.units) {
+        if (A.units && sub != kUnitWhole) {
             const uint64_t K = *A.unit_k;
             c_lo += (uint64_t)sub * K;
             c_hi = min(c_hi, c_lo + K);
@@ -1194,19 +1194,24 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
     }
 }
 
-// Work units of a fused-tail launch with few parents (hht_driver.cu tail_fused): K = max(4,
-// ceil(chunks / target)) chunks per unit, parent r of [r_lo, r_hi) split into ceil(chunks_r / K)
-// units (r, k), listed in parent order. One block; a chunked block scan over the parents.
+// Work units of a fused-tail launch (hht_driver.cu tail_fused). With few parents (k_split == 0):
+// K = max(4, ceil(chunks / target)) chunks per unit, parent r of [r_lo, r_hi) split into
+// ceil(chunks_r / K) units (r, k). With many parents (k_split = K > 0): parents before r_split are
+// whole units (r, kUnitWhole) and only the last ones, [r_split, r_hi), are split into units of K
+// chunks, so the warps that finish last finish with small pieces. Listed in parent order. One
+// block; a chunked block scan over the parents.
 __global__ void __launch_bounds__(1024) k_units(const uint64_t* __restrict__ p_choff, uint32_t r_lo, uint32_t r_hi,
-                                                 uint32_t target, uint2* __restrict__ units, uint32_t* __restrict__ nk) {
+                                                 uint32_t target, uint32_t r_split, uint32_t k_split,
+                                                 uint2* __restrict__ units, uint32_t* __restrict__ nk) {
     __shared__ uint32_t s_w[33];
     const uint64_t total = p_choff[r_hi] - p_choff[r_lo];
-    const uint32_t K = (uint32_t)max((uint64_t)4, (total + target - 1) / max(target, 1u));
+    const uint32_t K = k_split ? k_split : (uint32_t)max((uint64_t)4, (total + target - 1) / max(target, 1u));
+    if (!k_split) r_split = r_lo;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     uint32_t carry = 0;
     for (uint32_t base = r_lo; base < r_hi; base += blockDim.x) {
         const uint32_t r = base + tid;
-        const uint32_t n = r < r_hi ? (uint32_t)((p_choff[r + 1] - p_choff[r] + K - 1) / K) : 0u;
+        const uint32_t n = r >= r_hi ? 0u : r < r_split ? 1u : (uint32_t)((p_choff[r + 1] - p_choff[r] + K - 1) / K);
         uint32_t inc = n;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -1228,16 +1233,17 @@ __global__ void __launch_bounds__(1024) k_units(const uint64_t* __restrict__ p_c
         }
         __syncthreads();
         const uint32_t off = carry + s_w[wid] + inc - n;
-        for (uint32_t k = 0; k < n; ++k) units[off + k] = make_uint2(r, k);
+        if (r < r_split) units[off] = make_uint2(r, kUnitWhole);
+        else for (uint32_t k = 0; k < n; ++k) units[off + k] = make_uint2(r, k);
         carry += s_w[32];
         __syncthreads();
     }
     if (tid == 0) { nk[0] = carry; nk[1] = K; }
 }
 
-cudaError_t launch_units(const uint64_t* p_choff, uint32_t r_lo, uint32_t r_hi, uint32_t target_units, uint2* units,
-                         uint32_t* nunits_k, cudaStream_t st) {
-    k_units<<<1, 1024, 0, st>>>(p_choff, r_lo, r_hi, target_units, units, nunits_k);
+cudaError_t launch_units(const uint64_t* p_choff, uint32_t r_lo, uint32_t r_hi, uint32_t target_units, uint32_t r_split,
+                         uint32_t k_split, uint2* units, uint32_t* nunits_k, cudaStream_t st) {
+    k_units<<<1, 1024, 0, st>>>(p_choff, r_lo, r_hi, target_units, r_split, k_split, units, nunits_k);
     return cudaGetLastError();
 }
 

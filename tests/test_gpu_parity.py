@@ -243,12 +243,13 @@ def test_prefetch_modes(seed, prefetch, torch_dev):
         assert (h.stats()["tests"], h.stats()["votes"]) == (ref.tests, ref.votes)
 
 
-@pytest.mark.parametrize("tail_units", [0, 2])
+@pytest.mark.parametrize("tail_units", [0, 2, 3])
 @pytest.mark.parametrize("seed", range(6))
 def test_fused_tail_work_units(seed, tail_units, torch_dev):
     """The fused tail with each parent's chunks split into work units (auto: fewer parents than
-    8 x warps) and with one unit per parent (tail_units 2) give identical records and leaves,
-    also under a small budget (many ranges, some with very few parents)."""
+    8 x warps), with one unit per parent (tail_units 2) and with whole parents followed by the last
+    ones in 32-chunk pieces (tail_units 3, the many-parents scheme) give identical records and
+    leaves, also under a small budget (many ranges, some with very few parents)."""
     rng = np.random.default_rng(700 + seed)
     N = int(rng.choice([64, 200, 256]))
     D = int(rng.integers(6, 9))
