@@ -283,11 +283,11 @@ def run_reference(a):
     print(json.dumps(line), flush=True)
 
 
-def _lib_sha256():
-    import hashlib
-    from paper_1007_0547_b200 import build as b
-    with open(b.LIB, "rb") as f:
-        return hashlib.sha256(f.read()).hexdigest()
+def _lib_build_id():
+    """The loaded libhht.so's build id (hht_version: sha256 of its sources and nvcc flags)."""
+    from paper_1007_0547_b200 import hht
+    v = hht.version().split()
+    return v[v.index("build") + 1] if "build" in v else None
 
 
 def main():
@@ -396,12 +396,14 @@ def main():
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            if tj.get("libhht_sha256") == _lib_sha256():
+            bid = _lib_build_id()
+            if bid and bid != "unknown" and tj.get("libhht_build_id") == bid:
                 cap = tj.get(f"config{cfg.cid}", {}).get(dom, {}) or {}
                 traffic = cap.get("traffic")
+                ncu_note = f"profiles/ncu_traffic.json, captured on this build ({bid})"
             else:
                 ncu_note = (f"profiles/ncu_traffic.json was captured on another build "
-                            f"({str(tj.get('libhht_sha256'))[:12]}); not used")
+                            f"({tj.get('libhht_build_id')}; this one {bid}); not used")
         except Exception:  # noqa: BLE001
             cap = {}
     hbm = {"achieved": achieved_gbs, "peak": peak, "unit": "GB/s", "frac": achieved_gbs / peak,

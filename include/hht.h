@@ -304,7 +304,9 @@ const char* hht_status_str(hht_status s);
 /* Release every resource; NULL-safe; synchronises the ctx stream first. */
 void hht_destroy(hht_ctx* ctx);
 
-/* Library build identification: "hht <version> sm_100a". */
+/* Library build identification: "hht <version> sm_100a build <id>", id = 16 hex digits of the sha256
+ * of the CUDA sources, headers and nvcc flags it was built from (equal for every build of the same
+ * kernels, unlike the bytes of the .so). */
 const char* hht_version(void);
 
 #ifdef __cplusplus

@@ -34,13 +34,29 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def build_id() -> str:
+    """Identity of the kernels a build produces: sha256 (16 hex digits) of the CUDA sources, headers
+    and nvcc flags. nvcc embeds per-invocation module IDs in the host stubs, so two builds of the
+    same sources differ byte for byte; this id does not (bench.py matches ncu captures on it)."""
+    import hashlib
+    h = hashlib.sha256(" ".join(FLAGS).encode())
+    for f in [os.path.join(CSRC, s) for s in SOURCES] + [x if os.path.isabs(x) else os.path.join(CSRC, x)
+                                                         for x in HEADERS]:
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     nd = nccl_dir()
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), "-std=c++17", "-O3", "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
-           "-gencode", "arch=compute_100a,code=sm_100a",
+    cmd = [nvcc()] + FLAGS + [f"-DHHT_BUILD_ID=\"{build_id()}\"",
            "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(nd, "include"),
            "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES] + [

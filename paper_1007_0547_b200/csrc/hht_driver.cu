@@ -1492,7 +1492,12 @@ hht_status host_leaves(hht_ctx* x) {
 // =============================================================================================
 extern "C" {
 
-const char* hht_version(void) { return "hht 0.1.0 sm_100a"; }
+#ifndef HHT_BUILD_ID
+#define HHT_BUILD_ID "unknown"
+#endif
+// "hht <version> sm_100a build <id>": id = sha256 of the sources, headers and nvcc flags (build.py
+// build_id), the same for every build of the same kernels (bench.py matches ncu captures on it)
+const char* hht_version(void) { return "hht 0.1.0 sm_100a build " HHT_BUILD_ID; }
 
 const char* hht_status_str(hht_status s) {
     switch (s) {

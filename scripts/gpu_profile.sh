@@ -7,6 +7,7 @@
 set -x
 mkdir -p gpurun_out
 sha256sum paper_1007_0547_b200/libhht.so > gpurun_out/libhht.sha256
+python -c "from paper_1007_0547_b200 import hht; print(hht.version())" > gpurun_out/libhht.version
 python bench.py > gpurun_out/bench_default.log 2> gpurun_out/bench_default.err && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_c5.csv python bench.py > gpurun_out/ncu_launches.log 2>&1

@@ -94,6 +94,9 @@ def main():
     shaf = os.path.join(G, "libhht.sha256")
     # bench.py splices these counters into its line only when this hash equals the loaded library's
     traffic["libhht_sha256"] = open(shaf).read().split()[0] if os.path.exists(shaf) else None
+    verf = os.path.join(G, "libhht.version")
+    ver = open(verf).read().split() if os.path.exists(verf) else []
+    traffic["libhht_build_id"] = ver[ver.index("build") + 1] if "build" in ver else None
     wskip = 14
     wf = os.path.join(G, "write_skip.txt")
     if os.path.exists(wf):
@@ -130,7 +133,9 @@ def main():
     tot, cnt = launch_list()
     T = sum(tot.values())
     lines = [f"# Round {a.round} GPU profile summary (config 5, one B200)", "",
-             f"libhht.so sha256 of the profiled build: {traffic['libhht_sha256']}", ""]
+             f"Profiled build: id {traffic['libhht_build_id']} (sha256 of the CUDA sources, headers and nvcc "
+             f"flags; bench.py attaches these counters only to a library with the same id), .so sha256 "
+             f"{traffic['libhht_sha256']}", ""]
     if os.path.exists(os.path.join(G, "bench_default.log")):
         b = json.loads(open(os.path.join(G, "bench_default.log")).read().strip().splitlines()[-1])
         lines += ["## bench.py (default: config 5, 5 steps, 3 warm-up)", "",
