@@ -817,6 +817,15 @@ __device__ __forceinline__ void fill_tab16() {
 // (a, c), accumulated into `dst` (256 u32 counters, [16 * column + row]) with one atomic per
 // (lane, cell pair) per column block. Shared by the dense tail (batches = chunks of the region's
 // list) and the fused tail (batches = full shared-memory stacks of a child of a level-(D-5) region).
+#ifndef HHT_RASTER_ATOMIC_NOZ
+#define HHT_RASTER_ATOMIC_NOZ 1     // 1: the two cell atomics per lane unconditionally (0: skip zero cells; slower)
+#endif
+#ifndef HHT_RASTER_VALID_BRANCH
+#define HHT_RASTER_VALID_BRANCH 1   // 1: partial-batch lanes fixed up in a warp-uniform branch (0: per line)
+#endif
+#ifndef HHT_RASTER_SETUP_FMA
+#define HHT_RASTER_SETUP_FMA 0      // 1: entry unpacking on the FMA pipe (multiply-high), not PRMT
+#endif
 #ifndef HHT_RASTER_XRECOMP
 #define HHT_RASTER_XRECOMP 0      // 1: X of a column block's first boundary recomputed from Y (not carried)
 #endif
@@ -880,15 +889,37 @@ struct Raster16 {
 #else
         uint32_t Y[ITEMS], P[ITEMS], X[ITEMS];
 #endif
+#if HHT_RASTER_SETUP_FMA
+        // unpack on the FMA pipe: hi = w >> 16 (multiply-high by an opaque 2^16), lo = w - hi 2^16,
+        // with the half's coefficients chosen once per batch
+        const uint32_t c_hi = beta ? ey_s : alpha_s, c_lo = beta ? alpha_s : ey_s;
+        const uint32_t e_hi = beta ? 0u : ex_s, e_lo = beta ? ex_s : 0u;
+        const uint32_t c16 = one << 16, m16 = 0u - c16;
+#endif
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             const uint32_t w = p[it];
+#if HHT_RASTER_SETUP_FMA
+            uint32_t hi, lo, y0s, pex;
+            asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi) : "r"(w), "r"(c16));
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(lo) : "r"(hi), "r"(m16), "r"(w));
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(y0s) : "r"(hi), "r"(c_hi), "r"(beta_s));
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(y0s) : "r"(lo), "r"(c_lo), "r"(y0s));
+            asm("mul.lo.u32 %0, %1, %2;" : "=r"(pex) : "r"(hi), "r"(e_hi));
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(pex) : "r"(lo), "r"(e_lo), "r"(pex));
+#else
             const uint32_t ex = __byte_perm(w, 0, sel_ex);
             const uint32_t ey = __byte_perm(w, 0, sel_ey);
             const uint32_t y0s = ex * alpha_s + ey * ey_s + beta_s;         // (G(SW corner) - 1) 2^k
+            const uint32_t pex = ex * ex_s;
+#endif
             uint32_t yv, pv;
             asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(yv) : "r"(y0s), "r"(fx_m), "r"(bias));
-            asm("mul.hi.u32 %0, %1, %2;" : "=r"(pv) : "r"(ex * ex_s), "r"(fx_mlo));
+            asm("mul.hi.u32 %0, %1, %2;" : "=r"(pv) : "r"(pex), "r"(fx_mlo));
+#if HHT_RASTER_VALID_BRANCH
+            Y[it] = yv;
+            P[it] = pv;
+#else
             const bool valid = lane + kWarp * it < cnt;
             // lanes past the batch: f = -1 in every column (all-zero entries)
             Y[it] = valid ? yv : bias - (1u << 24) - 1u;
@@ -896,7 +927,25 @@ struct Raster16 {
 #if !HHT_RASTER_XRECOMP
             X[it] = boundary(Y[it], 0);
 #endif
+#endif
         }
+#if HHT_RASTER_VALID_BRANCH
+        // lanes past a partial batch: f = -1 in every column (all-zero entries); full batches (the
+        // common case) skip this warp-uniform block
+        if (__builtin_expect(cnt < kWarp * ITEMS, 0)) {
+#pragma unroll
+            for (int it = 0; it < ITEMS; ++it) {
+                if (lane + kWarp * it >= cnt) {
+                    Y[it] = bias - (1u << 24) - 1u;
+                    P[it] = 0u;
+                }
+            }
+        }
+#if !HHT_RASTER_XRECOMP
+#pragma unroll
+        for (int it = 0; it < ITEMS; ++it) X[it] = boundary(Y[it], 0);
+#endif
+#endif
 #pragma unroll   // a rolled column-block loop (half the code, 44 B of spills) measured 151.7 vs 120.9 ms
         for (int b = 0; b < 4; ++b) {
             uint32_t acc[8];                                  // [2 * column-in-block + row half], nibbles
@@ -956,8 +1005,13 @@ struct Raster16 {
             const uint32_t tot = (v1 & 0x00FF00FFu) + __shfl_xor_sync(kFull, (v1 >> 8) & 0x00FF00FFu, 1);
             const uint32_t col = 4 * b + red_u;
             const uint32_t c0 = tot & 0xFFFFu, c1 = tot >> 16;
+#if HHT_RASTER_ATOMIC_NOZ
+            atomicAdd(dst + 16 * col + red_row, c0);
+            atomicAdd(dst + 16 * col + red_row + 4, c1);
+#else
             if (c0) atomicAdd(dst + 16 * col + red_row, c0);
             if (c1) atomicAdd(dst + 16 * col + red_row + 4, c1);
+#endif
         }
     }
 };
@@ -1099,9 +1153,22 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
                 const uint32_t n = min(t, kFusedBatch);
                 const uint32_t base = t - n;               // raster the top n entries of stack q
                 uint32_t pq[kFusedItems];
+#if HHT_RASTER_VALID_BRANCH
+                // full batches (the common case) read the stack unpredicated; slots past a partial
+                // batch are zeroed (their lines are also masked inside the raster)
+                if (n == kFusedBatch) {
+#pragma unroll
+                    for (int it = 0; it < kFusedItems; ++it) pq[it] = Q[q * kQ + base + lane + kWarp * it];
+                } else {
+#pragma unroll
+                    for (int it = 0; it < kFusedItems; ++it)
+                        pq[it] = (lane + kWarp * it < (int)n) ? Q[q * kQ + base + lane + kWarp * it] : 0u;
+                }
+#else
 #pragma unroll
                 for (int it = 0; it < kFusedItems; ++it)
                     pq[it] = (lane + kWarp * it < (int)n) ? Q[q * kQ + base + lane + kWarp * it] : 0u;
+#endif
                 const uint32_t nf_q = __shfl_sync(kFull, my_nf, q);
                 R.template run<kFusedItems>(pq, (int)n, 2 * pa + quad_da(q), 2 * pc + quad_dc(q), beta,
                                             A.votes + (uint64_t)(nf_q - A.q0) * kTail16Cells, lane);
