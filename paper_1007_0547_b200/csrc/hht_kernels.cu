@@ -1054,6 +1054,9 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
 #ifndef HHT_FUSED_JIT
 #define HHT_FUSED_JIT 0                           // 1: load a chunk's entries when pushed, not ahead
 #endif
+#ifndef HHT_FUSED_BATCH_LEAN
+#define HHT_FUSED_BATCH_LEAN 1                    // per-batch bookkeeping without branches or atomics (0: the old form)
+#endif
 #ifndef HHT_FUSED_ITEMS
 #define HHT_FUSED_ITEMS 13                        // raster batches of 13 lines per lane (416 entries)
 #endif
@@ -1139,6 +1142,7 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
 #endif
         uint64_t ch = c_lo;
         uint32_t streamed = 0;                             // entries of this work unit (profiling)
+        uint32_t rastered = 0;                             // (child, line) pairs rastered (profiling)
         // One loop whose every iteration either rasters one stack (a full one, or once the parent's
         // chunks are exhausted any non-empty one) or pushes one chunk: the raster code is
         // instantiated once (four inlined copies measured 2x slower: instruction-cache misses).
@@ -1172,8 +1176,16 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
                 const uint32_t nf_q = __shfl_sync(kFull, my_nf, q);
                 R.template run<kFusedItems>(pq, (int)n, 2 * pa + quad_da(q), 2 * pc + quad_dc(q), beta,
                                             A.votes + (uint64_t)(nf_q - A.q0) * kTail16Cells, lane);
+#if HHT_FUSED_BATCH_LEAN
+                rastered += n;                             // flushed once per work unit
+                top0 = q == 0 ? base : top0;               // branch-free (the if-chain compiled to branches)
+                top1 = q == 1 ? base : top1;
+                top2 = q == 2 ? base : top2;
+                top3 = q == 3 ? base : top3;
+#else
                 if (lane == 0) atomicAdd(A.child_pairs, (unsigned long long)n);
                 if (q == 0) top0 = base; else if (q == 1) top1 = base; else if (q == 2) top2 = base; else top3 = base;
+#endif
                 __syncwarp();
                 continue;
             }
@@ -1258,6 +1270,11 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
 #endif
         }
         if (lane == 0) atomicAdd(A.child_pairs + 1, (unsigned long long)streamed);
+#if HHT_FUSED_BATCH_LEAN
+        if (lane == 0) atomicAdd(A.child_pairs, (unsigned long long)rastered);
+#else
+        (void)rastered;
+#endif
     }
 }
 
