@@ -19,10 +19,13 @@ pytestmark = pytest.mark.gpu
 AB = hht.ALPHA | hht.BETA
 
 
-def _run_ranks(pts, N, D, T, halves, world, dev, **kw):
+def _run_ranks(pts, N, D, T, halves, world, dev, setup=None, **kw):
     import torch
     g = hht.Group(world)
     hs = [hht.HHT(halves=halves, rank=r, world=world, group=g, **kw) for r in range(world)]
+    if setup:
+        for h in hs:
+            setup(h)
     errs = [None] * world
     bounds = [synth.shard(pts.shape[0], r, world) for r in range(world)]
     shards = [torch.from_numpy(np.ascontiguousarray(pts[lo:hi])).to(dev) for lo, hi in bounds]
@@ -118,5 +121,33 @@ def test_multirank_digest(cid, budget, cuda_device):
     if budget and cid == 3:
         assert min(h.stats()["ranges"] for h in hs) > 2 * cfg.D
     for h in hs:
+        h.close()
+    g.close()
+
+
+@pytest.mark.parametrize("budget", [0, 256 << 10])
+def test_multirank_packed_leaf_sink(budget, cuda_device):
+    """The packed leaf sink on 2 ranks (depth-first ranges under a small budget, where each range's
+    leaf-grid work is deferred behind the next range): every rank streams the global leaves, in
+    order, equal to the oracle's."""
+    from tests.test_gpu_parity import _unpack_rows
+    cfg = synth.CONFIGS[2]
+    pts, _ = synth.config_image(2)
+    ref = oracle.detect(pts, cfg.N, cfg.D, cfg.T, cfg.halves)
+    want = ref.leaves.shape[0]
+    sinks = {}
+
+    def setup(h):
+        sinks[id(h)] = np.zeros(want + 3, dtype=np.uint64)
+        h.set_leaf_sink_packed(sinks[id(h)])
+
+    hs, g, errs = _run_ranks(pts, cfg.N, cfg.D, cfg.T, cfg.halves, 2, cuda_device, setup=setup, mem_budget=budget)
+    assert errs == [None, None], errs
+    for h in hs:
+        st = h.stats()
+        assert st["leaves_streamed"] == st["leaves"] == want
+        rows = _unpack_rows(sinks[id(h)][:want], h.tree_offsets(), 2, cfg.halves)
+        assert np.array_equal(rows, h.leaves(-1))       # the streamed rows are the result ...
+        compare_all(h, ref, cfg.halves, cfg.D)           # ... and the result is the oracle's
         h.close()
     g.close()
