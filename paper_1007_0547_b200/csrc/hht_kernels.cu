@@ -266,8 +266,15 @@ __device__ __forceinline__ void sts_if(uint32_t m, uint32_t& sa, uint32_t v) {
 // Work loop of the pass and tail kernels: each warp walks chunks c_lo + warp0, + nwarps, ...; the
 // next chunk's descriptor and entries are in flight while the current chunk is processed
 // (PREF = true), or only the descriptor is (PREF = false, fewer registers).
-template <bool PREF, typename Body>
-__device__ __forceinline__ void chunk_loop(const PassArgs& A, int lane, Body body) {
+struct NoAhead {
+    __device__ __forceinline__ void operator()(const ChunkDesc&) const {}
+};
+
+// `ahead(dn)` is called with the next chunk's descriptor before the current chunk's body (and with
+// the first chunk's before the loop): per-chunk loads that only depend on the descriptor (the
+// list passes' child maps) are issued one chunk ahead there.
+template <bool PREF, typename Body, typename Ahead = NoAhead>
+__device__ __forceinline__ void chunk_loop(const PassArgs& A, int lane, Body body, Ahead ahead = NoAhead{}) {
     const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t c_lo = A.chunk_bounds[0], c_hi = A.chunk_bounds[1];
@@ -276,17 +283,20 @@ __device__ __forceinline__ void chunk_loop(const PassArgs& A, int lane, Body bod
     ChunkDesc dn = load_desc(A.chunks, ch + nwarps, c_hi);
     uint32_t p[kItems];
     load_items(p, A.list, A.list_base, d, lane);
+    ahead(d);
     for (; ch < c_hi; ch += nwarps) {
         if (PREF) {
             uint32_t pn[kItems];
             load_items(pn, A.list, A.list_base, dn, lane);
             const ChunkDesc dnn = load_desc(A.chunks, ch + 2 * nwarps, c_hi);
+            ahead(dn);
             body(d, p);
 #pragma unroll
             for (int it = 0; it < kItems; ++it) p[it] = pn[it];
             d = dn;
             dn = dnn;
         } else {
+            ahead(dn);
             body(d, p);
             d = dn;
             dn = load_desc(A.chunks, ch + 2 * nwarps, c_hi);
@@ -466,6 +476,9 @@ __device__ __forceinline__ void chunk_math_circle(const uint32_t (&p)[kItems], i
 // the last list pass 57, 4 blocks/SM. Measured on C5: forcing 5 blocks/SM on the last pass (48
 // registers, 40 B of spills) 44.4 vs 40.3 ms of list passes; an explicit minimum of 1 let the
 // count-ahead pass grow to 115 registers, 2 blocks/SM, 50.4 ms.)
+#ifndef HHT_PASS_MAP_AHEAD
+#define HHT_PASS_MAP_AHEAD 0   // child maps one chunk ahead: 1 in the last list pass, 2 in every writing pass
+#endif
 template <typename I, int MODE, int PF, int CIRCLE>
 __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
     constexpr bool PREF = PF == 1;
@@ -487,6 +500,24 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
         CR.init(A, lane);
     }
 
+    // lanes 0..3: next-frontier index and list offset of child `lane` (split children only), loaded
+    // one chunk ahead (kMapAhead) or when the chunk is processed
+    constexpr bool kMapAhead = !CIRCLE && PF != 2 && (MODE == MODE_WRITE_NC ? HHT_PASS_MAP_AHEAD >= 1
+                                                                 : (MODE != MODE_COUNT && HHT_PASS_MAP_AHEAD >= 2));
+    uint32_t cur_nf = kNone, nx_nf = kNone;
+    uint64_t cur_off = 0, nx_off = 0;
+    auto ahead = [&](const ChunkDesc& dn) {
+        if (kMapAhead) {
+            cur_nf = nx_nf;
+            cur_off = nx_off;
+            if (lane < 4 && dn.cnt != 0) {
+                const uint64_t k = 4 * (uint64_t)(dn.r - A.nf_rbase) + lane;
+                nx_nf = __ldg(A.nf + k);
+                if (kWrites) nx_off = __ldg(A.nfoff + k);
+            }
+        }
+    };
+
     auto body = [&](const ChunkDesc& d, const uint32_t (&p)[kItems]) {
         const int cnt = (int)d.cnt;
         const I i0 = (I)d.a << sh;
@@ -494,10 +525,12 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
         const I alpha = ((I)1 << D) - 2 * i0;          // g = ex*alpha + (ey << D) + beta_c
         const I beta_m1 = (N << D) - (I)3 * N * j0 - 1;
 
-        // lanes 0..3: next-frontier index and list offset of child `lane` (split children only)
         uint32_t my_nf = kNone;
         uint64_t my_off = 0;
-        if (MODE != MODE_COUNT && lane < 4) {
+        if (kMapAhead) {
+            my_nf = cur_nf;
+            my_off = cur_off;
+        } else if (MODE != MODE_COUNT && lane < 4) {
             const uint64_t k = 4 * (uint64_t)(d.r - A.nf_rbase) + lane;
             my_nf = __ldg(A.nf + k);
             if (kWrites) my_off = __ldg(A.nfoff + k);
@@ -623,6 +656,8 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
     if constexpr (PF == 2) {
         extern __shared__ uint4 s_tma_ring[];
         chunk_loop_tma(A, lane, (uint32_t)__cvta_generic_to_shared(s_tma_ring) + (threadIdx.x >> 5) * kTmaWarpBytes, body);
+    } else if constexpr (kMapAhead) {
+        chunk_loop<PREF>(A, lane, body, ahead);
     } else {
         chunk_loop<PREF>(A, lane, body);
     }

@@ -8,5 +8,5 @@ for tag in "$@"; do
   echo "$tag parity rc=$? $(tail -1 gpurun_out/ab_par_$tag.log)"
   timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/ab_$tag.log 2> gpurun_out/ab_$tag.err
   python -c "
-import json; l=[x for x in open('gpurun_out/ab_$tag.log') if x.startswith('{')][-1]; j=json.loads(l); print('$tag', round(j['ms_per_step'],2), 'tail', round(j['kernel_ms']['tail'],2))"
+import json; l=[x for x in open('gpurun_out/ab_$tag.log') if x.startswith('{')][-1]; j=json.loads(l); print('$tag', round(j['ms_per_step'],2), 'tail', round(j['kernel_ms']['tail'],2), 'write', round(j['kernel_ms']['write'],2))"
 done
