@@ -234,16 +234,32 @@ __device__ __forceinline__ void chunk_math(const uint32_t (&p)[kItems], int cnt,
     }
 }
 
+#ifndef HHT_DESC_NOPAD
+#define HHT_DESC_NOPAD 1
+#endif
 // Chunk descriptor (32 B, one broadcast load per warp) and the chunk's entries. Lanes past `cnt`
 // load nothing; a descriptor past the launch's chunk range reads as cnt = 0.
 __device__ __forceinline__ ChunkDesc load_desc(const ChunkDesc* __restrict__ d, uint64_t ch, uint64_t c_hi) {
     ChunkDesc z;
     if (ch < c_hi) {
         const uint4* q = reinterpret_cast<const uint4*>(d + ch);
+#if HHT_DESC_NOPAD
+        // the unused pad word is not loaded: a vector load's dead destination register is reused by
+        // the compiler right away, and that write then waits (write-after-write on the scoreboard)
+        // for the load of a descriptor two chunks ahead (ncu, C5 last list pass: 27 % of all stall
+        // samples on two such instructions)
+        const uint4 u0 = __ldg(q);
+        const uint2 e = __ldg(reinterpret_cast<const uint2*>(q + 1));
+        const uint32_t beta = __ldg(reinterpret_cast<const uint32_t*>(q + 1) + 2);
+        z.r = u0.x; z.cnt = u0.y; z.a = u0.z; z.c = u0.w;
+        z.e0 = ((uint64_t)e.y << 32) | e.x;
+        z.beta = beta; z.pad = 0;
+#else
         const uint4 u0 = __ldg(q), u1 = __ldg(q + 1);
         z.r = u0.x; z.cnt = u0.y; z.a = u0.z; z.c = u0.w;
         z.e0 = ((uint64_t)u1.y << 32) | u1.x;
         z.beta = u1.z; z.pad = 0;
+#endif
     } else {
         z.r = 0; z.cnt = 0; z.a = 0; z.c = 0; z.e0 = 0; z.beta = 0; z.pad = 0;
     }
@@ -273,7 +289,30 @@ struct NoAhead {
 // `ahead(dn)` is called with the next chunk's descriptor before the current chunk's body (and with
 // the first chunk's before the loop): per-chunk loads that only depend on the descriptor (the
 // list passes' child maps) are issued one chunk ahead there.
-template <bool PREF, typename Body, typename Ahead = NoAhead>
+// L2PF: lane 0 also keeps the entry span of the chunk two ahead and hands it to the TMA unit as an
+// L2 prefetch (cp.async.bulk.prefetch.L2: no registers or shared memory receive it), so the register
+// loads of that chunk one iteration later hit L2.
+__device__ __forceinline__ void span_of(const ChunkDesc* __restrict__ d, uint64_t ch, uint64_t c_hi, uint64_t& e0,
+                                        uint32_t& cnt) {
+    if (ch < c_hi) {
+        const uint32_t* q = reinterpret_cast<const uint32_t*>(d + ch);
+        cnt = __ldg(q + 1);
+        const uint2 e = __ldg(reinterpret_cast<const uint2*>(q + 4));
+        e0 = ((uint64_t)e.y << 32) | e.x;
+    } else {
+        cnt = 0;
+        e0 = 0;
+    }
+}
+__device__ __forceinline__ void l2_prefetch_span(const PassArgs& A, uint64_t e0, uint32_t cnt) {
+    if (cnt == 0) return;
+    const uint64_t e = e0 - A.list_base;
+    const uint32_t off = (uint32_t)(e & 3u);
+    const uint32_t bytes = ((off + cnt) * 4u + 15u) & ~15u;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(A.list + (e - off)), "r"(bytes) : "memory");
+}
+
+template <bool PREF, typename Body, typename Ahead = NoAhead, bool L2PF = false>
 __device__ __forceinline__ void chunk_loop(const PassArgs& A, int lane, Body body, Ahead ahead = NoAhead{}) {
     const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -284,7 +323,14 @@ __device__ __forceinline__ void chunk_loop(const PassArgs& A, int lane, Body bod
     uint32_t p[kItems];
     load_items(p, A.list, A.list_base, d, lane);
     ahead(d);
+    uint64_t pf_e0 = 0;
+    uint32_t pf_cnt = 0;
+    if (L2PF && lane == 0) span_of(A.chunks, ch + 2 * nwarps, c_hi, pf_e0, pf_cnt);
     for (; ch < c_hi; ch += nwarps) {
+        if (L2PF && lane == 0) {
+            l2_prefetch_span(A, pf_e0, pf_cnt);          // chunk ch + 2 nwarps
+            span_of(A.chunks, ch + 3 * nwarps, c_hi, pf_e0, pf_cnt);
+        }
         if (PREF) {
             uint32_t pn[kItems];
             load_items(pn, A.list, A.list_base, dn, lane);
@@ -476,6 +522,9 @@ __device__ __forceinline__ void chunk_math_circle(const uint32_t (&p)[kItems], i
 // the last list pass 57, 4 blocks/SM. Measured on C5: forcing 5 blocks/SM on the last pass (48
 // registers, 40 B of spills) 44.4 vs 40.3 ms of list passes; an explicit minimum of 1 let the
 // count-ahead pass grow to 115 registers, 2 blocks/SM, 50.4 ms.)
+#ifndef HHT_PASS_L2PF
+#define HHT_PASS_L2PF 0        // L2 bulk prefetch of the chunk two ahead: 1 in the last list pass, 2 in every writing pass
+#endif
 #ifndef HHT_PASS_MAP_AHEAD
 #define HHT_PASS_MAP_AHEAD 0   // child maps one chunk ahead: 1 in the last list pass, 2 in every writing pass
 #endif
@@ -656,10 +705,11 @@ __global__ void __launch_bounds__(256) k_pass(const PassArgs A) {
     if constexpr (PF == 2) {
         extern __shared__ uint4 s_tma_ring[];
         chunk_loop_tma(A, lane, (uint32_t)__cvta_generic_to_shared(s_tma_ring) + (threadIdx.x >> 5) * kTmaWarpBytes, body);
-    } else if constexpr (kMapAhead) {
-        chunk_loop<PREF>(A, lane, body, ahead);
     } else {
-        chunk_loop<PREF>(A, lane, body);
+        constexpr bool kL2pf = !CIRCLE && (MODE == MODE_WRITE_NC ? HHT_PASS_L2PF >= 1
+                                                              : (MODE != MODE_COUNT && HHT_PASS_L2PF >= 2));
+        if constexpr (kMapAhead) chunk_loop<PREF, decltype(body), decltype(ahead), kL2pf>(A, lane, body, ahead);
+        else chunk_loop<PREF, decltype(body), NoAhead, kL2pf>(A, lane, body);
     }
 }
 
