@@ -1142,6 +1142,9 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
 #ifndef HHT_FUSED_BATCH_LEAN
 #define HHT_FUSED_BATCH_LEAN 1                    // per-batch bookkeeping without branches or atomics (0: the old form)
 #endif
+#ifndef HHT_FUSED_DESC_AHEAD
+#define HHT_FUSED_DESC_AHEAD 0                    // 1: each chunk's list span loaded one chunk ahead
+#endif
 #ifndef HHT_FUSED_ITEMS
 #define HHT_FUSED_ITEMS 13                        // raster batches of 13 lines per lane (416 entries)
 #endif
@@ -1224,6 +1227,11 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
         uint32_t p[kItems];
 #if !HHT_FUSED_JIT
         load_items(p, A.list, A.list_base, d, lane);
+#endif
+#if HHT_FUSED_DESC_AHEAD
+        uint64_t n_e0;                                     // the next chunk's list offset and count
+        uint32_t n_cnt;
+        span_of(A.chunks, c_lo + 1, c_hi, n_e0, n_cnt);
 #endif
         uint64_t ch = c_lo;
         uint32_t streamed = 0;                             // entries of this work unit (profiling)
@@ -1349,7 +1357,16 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
             __syncwarp();
             // the next chunk's entries are in flight while the full stacks are rastered
             ++ch;
+#if HHT_FUSED_DESC_AHEAD
+            // the entries' addresses come from the span loaded one chunk earlier, so their loads
+            // issue at once (ncu: the address add waiting on a just-issued descriptor load was the
+            // fused tail's top stall site, 4 % of its samples)
+            d.cnt = n_cnt;
+            d.e0 = n_e0;
+            span_of(A.chunks, ch + 1, c_hi, n_e0, n_cnt);
+#else
             d = load_desc(A.chunks, ch, c_hi);
+#endif
 #if !HHT_FUSED_JIT
             load_items(p, A.list, A.list_base, d, lane);
 #endif
