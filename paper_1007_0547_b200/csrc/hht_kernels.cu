@@ -248,9 +248,12 @@ __device__ __forceinline__ ChunkDesc load_desc(const ChunkDesc* __restrict__ d, 
         // the compiler right away, and that write then waits (write-after-write on the scoreboard)
         // for the load of a descriptor two chunks ahead (ncu, C5 last list pass: 27 % of all stall
         // samples on two such instructions)
+        // (the flag word through a plain global load: ptxas merges adjacent non-coherent loads of the
+        // same kind back into one 128-bit load)
         const uint4 u0 = __ldg(q);
         const uint2 e = __ldg(reinterpret_cast<const uint2*>(q + 1));
-        const uint32_t beta = __ldg(reinterpret_cast<const uint32_t*>(q + 1) + 2);
+        uint32_t beta;
+        asm("ld.global.u32 %0, [%1];" : "=r"(beta) : "l"(reinterpret_cast<const uint32_t*>(q + 1) + 2));
         z.r = u0.x; z.cnt = u0.y; z.a = u0.z; z.c = u0.w;
         z.e0 = ((uint64_t)e.y << 32) | e.x;
         z.beta = beta; z.pad = 0;
@@ -1142,6 +1145,9 @@ __global__ void __launch_bounds__(256, PREF ? 2 : 3) k_tail16(const PassArgs A) 
 #ifndef HHT_FUSED_BATCH_LEAN
 #define HHT_FUSED_BATCH_LEAN 1                    // per-batch bookkeeping without branches or atomics (0: the old form)
 #endif
+#ifndef HHT_FUSED_LINEAR
+#define HHT_FUSED_LINEAR 1                        // 1: chunk spans derived from the first chunk (no descriptor loads)
+#endif
 #ifndef HHT_FUSED_DESC_AHEAD
 #define HHT_FUSED_DESC_AHEAD 0                    // 1: each chunk's list span loaded one chunk ahead
 #endif
@@ -1232,6 +1238,12 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
         uint64_t n_e0;                                     // the next chunk's list offset and count
         uint32_t n_cnt;
         span_of(A.chunks, c_lo + 1, c_hi, n_e0, n_cnt);
+#elif HHT_FUSED_LINEAR
+        // a region's chunks are consecutive kChunk-entry pieces of its list (k_chunk_map), so chunk
+        // ch starts kChunk (ch - c_lo) entries after chunk c_lo and holds kChunk entries except the
+        // region's last: no descriptor load per chunk (the next chunk's entry loads issue at once)
+        const uint32_t cnt_last =
+            c_hi - c_lo > 1 ? __ldg(reinterpret_cast<const uint32_t*>(A.chunks + (c_hi - 1)) + 1) : d.cnt;
 #endif
         uint64_t ch = c_lo;
         uint32_t streamed = 0;                             // entries of this work unit (profiling)
@@ -1364,6 +1376,9 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks) k_fused(const 
             d.cnt = n_cnt;
             d.e0 = n_e0;
             span_of(A.chunks, ch + 1, c_hi, n_e0, n_cnt);
+#elif HHT_FUSED_LINEAR
+            d.e0 += kChunk;
+            d.cnt = ch + 1 == c_hi ? cnt_last : (ch < c_hi ? (uint32_t)kChunk : 0u);
 #else
             d = load_desc(A.chunks, ch, c_hi);
 #endif
