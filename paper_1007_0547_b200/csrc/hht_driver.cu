@@ -1682,17 +1682,25 @@ hht_status hht_detect_image(hht_ctx* x, const uint8_t* img, int32_t N, int32_t m
     const uint32_t ntiles = (uint32_t)((npix + kEdgeTile - 1) / kEdgeTile);
     TRY(ensure(x, x->packed, npix * 4));
     TRY(ensure(x, x->edgeB, npix * 4));
-    TRY(ensure(x, x->edgetiles, (size_t)ntiles * 8 + 256));
-    CK(cudaMemsetAsync(x->edgetiles.p, 0, (size_t)ntiles * 8 + 256, x->st));
+    // header (ticket at 0, super-tile sums at 2048) | tile words | (rows of 16k pixels: one mask word
+    // per thread of the mask pass)
+    constexpr size_t kEdgeHdr = 4096;
+    TRY(ensure(x, x->edgetiles, kEdgeHdr + (size_t)ntiles * 8 + (size_t)ntiles * 256 * 4));
+    CK(cudaMemsetAsync(x->edgetiles.p, 0, kEdgeHdr + (N % 16 != 0 ? (size_t)ntiles * 8 : 0), x->st));
+    uint32_t super_shift = 7;
+    while ((ntiles >> super_shift) >= 256) ++super_shift;
     EdgeArgs a{};
     a.img = dimg;
     a.W = a.H = N;
     a.thr = mag_threshold;
     a.outA = (uint32_t*)x->packed.p;
     a.outB = (uint32_t*)x->edgeB.p;
-    a.tiles = (unsigned long long*)((char*)x->edgetiles.p + 256);
+    a.tiles = (unsigned long long*)((char*)x->edgetiles.p + kEdgeHdr);
+    a.supers = (unsigned long long*)((char*)x->edgetiles.p + 2048);
+    a.super_shift = super_shift;
     a.tile_ctr = (uint32_t*)x->edgetiles.p;
     a.ntiles = ntiles;
+    a.masks = (uint32_t*)((char*)x->edgetiles.p + kEdgeHdr + (size_t)ntiles * 8);
     a.totals = x->misc_m;
     CK(cudaEventRecord(x->ee0, x->st));
     CK(launch_edges(a, x->st));

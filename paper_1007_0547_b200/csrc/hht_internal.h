@@ -201,9 +201,12 @@ struct EdgeArgs {
     int W, H, thr;
     uint32_t* outA;                // packed (x << 16 | y) ALPHA points, raster order
     uint32_t* outB;                // BETA points
-    unsigned long long* tiles;     // [ntiles] look-back words (zeroed)
-    uint32_t* tile_ctr;            // zeroed
-    uint32_t ntiles;
+    unsigned long long* tiles;     // [ntiles] k_edges: look-back words (zeroed); W % 16 == 0: tile counts (ALPHA << 32 | BETA)
+    unsigned long long* supers;    // [<= 256] W % 16 == 0: sums of the tile counts per 2^super_shift tiles (zeroed)
+    uint32_t super_shift;
+    uint32_t* tile_ctr;            // zeroed (k_edges)
+    uint32_t ntiles;               // 4096-pixel block tiles (k_edges)
+    uint32_t* masks;               // [256 ntiles] W % 16 == 0: each thread's 16 edge bits | 16 ALPHA bits << 16
     uint64_t* totals;              // [2] (mapped host): ALPHA count, BETA count (written by the last tile)
 };
 constexpr int kEdgeTile = 4096;    // pixels per 256-thread tile (16 per lane, lane-interleaved)

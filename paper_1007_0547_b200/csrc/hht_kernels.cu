@@ -1593,12 +1593,16 @@ __global__ void __launch_bounds__(256) k_edges(const EdgeArgs A) {
 // Rows whose width is a multiple of 16 (every power-of-two image): thread t of tile g owns the 16
 // consecutive pixels 4096 g + 16 t of one row, read as one 16-byte vector per row (rows r-1, r, r+1)
 // plus two halo bytes, so raster order is thread order.
-__device__ __forceinline__ int byte_of(const uint4& v, int k) {
-    const uint32_t w = k < 4 ? v.x : k < 8 ? v.y : k < 12 ? v.z : v.w;
-    return (int)((w >> (8 * (k & 3))) & 0xFFu);
-}
-
 // Edge (em) and ALPHA (am) bit masks of the 16 pixels starting at raster index p; r, c0 set.
+// Two pixels per 32-bit word, 16 bits each (columns c and c + 2 of a 4-byte group: (0,2), (1,3),
+// (4,6), ...), and the Sobel sums separably: per column s = u + 2m + d and t = u - d (u, m, d the rows
+// above, at and below), gx = s[c+1] - s[c-1], gy = t[c-1] + 2 t[c] + t[c+1]. Every half carries a
+// positive bias so that plain 32-bit adds never borrow across the halves: t + 256, gx + 0x4000,
+// gy + 1024; |v| + bias = max(v + bias, 2 bias - (v + bias)) (VIMNMX.S16x2, values below 2^15). The
+// two decisions are the top bit of each half of
+//   |gx| + |gy| - thr + 0x8000   (edge: |gx| + |gy| >= thr; thr clamped to 2041 > max |gx| + |gy|)
+//   |gy| - |gx| + 0x8000         (ALPHA: |gx| <= |gy|)
+// ~11 instructions per pixel instead of ~45 for the per-pixel 3x3 form.
 __device__ __forceinline__ void edge_masks16(const EdgeArgs& A, uint64_t p, uint32_t& r, uint32_t& c0,
                                              uint32_t& em, uint32_t& am) {
     em = am = 0;
@@ -1606,117 +1610,168 @@ __device__ __forceinline__ void edge_masks16(const EdgeArgs& A, uint64_t p, uint
     c0 = (uint32_t)(p - (uint64_t)r * A.W);
     if (p >= (uint64_t)A.W * A.H || A.thr <= 0 || r < 1 || r + 1 >= (uint32_t)A.H) return;
     const uint8_t* m = A.img + (uint64_t)r * A.W + c0;
+    const bool hasl = c0 > 0, hasr = c0 + 16 < (uint32_t)A.W;
     uint4 rows[3];
-    int hl[3], hr[3];
+    uint32_t hl[3], hr[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {                 // j = 0: row above (geometric y+1), 1: this row, 2: below
         const uint8_t* q = m + (j - 1) * (int64_t)A.W;
         rows[j] = __ldg(reinterpret_cast<const uint4*>(q));
-        hl[j] = c0 > 0 ? __ldg(q - 1) : 0;
-        hr[j] = c0 + 16 < (uint32_t)A.W ? __ldg(q + 16) : 0;
+        hl[j] = hasl ? __ldg(q - 1) : 0;
+        hr[j] = hasr ? __ldg(q + 16) : 0;
     }
+    // S[2g], T[2g]: columns (4g, 4g+2); S[2g+1], T[2g+1]: columns (4g+1, 4g+3)
+    uint32_t S[8], T[8];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        const uint32_t c = c0 + k;
-        if (c >= 1 && c + 1 < (uint32_t)A.W) {
-            int v[3][3];
+    for (int g = 0; g < 4; ++g) {
+        const uint32_t u = g == 0 ? rows[0].x : g == 1 ? rows[0].y : g == 2 ? rows[0].z : rows[0].w;
+        const uint32_t c = g == 0 ? rows[1].x : g == 1 ? rows[1].y : g == 2 ? rows[1].z : rows[1].w;
+        const uint32_t d = g == 0 ? rows[2].x : g == 1 ? rows[2].y : g == 2 ? rows[2].z : rows[2].w;
+        const uint32_t ue = u & 0x00FF00FFu, ce = c & 0x00FF00FFu, de = d & 0x00FF00FFu;
+        const uint32_t uo = __byte_perm(u, 0, 0x4341), co = __byte_perm(c, 0, 0x4341), dd = __byte_perm(d, 0, 0x4341);
+        S[2 * g] = ue + 2 * ce + de;
+        S[2 * g + 1] = uo + 2 * co + dd;
+        T[2 * g] = ue - de + 0x01000100u;
+        T[2 * g + 1] = uo - dd + 0x01000100u;
+    }
+    const uint32_t sl = hl[0] + 2 * hl[1] + hl[2], sr = hr[0] + 2 * hr[1] + hr[2];   // columns -1 and 16
+    const uint32_t tl = hl[0] - hl[2] + 256u, tr = hr[0] - hr[2] + 256u;
+    uint32_t E = 0, Q = 0;
+    const uint32_t thr = (uint32_t)min(A.thr, 2041);
+    const uint32_t ke = 0x80008000u - 0x44004400u - thr * 0x10001u;
 #pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                v[j][0] = k == 0 ? hl[j] : byte_of(rows[j], k - 1);
-                v[j][1] = byte_of(rows[j], k);
-                v[j][2] = k == 15 ? hr[j] : byte_of(rows[j], k + 1);
-            }
-            const int gx = (v[0][2] - v[0][0]) + 2 * (v[1][2] - v[1][0]) + (v[2][2] - v[2][0]);
-            const int gy = (v[0][0] + 2 * v[0][1] + v[0][2]) - (v[2][0] + 2 * v[2][1] + v[2][2]);
-            const int ax = abs(gx), ay = abs(gy);
-            if (ax + ay >= A.thr) {
-                em |= 1u << k;
-                if (ax <= ay) am |= 1u << k;
-            }
+    for (int g = 0; g < 4; ++g) {
+        // left of (4g, 4g+2) = (4g-1, 4g+1); right of (4g+1, 4g+3) = (4g+2, 4g+4)
+        const uint32_t Sl = g == 0 ? __byte_perm(sl, S[1], 0x5410) : __byte_perm(S[2 * g - 1], S[2 * g + 1], 0x5432);
+        const uint32_t Tl = g == 0 ? __byte_perm(tl, T[1], 0x5410) : __byte_perm(T[2 * g - 1], T[2 * g + 1], 0x5432);
+        const uint32_t Sr = g == 3 ? __byte_perm(S[6], sr, 0x5432) : __byte_perm(S[2 * g], S[2 * g + 2], 0x5432);
+        const uint32_t Tr = g == 3 ? __byte_perm(T[6], tr, 0x5432) : __byte_perm(T[2 * g], T[2 * g + 2], 0x5432);
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+            // word w = 2g + o: o = 0 has neighbours (Sl, S[w+1]); o = 1 has (S[w-1], Sr)
+            const uint32_t s_lo = o == 0 ? Sl : S[2 * g], s_hi = o == 0 ? S[2 * g + 1] : Sr;
+            const uint32_t t_lo = o == 0 ? Tl : T[2 * g], t_hi = o == 0 ? T[2 * g + 1] : Tr;
+            const uint32_t gxb = s_hi - s_lo + 0x40004000u;
+            const uint32_t ax = __vmaxs2(gxb, 0x80008000u - gxb);            // |gx| + 0x4000
+            const uint32_t gyb = t_lo + t_hi + 2 * T[2 * g + o];               // gy + 1024
+            const uint32_t ay = __vmaxs2(gyb, 0x08000800u - gyb);            // |gy| + 1024
+            const uint32_t e = ax + ay + ke, q = ay - ax + 0xBC00BC00u;
+            // bit 15 -> column 4g + o, bit 31 -> bit 16 + 4g + o (column 4g + o + 2, folded below)
+            const int sh = 15 - (4 * g + o);
+            E |= (e >> sh) & (0x10001u << (4 * g + o));
+            Q |= (q >> sh) & (0x10001u << (4 * g + o));
         }
+    }
+    em = (E | (E >> 14)) & 0xFFFFu;
+    if (!hasl) em &= ~1u;                      // image columns 0 and W-1 have no gradient
+    if (!hasr) em &= ~0x8000u;
+    am = (Q | (Q >> 14)) & em;
+}
+
+// Rows whose width is a multiple of 16: two launches and no look-back. A single pass with a
+// decoupled look-back over the 4096-pixel tiles (round 1) spent 45 % of its stall samples at the
+// barrier behind warp 0's look-back: the ~1200 resident tiles of a wave publish their aggregates
+// together and the inclusive prefix then walks them 32 per L2 round trip (ncu, round 2; one
+// look-back word per warp instead was slower still, 0.26 vs 0.17 ms; a one-block scan kernel between
+// the two passes cost 23 us). Here
+//   k_edges16_masks  reads the image once, writes each thread's (em | am << 16) word and the tile's
+//                    (ALPHA count << 32 | BETA count), and adds the latter to its super-tile's sum
+//                    (2^super_shift tiles, at most 256 super-tiles: one 64-bit atomic per tile);
+//   k_edges16_write  warp 0 sums the earlier super-tiles and the earlier tiles of its own super-tile
+//                    (a few loads per lane, no dependence on other blocks) while the other warps
+//                    reread their mask words (1/4 B per pixel) and scan them in thread (= raster)
+//                    order; each warp then stages its points in shared memory (ALPHA from the front
+//                    of its 512 words, BETA from the back) and copies both runs out coalesced.
+__global__ void __launch_bounds__(256) k_edges16_masks(const EdgeArgs A) {
+    __shared__ uint32_t s_w[8];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t tile = blockIdx.x;
+    uint32_t r, c0, em, am;
+    edge_masks16(A, (uint64_t)tile * kEdgeTile + 16ull * tid, r, c0, em, am);
+    A.masks[(size_t)tile * 256 + tid] = em | (am << 16);
+    const uint32_t w = __reduce_add_sync(kFull, __popc(em & am) | (__popc(em & ~am) << 16));
+    if (lane == 0) s_w[wid] = w;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t += s_w[i];
+        const unsigned long long c = ((unsigned long long)(t & 0xFFFFu) << 32) | (t >> 16);
+        A.tiles[tile] = c;
+        if (c) atomicAdd(A.supers + (tile >> A.super_shift), c);
     }
 }
 
-// Single pass: masks, block scan in thread (= raster) order, look-back over the tiles (as k_edges),
-// direct writes of each thread's points. Measured faster than both a smem-staged copy-out and a
-// reduce-then-scan pair of passes (the per-pixel arithmetic, not the compaction, is the cost).
-__global__ void __launch_bounds__(256) k_edges16(const EdgeArgs A) {
-    __shared__ uint32_t s_tile;
+__global__ void __launch_bounds__(256) k_edges16_write(const EdgeArgs A) {
     __shared__ uint32_t s_w[8];
-    __shared__ uint32_t s_pa, s_pb;
+    __shared__ unsigned long long s_base;
+    __shared__ uint32_t s_pts[8][512];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(A.tile_ctr, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    uint32_t r, c0, em, am;
-    edge_masks16(A, (uint64_t)tile * kEdgeTile + 16ull * tid, r, c0, em, am);
-    const uint32_t own = __popc(em & am) | (__popc(em & ~am) << 16);
+    const uint32_t tile = blockIdx.x;
+    const uint32_t mw = A.masks[(size_t)tile * 256 + tid];
+    if (wid == 0) {
+        const uint32_t sb = tile >> A.super_shift;
+        unsigned long long sum = 0;
+        for (uint32_t i = lane; i < sb; i += 32) sum += A.supers[i];
+        for (uint32_t t = (sb << A.super_shift) + lane; t < tile; t += 32) sum += A.tiles[t];
+#pragma unroll
+        for (int dd = 16; dd; dd >>= 1) sum += __shfl_xor_sync(kFull, sum, dd);
+        if (lane == 0) s_base = sum;
+    }
+    const uint32_t em = mw & 0xFFFFu, ma = mw >> 16, mb = em & ~ma;   // am is a subset of em
+    const uint32_t own = __popc(ma) | (__popc(mb) << 16);
     uint32_t inc = own;
 #pragma unroll
     for (int dd = 1; dd < 32; dd <<= 1) {
         const uint32_t t = __shfl_up_sync(kFull, inc, dd);
         if (lane >= dd) inc += t;
     }
+    const uint32_t wtot = __shfl_sync(kFull, inc, 31);
     if (lane == 31) s_w[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-        const uint32_t vw = lane < 8 ? s_w[lane] : 0;
-        uint32_t iw = vw;
+    // stage: ALPHA points at s_pts[wid][0 ..), BETA points at s_pts[wid][511 ..) downwards
+    {
+        const uint64_t p = (uint64_t)tile * kEdgeTile + 16ull * tid;
+        const uint32_t r = (uint32_t)(p / (uint64_t)A.W), c0 = (uint32_t)(p - (uint64_t)r * A.W);
+        uint32_t pt = (c0 << 16) | ((uint32_t)(A.H - 1) - r);
+        const uint32_t excl = inc - own;
+        uint32_t* qa = &s_pts[wid][excl & 0xFFFFu];
+        uint32_t* qb = &s_pts[wid][511 - (excl >> 16)];
+        if (em) {
 #pragma unroll
-        for (int dd = 1; dd < 8; dd <<= 1) {
-            const uint32_t t = __shfl_up_sync(kFull, iw, dd);
-            if (lane >= dd) iw += t;
-        }
-        if (lane < 8) s_w[lane] = iw - vw;
-        const uint32_t tot = __shfl_sync(kFull, iw, 7);
-        const uint32_t ta = tot & 0xFFFFu, tb = tot >> 16;
-        using dev_u64w = cuda::atomic_ref<unsigned long long, cuda::thread_scope_device>;
-        uint32_t ea = 0, eb = 0;
-        if (tile == 0) {
-            if (lane == 0) dev_u64w(A.tiles[0]).store(edge_word(kEdgeInc, ta, tb), cuda::memory_order_relaxed);
-        } else {
-            if (lane == 0) dev_u64w(A.tiles[tile]).store(edge_word(kEdgeAgg, ta, tb), cuda::memory_order_relaxed);
-            int64_t pred = (int64_t)tile - 1;
-            while (true) {
-                const int64_t t = pred - lane;
-                unsigned long long wv = kEdgeInc;
-                if (t >= 0) {
-                    do { wv = dev_u64w(A.tiles[t]).load(cuda::memory_order_relaxed); } while ((wv >> 62) == 0);
-                }
-                const uint32_t pm = __ballot_sync(kFull, (wv >> 62) == 2);
-                const int stop = pm ? __ffs(pm) - 1 : 31;
-                uint32_t xa = (uint32_t)((wv >> 31) & kEdgeMask), xb = (uint32_t)(wv & kEdgeMask);
-                if (lane > stop || t < 0) { xa = 0; xb = 0; }
-                ea += __reduce_add_sync(kFull, xa);
-                eb += __reduce_add_sync(kFull, xb);
-                if (pm) break;
-                pred -= 32;
+            for (int k = 0; k < 16; ++k) {
+                if ((ma >> k) & 1u) *qa++ = pt;
+                if ((mb >> k) & 1u) *qb-- = pt;
+                pt += 1u << 16;
             }
-            if (lane == 0) dev_u64w(A.tiles[tile]).store(edge_word(kEdgeInc, ea + ta, eb + tb), cuda::memory_order_relaxed);
-        }
-        if (lane == 0) {
-            s_pa = ea;
-            s_pb = eb;
-            if (tile == A.ntiles - 1) { A.totals[0] = ea + ta; A.totals[1] = eb + tb; }
         }
     }
     __syncthreads();
-    const uint32_t excl = inc - own + s_w[wid];
-    uint32_t pa = s_pa + (excl & 0xFFFFu), pb = s_pb + (excl >> 16);
-    const uint32_t y = (uint32_t)(A.H - 1) - r;
-    while (em) {
-        const int k = __ffs(em) - 1;
-        em &= em - 1;
-        const uint32_t pt = ((c0 + k) << 16) | y;
-        if ((am >> k) & 1u) A.outA[pa++] = pt;
-        else A.outB[pb++] = pt;
+    uint32_t before = 0;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) before += i < wid ? s_w[i] : 0u;
+    const unsigned long long tb = s_base;
+    if (tid == 0 && tile == A.ntiles - 1) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t += s_w[i];
+        A.totals[0] = (tb >> 32) + (t & 0xFFFFu);
+        A.totals[1] = (tb & 0xFFFFFFFFull) + (t >> 16);
     }
+    const uint32_t na = wtot & 0xFFFFu, nb = wtot >> 16;
+    uint32_t* __restrict__ oa = A.outA + ((uint32_t)(tb >> 32) + (before & 0xFFFFu));
+    uint32_t* __restrict__ ob = A.outB + ((uint32_t)tb + (before >> 16));
+    for (uint32_t i = lane; i < na; i += 32) oa[i] = s_pts[wid][i];
+    for (uint32_t i = lane; i < nb; i += 32) ob[i] = s_pts[wid][511 - i];
 }
 
 cudaError_t launch_edges(const EdgeArgs& a, cudaStream_t st) {
     if (a.ntiles == 0) return cudaSuccess;
-    if (a.W % 16 == 0) k_edges16<<<a.ntiles, 256, 0, st>>>(a);
-    else k_edges<<<a.ntiles, 256, 0, st>>>(a);
+    if (a.W % 16 == 0) {
+        k_edges16_masks<<<a.ntiles, 256, 0, st>>>(a);
+        k_edges16_write<<<a.ntiles, 256, 0, st>>>(a);
+    } else {
+        k_edges<<<a.ntiles, 256, 0, st>>>(a);
+    }
     return cudaGetLastError();
 }
 

@@ -56,10 +56,10 @@ def _sampled_brute(h, pts, cfg, image, nsamp, rng):
             assert ((i, j) in cells) == (v > cfg.T), (half, i, j, v)
 
 
-@pytest.mark.parametrize("cid,int64", [(3, False), (4, False), (5, False), (3, True), (4, True)])
+@pytest.mark.parametrize("cid,int64", [(3, False), (4, False), (5, False), (3, True), (4, True), (5, True)])
 def test_fullsize_config(cid, int64, cuda_device):
     """The bench's launch configuration (int32, where exact for every config), and the int64
-    instantiation north_star names on configs 3 and 4, against the oracle's digests."""
+    instantiation north_star names on configs 3-5, against the oracle's digests."""
     import torch
     path = os.path.join(GOLD, f"c{cid}_digest.json")
     cfg = synth.CONFIGS[cid]
