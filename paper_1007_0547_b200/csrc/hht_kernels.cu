@@ -1712,7 +1712,9 @@ __global__ void __launch_bounds__(256) k_edges16_write(const EdgeArgs A) {
     if (wid == 0) {
         const uint32_t sb = tile >> A.super_shift;
         unsigned long long sum = 0;
+#pragma unroll 4
         for (uint32_t i = lane; i < sb; i += 32) sum += A.supers[i];
+#pragma unroll 4
         for (uint32_t t = (sb << A.super_shift) + lane; t < tile; t += 32) sum += A.tiles[t];
 #pragma unroll
         for (int dd = 16; dd; dd >>= 1) sum += __shfl_xor_sync(kFull, sum, dd);
@@ -1760,7 +1762,9 @@ __global__ void __launch_bounds__(256) k_edges16_write(const EdgeArgs A) {
     const uint32_t na = wtot & 0xFFFFu, nb = wtot >> 16;
     uint32_t* __restrict__ oa = A.outA + ((uint32_t)(tb >> 32) + (before & 0xFFFFu));
     uint32_t* __restrict__ ob = A.outB + ((uint32_t)tb + (before >> 16));
+#pragma unroll 1
     for (uint32_t i = lane; i < na; i += 32) oa[i] = s_pts[wid][i];
+#pragma unroll 1
     for (uint32_t i = lane; i < nb; i += 32) ob[i] = s_pts[wid][511 - i];
 }
 

@@ -36,3 +36,11 @@ timeout 900 ncu --set full --clock-control none --import-source on --kernel-name
     -k regex:"k_pass<int, \\(int\\)1," -s 6 -c 1 \
     -o gpurun_out/c5_write_ca python scripts/run_once.py --config 5 > gpurun_out/ncu_write_ca.log 2>&1
 echo "count-ahead capture rc=$?"
+# edge front end (NEXT-3) on the same build
+python scripts/frontend_bench.py --out gpurun_out/frontend.md > gpurun_out/frontend.log 2>&1
+echo "frontend rc=$?"
+# counters of this build into profiles/ncu_traffic.json (on the box), then the default bench line
+# again so that roofline.traffic carries them (bench.py attaches counters only by build id)
+python scripts/ncu_summary.py --round 2 > gpurun_out/ncu_summary.log 2>&1 && \
+python bench.py > gpurun_out/bench_default.log 2> gpurun_out/bench_default.err
+echo "bench with traffic rc=$?"
