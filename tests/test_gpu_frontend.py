@@ -51,6 +51,28 @@ def test_edges_match_oracle(name, img, thr, cuda_device):
     assert np.array_equal(a, a_ref) and np.array_equal(b, b_ref), (a.shape, a_ref.shape, b.shape, b_ref.shape)
 
 
+@pytest.mark.parametrize("N,kind", [(1040, "random"), (2048, "random"), (2048, "sparse")])
+def test_edges_many_tiles(N, kind, cuda_device):
+    """Widths that are a multiple of 16 with several super-tiles of 128 tiles (k_edges16_write sums
+    the earlier super-tiles and tiles itself): 1040^2 = 265 tiles (a width that is not a power of two),
+    2048^2 = 1024 tiles (8 super-tiles); dense random edges and a sparse image whose first super-tiles
+    are empty. The threshold is above the point count, so the trees stop at the root."""
+    import torch
+    rng = np.random.default_rng(N)
+    if kind == "random":
+        img, thr = rng.integers(0, 256, size=(N, N), dtype=np.uint8), 300
+    else:
+        img, thr = np.zeros((N, N), np.uint8), 200
+        img[N // 2 + 5, 7:N - 9:3] = 255
+        img[N - 40:N - 2, N - 33] = 250
+    a_ref, b_ref = oracle.edges(img, thr)
+    assert a_ref.shape[0] + b_ref.shape[0] > 0
+    h = hht.HHT(halves=AB)
+    h.detect_image(torch.from_numpy(img).to(cuda_device), thr, 3, N * N)
+    a, b = h.edges()
+    assert np.array_equal(a, a_ref) and np.array_equal(b, b_ref), (a.shape, a_ref.shape, b.shape, b_ref.shape)
+
+
 @pytest.mark.parametrize("N,seed,T", [(32, 11, 3), (64, 12, 6), (128, 13, 10), (256, 14, 24)])
 def test_detect_image_matches_oracle(N, seed, T, cuda_device):
     import torch
